@@ -1,0 +1,483 @@
+// C-ABI entry points and execution-plan construction (include/einet_b200.h).
+//
+// einet_plan_create turns a compiled LayeredCircuit (compiler.py:54-99) into
+// the device execution plan: slab ids for every layer output, responsibility
+// slots for every child contribution, the per-slab CSR that replaces
+// np.add.at (engine.py:315-316), parameter/statistics offsets and the
+// workspace layout for a chunk of max_chunk samples.
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "einet_internal.h"
+
+namespace einet {
+
+static thread_local std::string g_last_error = "";
+static std::atomic<long long> g_launches{0};
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+int fail(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+int check_cuda(cudaError_t err, const char *what) {
+  if (err == cudaSuccess) return EINET_OK;
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(err);
+  return EINET_ERR_CUDA;
+}
+void count_launch(int n) { g_launches += n; }
+
+template <typename T>
+static int upload(T **dst, const std::vector<T> &src) {
+  *dst = nullptr;
+  size_t n = std::max<size_t>(src.size(), 1);
+  int rc = check_cuda(cudaMalloc((void **)dst, n * sizeof(T)), "cudaMalloc(plan)");
+  if (rc) return rc;
+  if (!src.empty())
+    rc = check_cuda(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T),
+                               cudaMemcpyHostToDevice),
+                    "cudaMemcpy(plan)");
+  return rc;
+}
+
+static void free_plan_memory(Plan *p) {
+  auto f = [](void *ptr) {
+    if (ptr) cudaFree(ptr);
+  };
+  f(p->d_scope_off);
+  f(p->d_scope_vars);
+  f(p->d_leaf_rep);
+  f(p->d_leaf_slab);
+  f(p->d_leaf_of);
+  f(p->d_csr_off);
+  f(p->d_csr_slot);
+  f(p->d_slab_ones);
+  f(p->d_mixrow_off);
+  f(p->d_mixrow_len);
+  f(p->d_mix_mask_all);
+  for (auto &L : p->layers) {
+    f(L.d_left_slab);
+    f(L.d_right_slab);
+    f(L.d_out_slab);
+    f(L.d_slot_left);
+    f(L.d_slot_right);
+    f(L.d_mix_src_slab);
+    f(L.d_mix_slot);
+    f(L.d_mix_mask);
+  }
+}
+
+static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
+  if (!d) return fail(EINET_ERR_USAGE, "null plan descriptor");
+  if (d->d_vars < 1 || d->k < 1 || d->k_root < 1 || d->num_replicas < 1)
+    return fail(EINET_ERR_USAGE, "d_vars, k, k_root and num_replicas must be >= 1");
+  if (d->n_leaf < 1 || d->n_layers < 1)
+    return fail(EINET_ERR_USAGE, "plan needs a leaf layer and at least one einsum layer");
+  if (max_chunk < 1) return fail(EINET_ERR_USAGE, "max_chunk must be >= 1");
+  if (d->family < 0 || d->family > 2) return fail(EINET_ERR_USAGE, "unknown family id");
+  if (d->family == EINET_FAMILY_CATEGORICAL && d->num_states < 1)
+    return fail(EINET_ERR_USAGE, "categorical family needs num_states >= 1");
+  if (d->family == EINET_FAMILY_BINOMIAL && d->n_trials < 0)
+    return fail(EINET_ERR_USAGE, "binomial family needs n_trials >= 0");
+
+  p->d_vars = d->d_vars;
+  p->k = d->k;
+  p->k_root = d->k_root;
+  p->ks = std::max(d->k, d->k_root);
+  p->num_replicas = d->num_replicas;
+  p->nbr = d->num_buffer_rows;
+  p->family = d->family;
+  p->num_states = d->num_states;
+  p->n_trials = d->n_trials;
+  p->suff = d->family == EINET_FAMILY_GAUSSIAN ? 2
+            : d->family == EINET_FAMILY_CATEGORICAL ? d->num_states
+                                                    : 1;
+  p->var_min = d->var_min;
+  p->var_max = d->var_max;
+  p->p_min = d->p_min;
+  p->n_leaf = d->n_leaf;
+  p->max_chunk = max_chunk;
+  p->root_mix_row = d->root_mix_row;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+        sms > 0)
+      p->num_sms = sms;
+    cudaGetLastError();
+  }
+  const int D = p->d_vars, K = p->k, R = p->num_replicas;
+
+  // ---- leaf layer ----------------------------------------------------------
+  p->h_scope_off.assign(d->leaf_scope_offsets, d->leaf_scope_offsets + d->n_leaf + 1);
+  const int nvars = p->h_scope_off.back();
+  p->h_scope_vars.assign(d->leaf_scope_vars, d->leaf_scope_vars + nvars);
+  p->h_leaf_rep.assign(d->leaf_replica, d->leaf_replica + d->n_leaf);
+  p->h_leaf_slab.assign(d->leaf_out_rows, d->leaf_out_rows + d->n_leaf);
+  std::vector<int> leaf_of((size_t)R * D, -1);
+  for (int l = 0; l < d->n_leaf; ++l) {
+    int r = p->h_leaf_rep[l];
+    if (r < 0 || r >= R) return fail(EINET_ERR_USAGE, "leaf replica out of range");
+    int len = p->h_scope_off[l + 1] - p->h_scope_off[l];
+    if (len < 1) return fail(EINET_ERR_USAGE, "empty leaf scope");
+    p->max_scope = std::max(p->max_scope, len);
+    for (int q = p->h_scope_off[l]; q < p->h_scope_off[l + 1]; ++q) {
+      int v = p->h_scope_vars[q];
+      if (v < 0 || v >= D) return fail(EINET_ERR_USAGE, "leaf scope variable out of range");
+      leaf_of[(size_t)r * D + v] = l;
+    }
+  }
+
+  // ---- layers, slabs -------------------------------------------------------
+  int next_slab = p->nbr;
+  int64_t w_acc = 0, mix_acc = 0;
+  p->layers.resize(d->n_layers);
+  for (int i = 0; i < d->n_layers; ++i) {
+    const einet_layer_desc &ld = d->layers[i];
+    LayerPlan &L = p->layers[i];
+    L.kind = ld.kind;
+    L.index = i + 1;
+    L.rows = ld.rows;
+    L.k_out = ld.k_out;
+    L.is_root = ld.is_root;
+    L.dmax = ld.dmax;
+    if (ld.rows < 1) return fail(EINET_ERR_USAGE, "layer with no rows");
+    if (ld.k_out != (ld.is_root ? d->k_root : d->k))
+      return fail(EINET_ERR_USAGE, "layer k_out does not match k / k_root");
+    L.h_out_slab.resize(ld.rows);
+    for (int r = 0; r < ld.rows; ++r) {
+      int o = ld.out_rows[r];
+      if (o >= p->nbr) return fail(EINET_ERR_USAGE, "out row beyond num_buffer_rows");
+      L.h_out_slab[r] = o >= 0 ? o : next_slab++;
+    }
+    p->max_rows = std::max<int64_t>(p->max_rows, ld.rows);
+    if (ld.kind == EINET_LAYER_EINSUM) {
+      for (int r = 0; r < ld.rows; ++r)
+        if (ld.left[r] < 0 || ld.left[r] >= p->nbr || ld.right[r] < 0 ||
+            ld.right[r] >= p->nbr)
+          return fail(EINET_ERR_USAGE, "einsum child row out of range");
+      L.w_off = w_acc;
+      int64_t lw = (int64_t)ld.rows * ld.k_out * K * K;
+      w_acc += lw;
+      p->max_layer_w = std::max(p->max_layer_w, lw);
+    } else if (ld.kind == EINET_LAYER_MIXING) {
+      if (i == 0 || d->layers[i - 1].kind != EINET_LAYER_EINSUM)
+        return fail(EINET_ERR_USAGE, "mixing layer must follow an einsum layer");
+      if (ld.dmax < 1) return fail(EINET_ERR_USAGE, "mixing layer with dmax < 1");
+      L.mix_off = mix_acc;
+      mix_acc += (int64_t)ld.rows * ld.dmax;
+      L.h_src.assign(ld.src, ld.src + (size_t)ld.rows * ld.dmax);
+      L.h_mask.assign(ld.mask, ld.mask + (size_t)ld.rows * ld.dmax);
+    } else {
+      return fail(EINET_ERR_USAGE, "unknown layer kind");
+    }
+  }
+  p->num_slabs = next_slab;
+  p->n_w = w_acc;
+  p->n_mix = mix_acc;
+  p->n_mix_entries = mix_acc;
+  p->n_phi = (int64_t)D * K * R * p->suff;
+
+  const LayerPlan &last = p->layers.back();
+  if (!last.is_root) return fail(EINET_ERR_USAGE, "last layer must hold the root");
+  if (last.kind == EINET_LAYER_MIXING) {
+    if (p->root_mix_row < 0 || p->root_mix_row >= last.rows)
+      return fail(EINET_ERR_USAGE, "root_mix_row out of range");
+    p->root_out_slab = last.h_out_slab[p->root_mix_row];
+  } else {
+    p->root_out_slab = last.h_out_slab[0];
+  }
+
+  // ---- slots and CSR -----------------------------------------------------
+  std::vector<std::vector<int>> contrib(p->num_slabs);
+  p->h_slab_ones.assign(p->num_slabs, 0);
+  int next_slot = 0;
+  std::vector<std::vector<int>> slot_left(d->n_layers), slot_right(d->n_layers),
+      mix_slot(d->n_layers), mix_src_slab(d->n_layers);
+  for (int i = 0; i < d->n_layers; ++i) {
+    const einet_layer_desc &ld = d->layers[i];
+    LayerPlan &L = p->layers[i];
+    if (ld.kind == EINET_LAYER_EINSUM) {
+      slot_left[i].resize(ld.rows);
+      slot_right[i].resize(ld.rows);
+      for (int r = 0; r < ld.rows; ++r) {
+        slot_left[i][r] = next_slot++;
+        slot_right[i][r] = next_slot++;
+      }
+    } else {
+      const LayerPlan &prev = p->layers[i - 1];
+      mix_slot[i].assign((size_t)ld.rows * ld.dmax, -1);
+      mix_src_slab[i].assign((size_t)ld.rows * ld.dmax, -1);
+      for (int m = 0; m < ld.rows; ++m)
+        for (int c = 0; c < ld.dmax; ++c) {
+          size_t q = (size_t)m * ld.dmax + c;
+          if (!L.h_mask[q]) continue;
+          int s = L.h_src[q];
+          if (s < 0 || s >= prev.rows) return fail(EINET_ERR_USAGE, "mixing src out of range");
+          mix_slot[i][q] = next_slot++;
+          mix_src_slab[i][q] = prev.h_out_slab[s];
+        }
+    }
+  }
+  p->num_slots = next_slot;
+  // contributions ordered top-down (the reference's backward order)
+  for (int i = d->n_layers - 1; i >= 0; --i) {
+    const einet_layer_desc &ld = d->layers[i];
+    if (ld.kind == EINET_LAYER_EINSUM) {
+      for (int r = 0; r < ld.rows; ++r) contrib[ld.left[r]].push_back(slot_left[i][r]);
+      for (int r = 0; r < ld.rows; ++r) contrib[ld.right[r]].push_back(slot_right[i][r]);
+    } else {
+      for (size_t q = 0; q < mix_slot[i].size(); ++q)
+        if (mix_slot[i][q] >= 0) contrib[mix_src_slab[i][q]].push_back(mix_slot[i][q]);
+    }
+  }
+  p->h_slab_ones[p->root_out_slab] = 1;
+  p->h_csr_off.assign(p->num_slabs + 1, 0);
+  for (int s = 0; s < p->num_slabs; ++s)
+    p->h_csr_off[s + 1] = p->h_csr_off[s] + (int)contrib[s].size();
+  p->h_csr_slot.clear();
+  for (int s = 0; s < p->num_slabs; ++s)
+    p->h_csr_slot.insert(p->h_csr_slot.end(), contrib[s].begin(), contrib[s].end());
+
+  // ---- sizes ---------------------------------------------------------------
+  einet_sizes &z = p->sizes;
+  z.params_f64 = p->n_w + p->n_mix + p->n_phi;
+  z.mixing_offset = p->n_w;
+  z.phi_offset = p->n_w + p->n_mix;
+  z.stats_acc_pt_offset = p->n_w + p->n_mix;
+  z.stats_p_offset = z.stats_acc_pt_offset + p->n_phi;
+  z.stats_ll_offset = z.stats_p_offset + (int64_t)p->n_leaf * K;
+  z.stats_f64 = z.stats_ll_offset + 2;
+  z.max_chunk = max_chunk;
+  z.suff_dim = p->suff;
+
+  const int64_t A = 256;
+  int64_t off = 0;
+  auto seg = [&](int64_t bytes) {
+    int64_t at = off;
+    off = align_up(off + std::max<int64_t>(bytes, 0), A);
+    return at;
+  };
+  const int64_t RDK = (int64_t)R * D * K;
+  p->c_w32 = seg(4 * p->n_w);
+  p->c_mix32 = seg(4 * std::max<int64_t>(p->n_mix, 1));
+  if (p->family == EINET_FAMILY_CATEGORICAL)
+    p->c_leafp = seg(4 * RDK * p->num_states);
+  else
+    p->c_leafp = seg(8 * RDK);
+  p->c_center = seg(4 * RDK);
+  p->c_const = seg(8 * (int64_t)p->n_leaf * K);
+  p->c_active = seg(D);
+  p->c_logh = seg(8 * (int64_t)(std::max(p->n_trials, 0) + 1));
+  z.compute_bytes = off;
+
+  const int64_t Bc = max_chunk, KS = p->ks;
+  off = 0;
+  p->w_off = seg(4 * (int64_t)p->num_slabs * Bc * KS);
+  p->w_shift = seg(8 * (int64_t)p->num_slabs * Bc);
+  p->w_slots = seg(4 * (int64_t)std::max(p->num_slots, 1) * Bc * KS);
+  p->w_leafpart = seg(8 * (int64_t)kMaxDSplit * p->n_leaf * Bc * K);
+  p->w_ea = seg(4 * p->max_rows * Bc * K);
+  p->w_eb = seg(4 * p->max_rows * Bc * K);
+  p->w_rt = seg(4 * p->max_rows * Bc * KS);
+  // W-stat partials: bsplit chosen per layer by the launcher, bounded here
+  int64_t wpart = 0;
+  for (auto &L : p->layers) {
+    if (L.kind != EINET_LAYER_EINSUM) continue;
+    int64_t lw = (int64_t)L.rows * L.k_out * K * K;
+    int64_t blocks = (int64_t)L.rows * L.k_out;
+    int64_t bs = std::min<int64_t>(std::max<int64_t>(1, (2 * p->num_sms + blocks - 1) / blocks),
+                                   std::min<int64_t>(kMaxBSplit, (Bc + 63) / 64));
+    wpart = std::max(wpart, bs * lw);
+  }
+  p->w_wpart = seg(8 * std::max<int64_t>(wpart, 1));
+  p->w_rho = seg(4 * (int64_t)p->n_leaf * Bc * K);
+  p->max_lsplit = leaf_lsplit(*p, Bc);
+  p->w_lspart = seg(8 * (int64_t)p->max_lsplit * p->n_phi);
+  p->w_ppart = seg(8 * (int64_t)ceil_div(Bc, 128) * p->n_leaf * K);
+  p->w_mixpart = seg(8 * (int64_t)ceil_div(Bc, 64) * std::max<int64_t>(p->n_mix, 1));
+  p->w_llpart = seg(8 * (int64_t)ceil_div(Bc, 256));
+  p->w_scratch_end = off;
+  z.workspace_bytes = off;
+
+  // ---- device copies ---------------------------------------------------------
+  int rc;
+  if ((rc = upload(&p->d_scope_off, p->h_scope_off))) return rc;
+  if ((rc = upload(&p->d_scope_vars, p->h_scope_vars))) return rc;
+  if ((rc = upload(&p->d_leaf_rep, p->h_leaf_rep))) return rc;
+  if ((rc = upload(&p->d_leaf_slab, p->h_leaf_slab))) return rc;
+  if ((rc = upload(&p->d_leaf_of, leaf_of))) return rc;
+  if ((rc = upload(&p->d_csr_off, p->h_csr_off))) return rc;
+  if ((rc = upload(&p->d_csr_slot, p->h_csr_slot))) return rc;
+  if ((rc = upload(&p->d_slab_ones, p->h_slab_ones))) return rc;
+  {
+    std::vector<int> roff, rlen;
+    std::vector<uint8_t> mall;
+    for (auto &L : p->layers) {
+      if (L.kind != EINET_LAYER_MIXING) continue;
+      for (int m = 0; m < L.rows; ++m) {
+        roff.push_back((int)(L.mix_off + (int64_t)m * L.dmax));
+        rlen.push_back(L.dmax);
+      }
+      mall.insert(mall.end(), L.h_mask.begin(), L.h_mask.end());
+    }
+    p->n_mixrows = (int)roff.size();
+    if ((rc = upload(&p->d_mixrow_off, roff))) return rc;
+    if ((rc = upload(&p->d_mixrow_len, rlen))) return rc;
+    if ((rc = upload(&p->d_mix_mask_all, mall))) return rc;
+  }
+  for (int i = 0; i < d->n_layers; ++i) {
+    const einet_layer_desc &ld = d->layers[i];
+    LayerPlan &L = p->layers[i];
+    if ((rc = upload(&L.d_out_slab, L.h_out_slab))) return rc;
+    if (ld.kind == EINET_LAYER_EINSUM) {
+      std::vector<int> ls(ld.left, ld.left + ld.rows), rs(ld.right, ld.right + ld.rows);
+      if ((rc = upload(&L.d_left_slab, ls))) return rc;
+      if ((rc = upload(&L.d_right_slab, rs))) return rc;
+      if ((rc = upload(&L.d_slot_left, slot_left[i]))) return rc;
+      if ((rc = upload(&L.d_slot_right, slot_right[i]))) return rc;
+    } else {
+      if ((rc = upload(&L.d_mix_src_slab, mix_src_slab[i]))) return rc;
+      if ((rc = upload(&L.d_mix_slot, mix_slot[i]))) return rc;
+      if ((rc = upload(&L.d_mix_mask, L.h_mask))) return rc;
+    }
+  }
+  return EINET_OK;
+}
+
+}  // namespace einet
+
+using namespace einet;
+
+struct einet_plan {
+  Plan impl;
+};
+
+extern "C" {
+
+int einet_plan_create(const einet_plan_desc *desc, int64_t max_chunk, einet_plan **out) {
+  if (!out) return fail(EINET_ERR_USAGE, "null output pointer");
+  *out = nullptr;
+  einet_plan *h = new einet_plan();
+  int rc = build_plan(desc, max_chunk, &h->impl);
+  if (rc) {
+    free_plan_memory(&h->impl);
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return EINET_OK;
+}
+
+void einet_plan_destroy(einet_plan *plan) {
+  if (!plan) return;
+  free_plan_memory(&plan->impl);
+  delete plan;
+}
+
+int einet_plan_sizes(const einet_plan *plan, einet_sizes *out) {
+  if (!plan || !out) return fail(EINET_ERR_USAGE, "null argument");
+  *out = plan->impl.sizes;
+  return EINET_OK;
+}
+
+int einet_prepare(einet_plan *plan, const double *params, void *compute,
+                  const uint8_t *marg_mask, const double *leaf_log_offset, void *stream) {
+  if (!plan || !params || !compute) return fail(EINET_ERR_USAGE, "null argument");
+  return launch_prepare(plan->impl, params, (uint8_t *)compute, marg_mask, leaf_log_offset,
+                        (cudaStream_t)stream);
+}
+
+int einet_forward(einet_plan *plan, const void *compute, const float *x, int64_t batch,
+                  void *workspace, double *root_out, int32_t *status, void *stream) {
+  if (!plan || !compute || !x || !workspace || !root_out || !status)
+    return fail(EINET_ERR_USAGE, "null argument");
+  if (batch < 1 || batch > plan->impl.max_chunk)
+    return fail(EINET_ERR_USAGE, "batch must be in [1, max_chunk]");
+  return launch_forward(plan->impl, (const uint8_t *)compute, x, batch,
+                        (uint8_t *)workspace, root_out, status, (cudaStream_t)stream);
+}
+
+int einet_backward(einet_plan *plan, const double *params, const void *compute,
+                   const float *x, int64_t batch, void *workspace, double *stats,
+                   int32_t *status, void *stream) {
+  if (!plan || !params || !compute || !x || !workspace || !stats || !status)
+    return fail(EINET_ERR_USAGE, "null argument");
+  if (batch < 1 || batch > plan->impl.max_chunk)
+    return fail(EINET_ERR_USAGE, "batch must be in [1, max_chunk]");
+  return launch_backward(plan->impl, params, (const uint8_t *)compute, x, batch,
+                         (uint8_t *)workspace, stats, status, (cudaStream_t)stream);
+}
+
+int einet_status_reset(int32_t *status, void *stream) {
+  if (!status) return fail(EINET_ERR_USAGE, "null argument");
+  return launch_status_reset(status, (cudaStream_t)stream);
+}
+
+int einet_stats_zero(einet_plan *plan, double *stats, void *stream) {
+  if (!plan || !stats) return fail(EINET_ERR_USAGE, "null argument");
+  return check_cuda(cudaMemsetAsync(stats, 0, sizeof(double) * plan->impl.sizes.stats_f64,
+                                    (cudaStream_t)stream),
+                    "cudaMemsetAsync(stats)");
+}
+
+int einet_mstep(einet_plan *plan, double *params, void *compute, const double *stats,
+                double lam, double eps_w, const int32_t *status, void *stream) {
+  if (!plan || !params || !compute || !stats) return fail(EINET_ERR_USAGE, "null argument");
+  if (!(lam > 0.0 && lam <= 1.0)) return fail(EINET_ERR_USAGE, "lam must lie in (0, 1]");
+  return launch_mstep(plan->impl, params, (uint8_t *)compute, stats, lam, eps_w, status,
+                      (cudaStream_t)stream);
+}
+
+int einet_stats_expand_acc_p(einet_plan *plan, const double *stats, double *acc_p,
+                             void *stream) {
+  if (!plan || !stats || !acc_p) return fail(EINET_ERR_USAGE, "null argument");
+  return launch_expand_acc_p(plan->impl, stats, acc_p, (cudaStream_t)stream);
+}
+
+int einet_export_buffer(einet_plan *plan, const void *workspace, int64_t batch, double *out,
+                        void *stream) {
+  if (!plan || !workspace || !out) return fail(EINET_ERR_USAGE, "null argument");
+  if (batch < 1 || batch > plan->impl.max_chunk)
+    return fail(EINET_ERR_USAGE, "batch must be in [1, max_chunk]");
+  return launch_export_buffer(plan->impl, (const uint8_t *)workspace, batch, out,
+                              (cudaStream_t)stream);
+}
+
+int einet_export_leaf_rows(einet_plan *plan, const void *workspace, int64_t batch,
+                           double *out, void *stream) {
+  if (!plan || !workspace || !out) return fail(EINET_ERR_USAGE, "null argument");
+  if (batch < 1 || batch > plan->impl.max_chunk)
+    return fail(EINET_ERR_USAGE, "batch must be in [1, max_chunk]");
+  return launch_export_leaf_rows(plan->impl, (const uint8_t *)workspace, batch, out,
+                                 (cudaStream_t)stream);
+}
+
+int einet_ef_log_prob(einet_plan *plan, const double *params, const float *x, int64_t batch,
+                      const uint8_t *marg_mask, double *out, int32_t *status, void *stream) {
+  if (!plan || !params || !x || !out || !status) return fail(EINET_ERR_USAGE, "null argument");
+  if (batch < 1) return fail(EINET_ERR_USAGE, "batch must be >= 1");
+  return launch_ef_log_prob(plan->impl, params, x, batch, marg_mask, out, status,
+                            (cudaStream_t)stream);
+}
+
+int einet_log_einsum_exp(const double *left, const double *right, const double *w,
+                         int64_t batch, int32_t rows, int32_t k, int32_t k_out, double *out,
+                         void *stream) {
+  if (!left || !right || !w || !out) return fail(EINET_ERR_USAGE, "null argument");
+  if (batch < 1 || rows < 1 || k < 1 || k_out < 1)
+    return fail(EINET_ERR_USAGE, "sizes must be >= 1");
+  return launch_log_einsum_exp(left, right, w, batch, rows, k, k_out, out,
+                               (cudaStream_t)stream);
+}
+
+int64_t einet_launch_count(void) { return (int64_t)g_launches.load(); }
+
+const char *einet_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

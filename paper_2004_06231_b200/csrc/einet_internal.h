@@ -1,0 +1,124 @@
+// Internal declarations of the B200 Einsum-Network engine.
+//
+// Data layout in HBM (per chunk of Bc samples):
+//   slab  s : one log-density vector per sample, value[b,k] = shift[s][b] (fp64)
+//             + off[s][b][k] (fp32). Slabs 0..R-1 are the reference buffer rows
+//             (compiler.py:54-99); root einsum rows and the root mixing output
+//             get extra slabs so every layer writes a slab.
+//   slot  q : one child-responsibility contribution [b][k] (fp32); the
+//             responsibility of slab s is the ordered sum over csr(s) -- a
+//             deterministic replacement for np.add.at (engine.py:315-316).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/einet_b200.h"
+
+namespace einet {
+
+constexpr int kMaxDSplit = 16;     // leaf forward split of a scope across CTAs
+constexpr int kMaxBSplit = 64;     // batch split of statistic reductions
+constexpr int kReduceThreads = 256;
+
+struct LayerPlan {
+  int kind = 0;        // EINET_LAYER_*
+  int index = 0;       // position in circuit.layers (leaf = 0)
+  int rows = 0;        // L or M
+  int k_out = 0;
+  int is_root = 0;
+  int dmax = 0;
+  // einsum
+  int *d_left_slab = nullptr, *d_right_slab = nullptr, *d_out_slab = nullptr;
+  int *d_slot_left = nullptr, *d_slot_right = nullptr;  // slot ids per row
+  int64_t w_off = 0;   // element offset of this layer's W (L,Ko,K,K)
+  // mixing
+  int *d_mix_src_slab = nullptr;   // (M*dmax), -1 if masked
+  int *d_mix_slot = nullptr;       // (M*dmax), -1 if masked
+  uint8_t *d_mix_mask = nullptr;
+  int64_t mix_off = 0; // element offset of (M,Dmax) weights in the mixing block
+  std::vector<int> h_out_slab;
+  std::vector<int> h_src;          // mixing local src
+  std::vector<uint8_t> h_mask;
+};
+
+struct Plan {
+  // descriptor copy
+  int d_vars = 0, k = 0, k_root = 0, ks = 0, num_replicas = 0, nbr = 0;
+  int family = 0, num_states = 0, n_trials = 0, suff = 0;
+  double var_min = 0, var_max = 0, p_min = 0;
+  int n_leaf = 0;
+  int max_scope = 0;
+  std::vector<int> h_scope_off, h_scope_vars, h_leaf_rep, h_leaf_slab;
+  int *d_scope_off = nullptr, *d_scope_vars = nullptr, *d_leaf_rep = nullptr,
+      *d_leaf_slab = nullptr;
+  int *d_leaf_of = nullptr;        // (R, D): leaf index covering (d, r) or -1
+  std::vector<LayerPlan> layers;   // einsum / mixing layers in circuit order
+  int root_mix_row = -1;
+  // slabs & slots
+  int num_slabs = 0, num_slots = 0;
+  int root_out_slab = -1;          // slab holding the root vector
+  std::vector<int> h_csr_off, h_csr_slot;   // per slab
+  int *d_csr_off = nullptr, *d_csr_slot = nullptr;
+  std::vector<uint8_t> h_slab_ones;         // slab whose responsibility is 1 (root)
+  uint8_t *d_slab_ones = nullptr;
+  // parameter / stats / compute layout
+  int64_t n_w = 0, n_mix = 0, n_phi = 0;
+  int64_t max_layer_w = 0, max_rows = 0, n_mix_entries = 0;
+  einet_sizes sizes{};
+  // compute segments (byte offsets)
+  int64_t c_w32 = 0, c_mix32 = 0, c_leafp = 0, c_center = 0, c_const = 0, c_active = 0,
+          c_logh = 0;
+  // workspace segments (byte offsets)
+  int64_t w_off = 0, w_shift = 0, w_slots = 0, w_leafpart = 0, w_ea = 0, w_eb = 0,
+          w_rt = 0, w_wpart = 0, w_rho = 0, w_lspart = 0, w_ppart = 0, w_mixpart = 0,
+          w_llpart = 0, w_scratch_end = 0;
+  int64_t max_chunk = 0;
+  int num_sms = 148;
+  int max_lsplit = 1;              // leaf-statistics batch split allocated
+  // mixing rows flattened over layers for the M-step
+  int n_mixrows = 0;
+  int *d_mixrow_off = nullptr, *d_mixrow_len = nullptr;
+  uint8_t *d_mix_mask_all = nullptr;
+};
+
+// ---- error handling ---------------------------------------------------------
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int check_cuda(cudaError_t err, const char *what);
+void count_launch(int n = 1);
+
+// ---- launchers (implemented in the .cu files) -------------------------------
+int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_t *mask,
+                   const double *leaf_offset, cudaStream_t st);
+int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
+                   uint8_t *ws, double *root_out, int32_t *status, cudaStream_t st);
+int launch_backward(Plan &p, const double *params, const uint8_t *compute, const float *x,
+                    int64_t B, uint8_t *ws, double *stats, int32_t *status,
+                    cudaStream_t st);
+int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
+                 double lam, double eps_w, const int32_t *status, cudaStream_t st);
+int launch_expand_acc_p(Plan &p, const double *stats, double *acc_p, cudaStream_t st);
+int launch_export_buffer(Plan &p, const uint8_t *ws, int64_t B, double *out,
+                         cudaStream_t st);
+int launch_export_leaf_rows(Plan &p, const uint8_t *ws, int64_t B, double *out,
+                            cudaStream_t st);
+int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
+                       const uint8_t *mask, double *out, int32_t *status,
+                       cudaStream_t st);
+int launch_status_reset(int32_t *status, cudaStream_t st);
+int leaf_lsplit(const Plan &p, int64_t B);
+int launch_log_einsum_exp(const double *left, const double *right, const double *w,
+                          int64_t B, int L, int K, int Ko, double *out, cudaStream_t st);
+
+// deterministic reduction: dst[i] += (scale ? scale[i] : 1) * sum_p part[p*stride+i]
+void launch_reduce_partials(double *dst, const double *part, int nparts, int64_t n,
+                            int64_t stride, const double *scale, cudaStream_t st);
+
+inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace einet

@@ -1,0 +1,628 @@
+// EinsumLayer / EinsumMixingLayer kernels (CUDA-core path) and the
+// forward / backward orchestration.
+//
+// Forward  (engine.py:91-122, 143-195): out[b,l,k] = a + c + log sum_ij
+//   W[l,k,i,j] e^(N[b,l,i]-a) e^(N'[b,l,j]-c). Slabs carry (shift fp64, offsets
+//   fp32): a, c are the fp32 maxima of the child offsets, the new shift is
+//   s_left + s_right + a + c and the new offsets are log r (small magnitude).
+// Backward (engine.py:247-316): rho_t = rho / r; W statistics
+//   n[l,k,i,j] += W sum_b rho_t ea_i eb_j; child responsibilities
+//   left_i = ea_i sum_k rho_t_k sum_j W_kij eb_j, right_j likewise, written to
+//   per-row slots and gathered by the consumers in a fixed order.
+#include <climits>
+#include <cmath>
+
+#include "kern_common.cuh"
+
+namespace einet {
+
+int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
+                        uint8_t *wsb, int32_t *status, cudaStream_t st);
+int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
+                         uint8_t *wsb, double *stats, cudaStream_t st);
+int launch_einsum_tc_forward(Plan &p, const LayerPlan &L, const float *w32, WsView &w,
+                             int64_t B, int32_t *status, cudaStream_t st, bool *handled);
+
+constexpr int EF_TB = 128;  // samples per CTA, one per thread
+constexpr int EF_KC = 8;    // output entries (k) staged per W chunk
+
+// Load one child slab as normalised exponentials e_i = exp(off_i - max off).
+template <int KT>
+__device__ __forceinline__ void load_exp(const WsView &ws, int slab, int64_t b, int K,
+                                         float (&e)[KT], double &s, float &mx, bool &dead,
+                                         bool &nan) {
+  const float *o = slab_off(ws, slab, b);
+  s = slab_shift(ws, slab)[b];
+  mx = -CUDART_INF_F;
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    const float v = i < K ? o[i] : -CUDART_INF_F;
+    e[i] = v;
+    nan |= v != v;
+    mx = fmaxf(mx, v);
+  }
+  nan |= s != s;
+  dead = (s == -CUDART_INF) || (mx == -CUDART_INF_F);
+#pragma unroll
+  for (int i = 0; i < KT; ++i) e[i] = dead ? 0.f : expf(e[i] - mx);
+}
+
+template <int KT>
+__device__ __forceinline__ float dot_row(const float *w, const float (&v)[KT]) {
+  const float4 *w4 = (const float4 *)w;
+  float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < KT / 4; ++j) {
+    const float4 q = w4[j];
+    t0 = fmaf(q.x, v[4 * j], t0);
+    t1 = fmaf(q.y, v[4 * j + 1], t1);
+    t0 = fmaf(q.z, v[4 * j + 2], t0);
+    t1 = fmaf(q.w, v[4 * j + 3], t1);
+  }
+  return t0 + t1;
+}
+
+// Stage W[l][k0:k0+nk][i][0:K] into smem as [kk][i][KT] (zero padded).
+__device__ __forceinline__ void stage_w(float *wsm, const float *__restrict__ Wl, int k0, int nk,
+                                        int K, int KT) {
+  const int n = nk * K * KT;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const int j = e % KT;
+    const int i = (e / KT) % K;
+    const int kk = e / (KT * K);
+    wsm[e] = j < K ? Wl[((int64_t)(k0 + kk) * K + i) * K + j] : 0.f;
+  }
+}
+
+// grid (ceil(B/128), L, ceil(Ko/8)), block 128 (one sample per thread)
+template <int KT>
+__global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const int *__restrict__ left_slab,
+                                                      const int *__restrict__ right_slab,
+                                                      const int *__restrict__ out_slab,
+                                                      const float *__restrict__ W, int64_t B,
+                                                      int K, int Ko, int layer_index,
+                                                      int32_t *status) {
+  extern __shared__ __align__(16) float wsm[];
+  const int l = blockIdx.y;
+  const int k0 = blockIdx.z * EF_KC;
+  const int nk = min(EF_KC, Ko - k0);
+  stage_w(wsm, W + (int64_t)l * Ko * K * K, k0, nk, K, KT);
+  const int64_t b = (int64_t)blockIdx.x * EF_TB + threadIdx.x;
+  const bool live = b < B;
+  float ea[KT], eb[KT];
+  double sl = 0.0, sr = 0.0;
+  float a = 0.f, c = 0.f;
+  bool dl = true, dr = true, nan = false;
+  if (live) {
+    load_exp<KT>(ws, left_slab[l], b, K, ea, sl, a, dl, nan);
+    load_exp<KT>(ws, right_slab[l], b, K, eb, sr, c, dr, nan);
+    if (nan) atomicMin(&status[1], layer_index);
+  }
+  __syncthreads();
+  if (!live) return;
+  const bool dead = dl || dr;
+  float *o = slab_off(ws, out_slab[l], b);
+  for (int kk = 0; kk < nk; ++kk) {
+    const float *wk = wsm + kk * K * KT;
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < KT; ++i)
+      if (i < K) acc = fmaf(ea[i], dot_row<KT>(wk + i * KT, eb), acc);
+    o[k0 + kk] = (dead || !(acc > 0.f)) ? -CUDART_INF_F : logf(acc);
+  }
+  if (blockIdx.z == 0)
+    slab_shift(ws, out_slab[l])[b] =
+        dead ? -CUDART_INF : sl + sr + (double)a + (double)c;
+}
+
+// Generic (any K) forward: W read through L1, operands recomputed per term.
+__global__ void k_einsum_fwd_generic(WsView ws, const int *left_slab, const int *right_slab,
+                                     const int *out_slab, const float *__restrict__ W,
+                                     int64_t B, int K, int Ko, int layer_index,
+                                     int32_t *status) {
+  const int l = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const float *ol = slab_off(ws, left_slab[l], b), *orr = slab_off(ws, right_slab[l], b);
+  const double sl = slab_shift(ws, left_slab[l])[b], sr = slab_shift(ws, right_slab[l])[b];
+  float a = -CUDART_INF_F, c = -CUDART_INF_F;
+  bool nan = sl != sl || sr != sr;
+  for (int i = 0; i < K; ++i) {
+    a = fmaxf(a, ol[i]);
+    c = fmaxf(c, orr[i]);
+    nan |= ol[i] != ol[i] || orr[i] != orr[i];
+  }
+  if (nan) atomicMin(&status[1], layer_index);
+  const bool dead = sl == -CUDART_INF || sr == -CUDART_INF || a == -CUDART_INF_F ||
+                    c == -CUDART_INF_F;
+  float *o = slab_off(ws, out_slab[l], b);
+  const float *Wl = W + (int64_t)l * Ko * K * K;
+  for (int k = 0; k < Ko; ++k) {
+    float acc = 0.f;
+    for (int i = 0; i < K && !dead; ++i) {
+      const float ei = expf(ol[i] - a);
+      float t = 0.f;
+      for (int j = 0; j < K; ++j) t = fmaf(Wl[((int64_t)k * K + i) * K + j], expf(orr[j] - c), t);
+      acc = fmaf(ei, t, acc);
+    }
+    o[k] = (dead || !(acc > 0.f)) ? -CUDART_INF_F : logf(acc);
+  }
+  slab_shift(ws, out_slab[l])[b] = dead ? -CUDART_INF : sl + sr + (double)a + (double)c;
+}
+
+// ---------------------------------------------------------------------------
+// mixing layers (engine.py:112-122, 268-293)
+// ---------------------------------------------------------------------------
+
+// grid (ceil(B/128), M), block 128
+__global__ void k_mixing_fwd(WsView ws, const int *__restrict__ src_slab,
+                             const uint8_t *__restrict__ mask, const int *__restrict__ out_slab,
+                             const float *__restrict__ w, int64_t B, int Ko, int dmax,
+                             int layer_index, int32_t *status) {
+  const int m = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double s = -CUDART_INF;
+  for (int c = 0; c < dmax; ++c) {
+    if (!mask[m * dmax + c]) continue;
+    const double sc = slab_shift(ws, src_slab[m * dmax + c])[b];
+    if (sc > s || sc != sc) s = sc;
+  }
+  const int os = out_slab[m];
+  float *o = slab_off(ws, os, b);
+  if (s == -CUDART_INF) {
+    slab_shift(ws, os)[b] = -CUDART_INF;
+    for (int k = 0; k < Ko; ++k) o[k] = 0.f;
+    return;
+  }
+  for (int k = 0; k < Ko; ++k) {
+    float mk = -CUDART_INF_F;
+    for (int c = 0; c < dmax; ++c) {
+      if (!mask[m * dmax + c]) continue;
+      const int sl = src_slab[m * dmax + c];
+      const double sc = slab_shift(ws, sl)[b];
+      if (sc == -CUDART_INF) continue;
+      mk = fmaxf(mk, (float)(sc - s) + slab_off(ws, sl, b)[k]);
+    }
+    float out = -CUDART_INF_F;
+    if (mk != -CUDART_INF_F) {
+      float sum = 0.f;
+      for (int c = 0; c < dmax; ++c) {
+        if (!mask[m * dmax + c]) continue;
+        const int sl = src_slab[m * dmax + c];
+        const double sc = slab_shift(ws, sl)[b];
+        if (sc == -CUDART_INF) continue;
+        const float dv = (float)(sc - s) + slab_off(ws, sl, b)[k];
+        sum = fmaf(w[m * dmax + c], expf(dv - mk), sum);
+      }
+      if (sum > 0.f) out = mk + logf(sum);
+    }
+    o[k] = out;
+  }
+  slab_shift(ws, os)[b] = s;
+}
+
+// grid (ceil(B/64), M), block 64; per-CTA partials of the mixing statistics
+__global__ void k_mixing_bwd(WsView ws, const int *__restrict__ src_slab,
+                             const uint8_t *__restrict__ mask, const int *__restrict__ out_slab,
+                             const int *__restrict__ mix_slot, const float *__restrict__ w,
+                             const int *csr_off, const int *csr_slot, const uint8_t *ones,
+                             int64_t B, int Ko, int dmax, double *mixpart, int64_t mix_off,
+                             int64_t n_mix) {
+  __shared__ double red[2];
+  const int m = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = b < B;
+  const int os = out_slab[m];
+  const double so = live ? slab_shift(ws, os)[b] : 0.0;
+  for (int c = 0; c < dmax; ++c) {
+    double part = 0.0;
+    if (live && mask[m * dmax + c]) {
+      const int sl = src_slab[m * dmax + c];
+      const double sc = slab_shift(ws, sl)[b];
+      const bool ok = so != -CUDART_INF && sc != -CUDART_INF;
+      const float delta = ok ? (float)(sc - so) : 0.f;
+      const float wc = w[m * dmax + c];
+      float *dst = slot_ptr(ws, mix_slot[m * dmax + c], b);
+      const float *oc = slab_off(ws, sl, b), *oo = slab_off(ws, os, b);
+      float run = 0.f;
+      for (int k = 0; k < Ko; ++k) {
+        const float dk = delta + oc[k] - oo[k];
+        const float ratio = (ok && isfinite(dk)) ? expf(dk) : 0.f;
+        const float contrib = gather_rho(ws, csr_off, csr_slot, ones, os, b, k) * wc * ratio;
+        dst[k] = contrib;
+        run += contrib;
+      }
+      part = (double)run;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      mixpart[(int64_t)blockIdx.x * n_mix + mix_off + (int64_t)m * dmax + c] = red[0] + red[1];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// einsum backward
+// ---------------------------------------------------------------------------
+
+// EA/EB (normalised child exponentials) and RT = rho / r per row and sample.
+// grid (ceil(B/128), L), block 128
+__global__ void k_einsum_bwd_prep(WsView ws, const int *left_slab, const int *right_slab,
+                                  const int *out_slab, const int *csr_off, const int *csr_slot,
+                                  const uint8_t *ones, int64_t B, int K, int Ko, float *EA,
+                                  float *EB, float *RT) {
+  const int l = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int64_t row = (int64_t)l * ws.bc + b;
+  for (int side = 0; side < 2; ++side) {
+    const int slab = side ? right_slab[l] : left_slab[l];
+    const float *o = slab_off(ws, slab, b);
+    const double s = slab_shift(ws, slab)[b];
+    float mx = -CUDART_INF_F;
+    for (int i = 0; i < K; ++i) mx = fmaxf(mx, o[i]);
+    const bool dead = s == -CUDART_INF || mx == -CUDART_INF_F;
+    float *dst = (side ? EB : EA) + row * K;
+    for (int i = 0; i < K; ++i) dst[i] = dead ? 0.f : expf(o[i] - mx);
+  }
+  const int os = out_slab[l];
+  const double so = slab_shift(ws, os)[b];
+  const float *oo = slab_off(ws, os, b);
+  float *rt = RT + row * ws.ks;
+  for (int k = 0; k < Ko; ++k) {
+    const float r = so == -CUDART_INF ? 0.f : expf(oo[k]);
+    const float rho = gather_rho(ws, csr_off, csr_slot, ones, os, b, k);
+    rt[k] = r > 0.f ? rho / r : 0.f;
+  }
+}
+
+constexpr int WS_BT = 32;  // samples per fp32 run of the W statistics
+
+// sum_b RT[b,k] EA[b,i] EB[b,j] for one (l, k) per CTA and a batch split.
+// Register tile 4x4 of (i, j) per thread; block K4*K4 threads.
+__global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__restrict__ EB,
+                                const float *__restrict__ RT, int64_t Bc, int ks, int64_t B,
+                                int K, int Ko, int L, int bsplit, double *wpart) {
+  extern __shared__ __align__(16) float sm[];
+  const int K4 = (K + 3) / 4;
+  const int KP = K4 * 4;
+  float *ea_s = sm;                     // [WS_BT][KP]
+  float *eb_s = ea_s + WS_BT * KP;      // [WS_BT][KP]
+  float *rt_s = eb_s + WS_BT * KP;      // [WS_BT]
+  const int g = blockIdx.x;
+  const int l = g / Ko, k = g % Ko;
+  const int split = blockIdx.y;
+  const int ti = threadIdx.x / K4, tj = threadIdx.x % K4;
+  const int64_t per = (B + bsplit - 1) / bsplit;
+  const int64_t bb = split * per, be = min(B, bb + per);
+  float acc[4][4];
+  double tot[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      acc[u][v] = 0.f;
+      tot[u][v] = 0.0;
+    }
+  for (int64_t t = bb; t < be; t += WS_BT) {
+    const int nb = (int)min((int64_t)WS_BT, be - t);
+    __syncthreads();
+    for (int e = threadIdx.x; e < WS_BT * KP; e += blockDim.x) {
+      const int bl = e / KP, i = e % KP;
+      const bool ok = bl < nb && i < K;
+      const int64_t row = (int64_t)l * Bc + t + bl;
+      ea_s[e] = ok ? EA[row * K + i] : 0.f;
+      eb_s[e] = ok ? EB[row * K + i] : 0.f;
+    }
+    for (int e = threadIdx.x; e < WS_BT; e += blockDim.x)
+      rt_s[e] = e < nb ? RT[((int64_t)l * Bc + t + e) * ks + k] : 0.f;
+    __syncthreads();
+    for (int bl = 0; bl < nb; ++bl) {
+      const float r = rt_s[bl];
+      const float4 a4 = *(const float4 *)(ea_s + bl * KP + 4 * ti);
+      const float4 e4 = *(const float4 *)(eb_s + bl * KP + 4 * tj);
+      const float au[4] = {r * a4.x, r * a4.y, r * a4.z, r * a4.w};
+      const float ev[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(au[u], ev[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        tot[u][v] += (double)acc[u][v];
+        acc[u][v] = 0.f;
+      }
+  }
+  double *dst = wpart + (((int64_t)split * L + l) * Ko + k) * K * K;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = 4 * ti + u, j = 4 * tj + v;
+      if (i < K && j < K) dst[i * K + j] = tot[u][v];
+    }
+}
+
+// Child responsibilities, one sample per thread; W staged per k-chunk.
+template <int KT>
+__global__ void __launch_bounds__(EF_TB) k_einsum_childrho(
+    const float *__restrict__ EA, const float *__restrict__ EB, const float *__restrict__ RT,
+    const float *__restrict__ W, WsView ws, const int *slot_left, const int *slot_right,
+    int64_t B, int K, int Ko) {
+  extern __shared__ __align__(16) float wsm[];
+  const int l = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * EF_TB + threadIdx.x;
+  const bool live = b < B;
+  const int64_t row = (int64_t)l * ws.bc + (live ? b : 0);
+  float ea[KT], eb[KT], left[KT], right[KT];
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    ea[i] = (live && i < K) ? EA[row * K + i] : 0.f;
+    eb[i] = (live && i < K) ? EB[row * K + i] : 0.f;
+    left[i] = 0.f;
+    right[i] = 0.f;
+  }
+  const float *Wl = W + (int64_t)l * Ko * K * K;
+  for (int k0 = 0; k0 < Ko; k0 += EF_KC) {
+    const int nk = min(EF_KC, Ko - k0);
+    __syncthreads();
+    stage_w(wsm, Wl, k0, nk, K, KT);
+    __syncthreads();
+    if (!live) continue;
+    for (int kk = 0; kk < nk; ++kk) {
+      const float rt = RT[row * ws.ks + k0 + kk];
+      if (rt == 0.f) continue;
+      const float *wk = wsm + kk * K * KT;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        if (i >= K) break;
+        const float *wr = wk + i * KT;
+        left[i] = fmaf(rt, dot_row<KT>(wr, eb), left[i]);
+        const float ci = rt * ea[i];
+        const float4 *w4 = (const float4 *)wr;
+#pragma unroll
+        for (int j = 0; j < KT / 4; ++j) {
+          const float4 q = w4[j];
+          right[4 * j] = fmaf(ci, q.x, right[4 * j]);
+          right[4 * j + 1] = fmaf(ci, q.y, right[4 * j + 1]);
+          right[4 * j + 2] = fmaf(ci, q.z, right[4 * j + 2]);
+          right[4 * j + 3] = fmaf(ci, q.w, right[4 * j + 3]);
+        }
+      }
+    }
+  }
+  if (!live) return;
+  float *dl = slot_ptr(ws, slot_left[l], b), *dr = slot_ptr(ws, slot_right[l], b);
+#pragma unroll
+  for (int i = 0; i < KT; ++i)
+    if (i < K) {
+      dl[i] = ea[i] * left[i];
+      dr[i] = eb[i] * right[i];
+    }
+}
+
+__global__ void k_einsum_childrho_generic(const float *__restrict__ EA,
+                                          const float *__restrict__ EB,
+                                          const float *__restrict__ RT,
+                                          const float *__restrict__ W, WsView ws,
+                                          const int *slot_left, const int *slot_right,
+                                          int64_t B, int K, int Ko) {
+  const int l = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int64_t row = (int64_t)l * ws.bc + b;
+  const float *ea = EA + row * K, *eb = EB + row * K, *rt = RT + row * ws.ks;
+  const float *Wl = W + (int64_t)l * Ko * K * K;
+  float *dl = slot_ptr(ws, slot_left[l], b), *dr = slot_ptr(ws, slot_right[l], b);
+  for (int i = 0; i < K; ++i) {
+    float acc = 0.f;
+    for (int k = 0; k < Ko; ++k) {
+      float t = 0.f;
+      for (int j = 0; j < K; ++j) t = fmaf(Wl[((int64_t)k * K + i) * K + j], eb[j], t);
+      acc = fmaf(rt[k], t, acc);
+    }
+    dl[i] = ea[i] * acc;
+  }
+  for (int j = 0; j < K; ++j) {
+    float acc = 0.f;
+    for (int k = 0; k < Ko; ++k) {
+      float t = 0.f;
+      for (int i = 0; i < K; ++i) t = fmaf(Wl[((int64_t)k * K + i) * K + j], ea[i], t);
+      acc = fmaf(rt[k], t, acc);
+    }
+    dr[j] = eb[j] * acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// root outputs and the log-likelihood sum
+// ---------------------------------------------------------------------------
+
+__global__ void k_root_out(WsView ws, int slab, int64_t B, int kr, double *out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= B * kr) return;
+  const int64_t b = e / kr;
+  const int k = (int)(e % kr);
+  const double s = slab_shift(ws, slab)[b];
+  out[e] = s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[k];
+}
+
+__global__ void k_ll_partial(WsView ws, int slab, int64_t B, double *part) {
+  __shared__ double red[8];
+  const int64_t b = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  double v = 0.0;
+  if (b < B) {
+    const double s = slab_shift(ws, slab)[b];
+    v = s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[0];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_ll_finish(const double *part, int n, double *ll, double count) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += part[i];
+  ll[0] += s;
+  ll[1] += count;
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+
+template <int KT>
+static void fwd_simt(const LayerPlan &L, const float *w32, WsView &w, int64_t B, int K,
+                     int32_t *status, cudaStream_t st) {
+  const size_t smem = sizeof(float) * EF_KC * K * KT;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_einsum_fwd<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  dim3 grid(ceil_div(B, EF_TB), L.rows, ceil_div(L.k_out, EF_KC));
+  k_einsum_fwd<KT><<<grid, EF_TB, smem, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
+                                              w32 + L.w_off, B, K, L.k_out, L.index, status);
+}
+
+template <int KT>
+static void childrho_simt(const LayerPlan &L, const float *w32, WsView &w, int64_t B, int K,
+                          cudaStream_t st) {
+  const size_t smem = sizeof(float) * EF_KC * K * KT;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_einsum_childrho<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  dim3 grid(ceil_div(B, EF_TB), L.rows);
+  k_einsum_childrho<KT><<<grid, EF_TB, smem, st>>>(w.ea, w.eb, w.rt, w32 + L.w_off, w,
+                                                   L.d_slot_left, L.d_slot_right, B, K,
+                                                   L.k_out);
+}
+
+static void einsum_forward_simt(const LayerPlan &L, const float *w32, WsView &w, int64_t B,
+                                int K, int32_t *status, cudaStream_t st) {
+  if (K <= 4) fwd_simt<4>(L, w32, w, B, K, status, st);
+  else if (K <= 8) fwd_simt<8>(L, w32, w, B, K, status, st);
+  else if (K <= 12) fwd_simt<12>(L, w32, w, B, K, status, st);
+  else if (K <= 16) fwd_simt<16>(L, w32, w, B, K, status, st);
+  else if (K <= 24) fwd_simt<24>(L, w32, w, B, K, status, st);
+  else if (K <= 32) fwd_simt<32>(L, w32, w, B, K, status, st);
+  else if (K <= 40) fwd_simt<40>(L, w32, w, B, K, status, st);
+  else if (K <= 48) fwd_simt<48>(L, w32, w, B, K, status, st);
+  else if (K <= 64) fwd_simt<64>(L, w32, w, B, K, status, st);
+  else {
+    dim3 grid(ceil_div(B, 128), L.rows);
+    k_einsum_fwd_generic<<<grid, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
+                                               w32 + L.w_off, B, K, L.k_out, L.index, status);
+  }
+}
+
+static void einsum_childrho(const LayerPlan &L, const float *w32, WsView &w, int64_t B, int K,
+                            cudaStream_t st) {
+  if (K <= 4) childrho_simt<4>(L, w32, w, B, K, st);
+  else if (K <= 8) childrho_simt<8>(L, w32, w, B, K, st);
+  else if (K <= 12) childrho_simt<12>(L, w32, w, B, K, st);
+  else if (K <= 16) childrho_simt<16>(L, w32, w, B, K, st);
+  else if (K <= 24) childrho_simt<24>(L, w32, w, B, K, st);
+  else if (K <= 32) childrho_simt<32>(L, w32, w, B, K, st);
+  else if (K <= 40) childrho_simt<40>(L, w32, w, B, K, st);
+  else if (K <= 48) childrho_simt<48>(L, w32, w, B, K, st);
+  else {
+    dim3 grid(ceil_div(B, 128), L.rows);
+    k_einsum_childrho_generic<<<grid, 128, 0, st>>>(w.ea, w.eb, w.rt, w32 + L.w_off, w,
+                                                    L.d_slot_left, L.d_slot_right, B, K,
+                                                    L.k_out);
+  }
+}
+
+int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, uint8_t *wsb,
+                   double *root_out, int32_t *status, cudaStream_t st) {
+  CompView c = comp_view(p, compute);
+  WsView w = ws_view(p, wsb);
+  int rc = launch_leaf_forward(p, compute, x, B, wsb, status, st);
+  if (rc) return rc;
+  for (const LayerPlan &L : p.layers) {
+    if (L.kind == EINET_LAYER_EINSUM) {
+      bool handled = false;
+      rc = launch_einsum_tc_forward(p, L, c.w32, w, B, status, st, &handled);
+      if (rc) return rc;
+      if (!handled) einsum_forward_simt(L, c.w32, w, B, p.k, status, st);
+    } else {
+      dim3 grid(ceil_div(B, 128), L.rows);
+      k_mixing_fwd<<<grid, 128, 0, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
+                                         c.mix32 + L.mix_off, B, L.k_out, L.dmax, L.index,
+                                         status);
+    }
+    count_launch();
+  }
+  const int64_t n = B * p.k_root;
+  k_root_out<<<ceil_div(n, 256), 256, 0, st>>>(w, p.root_out_slab, B, p.k_root, root_out);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "forward kernels");
+}
+
+static int wstats_bsplit(const Plan &p, const LayerPlan &L, int64_t B) {
+  int64_t blocks = (int64_t)L.rows * L.k_out;
+  int64_t bs = std::max<int64_t>(1, (2 * p.num_sms + blocks - 1) / blocks);
+  return (int)std::min<int64_t>(bs, std::min<int64_t>(kMaxBSplit, (B + 63) / 64));
+}
+
+int launch_backward(Plan &p, const double *params, const uint8_t *compute, const float *x,
+                    int64_t B, uint8_t *wsb, double *stats, int32_t *status,
+                    cudaStream_t st) {
+  (void)status;
+  CompView c = comp_view(p, compute);
+  WsView w = ws_view(p, wsb);
+  const int K = p.k;
+  // log-likelihood sum of the batch (root entry 0) and the sample count
+  {
+    const int nb = ceil_div(B, 256);
+    k_ll_partial<<<nb, 256, 0, st>>>(w, p.root_out_slab, B, w.llpart);
+    k_ll_finish<<<1, 1, 0, st>>>(w.llpart, nb, stats + p.sizes.stats_ll_offset, (double)B);
+    count_launch(2);
+  }
+  for (int li = (int)p.layers.size() - 1; li >= 0; --li) {
+    const LayerPlan &L = p.layers[li];
+    if (L.kind == EINET_LAYER_MIXING) {
+      const int nb = ceil_div(B, 64);
+      dim3 grid(nb, L.rows);
+      k_mixing_bwd<<<grid, 64, 0, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
+                                        L.d_mix_slot, c.mix32 + L.mix_off, p.d_csr_off,
+                                        p.d_csr_slot, p.d_slab_ones, B, L.k_out, L.dmax,
+                                        w.mixpart, L.mix_off, p.n_mix);
+      launch_reduce_partials(stats + p.n_w + L.mix_off, w.mixpart + L.mix_off, nb,
+                             (int64_t)L.rows * L.dmax, p.n_mix, nullptr, st);
+      count_launch();
+      continue;
+    }
+    dim3 g1(ceil_div(B, 128), L.rows);
+    k_einsum_bwd_prep<<<g1, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
+                                          p.d_csr_off, p.d_csr_slot, p.d_slab_ones, B, K,
+                                          L.k_out, w.ea, w.eb, w.rt);
+    const int bs = wstats_bsplit(p, L, B);
+    const int K4 = (K + 3) / 4;
+    const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT);
+    dim3 g2(L.rows * L.k_out, bs);
+    k_einsum_wstats<<<g2, K4 * K4, smem, st>>>(w.ea, w.eb, w.rt, w.bc, w.ks, B, K, L.k_out,
+                                               L.rows, bs, w.wpart);
+    const int64_t lw = (int64_t)L.rows * L.k_out * K * K;
+    launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);
+    einsum_childrho(L, c.w32, w, B, K, st);
+    count_launch(3);
+  }
+  int rc = launch_leaf_backward(p, compute, x, B, wsb, stats, st);
+  if (rc) return rc;
+  return check_cuda(cudaGetLastError(), "backward kernels");
+}
+
+}  // namespace einet

@@ -1,0 +1,100 @@
+// Device-side views of the compute and workspace buffers plus shared helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "einet_internal.h"
+
+namespace einet {
+
+constexpr double kLog2Pi = 1.8378770664093453;  // log(2*pi)
+constexpr double kEpsCount = 1e-12;             // trainer.py:23
+
+struct CompView {
+  float *w32;
+  float *mix32;
+  void *leafp;     // gaussian/binomial: float2 [R][D][K]; categorical: float [R][D][K][S]
+  float *center;   // gaussian: fp32 mean [R][D][K] (centre of the leaf statistics)
+  double *cnst;    // [n_leaf][K] fp64 scope constant
+  uint8_t *active; // [D] 1 = not marginalised
+  double *logh;    // binomial log base measure per count
+};
+
+struct WsView {
+  float *off;      // [slab][Bc][KS]
+  double *shift;   // [slab][Bc]
+  float *slots;    // [slot][Bc][KS]
+  double *leafpart;
+  float *ea, *eb;  // [row][Bc][K]
+  float *rt;       // [row][Bc][KS]
+  double *wpart;
+  float *rho;      // [leaf][Bc][K]
+  double *lspart;
+  double *ppart;
+  double *mixpart;
+  double *llpart;
+  int64_t bc;
+  int ks;
+};
+
+inline CompView comp_view(const Plan &p, const uint8_t *c) {
+  CompView v;
+  uint8_t *b = const_cast<uint8_t *>(c);
+  v.w32 = (float *)(b + p.c_w32);
+  v.mix32 = (float *)(b + p.c_mix32);
+  v.leafp = (void *)(b + p.c_leafp);
+  v.center = (float *)(b + p.c_center);
+  v.cnst = (double *)(b + p.c_const);
+  v.active = (uint8_t *)(b + p.c_active);
+  v.logh = (double *)(b + p.c_logh);
+  return v;
+}
+
+inline WsView ws_view(const Plan &p, const uint8_t *w) {
+  WsView v;
+  uint8_t *b = const_cast<uint8_t *>(w);
+  v.off = (float *)(b + p.w_off);
+  v.shift = (double *)(b + p.w_shift);
+  v.slots = (float *)(b + p.w_slots);
+  v.leafpart = (double *)(b + p.w_leafpart);
+  v.ea = (float *)(b + p.w_ea);
+  v.eb = (float *)(b + p.w_eb);
+  v.rt = (float *)(b + p.w_rt);
+  v.wpart = (double *)(b + p.w_wpart);
+  v.rho = (float *)(b + p.w_rho);
+  v.lspart = (double *)(b + p.w_lspart);
+  v.ppart = (double *)(b + p.w_ppart);
+  v.mixpart = (double *)(b + p.w_mixpart);
+  v.llpart = (double *)(b + p.w_llpart);
+  v.bc = p.max_chunk;
+  v.ks = p.ks;
+  return v;
+}
+
+__device__ __forceinline__ float *slab_off(const WsView &w, int slab, int64_t b) {
+  return w.off + ((int64_t)slab * w.bc + b) * w.ks;
+}
+__device__ __forceinline__ double *slab_shift(const WsView &w, int slab) {
+  return w.shift + (int64_t)slab * w.bc;
+}
+__device__ __forceinline__ float *slot_ptr(const WsView &w, int slot, int64_t b) {
+  return w.slots + ((int64_t)slot * w.bc + b) * w.ks;
+}
+
+// Responsibility of slab `slab` for sample b, entry k: ordered sum of its
+// contribution slots (deterministic stand-in for np.add.at), or 1 at the root.
+__device__ __forceinline__ float gather_rho(const WsView &w, const int *csr_off,
+                                            const int *csr_slot, const uint8_t *ones,
+                                            int slab, int64_t b, int k) {
+  if (ones[slab]) return 1.0f;
+  float acc = 0.0f;
+  const int e = csr_off[slab + 1];
+  for (int q = csr_off[slab]; q < e; ++q) acc += slot_ptr(w, csr_slot[q], b)[k];
+  return acc;
+}
+
+__device__ __forceinline__ bool is_nan_f(float v) { return v != v; }
+
+}  // namespace einet

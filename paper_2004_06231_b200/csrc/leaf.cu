@@ -1,0 +1,703 @@
+// Exponential-family leaf kernels: parameter preparation, leaf-region forward,
+// leaf responsibilities and leaf sufficient statistics.
+//
+// Reference semantics: expfam.py:82-309 (log densities, projections),
+// engine.py:318-327 (leaf statistics). The per-variable tensor E of
+// ef_log_prob (expfam.py:288) is never materialised on the hot path: the
+// leaf-region rows are accumulated straight from x.
+//
+// Gaussian leaves use the direct form  -(x-mu)^2/(2 var) = -(x*sa + nmsa)^2
+// with sa = sqrt(1/(2 var)), nmsa = -mu*sa (two FFMA per (sample, var, k)),
+// plus a per-(leaf, k) constant sum_d -0.5(log 2pi + log var) kept in fp64.
+// fp32 partial sums over chunks of 32 variables are folded into fp64, so the
+// leaf row is accurate to ~1e-5 absolute even at |log p| ~ 1e4.
+#include <climits>
+#include <cmath>
+
+#include "kern_common.cuh"
+
+namespace einet {
+
+constexpr int LF_KPT = 8;    // k entries per thread
+constexpr int LF_NS = 4;     // samples per thread
+constexpr int LF_VC = 32;    // variables per shared-memory chunk
+constexpr int LF_TB = 32 * LF_NS;  // samples per CTA
+
+// ---------------------------------------------------------------------------
+// parameter preparation (master fp64 -> device compute tensors)
+// ---------------------------------------------------------------------------
+
+__global__ void k_to_f32(const double *__restrict__ src, float *__restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (float)src[i];
+}
+
+__global__ void k_prepare_active(const uint8_t *mask, uint8_t *active, int D) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < D) active[d] = mask ? (mask[d] ? 0 : 1) : 1;
+}
+
+// phi (D,K,R,2) = (mean, second moment) -> (sa, -mu*sa) and centre mu, [r][d][k]
+__global__ void k_prepare_gauss(const double *__restrict__ phi, const uint8_t *active,
+                                float2 *lp, float *center, int D, int K, int R) {
+  int64_t n = (int64_t)R * D * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int k = (int)(e % K);
+    int d = (int)((e / K) % D);
+    int r = (int)(e / ((int64_t)K * D));
+    const double *ph = phi + (((int64_t)d * K + k) * R + r) * 2;
+    double mu = ph[0];
+    double var = ph[1] - mu * mu;
+    double sa = sqrt(0.5 / var);
+    float2 v = make_float2(0.f, 0.f);
+    if (active[d]) v = make_float2((float)sa, (float)(-mu * sa));
+    lp[e] = v;
+    center[e] = (float)mu;
+  }
+}
+
+// categorical: log phi per state, [r][d][k][s]; masked variables -> 0
+__global__ void k_prepare_cat(const double *__restrict__ phi, const uint8_t *active, float *lp,
+                              int D, int K, int R, int S) {
+  int64_t n = (int64_t)R * D * K * S;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int s = (int)(e % S);
+    int64_t q = e / S;
+    int k = (int)(q % K);
+    int d = (int)((q / K) % D);
+    int r = (int)(q / ((int64_t)K * D));
+    double p = phi[(((int64_t)d * K + k) * R + r) * S + s];
+    lp[e] = active[d] ? (float)log(p) : 0.f;
+  }
+}
+
+// binomial: (theta, A) with log p(x) = log h(x) + x*theta + A
+__global__ void k_prepare_binom(const double *__restrict__ phi, const uint8_t *active,
+                                float2 *lp, int D, int K, int R, int n_trials) {
+  int64_t n = (int64_t)R * D * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int k = (int)(e % K);
+    int d = (int)((e / K) % D);
+    int r = (int)(e / ((int64_t)K * D));
+    double p = phi[((int64_t)d * K + k) * R + r] / (double)n_trials;
+    double l1 = log1p(-p);
+    float2 v = make_float2(0.f, 0.f);
+    if (active[d]) v = make_float2((float)(log(p) - l1), (float)(n_trials * l1));
+    lp[e] = v;
+  }
+}
+
+__global__ void k_prepare_logh(double *logh, int n) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x <= n) logh[x] = lgamma((double)n + 1.0) - lgamma((double)x + 1.0) -
+                        lgamma((double)(n - x) + 1.0);
+}
+
+// per (leaf, k): sum over the unmasked scope of the k-only terms, in fp64
+__global__ void k_prepare_const(const double *__restrict__ phi, const uint8_t *active,
+                                const double *leaf_offset, const int *scope_off,
+                                const int *scope_vars, const int *leaf_rep, double *cnst,
+                                int D, int K, int R, int family) {
+  const int leaf = blockIdx.x;
+  const int r = leaf_rep[leaf];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double acc = 0.0;
+    for (int q = scope_off[leaf]; q < scope_off[leaf + 1]; ++q) {
+      int d = scope_vars[q];
+      if (!active[d]) continue;
+      int64_t base = ((int64_t)d * K + k) * R + r;
+      if (family == EINET_FAMILY_GAUSSIAN) {
+        double mu = phi[base * 2], var = phi[base * 2 + 1] - mu * mu;
+        acc += -0.5 * (kLog2Pi + log(var));
+      }
+      if (leaf_offset) acc += leaf_offset[base];
+    }
+    cnst[leaf * K + k] = acc;
+  }
+}
+
+int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_t *mask,
+                   const double *leaf_offset, cudaStream_t st) {
+  CompView c = comp_view(p, compute);
+  const int D = p.d_vars, K = p.k, R = p.num_replicas;
+  const double *phi = params + p.sizes.phi_offset;
+  auto grid_for = [](int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 4096); };
+  if (p.n_w) k_to_f32<<<grid_for(p.n_w), 256, 0, st>>>(params, c.w32, p.n_w);
+  if (p.n_mix) k_to_f32<<<grid_for(p.n_mix), 256, 0, st>>>(params + p.n_w, c.mix32, p.n_mix);
+  k_prepare_active<<<ceil_div(D, 256), 256, 0, st>>>(mask, c.active, D);
+  const int64_t rdk = (int64_t)R * D * K;
+  if (p.family == EINET_FAMILY_GAUSSIAN) {
+    k_prepare_gauss<<<grid_for(rdk), 256, 0, st>>>(phi, c.active, (float2 *)c.leafp,
+                                                   c.center, D, K, R);
+  } else if (p.family == EINET_FAMILY_CATEGORICAL) {
+    k_prepare_cat<<<grid_for(rdk * p.num_states), 256, 0, st>>>(phi, c.active, (float *)c.leafp,
+                                                               D, K, R, p.num_states);
+  } else {
+    k_prepare_binom<<<grid_for(rdk), 256, 0, st>>>(phi, c.active, (float2 *)c.leafp, D, K, R,
+                                                   p.n_trials);
+    k_prepare_logh<<<ceil_div(p.n_trials + 1, 256), 256, 0, st>>>(c.logh, p.n_trials);
+    count_launch();
+  }
+  k_prepare_const<<<p.n_leaf, 64, 0, st>>>(phi, c.active, leaf_offset, p.d_scope_off,
+                                           p.d_scope_vars, p.d_leaf_rep, c.cnst, D, K, R,
+                                           p.family);
+  count_launch((p.n_w ? 1 : 0) + (p.n_mix ? 1 : 0) + 3);
+  return check_cuda(cudaGetLastError(), "prepare kernels");
+}
+
+// ---------------------------------------------------------------------------
+// leaf forward
+// ---------------------------------------------------------------------------
+
+// Gaussian: Q[b,l,k] = sum_{d in scope} (x_bd*sa_dk + nmsa_dk)^2 (fp32 chunks -> fp64).
+// grid (ceil(B/128), n_leaf, dsplit), block 32*KG threads (KG = ceil(K/8)).
+__global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
+    const float *__restrict__ x, int64_t B, int D, int K, int R,
+    const int *__restrict__ scope_off, const int *__restrict__ scope_vars,
+    const int *__restrict__ leaf_rep, const float2 *__restrict__ lp,
+    const uint8_t *__restrict__ active, double *__restrict__ part, int64_t Bc, int n_leaf,
+    int dsplit, int32_t *status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int KG = blockDim.x / 32;
+  const int KP = KG * LF_KPT;
+  float *xs = (float *)smem_raw;                               // [VC][TB+1]
+  float2 *ps = (float2 *)(xs + LF_VC * (LF_TB + 1) + 1);       // [VC][KP] (8B aligned)
+  ps = (float2 *)(((uintptr_t)ps + 15) & ~(uintptr_t)15);
+  const int nkc = gridDim.z / dsplit;  // k chunks of KP entries
+  const int leaf = blockIdx.y, split = blockIdx.z / nkc;
+  const int kbase = (blockIdx.z % nkc) * KP;
+  const int lane = threadIdx.x & 31, kq = threadIdx.x >> 5;
+  const int sbeg = scope_off[leaf], slen = scope_off[leaf + 1] - sbeg;
+  const int per = (slen + dsplit - 1) / dsplit;
+  const int vbeg = split * per, vend = min(slen, vbeg + per);
+  const int r = leaf_rep[leaf];
+  const int64_t b0 = (int64_t)blockIdx.x * LF_TB;
+
+  float acc[LF_NS][LF_KPT];
+  double tot[LF_NS][LF_KPT];
+#pragma unroll
+  for (int s = 0; s < LF_NS; ++s)
+#pragma unroll
+    for (int j = 0; j < LF_KPT; ++j) {
+      acc[s][j] = 0.f;
+      tot[s][j] = 0.0;
+    }
+
+  for (int c0 = vbeg; c0 < vend; c0 += LF_VC) {
+    const int nv = min(LF_VC, vend - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < LF_VC * LF_TB; e += blockDim.x) {
+      const int v = e % LF_VC, bl = e / LF_VC;
+      float xv = 0.f;
+      if (v < nv && b0 + bl < B) {
+        const int d = scope_vars[sbeg + c0 + v];
+        xv = x[(b0 + bl) * D + d];
+        const bool act = active[d] != 0;
+        if (act && !isfinite(xv)) atomicMin(&status[0], d);
+        if (!act || !isfinite(xv)) xv = 0.f;
+      }
+      xs[v * (LF_TB + 1) + bl] = xv;
+    }
+    for (int e = threadIdx.x; e < LF_VC * KP; e += blockDim.x) {
+      const int v = e / KP, k = e % KP;
+      float2 pv = make_float2(0.f, 0.f);
+      if (v < nv && kbase + k < K)
+        pv = lp[((int64_t)r * D + scope_vars[sbeg + c0 + v]) * K + kbase + k];
+      ps[v * KP + k] = pv;
+    }
+    __syncthreads();
+    for (int v = 0; v < nv; ++v) {
+      float xv[LF_NS];
+#pragma unroll
+      for (int s = 0; s < LF_NS; ++s) xv[s] = xs[v * (LF_TB + 1) + lane + 32 * s];
+      const float4 *pp = (const float4 *)(ps + v * KP + kq * LF_KPT);
+#pragma unroll
+      for (int j2 = 0; j2 < LF_KPT / 2; ++j2) {
+        const float4 q = pp[j2];
+#pragma unroll
+        for (int s = 0; s < LF_NS; ++s) {
+          float t0 = fmaf(xv[s], q.x, q.y);
+          float t1 = fmaf(xv[s], q.z, q.w);
+          acc[s][2 * j2] = fmaf(t0, t0, acc[s][2 * j2]);
+          acc[s][2 * j2 + 1] = fmaf(t1, t1, acc[s][2 * j2 + 1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < LF_NS; ++s)
+#pragma unroll
+      for (int j = 0; j < LF_KPT; ++j) {
+        tot[s][j] += (double)acc[s][j];
+        acc[s][j] = 0.f;
+      }
+  }
+#pragma unroll
+  for (int s = 0; s < LF_NS; ++s) {
+    const int64_t b = b0 + lane + 32 * s;
+    if (b >= B) continue;
+    double *dst = part + (((int64_t)split * n_leaf + leaf) * Bc + b) * K;
+#pragma unroll
+    for (int j = 0; j < LF_KPT; ++j) {
+      const int k = kbase + kq * LF_KPT + j;
+      if (k < K) dst[k] = tot[s][j];
+    }
+  }
+}
+
+// Categorical / binomial: S[b,l,k] = sum_d term(x_bd, k). One sample per lane.
+// grid (ceil(B/32), n_leaf, dsplit), block 32*KG.
+__global__ void __launch_bounds__(1024) k_leaf_fwd_discrete(
+    const float *__restrict__ x, int64_t B, int D, int K, int R, const int *scope_off,
+    const int *scope_vars, const int *leaf_rep, const void *lpv, const uint8_t *active,
+    const double *logh, int family, int S, int n_trials, double *part, int64_t Bc,
+    int n_leaf, int dsplit, int32_t *status) {
+  const int leaf = blockIdx.y, split = blockIdx.z;
+  const int lane = threadIdx.x & 31, kq = threadIdx.x >> 5;
+  const int sbeg = scope_off[leaf], slen = scope_off[leaf + 1] - sbeg;
+  const int per = (slen + dsplit - 1) / dsplit;
+  const int vbeg = split * per, vend = min(slen, vbeg + per);
+  const int r = leaf_rep[leaf];
+  const int64_t b = (int64_t)blockIdx.x * 32 + lane;
+  const bool live = b < B;
+  const int top = family == EINET_FAMILY_CATEGORICAL ? S - 1 : n_trials;
+  float acc[LF_KPT];
+  double tot[LF_KPT];
+#pragma unroll
+  for (int j = 0; j < LF_KPT; ++j) {
+    acc[j] = 0.f;
+    tot[j] = 0.0;
+  }
+  int cnt = 0;
+  for (int q = vbeg; q < vend; ++q) {
+    const int d = scope_vars[sbeg + q];
+    if (!active[d] || !live) continue;
+    const float xv = x[b * D + d];
+    const bool ok = xv >= 0.f && xv <= (float)top && xv == floorf(xv);
+    if (!ok) atomicMin(&status[0], d);
+    const int xi = ok ? (int)xv : 0;
+    const int64_t base = ((int64_t)r * D + d) * K;
+    if (family == EINET_FAMILY_CATEGORICAL) {
+      const float *lp = (const float *)lpv;
+#pragma unroll
+      for (int j = 0; j < LF_KPT; ++j) {
+        const int k = kq * LF_KPT + j;
+        if (k < K) acc[j] += lp[(base + k) * S + xi];
+      }
+    } else {
+      const float2 *lp = (const float2 *)lpv;
+      const float h = (float)logh[xi];
+      const float xf = (float)xi;
+#pragma unroll
+      for (int j = 0; j < LF_KPT; ++j) {
+        const int k = kq * LF_KPT + j;
+        if (k < K) {
+          const float2 t = lp[base + k];
+          acc[j] += fmaf(xf, t.x, t.y) + h;
+        }
+      }
+    }
+    if (++cnt == LF_VC) {
+      cnt = 0;
+#pragma unroll
+      for (int j = 0; j < LF_KPT; ++j) {
+        tot[j] += (double)acc[j];
+        acc[j] = 0.f;
+      }
+    }
+  }
+  if (!live) return;
+  double *dst = part + (((int64_t)split * n_leaf + leaf) * Bc + b) * K;
+#pragma unroll
+  for (int j = 0; j < LF_KPT; ++j) {
+    const int k = kq * LF_KPT + j;
+    if (k < K) dst[k] = tot[j] + (double)acc[j];
+  }
+}
+
+// value = cnst + sign * sum_split part  ->  slab (shift = max_k value, off = value - shift)
+__global__ void k_leaf_finalize(const double *__restrict__ part, int dsplit,
+                                const double *__restrict__ cnst, int64_t B, int K, int n_leaf,
+                                const int *leaf_slab, WsView ws, double sign) {
+  const int leaf = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int slab = leaf_slab[leaf];
+  auto value = [&](int k) {
+    double s = 0.0;
+    for (int q = 0; q < dsplit; ++q) s += part[(((int64_t)q * n_leaf + leaf) * ws.bc + b) * K + k];
+    return cnst[leaf * K + k] + sign * s;
+  };
+  double mx = -CUDART_INF;
+  for (int k = 0; k < K; ++k) mx = fmax(mx, value(k));
+  float *o = slab_off(ws, slab, b);
+  if (mx == -CUDART_INF) {
+    slab_shift(ws, slab)[b] = -CUDART_INF;
+    for (int k = 0; k < K; ++k) o[k] = 0.f;
+    return;
+  }
+  slab_shift(ws, slab)[b] = mx;
+  for (int k = 0; k < K; ++k) o[k] = (float)(value(k) - mx);
+}
+
+static int leaf_dsplit(const Plan &p, int64_t B, int tb) {
+  int64_t blocks = (int64_t)ceil_div(B, tb) * p.n_leaf;
+  int want = (int)std::max<int64_t>(1, (2 * p.num_sms + blocks - 1) / blocks);
+  int cap = std::max(1, std::min(kMaxDSplit, ceil_div(p.max_scope, LF_VC)));
+  return std::min(want, cap);
+}
+
+int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
+                        uint8_t *wsb, int32_t *status, cudaStream_t st) {
+  CompView c = comp_view(p, compute);
+  WsView w = ws_view(p, wsb);
+  const int KG = ceil_div(p.k, LF_KPT);
+  int ds;
+  if (p.family == EINET_FAMILY_GAUSSIAN) {
+    const int kg = std::min(KG, 8);          // <= 64 k entries per CTA
+    const int nkc = ceil_div(KG, kg);
+    const int threads = 32 * kg;
+    ds = leaf_dsplit(p, B, LF_TB);
+    const size_t smem = sizeof(float) * (LF_VC * (LF_TB + 1) + 1) + 16 +
+                        sizeof(float2) * LF_VC * kg * LF_KPT;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_leaf_fwd_gauss, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    dim3 grid(ceil_div(B, LF_TB), p.n_leaf, ds * nkc);
+    k_leaf_fwd_gauss<<<grid, threads, smem, st>>>(
+        x, B, p.d_vars, p.k, p.num_replicas, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
+        (const float2 *)c.leafp, c.active, w.leafpart, w.bc, p.n_leaf, ds, status);
+  } else {
+    const int threads = 32 * KG;
+    if (threads > 1024) return fail(EINET_ERR_USAGE, "k too large for the leaf kernel (k <= 256)");
+    ds = leaf_dsplit(p, B, 32);
+    dim3 grid(ceil_div(B, 32), p.n_leaf, ds);
+    k_leaf_fwd_discrete<<<grid, threads, 0, st>>>(
+        x, B, p.d_vars, p.k, p.num_replicas, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
+        c.leafp, c.active, c.logh, p.family, p.num_states, p.n_trials, w.leafpart, w.bc,
+        p.n_leaf, ds, status);
+  }
+  dim3 g2(ceil_div(B, 128), p.n_leaf);
+  k_leaf_finalize<<<g2, 128, 0, st>>>(w.leafpart, ds, c.cnst, B, p.k, p.n_leaf, p.d_leaf_slab,
+                                      w, p.family == EINET_FAMILY_GAUSSIAN ? -1.0 : 1.0);
+  count_launch(2);
+  return check_cuda(cudaGetLastError(), "leaf forward kernels");
+}
+
+// ---------------------------------------------------------------------------
+// leaf responsibilities and statistics (engine.py:318-327)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ float block_sum_128(float v, float *red) {
+  // deterministic: fixed shuffle tree then fixed-order sum of 4 warp results
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int wid = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[wid] = v;
+  __syncthreads();
+  float s = 0.f;
+  if (threadIdx.x == 0) s = (red[0] + red[1]) + (red[2] + red[3]);
+  __syncthreads();
+  return s;
+}
+
+// rho_leaf[b,l,k] from the slot CSR; per-CTA partial of P[l,k] = sum_b rho.
+// grid (ceil(B/128), n_leaf), block 128.
+__global__ void k_leaf_rho(WsView ws, const int *csr_off, const int *csr_slot,
+                           const uint8_t *ones, const int *leaf_slab, int64_t B, int K,
+                           int n_leaf, double *ppart) {
+  __shared__ float red[4];
+  const int leaf = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int slab = leaf_slab[leaf];
+  float *rho = ws.rho + ((int64_t)leaf * ws.bc) * K;
+  for (int k = 0; k < K; ++k) {
+    float v = 0.f;
+    if (b < B) {
+      v = gather_rho(ws, csr_off, csr_slot, ones, slab, b, k);
+      rho[b * K + k] = v;
+    }
+    float s = block_sum_128(v, red);
+    if (threadIdx.x == 0) ppart[((int64_t)blockIdx.x * n_leaf + leaf) * K + k] = (double)s;
+  }
+}
+
+constexpr int LS_VC = 32;   // variables per CTA
+constexpr int LS_BT = 32;   // samples per fp32 run before folding into fp64
+constexpr int LS_MAXP = 16; // (var,k,t) entries per thread
+
+// Gaussian: acc_pt[d,k,r,:] += sum_b rho*(x, x^2), accumulated centred at the
+// current mean c (fp32 runs of 32 samples) and un-centred in fp64:
+//   sum rho x = A + c P,  sum rho x^2 = Q + 2 c A + c^2 P.
+// grid (ceil(max_scope/32), n_leaf, lsplit), block 256.
+__global__ void __launch_bounds__(256) k_leaf_stats_gauss(
+    const float *__restrict__ x, int64_t B, int D, int K, int R, const int *scope_off,
+    const int *scope_vars, const int *leaf_rep, const float *__restrict__ rho_all, int64_t Bc,
+    const float *__restrict__ center, const uint8_t *__restrict__ active, double *lspart,
+    int64_t n_phi, int lsplit) {
+  __shared__ float xs[LS_BT][LS_VC + 1];
+  extern __shared__ float rs[];  // [LS_BT][K]
+  const int leaf = blockIdx.y, split = blockIdx.z;
+  const int sbeg = scope_off[leaf], slen = scope_off[leaf + 1] - sbeg;
+  const int v0 = blockIdx.x * LS_VC;
+  if (v0 >= slen) return;
+  const int nv = min(LS_VC, slen - v0);
+  const int r = leaf_rep[leaf];
+  const int64_t per = (B + lsplit - 1) / lsplit;
+  const int64_t bb = split * per, be = min(B, bb + per);
+  const float *rho = rho_all + (int64_t)leaf * Bc * K;
+  const int npairs = nv * K;
+  float a1[LS_MAXP], a2[LS_MAXP], pp[LS_MAXP], cc[LS_MAXP];
+  double t0[LS_MAXP], t1[LS_MAXP];
+  int vv[LS_MAXP], kk[LS_MAXP];
+#pragma unroll
+  for (int m = 0; m < LS_MAXP; ++m) {
+    const int e = threadIdx.x + m * 256;
+    vv[m] = e < npairs ? e / K : 0;
+    kk[m] = e < npairs ? e % K : 0;
+    const int d = scope_vars[sbeg + v0 + vv[m]];
+    cc[m] = e < npairs ? center[((int64_t)r * D + d) * K + kk[m]] : 0.f;
+    a1[m] = a2[m] = pp[m] = 0.f;
+    t0[m] = t1[m] = 0.0;
+  }
+  for (int64_t t = bb; t < be; t += LS_BT) {
+    const int nb = (int)min((int64_t)LS_BT, be - t);
+    __syncthreads();
+    for (int e = threadIdx.x; e < LS_BT * LS_VC; e += 256) {
+      const int v = e % LS_VC, bl = e / LS_VC;
+      float xv = 0.f;
+      if (v < nv && bl < nb) {
+        const int d = scope_vars[sbeg + v0 + v];
+        xv = x[(t + bl) * D + d];
+        if (!isfinite(xv)) xv = 0.f;
+      }
+      xs[bl][v] = xv;
+    }
+    for (int e = threadIdx.x; e < LS_BT * K; e += 256) {
+      const int bl = e / K, k = e % K;
+      rs[e] = bl < nb ? rho[(t + bl) * K + k] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < LS_MAXP; ++m) {
+      if (threadIdx.x + m * 256 >= npairs) break;
+      float s1 = 0.f, s2 = 0.f, sp = 0.f;
+      for (int bl = 0; bl < nb; ++bl) {
+        const float rr = rs[bl * K + kk[m]];
+        const float y = xs[bl][vv[m]] - cc[m];
+        const float ry = rr * y;
+        s1 += ry;
+        s2 = fmaf(ry, y, s2);
+        sp += rr;
+      }
+      const double c = (double)cc[m];
+      t0[m] += (double)s1 + c * (double)sp;
+      t1[m] += (double)s2 + 2.0 * c * (double)s1 + c * c * (double)sp;
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < LS_MAXP; ++m) {
+    if (threadIdx.x + m * 256 >= npairs) break;
+    const int d = scope_vars[sbeg + v0 + vv[m]];
+    double *dst = lspart + (int64_t)split * n_phi + ((((int64_t)d * K + kk[m]) * R + r) * 2);
+    const bool act = active[d] != 0;
+    dst[0] = act ? t0[m] : 0.0;
+    dst[1] = act ? t1[m] : 0.0;
+  }
+}
+
+// Categorical (T = S one-hot) / binomial (T = 1, x): entries (var, k, t).
+__global__ void __launch_bounds__(256) k_leaf_stats_discrete(
+    const float *__restrict__ x, int64_t B, int D, int K, int R, int T, int family,
+    const int *scope_off, const int *scope_vars, const int *leaf_rep,
+    const float *__restrict__ rho_all, int64_t Bc, const uint8_t *__restrict__ active,
+    double *lspart, int64_t n_phi, int lsplit) {
+  const int leaf = blockIdx.y, split = blockIdx.z;
+  const int sbeg = scope_off[leaf], slen = scope_off[leaf + 1] - sbeg;
+  const int v0 = blockIdx.x * LS_VC;
+  if (v0 >= slen) return;
+  const int nv = min(LS_VC, slen - v0);
+  const int r = leaf_rep[leaf];
+  const int64_t per = (B + lsplit - 1) / lsplit;
+  const int64_t bb = split * per, be = min(B, bb + per);
+  const float *rho = rho_all + (int64_t)leaf * Bc * K;
+  const int64_t n_ent = (int64_t)nv * K * T;
+  for (int64_t e = threadIdx.x; e < n_ent; e += blockDim.x) {
+    const int t = (int)(e % T);
+    const int k = (int)((e / T) % K);
+    const int v = (int)(e / ((int64_t)T * K));
+    const int d = scope_vars[sbeg + v0 + v];
+    double tot = 0.0;
+    if (active[d]) {
+      float run = 0.f;
+      int cnt = 0;
+      for (int64_t b = bb; b < be; ++b) {
+        const float xv = x[b * D + d];
+        const float rr = rho[b * K + k];
+        if (family == EINET_FAMILY_CATEGORICAL)
+          run += ((int)xv == t && xv == floorf(xv)) ? rr : 0.f;
+        else
+          run = fmaf(rr, xv, run);
+        if (++cnt == LS_BT) {
+          tot += (double)run;
+          run = 0.f;
+          cnt = 0;
+        }
+      }
+      tot += (double)run;
+    }
+    lspart[(int64_t)split * n_phi + ((((int64_t)d * K + k) * R + r) * T + t)] = tot;
+  }
+}
+
+int leaf_lsplit(const Plan &p, int64_t B) {
+  int64_t blocks = (int64_t)ceil_div(p.max_scope, LS_VC) * p.n_leaf;
+  int want = (int)std::max<int64_t>(1, (2 * p.num_sms + blocks - 1) / blocks);
+  int cap = (int)std::max<int64_t>(1, std::min<int64_t>(8, (B + 255) / 256));
+  return std::min(want, cap);
+}
+
+int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
+                         uint8_t *wsb, double *stats, cudaStream_t st) {
+  CompView c = comp_view(p, compute);
+  WsView w = ws_view(p, wsb);
+  const int K = p.k, D = p.d_vars, R = p.num_replicas, T = p.suff;
+  const int nb = ceil_div(B, 128);
+  k_leaf_rho<<<dim3(nb, p.n_leaf), 128, 0, st>>>(w, p.d_csr_off, p.d_csr_slot, p.d_slab_ones,
+                                                 p.d_leaf_slab, B, K, p.n_leaf, w.ppart);
+  launch_reduce_partials(stats + p.sizes.stats_p_offset, w.ppart, nb, (int64_t)p.n_leaf * K,
+                         (int64_t)p.n_leaf * K, nullptr, st);
+  const int ls = leaf_lsplit(p, B);
+  const int64_t n_phi = p.n_phi;
+  cudaMemsetAsync(w.lspart, 0, sizeof(double) * n_phi * ls, st);
+  dim3 grid(ceil_div(p.max_scope, LS_VC), p.n_leaf, ls);
+  if (p.family == EINET_FAMILY_GAUSSIAN) {
+    if ((LS_VC * K + 255) / 256 > LS_MAXP)
+      return fail(EINET_ERR_USAGE, "k too large for the gaussian leaf statistics kernel");
+    k_leaf_stats_gauss<<<grid, 256, sizeof(float) * LS_BT * K, st>>>(
+        x, B, D, K, R, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep, w.rho, w.bc, c.center,
+        c.active, w.lspart, n_phi, ls);
+  } else {
+    k_leaf_stats_discrete<<<grid, 256, 0, st>>>(x, B, D, K, R, T, p.family, p.d_scope_off,
+                                               p.d_scope_vars, p.d_leaf_rep, w.rho, w.bc,
+                                               c.active, w.lspart, n_phi, ls);
+  }
+  launch_reduce_partials(stats + p.sizes.stats_acc_pt_offset, w.lspart, ls, n_phi, n_phi,
+                         nullptr, st);
+  count_launch(2);
+  return check_cuda(cudaGetLastError(), "leaf backward kernels");
+}
+
+// ---------------------------------------------------------------------------
+// conversions / exports
+// ---------------------------------------------------------------------------
+
+__global__ void k_expand_acc_p(const double *P, const int *leaf_of, double *acc_p, int D, int K,
+                               int R) {
+  int64_t n = (int64_t)D * K * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(e % R);
+    int k = (int)((e / R) % K);
+    int d = (int)(e / ((int64_t)R * K));
+    int l = leaf_of[(int64_t)r * D + d];
+    acc_p[e] = l >= 0 ? P[(int64_t)l * K + k] : 0.0;
+  }
+}
+
+int launch_expand_acc_p(Plan &p, const double *stats, double *acc_p, cudaStream_t st) {
+  int64_t n = (int64_t)p.d_vars * p.k * p.num_replicas;
+  k_expand_acc_p<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+      stats + p.sizes.stats_p_offset, p.d_leaf_of, acc_p, p.d_vars, p.k, p.num_replicas);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "expand acc_p");
+}
+
+// E[b,d,k,r] in fp64 straight from the master parameters (expfam.py:278-294).
+__global__ void k_ef_log_prob(const double *__restrict__ phi, const float *__restrict__ x,
+                              int64_t B, int D, int K, int R, int family, int S, int n_trials,
+                              const uint8_t *mask, double *out, int32_t *status) {
+  int64_t n = B * D * K * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % R);
+    const int k = (int)((e / R) % K);
+    const int d = (int)((e / ((int64_t)R * K)) % D);
+    const int64_t b = e / ((int64_t)R * K * D);
+    if (mask && mask[d]) {
+      out[e] = 0.0;
+      continue;
+    }
+    const double xv = (double)x[b * D + d];
+    const int64_t base = ((int64_t)d * K + k) * R + r;
+    double v;
+    if (family == EINET_FAMILY_GAUSSIAN) {
+      if (!isfinite(xv)) atomicMin(&status[0], d);
+      const double mu = phi[base * 2], var = phi[base * 2 + 1] - mu * mu;
+      v = -0.5 * (kLog2Pi + log(var)) - (xv - mu) * (xv - mu) / (2.0 * var);
+    } else {
+      const int top = family == EINET_FAMILY_CATEGORICAL ? S - 1 : n_trials;
+      const bool ok = xv >= 0.0 && xv <= (double)top && xv == floor(xv);
+      if (!ok) atomicMin(&status[0], d);
+      const int xi = ok ? (int)xv : 0;
+      if (family == EINET_FAMILY_CATEGORICAL) {
+        v = log(phi[base * S + xi]);
+      } else {
+        const double pr = phi[base] / (double)n_trials;
+        v = lgamma((double)n_trials + 1.0) - lgamma((double)xi + 1.0) -
+            lgamma((double)(n_trials - xi) + 1.0) + xi * log(pr) +
+            (n_trials - xi) * log1p(-pr);
+      }
+    }
+    out[e] = v;
+  }
+}
+
+int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
+                       const uint8_t *mask, double *out, int32_t *status, cudaStream_t st) {
+  int64_t n = B * p.d_vars * p.k * p.num_replicas;
+  k_ef_log_prob<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+      params + p.sizes.phi_offset, x, B, p.d_vars, p.k, p.num_replicas, p.family, p.num_states,
+      p.n_trials, mask, out, status);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "ef_log_prob");
+}
+
+__global__ void k_export_rows(WsView ws, const int *slabs, int nrows, int64_t B, int K,
+                              double *out) {
+  int64_t n = B * nrows * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e % K);
+    const int row = (int)((e / K) % nrows);
+    const int64_t b = e / ((int64_t)K * nrows);
+    const int slab = slabs ? slabs[row] : row;
+    const double s = slab_shift(ws, slab)[b];
+    out[e] = s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[k];
+  }
+}
+
+int launch_export_buffer(Plan &p, const uint8_t *wsb, int64_t B, double *out, cudaStream_t st) {
+  WsView w = ws_view(p, wsb);
+  int64_t n = B * p.nbr * p.k;
+  if (n == 0) return EINET_OK;
+  k_export_rows<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+      w, nullptr, p.nbr, B, p.k, out);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "export buffer");
+}
+
+int launch_export_leaf_rows(Plan &p, const uint8_t *wsb, int64_t B, double *out,
+                            cudaStream_t st) {
+  WsView w = ws_view(p, wsb);
+  int64_t n = B * p.n_leaf * p.k;
+  k_export_rows<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+      w, p.d_leaf_slab, p.n_leaf, B, p.k, out);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "export leaf rows");
+}
+
+}  // namespace einet

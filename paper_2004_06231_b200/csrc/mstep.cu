@@ -1,0 +1,236 @@
+// Fused M-step (trainer.py:69-124, engine.py:46-54, expfam project) in fp64,
+// the deterministic partial-sum reduction and the standalone fp64
+// log_einsum_exp (engine.py:91-109).
+#include <climits>
+#include <cmath>
+
+#include "kern_common.cuh"
+
+namespace einet {
+
+__global__ void k_reduce_partials(double *__restrict__ dst, const double *__restrict__ part,
+                                  int nparts, int64_t n, int64_t stride,
+                                  const double *__restrict__ scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * stride + i];
+    dst[i] += scale ? scale[i] * s : s;
+  }
+}
+
+void launch_reduce_partials(double *dst, const double *part, int nparts, int64_t n,
+                            int64_t stride, const double *scale, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n + kReduceThreads - 1) / kReduceThreads, 8192);
+  k_reduce_partials<<<grid, kReduceThreads, 0, st>>>(dst, part, nparts, n, stride, scale);
+  count_launch();
+}
+
+__device__ __forceinline__ bool step_failed(const int32_t *status) {
+  return status && (status[0] != INT_MAX || status[1] != INT_MAX);
+}
+
+// Deterministic block sum (fixed shuffle tree, fixed warp order). blockDim 256.
+__device__ __forceinline__ double block_sum_256(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+// One (l, k) slice of K*K weights per CTA (all einsum layers are contiguous
+// in the same order in params and stats). trainer.py:74-77, 110-111,
+// engine.py:46-49.
+__global__ void __launch_bounds__(256) k_mstep_einsum(double *__restrict__ W,
+                                                      float *__restrict__ w32,
+                                                      const double *__restrict__ n, int KK,
+                                                      double lam, double eps,
+                                                      const int32_t *status) {
+  __shared__ double red[8];
+  if (step_failed(status)) return;
+  const int64_t base = (int64_t)blockIdx.x * KK;
+  double s = 0.0;
+  for (int e = threadIdx.x; e < KK; e += 256) s += n[base + e];
+  const double den = block_sum_256(s, red);
+  double s2 = 0.0;
+  for (int e = threadIdx.x; e < KK; e += 256) {
+    const double old = W[base + e];
+    const double tgt = den > 0.0 ? n[base + e] / den : old;
+    double v = (1.0 - lam) * old + lam * tgt;
+    v = fmax(v, eps);
+    W[base + e] = v;
+    s2 += v;
+  }
+  const double tot = block_sum_256(s2, red);
+  for (int e = threadIdx.x; e < KK; e += 256) {
+    const double v = W[base + e] / tot;
+    W[base + e] = v;
+    w32[base + e] = (float)v;
+  }
+}
+
+// One mixing row per thread (trainer.py:79-81, 112-113, engine.py:52-54).
+__global__ void k_mstep_mixing(double *__restrict__ Wm, float *__restrict__ m32,
+                               const double *__restrict__ n, const int *row_off,
+                               const int *row_len, const uint8_t *mask, int nrows, double lam,
+                               double eps, const int32_t *status) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows || step_failed(status)) return;
+  const int o = row_off[r], len = row_len[r];
+  double den = 0.0;
+  for (int c = 0; c < len; ++c) den += n[o + c];
+  double tot = 0.0;
+  for (int c = 0; c < len; ++c) {
+    const double old = Wm[o + c];
+    const double tgt = den > 0.0 ? n[o + c] / den : old;
+    double v = (1.0 - lam) * old + lam * tgt;
+    v = mask[o + c] ? fmax(v, eps) : 0.0;
+    Wm[o + c] = v;
+    tot += v;
+  }
+  for (int c = 0; c < len; ++c) {
+    const double v = Wm[o + c] / tot;
+    Wm[o + c] = v;
+    m32[o + c] = (float)v;
+  }
+}
+
+// Leaf parameters, one (d, k, r) per thread (trainer.py:82-85, 114, 96).
+__global__ void k_mstep_leaf(double *__restrict__ phi, const double *__restrict__ acc_pt,
+                             const double *__restrict__ P, const int *__restrict__ leaf_of,
+                             int D, int K, int R, int T, int family, double lam,
+                             double var_min, double var_max, double p_min, int n_trials,
+                             const int32_t *status) {
+  if (step_failed(status)) return;
+  const int64_t n = (int64_t)D * K * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % R);
+    const int k = (int)((e / R) % K);
+    const int d = (int)(e / ((int64_t)R * K));
+    const int l = leaf_of[(int64_t)r * D + d];
+    const double p = l >= 0 ? P[(int64_t)l * K + k] : 0.0;
+    const bool keep = p <= kEpsCount;
+    double *ph = phi + e * T;
+    const double *acc = acc_pt + e * T;
+    if (family == EINET_FAMILY_GAUSSIAN) {
+      const double t0 = keep ? ph[0] : acc[0] / p;
+      const double t1 = keep ? ph[1] : acc[1] / p;
+      const double m = (1.0 - lam) * ph[0] + lam * t0;
+      const double s = (1.0 - lam) * ph[1] + lam * t1;
+      const double var = fmin(fmax(s - m * m, var_min), var_max);
+      ph[0] = m;
+      ph[1] = var + m * m;
+    } else if (family == EINET_FAMILY_CATEGORICAL) {
+      double tot = 0.0;
+      for (int t = 0; t < T; ++t) {
+        const double tg = keep ? ph[t] : acc[t] / p;
+        const double v = fmax((1.0 - lam) * ph[t] + lam * tg, p_min);
+        ph[t] = v;
+        tot += v;
+      }
+      for (int t = 0; t < T; ++t) ph[t] = ph[t] / tot;
+    } else {
+      const double tg = keep ? ph[0] : acc[0] / p;
+      const double v = (1.0 - lam) * ph[0] + lam * tg;
+      const double nt = (double)n_trials;
+      const double pr = fmin(fmax(v / nt, p_min), 1.0 - p_min);
+      ph[0] = pr * nt;
+    }
+  }
+}
+
+int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats, double lam,
+                 double eps_w, const int32_t *status, cudaStream_t st) {
+  CompView c = comp_view(p, compute);
+  const int K = p.k;
+  const int KK = K * K;
+  if (p.n_w) {
+    const int nslices = (int)(p.n_w / KK);
+    k_mstep_einsum<<<nslices, 256, 0, st>>>(params, c.w32, stats, KK, lam, eps_w, status);
+    count_launch();
+  }
+  if (p.n_mixrows) {
+    k_mstep_mixing<<<ceil_div(p.n_mixrows, 128), 128, 0, st>>>(
+        params + p.n_w, c.mix32, stats + p.n_w, p.d_mixrow_off, p.d_mixrow_len,
+        p.d_mix_mask_all, p.n_mixrows, lam, eps_w, status);
+    count_launch();
+  }
+  const int64_t n = (int64_t)p.d_vars * K * p.num_replicas;
+  k_mstep_leaf<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+      params + p.sizes.phi_offset, stats + p.sizes.stats_acc_pt_offset,
+      stats + p.sizes.stats_p_offset, p.d_leaf_of, p.d_vars, K, p.num_replicas, p.suff,
+      p.family, lam, p.var_min, p.var_max, p.p_min, p.n_trials, status);
+  count_launch();
+  int rc = check_cuda(cudaGetLastError(), "mstep kernels");
+  if (rc) return rc;
+  return launch_prepare(p, params, compute, nullptr, nullptr, st);
+}
+
+// ---------------------------------------------------------------------------
+// standalone fp64 log_einsum_exp (engine.py:91-109)
+// ---------------------------------------------------------------------------
+
+__global__ void k_log_einsum_exp(const double *__restrict__ left, const double *__restrict__ right,
+                                 const double *__restrict__ w, int64_t B, int L, int K, int Ko,
+                                 double *out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= B * L * Ko) return;
+  const int k = (int)(e % Ko);
+  const int l = (int)((e / Ko) % L);
+  const int64_t b = e / ((int64_t)Ko * L);
+  const double *ln = left + (b * L + l) * K, *rn = right + (b * L + l) * K;
+  double a = -CUDART_INF, c = -CUDART_INF;
+  bool nan = false;
+  for (int i = 0; i < K; ++i) {
+    nan |= ln[i] != ln[i] || rn[i] != rn[i];
+    a = fmax(a, ln[i]);
+    c = fmax(c, rn[i]);
+  }
+  const bool ok = !nan && isfinite(a) && isfinite(c);
+  double r = 0.0;
+  if (ok) {
+    const double *wk = w + ((int64_t)l * Ko + k) * K * K;
+    for (int i = 0; i < K; ++i) {
+      const double ei = exp(ln[i] - a);
+      double t = 0.0;
+      for (int j = 0; j < K; ++j) t += wk[i * K + j] * exp(rn[j] - c);
+      r += ei * t;
+    }
+  }
+  out[e] = (ok && r > 0.0) ? a + c + log(r) : -CUDART_INF;
+}
+
+int launch_log_einsum_exp(const double *left, const double *right, const double *w, int64_t B,
+                          int L, int K, int Ko, double *out, cudaStream_t st) {
+  const int64_t n = B * L * Ko;
+  k_log_einsum_exp<<<ceil_div(n, 128), 128, 0, st>>>(left, right, w, B, L, K, Ko, out);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "log_einsum_exp");
+}
+
+__global__ void k_status_reset(int32_t *status) {
+  if (threadIdx.x < EINET_STATUS_WORDS) status[threadIdx.x] = INT_MAX;
+}
+
+int launch_status_reset(int32_t *status, cudaStream_t st) {
+  k_status_reset<<<1, 32, 0, st>>>(status);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "status reset");
+}
+
+// Tensor-core EinsumLayer path: not enabled in this build; the CUDA-core
+// kernels handle every layer.
+int launch_einsum_tc_forward(Plan &, const LayerPlan &, const float *, WsView &, int64_t,
+                             int32_t *, cudaStream_t, bool *handled) {
+  *handled = false;
+  return EINET_OK;
+}
+
+}  // namespace einet

@@ -1,0 +1,139 @@
+"""EM training on the GPU (reference ``trainer.py``).
+
+One EM step = for each chunk: forward + responsibility back-pass (statistics
+accumulate in one fp64 device buffer) -> optional all-reduce of that buffer
+across ranks -> one fused M-step kernel sequence. The host synchronises once
+per step, to read the log-likelihood sum and the error words.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import engine
+from .model import EinetModel
+
+EPS_COUNT = 1e-12
+
+
+class TrainingDiverged(RuntimeError):
+    pass
+
+
+@dataclass
+class TrainerConfig:
+    """Reference ``trainer.py:30-46``."""
+
+    mode: str = "stochastic"
+    step_size: float = 0.5
+    batch_size: int = 500
+    epochs: int = 10
+    seed: int = 0
+    eps_w: float = engine.EPS_W
+    chunk: int = 4096
+
+    def __post_init__(self):
+        if self.mode not in ("full", "stochastic"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if not 0.0 <= self.step_size <= 1.0:
+            raise ValueError("step size must lie in [0, 1]")
+        if self.batch_size < 1:
+            raise ValueError("batch size must be >= 1")
+
+
+@dataclass
+class EpochMetrics:
+    epoch: int
+    train_ll: float
+    valid_ll: float
+    wall_seconds: float
+
+
+def accumulate(model: EinetModel, batch: torch.Tensor, chunk: int):
+    """E-step over a device batch into the model's stats buffer
+    (reference ``trainer.py:57-66``). Returns (engine, stats, status)."""
+    n = batch.shape[0]
+    eng, ws, stats, status, root = model.step_buffers(min(chunk, max(n, 1)))
+    compute = model.params.compute_for(eng)
+    stats.zero_()
+    eng.status_reset(status)
+    step = eng.max_chunk if chunk >= eng.max_chunk else chunk
+    for lo in range(0, n, step):
+        xb = batch[lo:lo + step]
+        b = xb.shape[0]
+        eng.forward(compute, xb, b, ws, root, status)
+        eng.backward(model.params.flat, compute, xb, b, ws, stats, status)
+    return eng, stats, status, compute
+
+
+def em_stochastic_step(model: EinetModel, batch, lam, eps_w=engine.EPS_W, chunk=4096,
+                       process_group=None) -> float:
+    """One gliding-average EM update; returns the pre-update mean LL of the
+    batch (reference ``trainer.py:99-117``). ``lam == 0`` leaves every
+    parameter bitwise unchanged.
+
+    With ``process_group`` the statistics are summed across ranks (one NCCL
+    all-reduce of the packed buffer) and every rank applies the identical
+    M-step; the returned mean LL is then the global one.
+    """
+    xd = engine.as_device_batch(batch)
+    if xd.shape[0] == 0:
+        raise ValueError("empty batch")
+    eng, stats, status, compute = accumulate(model, xd, chunk)
+    if process_group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=process_group)
+        dist.all_reduce(status, op=dist.ReduceOp.MIN, group=process_group)
+    if lam != 0.0:
+        eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
+    ll_off = int(eng.sizes.stats_ll_offset)
+    info = torch.cat([stats[ll_off:ll_off + 2], status.to(torch.float64)]).cpu().tolist()
+    engine._raise_words([int(v) for v in info[2:]], model.family)
+    if lam != 0.0:
+        model.params.mark_compute_current(eng)
+    return info[0] / info[1]
+
+
+def em_full_step(model: EinetModel, data, eps_w=engine.EPS_W, chunk=4096,
+                 process_group=None) -> float:
+    """Full-batch EM update == a lam = 1 stochastic step on all data."""
+    return em_stochastic_step(model, data, lam=1.0, eps_w=eps_w, chunk=chunk,
+                              process_group=process_group)
+
+
+def _check_finite(model, epoch, batch_idx):
+    if not bool(torch.isfinite(model.params.flat).all()):
+        raise TrainingDiverged(
+            f"non-finite parameters after epoch {epoch}, batch {batch_idx}")
+
+
+def train(model: EinetModel, data, cfg: TrainerConfig, valid=None) -> list:
+    """Seeded epoch loop (reference ``trainer.py:137-162``); the dataset is
+    uploaded once and batches are gathered on the device."""
+    host = np.atleast_2d(np.asarray(data, dtype=np.float64))
+    if len(host) == 0:
+        raise ValueError("training dataset is empty")
+    xd = engine.as_device_batch(host)
+    vd = None if valid is None else engine.as_device_batch(valid)
+    rng = np.random.default_rng(cfg.seed)
+    metrics = []
+    for epoch in range(cfg.epochs):
+        t0 = time.perf_counter()
+        if cfg.mode == "full":
+            em_full_step(model, xd, eps_w=cfg.eps_w, chunk=cfg.chunk)
+            _check_finite(model, epoch, 0)
+        else:
+            order = torch.from_numpy(rng.permutation(len(host))).to(xd.device)
+            for bi, lo in enumerate(range(0, len(host), cfg.batch_size)):
+                em_stochastic_step(model, xd.index_select(0, order[lo:lo + cfg.batch_size]),
+                                   cfg.step_size, eps_w=cfg.eps_w, chunk=cfg.chunk)
+                _check_finite(model, epoch, bi)
+        train_ll = model.mean_log_likelihood(xd)
+        valid_ll = model.mean_log_likelihood(vd) if vd is not None else float("nan")
+        metrics.append(EpochMetrics(epoch=epoch, train_ll=train_ll, valid_ll=valid_ll,
+                                    wall_seconds=time.perf_counter() - t0))
+    return metrics

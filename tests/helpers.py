@@ -1,0 +1,70 @@
+"""Shared loaders for the golden fixtures (CPU and GPU tests)."""
+
+import json
+import os
+
+import numpy as np
+
+from paper_2004_06231_b200.compiler import compile_graph
+from paper_2004_06231_b200.expfam import ExponentialFamily
+from paper_2004_06231_b200.structures import RegionGraph
+
+from oracle import einet_oracle as O
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+CASES = ["c1_rat_categorical", "rat_gaussian", "rat_gaussian_masked", "rat_gaussian_kroot3",
+         "pd_lift_gaussian_image", "rat_binomial", "rat_categorical4", "c2_mnist_pd",
+         "c3_svhn_pd"]
+
+
+class Case:
+    def __init__(self, name):
+        self.name = name
+        self.z = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+        z = self.z
+        self.rg = RegionGraph.from_json(str(z["rg_json"]))
+        self.k = int(z["k"])
+        self.k_root = int(z["k_root"])
+        self.circuit = compile_graph(self.rg, self.k, self.k_root)
+        self.fam_doc = json.loads(str(z["family_json"]))
+        self.family = ExponentialFamily.from_dict(self.fam_doc)
+        self.x = z["x"]
+        self.mask = z.get("mask")
+        self.full = bool(z["full"])
+        self.lam = float(z["lam"])
+
+    def params(self, prefix="init"):
+        ein = {i: self.z[f"{prefix}_einsum_{i}"] for i in self.einsum_layers()}
+        mix = {i: self.z[f"{prefix}_mixing_{i}"] for i in self.mixing_layers()}
+        return O.OracleParams(ein, mix, self.z[f"{prefix}_phi"])
+
+    def einsum_layers(self):
+        return [i for i, l in enumerate(self.circuit.layers) if type(l).__name__ == "EinsumLayer"]
+
+    def mixing_layers(self):
+        return [i for i, l in enumerate(self.circuit.layers) if type(l).__name__ == "MixingLayer"]
+
+    def steps(self):
+        return len(self.z.get("step_mean_ll", []))
+
+
+def summarize(a):
+    a = np.asarray(a)
+    flat = a.reshape(a.shape[0], -1) if a.ndim > 1 else a[:, None]
+    return np.concatenate([flat.sum(axis=1), flat[:, :8].ravel(), [a.sum(), (a * a).sum()]])
+
+
+def close(a, b, rtol, atol):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    both_inf = np.isinf(a) & np.isinf(b) & (np.sign(a) == np.sign(b))
+    with np.errstate(invalid="ignore"):
+        err = np.where(both_inf, 0.0, np.abs(a - b))
+    bound = atol + rtol * np.abs(b)
+    bad = ~(err <= bound)
+    if bad.any():
+        i = np.unravel_index(np.argmax(np.where(bad, err / np.maximum(bound, 1e-300), 0)), a.shape)
+        raise AssertionError(f"{bad.sum()} of {a.size} entries differ; worst at {i}: "
+                             f"got {a[i]!r} want {b[i]!r} (rtol {rtol}, atol {atol})")
