@@ -1,0 +1,391 @@
+"""EM-step throughput of the SVHN-shaped Poon-Domingos EiNet (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one em_stochastic_step (forward + responsibility back-pass over the
+rank's batch shard, one NCCL all-reduce of the packed fp64 statistics when
+N > 1, fused M-step) -- the reference ``trainer.em_stochastic_step``
+(trainer.py:99-117) on the GPU. Workload: config C3 of BASELINE.json
+(32x32x3 lifted PD, delta 8 vertical, K=40, Gaussian image-mode leaves),
+synthetic image data, a fixed per-GPU batch (weak scaling). Inputs are larger
+than L2 (16384 x 3072 fp32 = 201 MB > 126 MB), so no flush is needed.
+
+``--impl reference`` times the CPU restatement of the reference's EM step
+(oracle/einet_oracle.py; the Python reference itself cannot travel to the GPU
+box) on all host cores with a bounded sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EM-step samples/s, SVHN-shape PD EiNet K=40"
+UNIT = "samples/s"
+CONFIG = "C3"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=16384, help="samples per GPU per step")
+    ap.add_argument("--chunk", type=int, default=16384)
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=96,
+                    help="samples per oracle EM step for the CPU legs")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi samples of SM clock and throttle reasons during a region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for n, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per sample, per kernel class
+# ---------------------------------------------------------------------------
+
+def work_per_sample(circuit):
+    """Algorithmic flops and HBM bytes per sample for each kernel class."""
+    k = circuit.k
+    d, r = circuit.d_vars, circuit.num_replicas
+    ein = 0
+    for layer in circuit.layers[1:]:
+        if type(layer).__name__ == "EinsumLayer":
+            ein += len(layer.left_src) * layer.k_out * k * k
+    leaf_elems = d * k * r
+    return {
+        # 2 FMA per (var, k): (x*sa + nmsa)^2 accumulated; x read once
+        "leaf_fwd": {"flops": 4 * leaf_elems, "bytes": 4 * d},
+        "einsum_fwd": {"flops": 2 * ein, "bytes": 0},
+        "einsum_wstats": {"flops": 2 * ein, "bytes": 0},
+        "einsum_childrho": {"flops": 4 * ein, "bytes": 0},
+        # rho*y and rho*y^2 per (var, k); x read once
+        "leaf_stats": {"flops": 4 * leaf_elems, "bytes": 4 * d},
+    }
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            doc = json.load(f)
+        return doc.get("hbm_gbs", 6650.0), doc.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port of the reference EM step)
+# ---------------------------------------------------------------------------
+
+def _oracle_setup(config, n, seed):
+    from paper_2004_06231_b200 import engine
+    from paper_2004_06231_b200.compiler import compile_graph
+    from paper_2004_06231_b200.data import config as cfg
+    from oracle import einet_oracle as O
+    rg, fam, k, gen = cfg(config)
+    circuit = compile_graph(rg, k)
+    x = gen(n, seed=seed).astype(np.float32).astype(np.float64)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=x)
+    return circuit, fam.to_dict(), x, O.OracleParams(ein, mix, phi)
+
+
+def _oracle_shard(args):
+    config, n, seed, lo, hi = args
+    from oracle import einet_oracle as O
+    circuit, fam, x, p = _oracle_setup(config, n, seed)
+    tr = O.forward(circuit, p, fam, x[lo:hi])
+    return O.backward(circuit, p, fam, tr)
+
+
+def cpu_reference_steps(config, n, steps, warmup, procs):
+    """Reference EM step (trainer.py:99-117) restated in oracle/, sharded over
+    `procs` worker processes (merge = sum, engine.py:228-236)."""
+    import multiprocessing as mp
+    from oracle import einet_oracle as O
+    circuit, fam, x, p = _oracle_setup(config, n, 0)
+    bounds = np.linspace(0, n, procs + 1).astype(int)
+    jobs = [(config, n, 0, int(bounds[i]), int(bounds[i + 1])) for i in range(procs)
+            if bounds[i + 1] > bounds[i]]
+    times = []
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(jobs)) as pool:
+        for it in range(warmup + steps):
+            t0 = time.perf_counter()
+            parts = pool.map(_oracle_shard, jobs) if len(jobs) > 1 else [_oracle_shard(jobs[0])]
+            st = parts[0]
+            for q in parts[1:]:
+                st.merge(q)
+            O.apply_update(circuit, p, fam, st, 0.5)
+            dt = time.perf_counter() - t0
+            if it >= warmup:
+                times.append(dt)
+    return times
+
+
+def cpu_baseline(config, n):
+    """Single-core oracle EM step on a bounded sample (~10-30 s of CPU work)."""
+    from oracle import einet_oracle as O
+    circuit, fam, x, p = _oracle_setup(config, n, 0)
+    t0 = time.perf_counter()
+    O.em_step(circuit, p, fam, x, 0.5)
+    first = time.perf_counter() - t0
+    reps = max(1, min(5, int(15.0 / max(first, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        O.em_step(circuit, p, fam, x, 0.5)
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{reps}+1 oracle EM steps of {n} {config} samples (numpy fp64, "
+                      f"oracle/einet_oracle.py), {dt:.2f} s per step"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    procs = max(1, len(os.sched_getaffinity(0)))
+    n = max(procs, args.cpu_sample)
+    steps, warmup = max(1, min(args.steps, 3)), min(args.warmup, 1)
+    times = cpu_reference_steps(args.config, n, steps, warmup, procs)
+    sec = statistics.median(times)
+    value = n / sec
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": len(times), "warmup": warmup, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} SVHN-shape 32x32x3 PD EiNet K=40, "
+                                   f"delta 8 vertical, Gaussian leaves, EM lambda 0.5",
+                       "batch_per_step": n, "procs": procs},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                             "sample": f"{n} samples per EM step, sharded over {procs} "
+                                       f"processes (oracle/einet_oracle.py)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2004_06231_b200 import _native, engine, trainer
+    from paper_2004_06231_b200.compiler import compile_graph
+    from paper_2004_06231_b200.data import config as cfg
+    from paper_2004_06231_b200.model import EinetModel
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    dev = torch.device("cuda", local)
+
+    rg, fam, k, gen = cfg(args.config)
+    circuit = compile_graph(rg, k)
+    B = args.batch
+    x_host = torch.from_numpy(gen(B, seed=1000 + rank).astype(np.float32)).pin_memory()
+    x_dev = x_host.to(dev)
+    init_x = gen(4096, seed=7).astype(np.float32).astype(np.float64)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=init_x)
+    params = engine.Parameters.from_numpy(circuit, fam, ein, mix, phi, device=dev)
+    model = EinetModel(circuit, params, fam)
+
+    def step(x):
+        return trainer.em_stochastic_step(model, x, 0.5, chunk=args.chunk,
+                                          process_group=group)
+
+    for _ in range(args.warmup):
+        step(x_dev)
+    torch.cuda.synchronize()
+
+    def timed(fn, k):
+        if group is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(k):
+            fn()
+        stop.record()
+        torch.cuda.synchronize()
+        if group is not None:
+            dist.barrier()
+        ms = torch.tensor([start.elapsed_time(stop)], dtype=torch.float64, device=dev)
+        if group is not None:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
+    launches0 = _native.launch_count()
+    with ClockSampler(local) as clocks:
+        ms = timed(lambda: step(x_dev), args.steps)
+    launches = (_native.launch_count() - launches0) // args.steps
+
+    # end to end: pinned host batch -> device each step, mean LL read back
+    ms_e2e = timed(lambda: step(x_host.to(dev, non_blocking=True)), max(3, args.steps // 2))
+    e2e_steps = max(3, args.steps // 2)
+
+    # per-kernel-class device time of the same step (CUDA events, separate pass)
+    _native.profile_enable(True)
+    prof_steps = 3
+    for _ in range(prof_steps):
+        step(x_dev)
+    torch.cuda.synchronize()
+    prof = _native.profile_read()
+    _native.profile_enable(False)
+
+    if rank != 0:
+        if group is not None:
+            dist.destroy_process_group()
+        return
+
+    value = world * B * args.steps / (ms / 1e3)
+    e2e = world * B * e2e_steps / (ms_e2e / 1e3)
+    hbm, bf16, peak_kind = load_peaks()
+    work = work_per_sample(circuit)
+    classes = {}
+    for name, (tot_ms, cnt) in prof.items():
+        per_step = tot_ms / prof_steps
+        w = work.get(name, {"flops": 0, "bytes": 0})
+        classes[name] = {"ms_per_step": per_step, "launch_groups_per_step": cnt / prof_steps,
+                         "share": None,
+                         "tflops": w["flops"] * B / (per_step / 1e3) / 1e12 if w["flops"] else None,
+                         "gbs": w["bytes"] * B / (per_step / 1e3) / 1e9 if w["bytes"] else None}
+    total_prof = sum(c["ms_per_step"] for n, c in classes.items() if n not in ("prepare",))
+    for c in classes.values():
+        c["share"] = c["ms_per_step"] / total_prof if total_prof else None
+    top = max((n for n in classes if n in work), key=lambda n: classes[n]["ms_per_step"])
+    tw = work[top]
+    per_launch_ms = prof[top][0] / prof[top][1]
+    groups = prof[top][1] / prof_steps
+    if top.startswith("einsum"):
+        achieved = tw["flops"] * B / groups / (per_launch_ms / 1e3) / 1e12
+        roof = {"kernel": top, "bound": "tensor", "achieved": achieved, "peak": bf16,
+                "unit": "TFLOP/s", "frac": achieved / bf16,
+                "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json)"}
+    else:
+        achieved = tw["bytes"] * B / groups / (per_launch_ms / 1e3) / 1e9
+        roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
+    roof["traffic"] = None
+    roof["per_launch_ms"] = per_launch_ms
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args.config, args.cpu_sample)
+        except Exception as exc:  # reported, never fatal for the GPU number
+            cpu = {"value": None, "error": repr(exc)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 stats/M-step)",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config} SVHN-shape 32x32x3 PD EiNet K=40, delta 8 "
+                               f"vertical, Gaussian image-mode leaves, EM lambda 0.5",
+                   "batch_per_gpu": B, "global_batch": B * world, "chunk": args.chunk,
+                   "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (B*3072*4 bytes per GPU > 126 MB)"},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(B * rg.d_vars * 4),
+                "d2h_bytes_per_step": 48},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "kernels": classes,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

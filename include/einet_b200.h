@@ -169,6 +169,14 @@ int einet_log_einsum_exp(const double *left, const double *right, const double *
 /* Number of kernels this library has launched in this process. */
 int64_t einet_launch_count(void);
 
+/* Per-kernel-class CUDA-event timing of this library's launches (bench.py).
+ * enable(1) clears and starts recording; query(i) returns class i's name,
+ * summed device milliseconds and launch-group count (EINET_ERR_USAGE past the
+ * last class). */
+int einet_profile_enable(int on);
+int einet_profile_query(int32_t index, char *name, int32_t name_len, double *total_ms,
+                        int64_t *count);
+
 /* Message of the last failing call on this thread (never NULL). */
 const char *einet_last_error(void);
 

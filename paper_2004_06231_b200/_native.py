@@ -75,6 +75,9 @@ EXPORTS = {
     "einet_log_einsum_exp": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                        c_int32, c_int32, c_void_p, c_void_p]),
     "einet_launch_count": (c_int64, []),
+    "einet_profile_enable": (c_int32, [c_int32]),
+    "einet_profile_query": (c_int32, [c_int32, ctypes.c_char_p, c_int32,
+                                      POINTER(c_double), POINTER(c_int64)]),
     "einet_last_error": (ctypes.c_char_p, []),
 }
 
@@ -132,3 +135,23 @@ def check(rc: int, what: str):
 
 def launch_count() -> int:
     return int(load().einet_launch_count())
+
+
+def profile_enable(on: bool = True):
+    load().einet_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kernel class: (total device ms, launch groups)} since profile_enable."""
+    lib = load()
+    out = {}
+    i = 0
+    name = ctypes.create_string_buffer(64)
+    while True:
+        ms = c_double()
+        cnt = c_int64()
+        if lib.einet_profile_query(i, name, 64, ctypes.byref(ms), ctypes.byref(cnt)) != OK:
+            break
+        out[name.value.decode()] = (ms.value, cnt.value)
+        i += 1
+    return out

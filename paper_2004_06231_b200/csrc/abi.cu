@@ -31,6 +31,30 @@ int check_cuda(cudaError_t err, const char *what) {
 }
 void count_launch(int n) { g_launches += n; }
 
+static bool g_profiling = false;
+struct ProfClass {
+  std::string name;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+};
+static std::vector<ProfClass> g_prof;
+bool profiling_enabled() { return g_profiling; }
+void profile_record(const char *name, cudaEvent_t start, cudaEvent_t stop) {
+  for (auto &c : g_prof)
+    if (c.name == name) {
+      c.events.emplace_back(start, stop);
+      return;
+    }
+  g_prof.push_back(ProfClass{name, {{start, stop}}});
+}
+static void profile_clear() {
+  for (auto &c : g_prof)
+    for (auto &e : c.events) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  g_prof.clear();
+}
+
 template <typename T>
 static int upload(T **dst, const std::vector<T> &src) {
   *dst = nullptr;
@@ -477,6 +501,33 @@ int einet_log_einsum_exp(const double *left, const double *right, const double *
 }
 
 int64_t einet_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int einet_profile_enable(int on) {
+  cudaDeviceSynchronize();
+  profile_clear();
+  g_profiling = on != 0;
+  return EINET_OK;
+}
+
+int einet_profile_query(int32_t index, char *name, int32_t name_len, double *total_ms,
+                        int64_t *count) {
+  if (index < 0 || index >= (int)g_prof.size()) return EINET_ERR_USAGE;
+  ProfClass &c = g_prof[index];
+  double tot = 0.0;
+  for (auto &e : c.events) {
+    cudaEventSynchronize(e.second);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.first, e.second);
+    tot += ms;
+  }
+  if (name && name_len > 0) {
+    std::strncpy(name, c.name.c_str(), name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (total_ms) *total_ms = tot;
+  if (count) *count = (int64_t)c.events.size();
+  return EINET_OK;
+}
 
 const char *einet_last_error(void) { return g_last_error.c_str(); }
 

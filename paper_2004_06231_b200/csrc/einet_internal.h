@@ -91,6 +91,30 @@ int fail(int code, const std::string &msg);
 int check_cuda(cudaError_t err, const char *what);
 void count_launch(int n = 1);
 
+// Optional per-kernel-class CUDA-event timing (einet_profile_*). When enabled,
+// a ProfScope records an event pair on the launching stream around a group of
+// launches; einet_profile_query sums the elapsed times per class.
+bool profiling_enabled();
+void profile_record(const char *name, cudaEvent_t start, cudaEvent_t stop);
+struct ProfScope {
+  const char *name;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(const char *n, cudaStream_t s) : name(n), st(s) {
+    if (profiling_enabled()) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEventRecord(b, st);
+      profile_record(name, a, b);
+    }
+  }
+};
+
 // ---- launchers (implemented in the .cu files) -------------------------------
 int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_t *mask,
                    const double *leaf_offset, cudaStream_t st);

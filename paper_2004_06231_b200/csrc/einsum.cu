@@ -553,11 +553,13 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
   if (rc) return rc;
   for (const LayerPlan &L : p.layers) {
     if (L.kind == EINET_LAYER_EINSUM) {
+      ProfScope prof("einsum_fwd", st);
       bool handled = false;
       rc = launch_einsum_tc_forward(p, L, c.w32, w, B, status, st, &handled);
       if (rc) return rc;
       if (!handled) einsum_forward_simt(L, c.w32, w, B, p.k, status, st);
     } else {
+      ProfScope prof("mixing_fwd", st);
       dim3 grid(ceil_div(B, 128), L.rows);
       k_mixing_fwd<<<grid, 128, 0, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
                                          c.mix32 + L.mix_off, B, L.k_out, L.dmax, L.index,
@@ -586,6 +588,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   const int K = p.k;
   // log-likelihood sum of the batch (root entry 0) and the sample count
   {
+    ProfScope prof("ll_sum", st);
     const int nb = ceil_div(B, 256);
     k_ll_partial<<<nb, 256, 0, st>>>(w, p.root_out_slab, B, w.llpart);
     k_ll_finish<<<1, 1, 0, st>>>(w.llpart, nb, stats + p.sizes.stats_ll_offset, (double)B);
@@ -594,6 +597,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   for (int li = (int)p.layers.size() - 1; li >= 0; --li) {
     const LayerPlan &L = p.layers[li];
     if (L.kind == EINET_LAYER_MIXING) {
+      ProfScope prof("mixing_bwd", st);
       const int nb = ceil_div(B, 64);
       dim3 grid(nb, L.rows);
       k_mixing_bwd<<<grid, 64, 0, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
@@ -605,10 +609,15 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
       count_launch();
       continue;
     }
+    {
+    ProfScope prof("einsum_bwd_prep", st);
     dim3 g1(ceil_div(B, 128), L.rows);
     k_einsum_bwd_prep<<<g1, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
                                           p.d_csr_off, p.d_csr_slot, p.d_slab_ones, B, K,
                                           L.k_out, w.ea, w.eb, w.rt);
+    }
+    {
+    ProfScope prof("einsum_wstats", st);
     const int bs = wstats_bsplit(p, L, B);
     const int K4 = (K + 3) / 4;
     const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT);
@@ -617,7 +626,11 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
                                                L.rows, bs, w.wpart);
     const int64_t lw = (int64_t)L.rows * L.k_out * K * K;
     launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);
+    }
+    {
+    ProfScope prof("einsum_childrho", st);
     einsum_childrho(L, c.w32, w, B, K, st);
+    }
     count_launch(3);
   }
   int rc = launch_leaf_backward(p, compute, x, B, wsb, stats, st);

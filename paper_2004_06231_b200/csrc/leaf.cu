@@ -122,6 +122,7 @@ __global__ void k_prepare_const(const double *__restrict__ phi, const uint8_t *a
 
 int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_t *mask,
                    const double *leaf_offset, cudaStream_t st) {
+  ProfScope prof("prepare", st);
   CompView c = comp_view(p, compute);
   const int D = p.d_vars, K = p.k, R = p.num_replicas;
   const double *phi = params + p.sizes.phi_offset;
@@ -352,6 +353,7 @@ static int leaf_dsplit(const Plan &p, int64_t B, int tb) {
 
 int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
                         uint8_t *wsb, int32_t *status, cudaStream_t st) {
+  ProfScope prof("leaf_fwd", st);
   CompView c = comp_view(p, compute);
   WsView w = ws_view(p, wsb);
   const int KG = ceil_div(p.k, LF_KPT);
@@ -566,10 +568,14 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
   WsView w = ws_view(p, wsb);
   const int K = p.k, D = p.d_vars, R = p.num_replicas, T = p.suff;
   const int nb = ceil_div(B, 128);
+  {
+  ProfScope prof("leaf_rho", st);
   k_leaf_rho<<<dim3(nb, p.n_leaf), 128, 0, st>>>(w, p.d_csr_off, p.d_csr_slot, p.d_slab_ones,
                                                  p.d_leaf_slab, B, K, p.n_leaf, w.ppart);
   launch_reduce_partials(stats + p.sizes.stats_p_offset, w.ppart, nb, (int64_t)p.n_leaf * K,
                          (int64_t)p.n_leaf * K, nullptr, st);
+  }
+  ProfScope prof("leaf_stats", st);
   const int ls = leaf_lsplit(p, B);
   const int64_t n_phi = p.n_phi;
   cudaMemsetAsync(w.lspart, 0, sizeof(double) * n_phi * ls, st);

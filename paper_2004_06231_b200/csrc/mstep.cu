@@ -151,6 +151,7 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
   CompView c = comp_view(p, compute);
   const int K = p.k;
   const int KK = K * K;
+  ProfScope prof("mstep", st);
   if (p.n_w) {
     const int nslices = (int)(p.n_w / KK);
     k_mstep_einsum<<<nslices, 256, 0, st>>>(params, c.w32, stats, KK, lam, eps_w, status);

@@ -1,0 +1,308 @@
+"""CUDA engine vs the reference (golden vectors) and the CPU oracle.
+
+Tolerances (north star, BASELINE.json): per-sample log-likelihoods within
+1e-4 relative (|d| <= 1e-4 * max(|LL|, 1)), backward statistics
+rtol 1e-4 + atol 1e-6 * B, EM-updated parameters rtol 1e-4 (W with atol 1e-9
+for the 1e-12 floor). The device computes in fp32 with fp64 statistics, fp64
+master parameters and an fp64 M-step.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2004_06231_b200 as E
+from paper_2004_06231_b200 import _native, engine, trainer
+from paper_2004_06231_b200.data import config
+from paper_2004_06231_b200.structures import StructureConfig, random_binary_tree
+
+from oracle import einet_oracle as O
+from tests.helpers import CASES, Case, close, summarize
+
+pytestmark = pytest.mark.gpu
+
+LL_RTOL = 1e-4
+P_RTOL = 1e-4
+
+
+def device_params(case, prefix="init"):
+    p = case.params(prefix)
+    return engine.Parameters.from_numpy(case.circuit, case.family, p.einsum, p.mixing, p.phi)
+
+
+def ll_close(got, want):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    fin = np.isfinite(want)
+    assert np.array_equal(np.isfinite(got), fin)
+    err = np.abs(got[fin] - want[fin])
+    bound = LL_RTOL * np.maximum(np.abs(want[fin]), 1.0)
+    assert (err <= bound).all(), (err / bound).max()
+
+
+def stats_close(case, st, B):
+    atol = 1e-6 * B
+    for i in case.einsum_layers():
+        want = case.z[f"stats_einsum_{i}"]
+        got = st.einsum[i]
+        if not case.full:
+            got = summarize(got)
+        close(got, want, P_RTOL, atol)
+    for i in case.mixing_layers():
+        close(st.mixing[i], case.z[f"stats_mixing_{i}"], P_RTOL, atol)
+    for key, got in (("stats_acc_p", st.acc_p), ("stats_acc_pt", st.acc_pt)):
+        if not case.full:
+            got = summarize(got)
+        close(got, case.z[key], P_RTOL, atol)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_forward_matches_reference(name):
+    case = Case(name)
+    if case.full:
+        p = device_params(case)
+    else:
+        ein, mix, phi = engine.init_parameters_host(case.circuit, case.family, 0, case.x)
+        f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+        p = engine.Parameters.from_numpy(case.circuit, case.family,
+                                         {i: f32(w) for i, w in ein.items()},
+                                         {i: f32(w) for i, w in mix.items()}, f32(phi))
+    tr = engine.forward(case.circuit, p, case.family, case.x, marg_mask=case.mask)
+    ll_close(tr.root, case.z["root"])
+    st = engine.backward(case.circuit, p, case.family, tr)
+    stats_close(case, st, len(case.x))
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if c not in
+                                  ("rat_gaussian_masked", "rat_gaussian_kroot3")])
+def test_em_steps_match_reference(name):
+    case = Case(name)
+    if case.full:
+        p = device_params(case)
+    else:
+        ein, mix, phi = engine.init_parameters_host(case.circuit, case.family, 0, case.x)
+        f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+        p = engine.Parameters.from_numpy(case.circuit, case.family,
+                                         {i: f32(w) for i, w in ein.items()},
+                                         {i: f32(w) for i, w in mix.items()}, f32(phi))
+    model = E.EinetModel(case.circuit, p, case.family)
+    for s in range(case.steps()):
+        ll = trainer.em_stochastic_step(model, case.x, case.lam, chunk=10 if
+                                        name == "rat_categorical4" else 4096)
+        want_ll = case.z["step_mean_ll"][s]
+        assert abs(ll - want_ll) <= LL_RTOL * max(abs(want_ll), 1.0)
+        ein, mix, phi = p.to_numpy()
+        for i, w in ein.items():
+            want = case.z[f"step{s + 1}_einsum_{i}"]
+            close(w if case.full else summarize(w), want, P_RTOL, 1e-9)
+        for i, w in mix.items():
+            close(w, case.z[f"step{s + 1}_mixing_{i}"], P_RTOL, 1e-9)
+        close(phi if case.full else summarize(phi), case.z[f"step{s + 1}_phi"], P_RTOL, 1e-9)
+
+
+def _random_model(seed, family_kind="gaussian"):
+    rng = np.random.default_rng(seed)
+    d = int(rng.integers(2, 9))
+    depth = int(rng.integers(1, min(3, int(np.floor(np.log2(d)))) + 1))
+    rg = random_binary_tree(d, StructureConfig(depth=depth, replicas=int(rng.integers(1, 4)),
+                                               seed=int(rng.integers(1 << 30))))
+    k = int(rng.integers(1, 6))
+    if family_kind == "gaussian":
+        fam = E.GaussianFamily()
+        data = rng.normal(size=(16, d))
+    else:
+        fam = E.CategoricalFamily(int(rng.integers(2, 5)))
+        data = rng.integers(0, fam.num_states, size=(16, d)).astype(float)
+    data = data.astype(np.float32).astype(np.float64)
+    circuit = E.compile_graph(rg, k)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=seed, data=data)
+    return circuit, fam, data, (ein, mix, phi)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_fixtures_vs_oracle(seed):
+    circuit, fam, data, (ein, mix, phi) = _random_model(seed, ["gaussian", "categorical"][seed % 2])
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    op = O.OracleParams({i: f32(w) for i, w in ein.items()}, {i: f32(w) for i, w in mix.items()},
+                        f32(phi))
+    p = engine.Parameters.from_numpy(circuit, fam, op.einsum, op.mixing, op.phi)
+    tr = engine.forward(circuit, p, fam, data)
+    otr = O.forward(circuit, op, fam.to_dict(), data)
+    ll_close(tr.log_likelihood, otr.log_likelihood)
+    st = engine.backward(circuit, p, fam, tr)
+    ost = O.backward(circuit, op, fam.to_dict(), otr)
+    for i in ost.einsum:
+        close(st.einsum[i], ost.einsum[i], P_RTOL, 1e-6 * len(data))
+    close(st.acc_p, ost.acc_p, P_RTOL, 1e-6 * len(data))
+    close(st.acc_pt, ost.acc_pt, P_RTOL, 1e-6 * len(data))
+
+
+def test_c3_full_batch_vs_oracle():
+    """The headline configuration at B=64 through the whole EM step."""
+    rg, fam, k, gen = config("C3")
+    circuit = E.compile_graph(rg, k)
+    x = gen(64, seed=5).astype(np.float32).astype(np.float64)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=x)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    op = O.OracleParams({i: f32(w) for i, w in ein.items()}, {i: f32(w) for i, w in mix.items()},
+                        f32(phi))
+    p = engine.Parameters.from_numpy(circuit, fam, op.einsum, op.mixing, op.phi)
+    model = E.EinetModel(circuit, p, fam)
+    for step in range(2):
+        want_ll, op = O.em_step(circuit, op, fam.to_dict(), x, 0.5)
+        ll = trainer.em_stochastic_step(model, x, 0.5)
+        assert abs(ll - want_ll) <= LL_RTOL * abs(want_ll)
+        e2, m2, phi2 = p.to_numpy()
+        for i in e2:
+            close(e2[i], op.einsum[i], P_RTOL, 1e-9)
+        close(phi2, op.phi, P_RTOL, 1e-9)
+
+
+# ---------------------------------------------------------------------------
+# reference properties (test_trainer.py, test_engine.py, test_acceptance.py)
+# ---------------------------------------------------------------------------
+
+def _gauss_model(seed=0, d=4, k=3, replicas=2, data=None):
+    rg = E.random_binary_tree(d, StructureConfig(depth=2, replicas=replicas, seed=seed))
+    return E.build_model(rg, E.GaussianFamily(), k=k, seed=seed + 1, data=data)
+
+
+def test_lambda_zero_is_bitwise_noop():
+    data = np.random.default_rng(1).normal(size=(50, 4))
+    m = _gauss_model(1, data=data)
+    before = m.params.flat.clone()
+    trainer.em_stochastic_step(m, data, lam=0.0)
+    assert torch.equal(before, m.params.flat)
+
+
+def test_lambda_one_equals_full_step_bitwise():
+    data = np.random.default_rng(2).normal(size=(80, 4))
+    a, b = _gauss_model(2, data=data), _gauss_model(2, data=data)
+    trainer.em_full_step(a, data)
+    trainer.em_stochastic_step(b, data, lam=1.0)
+    assert torch.equal(a.params.flat, b.params.flat)
+
+
+def test_training_is_deterministic():
+    data = np.random.default_rng(5).normal(size=(120, 4))
+    cfg = trainer.TrainerConfig(mode="stochastic", step_size=0.5, batch_size=40, epochs=3,
+                                seed=11)
+    a, b = _gauss_model(5, data=data), _gauss_model(5, data=data)
+    ma, mb = trainer.train(a, data, cfg), trainer.train(b, data, cfg)
+    assert [m.train_ll for m in ma] == [m.train_ll for m in mb]
+    assert torch.equal(a.params.flat, b.params.flat)
+
+
+def test_full_em_monotone():
+    rng = np.random.default_rng(3)
+    data = np.concatenate([rng.normal(-2, 0.5, (150, 4)), rng.normal(2, 0.5, (150, 4))])
+    m = _gauss_model(3, data=data)
+    lls = [trainer.em_full_step(m, data) for _ in range(30)]
+    lls.append(m.mean_log_likelihood(data))
+    assert np.all(np.diff(lls) >= -1e-4)
+
+
+def test_single_gaussian_one_step():
+    rng = np.random.default_rng(0)
+    data = rng.normal(2.0, 1.5, size=(200, 4))
+    rg = E.random_binary_tree(4, StructureConfig(depth=2, replicas=1, seed=0))
+    m = E.build_model(rg, E.GaussianFamily(), k=1, seed=1, data=data)
+    trainer.em_full_step(m, data)
+    phi = m.params.phi
+    mu = phi[:, 0, 0, 0]
+    var = phi[:, 0, 0, 1] - mu ** 2
+    x32 = data.astype(np.float32).astype(np.float64)
+    assert np.allclose(mu, x32.mean(axis=0), atol=1e-6)
+    assert np.allclose(var, x32.var(axis=0), rtol=1e-5)
+
+
+def test_chunked_equals_unchunked():
+    data = np.random.default_rng(7).normal(size=(300, 4))
+    a, b = _gauss_model(7, data=data), _gauss_model(7, data=data)
+    la = trainer.em_stochastic_step(a, data, 0.5, chunk=4096)
+    lb = trainer.em_stochastic_step(b, data, 0.5, chunk=64)
+    # fp32 partial sums restart per chunk; the fp64 merge itself is exact
+    assert abs(la - lb) <= 1e-7 * abs(la)
+    assert torch.allclose(a.params.flat, b.params.flat, rtol=1e-5, atol=1e-9)
+
+
+def test_all_marginalised_is_zero():
+    data = np.random.default_rng(8).normal(size=(6, 4))
+    m = _gauss_model(8, data=data)
+    ll = m.forward(data, marg_mask=np.ones(4, dtype=bool)).log_likelihood
+    assert np.max(np.abs(ll)) < 1e-6
+
+
+def test_categorical_normalises():
+    rg = E.random_binary_tree(6, StructureConfig(depth=2, replicas=2, seed=4))
+    fam = E.CategoricalFamily(2)
+    m = E.build_model(rg, fam, k=3, seed=4)
+    grid = np.array(np.meshgrid(*[[0, 1]] * 6)).reshape(6, -1).T.astype(float)
+    ll = m.log_likelihood(grid)
+    assert abs(np.exp(ll).sum() - 1.0) < 1e-5
+
+
+def test_root_responsibility_mass_is_batch():
+    data = np.random.default_rng(9).normal(size=(33, 4))
+    m = _gauss_model(9, data=data)
+    tr = m.forward(data)
+    st = E.backward(m.circuit, m.params, m.family, tr)
+    top = max(st.einsum)
+    assert abs(st.einsum[top].sum() - 33) < 1e-4
+    assert st.n_samples == 33
+
+
+def test_unsupported_values_raise():
+    m = _gauss_model(10, data=np.zeros((4, 4)))
+    x = np.zeros((3, 4))
+    x[1, 2] = np.nan
+    with pytest.raises(E.UnsupportedValueError, match="variable 2"):
+        m.forward(x)
+    before = m.params.flat.clone()
+    with pytest.raises(E.UnsupportedValueError):
+        trainer.em_stochastic_step(m, x, 0.5)
+    assert torch.equal(before, m.params.flat)
+    rg = E.random_binary_tree(3, StructureConfig(depth=1, replicas=2, seed=0))
+    mc = E.build_model(rg, E.CategoricalFamily(3), k=2, seed=1)
+    with pytest.raises(E.UnsupportedValueError, match="outside"):
+        mc.forward(np.array([[0.0, 3.0, 1.0]]))
+
+
+def test_shape_mismatch_raises():
+    m = _gauss_model(11, data=np.zeros((4, 4)))
+    with pytest.raises(E.EngineError):
+        m.forward(np.zeros((2, 5)))
+
+
+def test_log_einsum_exp_device_known_answers():
+    out = E.log_einsum_exp(np.zeros((1, 1)), np.zeros((1, 1)), np.ones((1, 1, 1, 1)))
+    assert abs(out[0, 0]) < 1e-15
+    w = np.full((1, 2, 2, 2), 0.25)
+    half = np.log(0.5) * np.ones((1, 2))
+    assert np.allclose(E.log_einsum_exp(half, half, w), np.log(0.25), atol=1e-12)
+    out = E.log_einsum_exp(np.array([[-np.inf, -np.inf]]), np.array([[0.0, 0.0]]),
+                           np.full((1, 1, 2, 2), 0.25))
+    assert np.isneginf(out).all()
+    left, right = np.array([[-1000.0, -1001.0]]), np.array([[-1000.0, -1000.0]])
+    want = O.log_einsum_exp(left, right, w)
+    assert np.allclose(E.log_einsum_exp(left, right, w), want, atol=1e-10)
+
+
+def test_ef_log_prob_matches_oracle():
+    rng = np.random.default_rng(12)
+    fam = E.GaussianFamily()
+    phi = fam.init_phi((5, 3, 2), rng)
+    x = rng.normal(size=(4, 5)).astype(np.float32).astype(np.float64)
+    mask = np.array([False, True, False, False, True])
+    e = E.ef_log_prob(fam, phi, x, marg_mask=mask)
+    assert np.all(e[:, 1] == 0.0) and np.all(e[:, 4] == 0.0)
+    for d in (0, 2, 3):
+        want = O.log_density(fam.to_dict(), phi[d], x[:, d])
+        assert np.allclose(e[:, d], want, rtol=1e-12)
+
+
+def test_launch_counter_moves():
+    before = _native.launch_count()
+    data = np.random.default_rng(13).normal(size=(8, 4))
+    _gauss_model(13, data=data).forward(data)
+    assert _native.launch_count() > before
