@@ -166,6 +166,11 @@ int einet_log_einsum_exp(const double *left, const double *right, const double *
                          int64_t batch, int32_t rows, int32_t k, int32_t k_out,
                          double *out, void *stream);
 
+/* Diagnostic: D[128 x N] = A[128 x K] B[N x K]^T (fp32, row-major, device) on
+ * one CTA with tcgen05 3xTF32 MMAs; validates the tensor-core plumbing. */
+int einet_selftest_tf32_gemm(const float *A, const float *B, float *D, int32_t N, int32_t K,
+                             void *stream);
+
 /* Number of kernels this library has launched in this process. */
 int64_t einet_launch_count(void);
 

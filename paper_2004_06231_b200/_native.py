@@ -74,6 +74,8 @@ EXPORTS = {
                                     c_void_p, c_void_p, c_void_p]),
     "einet_log_einsum_exp": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                        c_int32, c_int32, c_void_p, c_void_p]),
+    "einet_selftest_tf32_gemm": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32,
+                                           c_void_p]),
     "einet_launch_count": (c_int64, []),
     "einet_profile_enable": (c_int32, [c_int32]),
     "einet_profile_query": (c_int32, [c_int32, ctypes.c_char_p, c_int32,

@@ -500,6 +500,12 @@ int einet_log_einsum_exp(const double *left, const double *right, const double *
                                (cudaStream_t)stream);
 }
 
+int einet_selftest_tf32_gemm(const float *A, const float *B, float *D, int32_t N, int32_t K,
+                             void *stream) {
+  if (!A || !B || !D) return fail(EINET_ERR_USAGE, "null argument");
+  return launch_selftest_gemm(A, B, D, N, K, (cudaStream_t)stream);
+}
+
 int64_t einet_launch_count(void) { return (int64_t)g_launches.load(); }
 
 int einet_profile_enable(int on) {

@@ -134,6 +134,8 @@ int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
                        const uint8_t *mask, double *out, int32_t *status,
                        cudaStream_t st);
 int launch_status_reset(int32_t *status, cudaStream_t st);
+int launch_selftest_gemm(const float *A, const float *B, float *D, int N, int K,
+                         cudaStream_t st);
 int leaf_lsplit(const Plan &p, int64_t B);
 int launch_log_einsum_exp(const double *left, const double *right, const double *w,
                           int64_t B, int L, int K, int Ko, double *out, cudaStream_t st);

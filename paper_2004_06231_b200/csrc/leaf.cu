@@ -54,7 +54,6 @@ __global__ void k_prepare_gauss(const double *__restrict__ phi, const uint8_t *a
     float2 v = make_float2(0.f, 0.f);
     if (active[d]) v = make_float2((float)sa, (float)(-mu * sa));
     lp[e] = v;
-    center[e] = (float)mu;
   }
 }
 
@@ -97,27 +96,47 @@ __global__ void k_prepare_logh(double *logh, int n) {
                         lgamma((double)(n - x) + 1.0);
 }
 
-// per (leaf, k): sum over the unmasked scope of the k-only terms, in fp64
-__global__ void k_prepare_const(const double *__restrict__ phi, const uint8_t *active,
-                                const double *leaf_offset, const int *scope_off,
-                                const int *scope_vars, const int *leaf_rep, double *cnst,
-                                int D, int K, int R, int family) {
-  const int leaf = blockIdx.x;
+// per (leaf, k): sum over the unmasked scope of the k-only terms, in fp64.
+// grid (n_leaf, K), block 256: strided partial sums + fixed-order tree.
+__global__ void __launch_bounds__(256) k_prepare_const(
+    const double *__restrict__ phi, const uint8_t *active, const double *leaf_offset,
+    const int *scope_off, const int *scope_vars, const int *leaf_rep, double *cnst, int D,
+    int K, int R, int family) {
+  __shared__ double red[8];
+  const int leaf = blockIdx.x, k = blockIdx.y;
   const int r = leaf_rep[leaf];
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    double acc = 0.0;
-    for (int q = scope_off[leaf]; q < scope_off[leaf + 1]; ++q) {
-      int d = scope_vars[q];
-      if (!active[d]) continue;
-      int64_t base = ((int64_t)d * K + k) * R + r;
-      if (family == EINET_FAMILY_GAUSSIAN) {
-        double mu = phi[base * 2], var = phi[base * 2 + 1] - mu * mu;
-        acc += -0.5 * (kLog2Pi + log(var));
-      }
-      if (leaf_offset) acc += leaf_offset[base];
+  double acc = 0.0;
+  for (int q = scope_off[leaf] + threadIdx.x; q < scope_off[leaf + 1]; q += 256) {
+    const int d = scope_vars[q];
+    if (!active[d]) continue;
+    const int64_t base = ((int64_t)d * K + k) * R + r;
+    if (family == EINET_FAMILY_GAUSSIAN) {
+      const double mu = phi[base * 2], var = phi[base * 2 + 1] - mu * mu;
+      acc += -0.5 * (kLog2Pi + log(var));
     }
-    cnst[leaf * K + k] = acc;
+    if (leaf_offset) acc += leaf_offset[base];
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    cnst[leaf * K + k] = s;
+  }
+}
+
+// Gaussian statistics centre per (r, d): mean over k of the component means.
+// Centring the fp32 batch partial sums keeps E[x^2] - E[x]^2 well conditioned.
+__global__ void k_prepare_center(const double *__restrict__ phi, float *center, int D, int K,
+                                 int R) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)R * D) return;
+  const int d = (int)(e % D), r = (int)(e / D);
+  double s = 0.0;
+  for (int k = 0; k < K; ++k) s += phi[(((int64_t)d * K + k) * R + r) * 2];
+  center[e] = (float)(s / K);
 }
 
 int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_t *mask,
@@ -143,9 +162,13 @@ int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_
     k_prepare_logh<<<ceil_div(p.n_trials + 1, 256), 256, 0, st>>>(c.logh, p.n_trials);
     count_launch();
   }
-  k_prepare_const<<<p.n_leaf, 64, 0, st>>>(phi, c.active, leaf_offset, p.d_scope_off,
-                                           p.d_scope_vars, p.d_leaf_rep, c.cnst, D, K, R,
-                                           p.family);
+  k_prepare_const<<<dim3(p.n_leaf, K), 256, 0, st>>>(phi, c.active, leaf_offset,
+                                                     p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
+                                                     c.cnst, D, K, R, p.family);
+  if (p.family == EINET_FAMILY_GAUSSIAN) {
+    k_prepare_center<<<ceil_div((int64_t)R * D, 256), 256, 0, st>>>(phi, c.center, D, K, R);
+    count_launch();
+  }
   count_launch((p.n_w ? 1 : 0) + (p.n_mix ? 1 : 0) + 3);
   return check_cuda(cudaGetLastError(), "prepare kernels");
 }
@@ -154,8 +177,24 @@ int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_
 // leaf forward
 // ---------------------------------------------------------------------------
 
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 // Gaussian: Q[b,l,k] = sum_{d in scope} (x_bd*sa_dk + nmsa_dk)^2 (fp32 chunks -> fp64).
-// grid (ceil(B/128), n_leaf, dsplit), block 32*KG threads (KG = ceil(K/8)).
+// grid (ceil(B/128), n_leaf, dsplit*nkc), block 32*KG threads (KG = ceil(K/8) <= 8).
+// Chunks of 32 scope variables are gathered with cp.async into a double buffer
+// so the next chunk's loads overlap the current chunk's FFMAs.
 __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
     const float *__restrict__ x, int64_t B, int D, int K, int R,
     const int *__restrict__ scope_off, const int *__restrict__ scope_vars,
@@ -165,9 +204,9 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int KG = blockDim.x / 32;
   const int KP = KG * LF_KPT;
-  float *xs = (float *)smem_raw;                               // [VC][TB+1]
-  float2 *ps = (float2 *)(xs + LF_VC * (LF_TB + 1) + 1);       // [VC][KP] (8B aligned)
-  ps = (float2 *)(((uintptr_t)ps + 15) & ~(uintptr_t)15);
+  constexpr int XS = LF_VC * (LF_TB + 1);                      // floats per x buffer
+  float *xs = (float *)smem_raw;                               // [2][VC][TB+1]
+  float2 *ps = (float2 *)(smem_raw + ((2 * XS * 4 + 15) & ~15));  // [2][VC][KP]
   const int nkc = gridDim.z / dsplit;  // k chunks of KP entries
   const int leaf = blockIdx.y, split = blockIdx.z / nkc;
   const int kbase = (blockIdx.z % nkc) * KP;
@@ -177,6 +216,49 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
   const int vbeg = split * per, vend = min(slen, vbeg + per);
   const int r = leaf_rep[leaf];
   const int64_t b0 = (int64_t)blockIdx.x * LF_TB;
+  const int nbl = (int)min((int64_t)LF_TB, B - b0);
+
+  // thread -> (variable lane, sample rows) of the gather; fixed across chunks
+  auto stage = [&](int buf, int c0) {
+    const int nv = min(LF_VC, vend - c0);
+    float *xb = xs + buf * XS;
+    const int v = lane;
+    if (v < nv) {
+      const int d = scope_vars[sbeg + c0 + v];
+      const float *src = x + b0 * D + d;
+      for (int bl = kq; bl < LF_TB; bl += KG) {
+        if (bl < nbl) cp_async4(xb + v * (LF_TB + 1) + bl, src + (int64_t)bl * D);
+        else xb[v * (LF_TB + 1) + bl] = 0.f;
+      }
+    } else {
+      for (int bl = kq; bl < LF_TB; bl += KG) xb[v * (LF_TB + 1) + bl] = 0.f;
+    }
+    float2 *pb = ps + buf * LF_VC * KP;
+    for (int e = threadIdx.x; e < LF_VC * KP; e += blockDim.x) {
+      const int vv = e / KP, k = e % KP;
+      if (vv < nv && kbase + k < K)
+        cp_async8(pb + e, lp + ((int64_t)r * D + scope_vars[sbeg + c0 + vv]) * K + kbase + k);
+      else
+        pb[e] = make_float2(0.f, 0.f);
+    }
+    cp_async_commit();
+  };
+  // masked / non-finite entries -> 0 (and the support error) by the issuing thread
+  auto fixup = [&](int buf, int c0) {
+    const int nv = min(LF_VC, vend - c0);
+    const int v = lane;
+    if (v >= nv) return;
+    const int d = scope_vars[sbeg + c0 + v];
+    const bool act = active[d] != 0;
+    float *xb = xs + buf * XS + v * (LF_TB + 1);
+    for (int bl = kq; bl < nbl; bl += KG) {
+      const float xv = xb[bl];
+      if (!act || !isfinite(xv)) {
+        if (act) atomicMin(&status[0], d);
+        xb[bl] = 0.f;
+      }
+    }
+  };
 
   float acc[LF_NS][LF_KPT];
   double tot[LF_NS][LF_KPT];
@@ -188,34 +270,26 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
       tot[s][j] = 0.0;
     }
 
-  for (int c0 = vbeg; c0 < vend; c0 += LF_VC) {
+  if (vbeg < vend) stage(0, vbeg);
+  int it = 0;
+  for (int c0 = vbeg; c0 < vend; c0 += LF_VC, ++it) {
+    const int buf = it & 1;
     const int nv = min(LF_VC, vend - c0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < LF_VC * LF_TB; e += blockDim.x) {
-      const int v = e % LF_VC, bl = e / LF_VC;
-      float xv = 0.f;
-      if (v < nv && b0 + bl < B) {
-        const int d = scope_vars[sbeg + c0 + v];
-        xv = x[(b0 + bl) * D + d];
-        const bool act = active[d] != 0;
-        if (act && !isfinite(xv)) atomicMin(&status[0], d);
-        if (!act || !isfinite(xv)) xv = 0.f;
-      }
-      xs[v * (LF_TB + 1) + bl] = xv;
+    if (c0 + LF_VC < vend) {
+      stage(buf ^ 1, c0 + LF_VC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-    for (int e = threadIdx.x; e < LF_VC * KP; e += blockDim.x) {
-      const int v = e / KP, k = e % KP;
-      float2 pv = make_float2(0.f, 0.f);
-      if (v < nv && kbase + k < K)
-        pv = lp[((int64_t)r * D + scope_vars[sbeg + c0 + v]) * K + kbase + k];
-      ps[v * KP + k] = pv;
-    }
+    fixup(buf, c0);
     __syncthreads();
+    const float *xb = xs + buf * XS;
+    const float2 *pb = ps + buf * LF_VC * KP;
     for (int v = 0; v < nv; ++v) {
       float xv[LF_NS];
 #pragma unroll
-      for (int s = 0; s < LF_NS; ++s) xv[s] = xs[v * (LF_TB + 1) + lane + 32 * s];
-      const float4 *pp = (const float4 *)(ps + v * KP + kq * LF_KPT);
+      for (int s = 0; s < LF_NS; ++s) xv[s] = xb[v * (LF_TB + 1) + lane + 32 * s];
+      const float4 *pp = (const float4 *)(pb + v * KP + kq * LF_KPT);
 #pragma unroll
       for (int j2 = 0; j2 < LF_KPT / 2; ++j2) {
         const float4 q = pp[j2];
@@ -235,6 +309,7 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
         tot[s][j] += (double)acc[s][j];
         acc[s][j] = 0.f;
       }
+    __syncthreads();
   }
 #pragma unroll
   for (int s = 0; s < LF_NS; ++s) {
@@ -363,8 +438,8 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
     const int nkc = ceil_div(KG, kg);
     const int threads = 32 * kg;
     ds = leaf_dsplit(p, B, LF_TB);
-    const size_t smem = sizeof(float) * (LF_VC * (LF_TB + 1) + 1) + 16 +
-                        sizeof(float2) * LF_VC * kg * LF_KPT;
+    const size_t smem = ((2 * LF_VC * (LF_TB + 1) * sizeof(float) + 15) & ~(size_t)15) +
+                        2 * sizeof(float2) * LF_VC * kg * LF_KPT;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_leaf_fwd_gauss, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
@@ -431,83 +506,118 @@ constexpr int LS_VC = 32;   // variables per CTA
 constexpr int LS_BT = 32;   // samples per fp32 run before folding into fp64
 constexpr int LS_MAXP = 16; // (var,k,t) entries per thread
 
-// Gaussian: acc_pt[d,k,r,:] += sum_b rho*(x, x^2), accumulated centred at the
-// current mean c (fp32 runs of 32 samples) and un-centred in fp64:
+// Gaussian: acc_pt[d,k,r,:] += sum_b rho*(x, x^2). fp32 runs of 32 samples are
+// accumulated centred at c = centre[r][d] (y = x - c) and un-centred in fp64:
 //   sum rho x = A + c P,  sum rho x^2 = Q + 2 c A + c^2 P.
-// grid (ceil(max_scope/32), n_leaf, lsplit), block 256.
+// Register tile of 4 variables x 4 k per thread: per sample 3 LDS.128 feed
+// 32 FFMA. grid (ceil(max_scope/64) * nkc, n_leaf, lsplit), block 16*KQ.
+constexpr int LS_VT = 64;
 __global__ void __launch_bounds__(256) k_leaf_stats_gauss(
     const float *__restrict__ x, int64_t B, int D, int K, int R, const int *scope_off,
     const int *scope_vars, const int *leaf_rep, const float *__restrict__ rho_all, int64_t Bc,
     const float *__restrict__ center, const uint8_t *__restrict__ active, double *lspart,
-    int64_t n_phi, int lsplit) {
-  __shared__ float xs[LS_BT][LS_VC + 1];
-  extern __shared__ float rs[];  // [LS_BT][K]
+    int64_t n_phi, int lsplit, int nkc) {
+  __shared__ __align__(16) float ys[LS_BT][LS_VT];
+  __shared__ __align__(16) float y2s[LS_BT][LS_VT];
+  extern __shared__ __align__(16) float rs[];  // [LS_BT][KPC]
+  __shared__ int dv[LS_VT];
+  __shared__ float cv[LS_VT];
+  const int KQ = blockDim.x / 16;  // k quads in this CTA
+  const int KPC = KQ * 4;
   const int leaf = blockIdx.y, split = blockIdx.z;
+  const int vchunk = blockIdx.x / nkc;
+  const int kbase = (blockIdx.x % nkc) * KPC;
   const int sbeg = scope_off[leaf], slen = scope_off[leaf + 1] - sbeg;
-  const int v0 = blockIdx.x * LS_VC;
+  const int v0 = vchunk * LS_VT;
   if (v0 >= slen) return;
-  const int nv = min(LS_VC, slen - v0);
+  const int nv = min(LS_VT, slen - v0);
   const int r = leaf_rep[leaf];
   const int64_t per = (B + lsplit - 1) / lsplit;
   const int64_t bb = split * per, be = min(B, bb + per);
   const float *rho = rho_all + (int64_t)leaf * Bc * K;
-  const int npairs = nv * K;
-  float a1[LS_MAXP], a2[LS_MAXP], pp[LS_MAXP], cc[LS_MAXP];
-  double t0[LS_MAXP], t1[LS_MAXP];
-  int vv[LS_MAXP], kk[LS_MAXP];
-#pragma unroll
-  for (int m = 0; m < LS_MAXP; ++m) {
-    const int e = threadIdx.x + m * 256;
-    vv[m] = e < npairs ? e / K : 0;
-    kk[m] = e < npairs ? e % K : 0;
-    const int d = scope_vars[sbeg + v0 + vv[m]];
-    cc[m] = e < npairs ? center[((int64_t)r * D + d) * K + kk[m]] : 0.f;
-    a1[m] = a2[m] = pp[m] = 0.f;
-    t0[m] = t1[m] = 0.0;
+  const int tv = threadIdx.x % 16, tk = threadIdx.x / 16;
+  for (int v = threadIdx.x; v < LS_VT; v += blockDim.x) {
+    const int d = v < nv ? scope_vars[sbeg + v0 + v] : -1;
+    dv[v] = (d >= 0 && active[d]) ? d : -1;
+    cv[v] = d >= 0 ? center[(int64_t)r * D + d] : 0.f;
   }
+  __syncthreads();
+  float c[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) c[u] = cv[4 * tv + u];
+  float a1[4][4], a2[4][4], pk[4];
+  double t0[4][4], t1[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a1[u][j] = a2[u][j] = 0.f;
+      t0[u][j] = t1[u][j] = 0.0;
+    }
   for (int64_t t = bb; t < be; t += LS_BT) {
     const int nb = (int)min((int64_t)LS_BT, be - t);
     __syncthreads();
-    for (int e = threadIdx.x; e < LS_BT * LS_VC; e += 256) {
-      const int v = e % LS_VC, bl = e / LS_VC;
-      float xv = 0.f;
-      if (v < nv && bl < nb) {
-        const int d = scope_vars[sbeg + v0 + v];
-        xv = x[(t + bl) * D + d];
-        if (!isfinite(xv)) xv = 0.f;
+    for (int e = threadIdx.x; e < LS_BT * LS_VT; e += blockDim.x) {
+      const int v = e % LS_VT, bl = e / LS_VT;
+      const int d = dv[v];
+      float y = 0.f;
+      if (d >= 0 && bl < nb) {
+        const float xv = x[(t + bl) * D + d];
+        y = isfinite(xv) ? xv - cv[v] : 0.f;
       }
-      xs[bl][v] = xv;
+      ys[bl][v] = y;
+      y2s[bl][v] = y * y;
     }
-    for (int e = threadIdx.x; e < LS_BT * K; e += 256) {
-      const int bl = e / K, k = e % K;
-      rs[e] = bl < nb ? rho[(t + bl) * K + k] : 0.f;
+    for (int e = threadIdx.x; e < LS_BT * KPC; e += blockDim.x) {
+      const int bl = e / KPC, k = kbase + e % KPC;
+      rs[e] = (bl < nb && k < K) ? rho[(t + bl) * K + k] : 0.f;
     }
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < LS_MAXP; ++m) {
-      if (threadIdx.x + m * 256 >= npairs) break;
-      float s1 = 0.f, s2 = 0.f, sp = 0.f;
-      for (int bl = 0; bl < nb; ++bl) {
-        const float rr = rs[bl * K + kk[m]];
-        const float y = xs[bl][vv[m]] - cc[m];
-        const float ry = rr * y;
-        s1 += ry;
-        s2 = fmaf(ry, y, s2);
-        sp += rr;
+    for (int j = 0; j < 4; ++j) pk[j] = 0.f;
+    for (int bl = 0; bl < nb; ++bl) {
+      const float4 y4 = *(const float4 *)&ys[bl][4 * tv];
+      const float4 q4 = *(const float4 *)&y2s[bl][4 * tv];
+      const float4 r4 = *(const float4 *)&rs[bl * KPC + 4 * tk];
+      const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+      const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
+      const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        pk[j] += rv[j];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a1[u][j] = fmaf(rv[j], yv[u], a1[u][j]);
+          a2[u][j] = fmaf(rv[j], qv[u], a2[u][j]);
+        }
       }
-      const double c = (double)cc[m];
-      t0[m] += (double)s1 + c * (double)sp;
-      t1[m] += (double)s2 + 2.0 * c * (double)s1 + c * c * (double)sp;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double cu = (double)c[u];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double A = a1[u][j], Q = a2[u][j], P = pk[j];
+        t0[u][j] += A + cu * P;
+        t1[u][j] += Q + 2.0 * cu * A + cu * cu * P;
+        a1[u][j] = a2[u][j] = 0.f;
+      }
     }
   }
 #pragma unroll
-  for (int m = 0; m < LS_MAXP; ++m) {
-    if (threadIdx.x + m * 256 >= npairs) break;
-    const int d = scope_vars[sbeg + v0 + vv[m]];
-    double *dst = lspart + (int64_t)split * n_phi + ((((int64_t)d * K + kk[m]) * R + r) * 2);
-    const bool act = active[d] != 0;
-    dst[0] = act ? t0[m] : 0.0;
-    dst[1] = act ? t1[m] : 0.0;
+  for (int u = 0; u < 4; ++u) {
+    const int v = 4 * tv + u;
+    if (v >= nv) continue;
+    const int d = scope_vars[sbeg + v0 + v];
+    const bool act = dv[v] >= 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = kbase + 4 * tk + j;
+      if (k >= K) continue;
+      double *dst = lspart + (int64_t)split * n_phi + ((((int64_t)d * K + k) * R + r) * 2);
+      dst[0] = act ? t0[u][j] : 0.0;
+      dst[1] = act ? t1[u][j] : 0.0;
+    }
   }
 }
 
@@ -556,7 +666,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats_discrete(
 }
 
 int leaf_lsplit(const Plan &p, int64_t B) {
-  int64_t blocks = (int64_t)ceil_div(p.max_scope, LS_VC) * p.n_leaf;
+  int64_t blocks = (int64_t)ceil_div(p.max_scope, LS_VT) * p.n_leaf;
   int want = (int)std::max<int64_t>(1, (2 * p.num_sms + blocks - 1) / blocks);
   int cap = (int)std::max<int64_t>(1, std::min<int64_t>(8, (B + 255) / 256));
   return std::min(want, cap);
@@ -581,11 +691,13 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
   cudaMemsetAsync(w.lspart, 0, sizeof(double) * n_phi * ls, st);
   dim3 grid(ceil_div(p.max_scope, LS_VC), p.n_leaf, ls);
   if (p.family == EINET_FAMILY_GAUSSIAN) {
-    if ((LS_VC * K + 255) / 256 > LS_MAXP)
-      return fail(EINET_ERR_USAGE, "k too large for the gaussian leaf statistics kernel");
-    k_leaf_stats_gauss<<<grid, 256, sizeof(float) * LS_BT * K, st>>>(
+    const int K4 = ceil_div(K, 4);
+    const int kq = std::min(K4, 16);
+    const int nkc = ceil_div(K4, kq);
+    dim3 g(ceil_div(p.max_scope, LS_VT) * nkc, p.n_leaf, ls);
+    k_leaf_stats_gauss<<<g, 16 * kq, sizeof(float) * LS_BT * kq * 4, st>>>(
         x, B, D, K, R, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep, w.rho, w.bc, c.center,
-        c.active, w.lspart, n_phi, ls);
+        c.active, w.lspart, n_phi, ls, nkc);
   } else {
     k_leaf_stats_discrete<<<grid, 256, 0, st>>>(x, B, D, K, R, T, p.family, p.d_scope_off,
                                                p.d_scope_vars, p.d_leaf_rep, w.rho, w.bc,

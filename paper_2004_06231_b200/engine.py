@@ -378,7 +378,7 @@ class Parameters:
         """Device compute tensors for a forward pass (cached when unmasked)."""
         if marg_mask is None and leaf_log_offset is None:
             if (self._compute is None or self._compute_version != self.version
-                    or self._compute_owner is not engine.sizes.compute_bytes):
+                    or self._compute_owner != engine.sizes.compute_bytes):
                 if self._compute is None or self._compute.numel() != engine.sizes.compute_bytes:
                     self._compute = torch.empty(int(engine.sizes.compute_bytes),
                                                 dtype=torch.uint8, device=self.flat.device)
