@@ -125,6 +125,11 @@ int einet_backward(einet_plan *plan, const double *params, const void *compute,
                    const float *x, int64_t batch, void *workspace, double *stats,
                    int32_t *status, void *stream);
 
+/* Enable (default) or disable the tcgen05 EinsumLayer kernels of this plan
+ * (the CUDA-core kernels are used for layers the tensor-core path does not
+ * cover; EINET_DISABLE_TC=1 in the environment disables them at creation). */
+int einet_plan_set_tensor_cores(einet_plan *plan, int enable);
+
 /* Set the int32[EINET_STATUS_WORDS] status words to "no error" (INT32_MAX).
  * Call once per step; forward/backward only lower them (atomicMin). */
 int einet_status_reset(int32_t *status, void *stream);

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -186,6 +187,8 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
             ld.right[r] >= p->nbr)
           return fail(EINET_ERR_USAGE, "einsum child row out of range");
       L.w_off = w_acc;
+      L.erow_base = p->n_erows;
+      p->n_erows += ld.rows;
       int64_t lw = (int64_t)ld.rows * ld.k_out * K * K;
       w_acc += lw;
       p->max_layer_w = std::max(p->max_layer_w, lw);
@@ -291,13 +294,23 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   p->c_w32 = seg(4 * p->n_w);
   p->c_mix32 = seg(4 * std::max<int64_t>(p->n_mix, 1));
   if (p->family == EINET_FAMILY_CATEGORICAL)
-    p->c_leafp = seg(4 * RDK * p->num_states);
+    p->c_leafp = seg(8 * RDK * p->num_states);
   else
-    p->c_leafp = seg(8 * RDK);
+    p->c_leafp = seg(16 * RDK);
   p->c_center = seg(4 * RDK);
   p->c_const = seg(8 * (int64_t)p->n_leaf * K);
   p->c_active = seg(D);
   p->c_logh = seg(8 * (int64_t)(std::max(p->n_trials, 0) + 1));
+  {
+    const char *env = getenv("EINET_DISABLE_TC");
+    p->use_tc = !(env && env[0] == '1');
+  }
+  plan_tc_tiling(*p);
+  for (auto &L : p->layers) {
+    if (!L.tc) continue;
+    L.fw_off = seg(L.fw_tile * L.rows * L.ng);
+    L.uw_off = seg(L.uw_tile * L.rows * L.ni);
+  }
   z.compute_bytes = off;
 
   const int64_t Bc = max_chunk, KS = p->ks;
@@ -306,8 +319,8 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   p->w_shift = seg(8 * (int64_t)p->num_slabs * Bc);
   p->w_slots = seg(4 * (int64_t)std::max(p->num_slots, 1) * Bc * KS);
   p->w_leafpart = seg(8 * (int64_t)kMaxDSplit * p->n_leaf * Bc * K);
-  p->w_ea = seg(4 * p->max_rows * Bc * K);
-  p->w_eb = seg(4 * p->max_rows * Bc * K);
+  p->w_ea = seg(4 * (int64_t)p->n_erows * Bc * K);
+  p->w_eb = seg(4 * (int64_t)p->n_erows * Bc * K);
   p->w_rt = seg(4 * p->max_rows * Bc * KS);
   // W-stat partials: bsplit chosen per layer by the launcher, bounded here
   int64_t wpart = 0;
@@ -317,7 +330,12 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     int64_t blocks = (int64_t)L.rows * L.k_out;
     int64_t bs = std::min<int64_t>(std::max<int64_t>(1, (2 * p->num_sms + blocks - 1) / blocks),
                                    std::min<int64_t>(kMaxBSplit, (Bc + 63) / 64));
-    wpart = std::max(wpart, bs * lw);
+    // tensor-core W statistics split their batch as well (einsum_tc.cu)
+    int64_t tc_blocks = (int64_t)((K * K + 127) / 128) * L.rows;
+    int64_t tc_bs = std::max<int64_t>(1, std::min<int64_t>((p->num_sms + tc_blocks - 1) / tc_blocks,
+                                                          std::min<int64_t>((Bc + 31) / 32,
+                                                                            kMaxBSplit)));
+    wpart = std::max(wpart, std::max(bs, tc_bs) * lw);
   }
   p->w_wpart = seg(8 * std::max<int64_t>(wpart, 1));
   p->w_rho = seg(4 * (int64_t)p->n_leaf * Bc * K);
@@ -441,6 +459,12 @@ int einet_backward(einet_plan *plan, const double *params, const void *compute,
 int einet_status_reset(int32_t *status, void *stream) {
   if (!status) return fail(EINET_ERR_USAGE, "null argument");
   return launch_status_reset(status, (cudaStream_t)stream);
+}
+
+int einet_plan_set_tensor_cores(einet_plan *plan, int enable) {
+  if (!plan) return fail(EINET_ERR_USAGE, "null argument");
+  plan->impl.use_tc = enable != 0;
+  return EINET_OK;
 }
 
 int einet_stats_zero(einet_plan *plan, double *stats, void *stream) {

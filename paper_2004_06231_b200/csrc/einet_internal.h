@@ -40,6 +40,15 @@ struct LayerPlan {
   int *d_mix_slot = nullptr;       // (M*dmax), -1 if masked
   uint8_t *d_mix_mask = nullptr;
   int64_t mix_off = 0; // element offset of (M,Dmax) weights in the mixing block
+  int erow_base = 0;   // first global einsum row (per-layer EA/EB storage)
+  // tensor-core tiling (einsum layers with tc != 0), DESIGN.md "EinsumLayer"
+  int tc = 0;
+  int kg = 0, ng = 0, fw_rows = 0;  // forward: k per N tile, #tiles, tile rows (N_max)
+  int ig = 0, ni = 0, uw_rows = 0;  // child-rho: i per N tile, #tiles, tile rows
+  int ko8 = 0;                      // K_out padded to 8 (child-rho MMA K dimension)
+  int nn = 0;                       // W-stats MMA N: K_out padded to 16
+  int64_t fw_off = 0, fw_tile = 0;  // compute byte offset, bytes per forward tile
+  int64_t uw_off = 0, uw_tile = 0;  // compute byte offset, bytes per child-rho tile
   std::vector<int> h_out_slab;
   std::vector<int> h_src;          // mixing local src
   std::vector<uint8_t> h_mask;
@@ -79,6 +88,8 @@ struct Plan {
   int64_t max_chunk = 0;
   int num_sms = 148;
   int max_lsplit = 1;              // leaf-statistics batch split allocated
+  int n_erows = 0;                 // einsum rows over all layers
+  int use_tc = 1;                  // tcgen05 EinsumLayer path enabled
   // mixing rows flattened over layers for the M-step
   int n_mixrows = 0;
   int *d_mixrow_off = nullptr, *d_mixrow_len = nullptr;
@@ -134,6 +145,8 @@ int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
                        const uint8_t *mask, double *out, int32_t *status,
                        cudaStream_t st);
 int launch_status_reset(int32_t *status, cudaStream_t st);
+void plan_tc_tiling(Plan &p);
+int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_selftest_gemm(const float *A, const float *B, float *D, int N, int K,
                          cudaStream_t st);
 int leaf_lsplit(const Plan &p, int64_t B);

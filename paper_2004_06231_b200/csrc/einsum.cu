@@ -20,31 +20,52 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
                         uint8_t *wsb, int32_t *status, cudaStream_t st);
 int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
                          uint8_t *wsb, double *stats, cudaStream_t st);
-int launch_einsum_tc_forward(Plan &p, const LayerPlan &L, const float *w32, WsView &w,
-                             int64_t B, int32_t *status, cudaStream_t st, bool *handled);
+int launch_einsum_fwd_tc(Plan &p, const LayerPlan &L, const uint8_t *compute, const float *EA,
+                         const float *EB, WsView &w, int64_t B, cudaStream_t st);
+int launch_einsum_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB,
+                            WsView &w, int64_t B, int *bsplit, cudaStream_t st);
+int launch_einsum_childrho_tc(Plan &p, const LayerPlan &L, const uint8_t *compute,
+                              const float *EA, const float *EB, WsView &w, int64_t B,
+                              cudaStream_t st);
 
 constexpr int EF_TB = 128;  // samples per CTA, one per thread
 constexpr int EF_KC = 8;    // output entries (k) staged per W chunk
 
-// Load one child slab as normalised exponentials e_i = exp(off_i - max off).
-template <int KT>
-__device__ __forceinline__ void load_exp(const WsView &ws, int slab, int64_t b, int K,
-                                         float (&e)[KT], double &s, float &mx, bool &dead,
-                                         bool &nan) {
-  const float *o = slab_off(ws, slab, b);
-  s = slab_shift(ws, slab)[b];
-  mx = -CUDART_INF_F;
-#pragma unroll
-  for (int i = 0; i < KT; ++i) {
-    const float v = i < K ? o[i] : -CUDART_INF_F;
-    e[i] = v;
-    nan |= v != v;
-    mx = fmaxf(mx, v);
+// Forward prep (one thread per sample and row): normalised child exponentials
+// EA = exp(off_left - a), EB = exp(off_right - c) with a, c the fp32 maxima
+// (engine.py:99-104), kept per layer for the backward; the output shift
+// s_left + s_right + a + c (engine.py:108); NaN entering the layer -> status.
+// grid (ceil(B/128), L), block 128.
+__global__ void k_einsum_prep_fwd(WsView ws, const int *__restrict__ left_slab,
+                                  const int *__restrict__ right_slab,
+                                  const int *__restrict__ out_slab, int64_t B, int K,
+                                  float *__restrict__ EA, float *__restrict__ EB,
+                                  int layer_index, int32_t *status) {
+  const int l = blockIdx.y;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int64_t row = (int64_t)l * ws.bc + b;
+  bool nan = false, dead = false;
+  double shift = 0.0;
+  for (int side = 0; side < 2; ++side) {
+    const int slab = side ? right_slab[l] : left_slab[l];
+    const float *o = slab_off(ws, slab, b);
+    const double s = slab_shift(ws, slab)[b];
+    float mx = -CUDART_INF_F;
+    for (int i = 0; i < K; ++i) {
+      const float v = o[i];
+      nan |= v != v;
+      mx = fmaxf(mx, v);
+    }
+    nan |= s != s;
+    const bool d = s == -CUDART_INF || mx == -CUDART_INF_F;
+    dead |= d;
+    shift += s + (double)mx;
+    float *dst = (side ? EB : EA) + row * K;
+    for (int i = 0; i < K; ++i) dst[i] = d ? 0.f : expf(o[i] - mx);
   }
-  nan |= s != s;
-  dead = (s == -CUDART_INF) || (mx == -CUDART_INF_F);
-#pragma unroll
-  for (int i = 0; i < KT; ++i) e[i] = dead ? 0.f : expf(e[i] - mx);
+  if (nan) atomicMin(&status[1], layer_index);
+  slab_shift(ws, out_slab[l])[b] = dead ? -CUDART_INF : shift;
 }
 
 template <int KT>
@@ -74,14 +95,14 @@ __device__ __forceinline__ void stage_w(float *wsm, const float *__restrict__ Wl
   }
 }
 
-// grid (ceil(B/128), L, ceil(Ko/8)), block 128 (one sample per thread)
+// SIMT forward GEMM: one sample per thread, ea/eb in registers, W chunk in smem.
+// grid (ceil(B/128), L, ceil(Ko/8)), block 128
 template <int KT>
-__global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const int *__restrict__ left_slab,
-                                                      const int *__restrict__ right_slab,
+__global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const float *__restrict__ EA,
+                                                      const float *__restrict__ EB,
                                                       const int *__restrict__ out_slab,
                                                       const float *__restrict__ W, int64_t B,
-                                                      int K, int Ko, int layer_index,
-                                                      int32_t *status) {
+                                                      int K, int Ko) {
   extern __shared__ __align__(16) float wsm[];
   const int l = blockIdx.y;
   const int k0 = blockIdx.z * EF_KC;
@@ -89,18 +110,15 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const int *__re
   stage_w(wsm, W + (int64_t)l * Ko * K * K, k0, nk, K, KT);
   const int64_t b = (int64_t)blockIdx.x * EF_TB + threadIdx.x;
   const bool live = b < B;
+  const int64_t row = (int64_t)l * ws.bc + (live ? b : 0);
   float ea[KT], eb[KT];
-  double sl = 0.0, sr = 0.0;
-  float a = 0.f, c = 0.f;
-  bool dl = true, dr = true, nan = false;
-  if (live) {
-    load_exp<KT>(ws, left_slab[l], b, K, ea, sl, a, dl, nan);
-    load_exp<KT>(ws, right_slab[l], b, K, eb, sr, c, dr, nan);
-    if (nan) atomicMin(&status[1], layer_index);
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    ea[i] = (live && i < K) ? EA[row * K + i] : 0.f;
+    eb[i] = (live && i < K) ? EB[row * K + i] : 0.f;
   }
   __syncthreads();
   if (!live) return;
-  const bool dead = dl || dr;
   float *o = slab_off(ws, out_slab[l], b);
   for (int kk = 0; kk < nk; ++kk) {
     const float *wk = wsm + kk * K * KT;
@@ -108,46 +126,30 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const int *__re
 #pragma unroll
     for (int i = 0; i < KT; ++i)
       if (i < K) acc = fmaf(ea[i], dot_row<KT>(wk + i * KT, eb), acc);
-    o[k0 + kk] = (dead || !(acc > 0.f)) ? -CUDART_INF_F : logf(acc);
+    o[k0 + kk] = acc > 0.f ? logf(acc) : -CUDART_INF_F;
   }
-  if (blockIdx.z == 0)
-    slab_shift(ws, out_slab[l])[b] =
-        dead ? -CUDART_INF : sl + sr + (double)a + (double)c;
 }
 
-// Generic (any K) forward: W read through L1, operands recomputed per term.
-__global__ void k_einsum_fwd_generic(WsView ws, const int *left_slab, const int *right_slab,
-                                     const int *out_slab, const float *__restrict__ W,
-                                     int64_t B, int K, int Ko, int layer_index,
-                                     int32_t *status) {
+// Generic (any K) forward from EA/EB, W read through L1.
+__global__ void k_einsum_fwd_generic(WsView ws, const float *__restrict__ EA,
+                                     const float *__restrict__ EB, const int *out_slab,
+                                     const float *__restrict__ W, int64_t B, int K, int Ko) {
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const float *ol = slab_off(ws, left_slab[l], b), *orr = slab_off(ws, right_slab[l], b);
-  const double sl = slab_shift(ws, left_slab[l])[b], sr = slab_shift(ws, right_slab[l])[b];
-  float a = -CUDART_INF_F, c = -CUDART_INF_F;
-  bool nan = sl != sl || sr != sr;
-  for (int i = 0; i < K; ++i) {
-    a = fmaxf(a, ol[i]);
-    c = fmaxf(c, orr[i]);
-    nan |= ol[i] != ol[i] || orr[i] != orr[i];
-  }
-  if (nan) atomicMin(&status[1], layer_index);
-  const bool dead = sl == -CUDART_INF || sr == -CUDART_INF || a == -CUDART_INF_F ||
-                    c == -CUDART_INF_F;
+  const int64_t row = (int64_t)l * ws.bc + b;
+  const float *ea = EA + row * K, *eb = EB + row * K;
   float *o = slab_off(ws, out_slab[l], b);
   const float *Wl = W + (int64_t)l * Ko * K * K;
   for (int k = 0; k < Ko; ++k) {
     float acc = 0.f;
-    for (int i = 0; i < K && !dead; ++i) {
-      const float ei = expf(ol[i] - a);
+    for (int i = 0; i < K; ++i) {
       float t = 0.f;
-      for (int j = 0; j < K; ++j) t = fmaf(Wl[((int64_t)k * K + i) * K + j], expf(orr[j] - c), t);
-      acc = fmaf(ei, t, acc);
+      for (int j = 0; j < K; ++j) t = fmaf(Wl[((int64_t)k * K + i) * K + j], eb[j], t);
+      acc = fmaf(ea[i], t, acc);
     }
-    o[k] = (dead || !(acc > 0.f)) ? -CUDART_INF_F : logf(acc);
+    o[k] = acc > 0.f ? logf(acc) : -CUDART_INF_F;
   }
-  slab_shift(ws, out_slab[l])[b] = dead ? -CUDART_INF : sl + sr + (double)a + (double)c;
 }
 
 // ---------------------------------------------------------------------------
@@ -249,26 +251,15 @@ __global__ void k_mixing_bwd(WsView ws, const int *__restrict__ src_slab,
 // einsum backward
 // ---------------------------------------------------------------------------
 
-// EA/EB (normalised child exponentials) and RT = rho / r per row and sample.
-// grid (ceil(B/128), L), block 128
-__global__ void k_einsum_bwd_prep(WsView ws, const int *left_slab, const int *right_slab,
-                                  const int *out_slab, const int *csr_off, const int *csr_slot,
-                                  const uint8_t *ones, int64_t B, int K, int Ko, float *EA,
-                                  float *EB, float *RT) {
+// RT = rho / r per row and sample (engine.py:310-311), r = exp(log r) from the
+// forward offsets. grid (ceil(B/128), L), block 128
+__global__ void k_einsum_bwd_rt(WsView ws, const int *out_slab, const int *csr_off,
+                                const int *csr_slot, const uint8_t *ones, int64_t B, int Ko,
+                                float *RT) {
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int64_t row = (int64_t)l * ws.bc + b;
-  for (int side = 0; side < 2; ++side) {
-    const int slab = side ? right_slab[l] : left_slab[l];
-    const float *o = slab_off(ws, slab, b);
-    const double s = slab_shift(ws, slab)[b];
-    float mx = -CUDART_INF_F;
-    for (int i = 0; i < K; ++i) mx = fmaxf(mx, o[i]);
-    const bool dead = s == -CUDART_INF || mx == -CUDART_INF_F;
-    float *dst = (side ? EB : EA) + row * K;
-    for (int i = 0; i < K; ++i) dst[i] = dead ? 0.f : expf(o[i] - mx);
-  }
   const int os = out_slab[l];
   const double so = slab_shift(ws, os)[b];
   const float *oo = slab_off(ws, os, b);
@@ -485,64 +476,73 @@ __global__ void k_ll_finish(const double *part, int n, double *ll, double count)
 // ---------------------------------------------------------------------------
 
 template <int KT>
-static void fwd_simt(const LayerPlan &L, const float *w32, WsView &w, int64_t B, int K,
-                     int32_t *status, cudaStream_t st) {
+static void fwd_simt(const LayerPlan &L, const float *w32, const float *EA, const float *EB,
+                     WsView &w, int64_t B, int K, cudaStream_t st) {
   const size_t smem = sizeof(float) * EF_KC * K * KT;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_einsum_fwd<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   dim3 grid(ceil_div(B, EF_TB), L.rows, ceil_div(L.k_out, EF_KC));
-  k_einsum_fwd<KT><<<grid, EF_TB, smem, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
-                                              w32 + L.w_off, B, K, L.k_out, L.index, status);
+  k_einsum_fwd<KT><<<grid, EF_TB, smem, st>>>(w, EA, EB, L.d_out_slab, w32 + L.w_off, B, K,
+                                              L.k_out);
 }
 
 template <int KT>
-static void childrho_simt(const LayerPlan &L, const float *w32, WsView &w, int64_t B, int K,
-                          cudaStream_t st) {
+static void childrho_simt(const LayerPlan &L, const float *w32, const float *EA,
+                          const float *EB, WsView &w, int64_t B, int K, cudaStream_t st) {
   const size_t smem = sizeof(float) * EF_KC * K * KT;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_einsum_childrho<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   dim3 grid(ceil_div(B, EF_TB), L.rows);
-  k_einsum_childrho<KT><<<grid, EF_TB, smem, st>>>(w.ea, w.eb, w.rt, w32 + L.w_off, w,
+  k_einsum_childrho<KT><<<grid, EF_TB, smem, st>>>(EA, EB, w.rt, w32 + L.w_off, w,
                                                    L.d_slot_left, L.d_slot_right, B, K,
                                                    L.k_out);
 }
 
-static void einsum_forward_simt(const LayerPlan &L, const float *w32, WsView &w, int64_t B,
-                                int K, int32_t *status, cudaStream_t st) {
-  if (K <= 4) fwd_simt<4>(L, w32, w, B, K, status, st);
-  else if (K <= 8) fwd_simt<8>(L, w32, w, B, K, status, st);
-  else if (K <= 12) fwd_simt<12>(L, w32, w, B, K, status, st);
-  else if (K <= 16) fwd_simt<16>(L, w32, w, B, K, status, st);
-  else if (K <= 24) fwd_simt<24>(L, w32, w, B, K, status, st);
-  else if (K <= 32) fwd_simt<32>(L, w32, w, B, K, status, st);
-  else if (K <= 40) fwd_simt<40>(L, w32, w, B, K, status, st);
-  else if (K <= 48) fwd_simt<48>(L, w32, w, B, K, status, st);
-  else if (K <= 64) fwd_simt<64>(L, w32, w, B, K, status, st);
+static void einsum_forward_simt(const LayerPlan &L, const float *w32, const float *EA,
+                                const float *EB, WsView &w, int64_t B, int K,
+                                cudaStream_t st) {
+  if (K <= 4) fwd_simt<4>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 8) fwd_simt<8>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 12) fwd_simt<12>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 16) fwd_simt<16>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 24) fwd_simt<24>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 32) fwd_simt<32>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 40) fwd_simt<40>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 48) fwd_simt<48>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 64) fwd_simt<64>(L, w32, EA, EB, w, B, K, st);
   else {
     dim3 grid(ceil_div(B, 128), L.rows);
-    k_einsum_fwd_generic<<<grid, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
-                                               w32 + L.w_off, B, K, L.k_out, L.index, status);
+    k_einsum_fwd_generic<<<grid, 128, 0, st>>>(w, EA, EB, L.d_out_slab, w32 + L.w_off, B, K,
+                                               L.k_out);
   }
 }
 
-static void einsum_childrho(const LayerPlan &L, const float *w32, WsView &w, int64_t B, int K,
-                            cudaStream_t st) {
-  if (K <= 4) childrho_simt<4>(L, w32, w, B, K, st);
-  else if (K <= 8) childrho_simt<8>(L, w32, w, B, K, st);
-  else if (K <= 12) childrho_simt<12>(L, w32, w, B, K, st);
-  else if (K <= 16) childrho_simt<16>(L, w32, w, B, K, st);
-  else if (K <= 24) childrho_simt<24>(L, w32, w, B, K, st);
-  else if (K <= 32) childrho_simt<32>(L, w32, w, B, K, st);
-  else if (K <= 40) childrho_simt<40>(L, w32, w, B, K, st);
-  else if (K <= 48) childrho_simt<48>(L, w32, w, B, K, st);
+static void einsum_childrho_simt(const LayerPlan &L, const float *w32, const float *EA,
+                                 const float *EB, WsView &w, int64_t B, int K,
+                                 cudaStream_t st) {
+  if (K <= 4) childrho_simt<4>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 8) childrho_simt<8>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 12) childrho_simt<12>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 16) childrho_simt<16>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 24) childrho_simt<24>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 32) childrho_simt<32>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 40) childrho_simt<40>(L, w32, EA, EB, w, B, K, st);
+  else if (K <= 48) childrho_simt<48>(L, w32, EA, EB, w, B, K, st);
   else {
     dim3 grid(ceil_div(B, 128), L.rows);
-    k_einsum_childrho_generic<<<grid, 128, 0, st>>>(w.ea, w.eb, w.rt, w32 + L.w_off, w,
+    k_einsum_childrho_generic<<<grid, 128, 0, st>>>(EA, EB, w.rt, w32 + L.w_off, w,
                                                     L.d_slot_left, L.d_slot_right, B, K,
                                                     L.k_out);
   }
+}
+
+static inline const float *layer_ea(const Plan &p, const WsView &w, const LayerPlan &L) {
+  return w.ea + (int64_t)L.erow_base * w.bc * p.k;
+}
+static inline const float *layer_eb(const Plan &p, const WsView &w, const LayerPlan &L) {
+  return w.eb + (int64_t)L.erow_base * w.bc * p.k;
 }
 
 int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, uint8_t *wsb,
@@ -553,19 +553,28 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
   if (rc) return rc;
   for (const LayerPlan &L : p.layers) {
     if (L.kind == EINET_LAYER_EINSUM) {
+      float *EA = (float *)layer_ea(p, w, L), *EB = (float *)layer_eb(p, w, L);
+      {
+        ProfScope prof("einsum_prep", st);
+        dim3 grid(ceil_div(B, 128), L.rows);
+        k_einsum_prep_fwd<<<grid, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
+                                                B, p.k, EA, EB, L.index, status);
+      }
       ProfScope prof("einsum_fwd", st);
-      bool handled = false;
-      rc = launch_einsum_tc_forward(p, L, c.w32, w, B, status, st, &handled);
+      if (p.use_tc && L.tc)
+        rc = launch_einsum_fwd_tc(p, L, compute, EA, EB, w, B, st);
+      else
+        einsum_forward_simt(L, c.w32, EA, EB, w, B, p.k, st);
       if (rc) return rc;
-      if (!handled) einsum_forward_simt(L, c.w32, w, B, p.k, status, st);
+      count_launch(2);
     } else {
       ProfScope prof("mixing_fwd", st);
       dim3 grid(ceil_div(B, 128), L.rows);
       k_mixing_fwd<<<grid, 128, 0, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
                                          c.mix32 + L.mix_off, B, L.k_out, L.dmax, L.index,
                                          status);
+      count_launch();
     }
-    count_launch();
   }
   const int64_t n = B * p.k_root;
   k_root_out<<<ceil_div(n, 256), 256, 0, st>>>(w, p.root_out_slab, B, p.k_root, root_out);
@@ -609,27 +618,38 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
       count_launch();
       continue;
     }
+    const float *EA = layer_ea(p, w, L), *EB = layer_eb(p, w, L);
     {
-    ProfScope prof("einsum_bwd_prep", st);
-    dim3 g1(ceil_div(B, 128), L.rows);
-    k_einsum_bwd_prep<<<g1, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
-                                          p.d_csr_off, p.d_csr_slot, p.d_slab_ones, B, K,
-                                          L.k_out, w.ea, w.eb, w.rt);
+      ProfScope prof("einsum_bwd_rt", st);
+      dim3 g1(ceil_div(B, 128), L.rows);
+      k_einsum_bwd_rt<<<g1, 128, 0, st>>>(w, L.d_out_slab, p.d_csr_off, p.d_csr_slot,
+                                          p.d_slab_ones, B, L.k_out, w.rt);
     }
-    {
-    ProfScope prof("einsum_wstats", st);
-    const int bs = wstats_bsplit(p, L, B);
-    const int K4 = (K + 3) / 4;
-    const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT);
-    dim3 g2(L.rows * L.k_out, bs);
-    k_einsum_wstats<<<g2, K4 * K4, smem, st>>>(w.ea, w.eb, w.rt, w.bc, w.ks, B, K, L.k_out,
-                                               L.rows, bs, w.wpart);
     const int64_t lw = (int64_t)L.rows * L.k_out * K * K;
-    launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);
+    {
+      ProfScope prof("einsum_wstats", st);
+      int bs;
+      if (p.use_tc && L.tc) {
+        int rc = launch_einsum_wstats_tc(p, L, EA, EB, w, B, &bs, st);
+        if (rc) return rc;
+      } else {
+        bs = wstats_bsplit(p, L, B);
+        const int K4 = (K + 3) / 4;
+        const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT);
+        dim3 g2(L.rows * L.k_out, bs);
+        k_einsum_wstats<<<g2, K4 * K4, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K, L.k_out,
+                                                   L.rows, bs, w.wpart);
+      }
+      launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);
     }
     {
-    ProfScope prof("einsum_childrho", st);
-    einsum_childrho(L, c.w32, w, B, K, st);
+      ProfScope prof("einsum_childrho", st);
+      if (p.use_tc && L.tc) {
+        int rc = launch_einsum_childrho_tc(p, L, compute, EA, EB, w, B, st);
+        if (rc) return rc;
+      } else {
+        einsum_childrho_simt(L, c.w32, EA, EB, w, B, K, st);
+      }
     }
     count_launch(3);
   }

@@ -91,4 +91,557 @@ int launch_selftest_gemm(const float *A, const float *B, float *D, int N, int K,
   return check_cuda(cudaGetLastError(), "selftest gemm");
 }
 
+// ===========================================================================
+// production EinsumLayer kernels
+// ===========================================================================
+
+constexpr int TC_M = 128;                    // batch (or (i,j)) rows per MMA tile
+constexpr int64_t TC_SMEM_MAX = 200 * 1024;  // dynamic smem budget per CTA
+constexpr int WS_STAGE = 32;                 // samples per W-statistics MMA stage
+constexpr int WS_DRAIN = 8;                  // stages accumulated in TMEM before fp64 drain
+
+static inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+static int64_t fwd_smem(int rows_tile, int K) {
+  return 2LL * rows_tile * K * 4 + 2LL * 2 * TC_M * K * 4;
+}
+static int64_t cr_smem(int rows_tile, int ko8) {
+  return 2LL * TC_M * ko8 * 4 + 2LL * (2LL * rows_tile * ko8 * 4);
+}
+static int64_t ws_smem(int K, int nn) {
+  return 2LL * 2 * TC_M * WS_STAGE * 4 + 2LL * 2 * nn * WS_STAGE * 4 + 2LL * WS_STAGE * K * 4 +
+         (int64_t)TC_M * nn * 8;
+}
+
+void plan_tc_tiling(Plan &p) {
+  const int K = p.k;
+  for (auto &L : p.layers) {
+    L.tc = 0;
+    if (L.kind != EINET_LAYER_EINSUM) continue;
+    if (K % 8 != 0 || K < 8 || K > 64) continue;
+    const int Ko = L.k_out;
+    int kg = std::max(1, std::min(Ko, 256 / K));
+    while (kg > 1 && fwd_smem(round_up(kg * K, 16), K) > TC_SMEM_MAX) --kg;
+    L.kg = kg;
+    L.ng = ceil_div(Ko, kg);
+    L.fw_rows = round_up(kg * K, 16);
+    L.fw_tile = 2LL * L.fw_rows * K * 4;
+    L.ko8 = round_up(Ko, 8);
+    int ig = std::max(1, std::min(K, 256 / K));
+    while (ig > 1 && cr_smem(round_up(ig * K, 16), L.ko8) > TC_SMEM_MAX) --ig;
+    L.ig = ig;
+    L.ni = ceil_div(K, ig);
+    L.uw_rows = round_up(ig * K, 16);
+    L.uw_tile = 2LL * L.uw_rows * L.ko8 * 4;
+    L.nn = round_up(Ko, 16);
+    if (L.fw_rows > 256 || L.uw_rows > 256 || L.nn > 64 || L.ko8 > 256) continue;
+    if (fwd_smem(L.fw_rows, K) > TC_SMEM_MAX || cr_smem(L.uw_rows, L.ko8) > TC_SMEM_MAX ||
+        ws_smem(K, L.nn) > TC_SMEM_MAX)
+      continue;
+    L.tc = 1;
+  }
+}
+
+// --- pre-tiled weight images (built by prepare after every parameter change) ---
+// forward tile g of row l: rows n = kl*K + i (k = g*kg + kl), K dim = j
+// child-rho tile h of row l: rows n = il*K + j (i = h*ig + il), K dim = k
+__global__ void k_build_tiles(const float *__restrict__ W, uint8_t *fw, uint8_t *uw, int L,
+                              int Ko, int K, int kg, int ng, int fw_rows, int ig, int ni,
+                              int uw_rows, int ko8) {
+  const int64_t n_fw = (int64_t)L * ng * fw_rows * K;
+  const int64_t n_uw = (int64_t)L * ni * uw_rows * ko8;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_fw + n_uw;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    float *hi, *lo;
+    if (e < n_fw) {
+      const int kk = (int)(e % K);
+      const int n = (int)((e / K) % fw_rows);
+      const int64_t tile = e / ((int64_t)K * fw_rows);  // l * ng + g
+      const int l = (int)(tile / ng), g = (int)(tile % ng);
+      const int kl = n / K, i = n % K, k = g * kg + kl;
+      if (kl < kg && k < Ko) v = W[(((int64_t)l * Ko + k) * K + i) * K + kk];
+      float *base = (float *)(fw + tile * (2LL * fw_rows * K * 4));
+      hi = base + tc::kmaj_off(n, kk, fw_rows) / 4;
+      lo = hi + fw_rows * K;
+    } else {
+      const int64_t q = e - n_fw;
+      const int kk = (int)(q % ko8);
+      const int n = (int)((q / ko8) % uw_rows);
+      const int64_t tile = q / ((int64_t)ko8 * uw_rows);  // l * ni + h
+      const int l = (int)(tile / ni), h = (int)(tile % ni);
+      const int il = n / K, j = n % K, i = h * ig + il;
+      if (il < ig && i < K && kk < Ko) v = W[(((int64_t)l * Ko + kk) * K + i) * K + j];
+      float *base = (float *)(uw + tile * (2LL * uw_rows * ko8 * 4));
+      hi = base + tc::kmaj_off(n, kk, uw_rows) / 4;
+      lo = hi + uw_rows * ko8;
+    }
+    float h, l2;
+    tc::split_tf32(v, h, l2);
+    *hi = h;
+    *lo = l2;
+  }
+}
+
+int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st) {
+  CompView c = comp_view(p, compute);
+  for (auto &L : p.layers) {
+    if (!L.tc) continue;
+    const int64_t n = (int64_t)L.rows * (L.ng * L.fw_rows * p.k + L.ni * L.uw_rows * L.ko8);
+    k_build_tiles<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+        c.w32 + L.w_off, compute + L.fw_off, compute + L.uw_off, L.rows, L.k_out, p.k, L.kg,
+        L.ng, L.fw_rows, L.ig, L.ni, L.uw_rows, L.ko8);
+    count_launch();
+  }
+  return check_cuda(cudaGetLastError(), "build tc tiles");
+}
+
+__device__ __forceinline__ void store_split4(float *hi, float *lo, float4 v) {
+  float4 h, l;
+  tc::split_tf32(v.x, h.x, l.x);
+  tc::split_tf32(v.y, h.y, l.y);
+  tc::split_tf32(v.z, h.z, l.z);
+  tc::split_tf32(v.w, h.w, l.w);
+  *(float4 *)hi = h;
+  *(float4 *)lo = l;
+}
+
+// Issue the 3xTF32 MMAs of one (M=128) x N tile over ksteps K-steps.
+__device__ __forceinline__ void mma_3xtf32(uint32_t d, uint32_t a_hi, uint32_t a_lo, int a_rows,
+                                           uint32_t b_hi, uint32_t b_lo, int b_rows, int N,
+                                           int ksteps, bool accumulate_first) {
+  const uint32_t id = tc::idesc_tf32(TC_M, N);
+  for (int s = 0; s < ksteps; ++s) {
+    const uint64_t ah = tc::kstep_desc(a_hi, a_rows, s), al = tc::kstep_desc(a_lo, a_rows, s);
+    const uint64_t bh = tc::kstep_desc(b_hi, b_rows, s), bl = tc::kstep_desc(b_lo, b_rows, s);
+    tc::mma_tf32(d, ah, bh, id, (s > 0 || accumulate_first) ? 1u : 0u);
+    tc::mma_tf32(d, ah, bl, id, 1u);
+    tc::mma_tf32(d, al, bh, id, 1u);
+  }
+}
+
+// ---- forward: T[b,(kl,i)] = sum_j EB[b,j] W[k,i,j]; out[b,k] = log sum_i EA[b,i] T ----
+// grid (ng, L, bsplit), block 128; weights of (l, g) arrive by one bulk copy.
+template <int K>
+__global__ void __launch_bounds__(128, 1) k_einsum_fwd_tc(
+    const float *__restrict__ EA, const float *__restrict__ EB, WsView ws,
+    const int *__restrict__ out_slab, const uint8_t *__restrict__ tiles, int64_t tile_bytes,
+    int ng, int kg, int rows_tile, int Ko, int64_t B, int tiles_per_split) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t bars[3];
+  __shared__ uint32_t tbase;
+  const int g = blockIdx.x, l = blockIdx.y;
+  const int t = threadIdx.x, w = t >> 5;
+  float *wt = (float *)sm;
+  float *abuf = (float *)(sm + tile_bytes);
+  const int nk = min(kg, Ko - g * kg);
+  const int nmma = (nk * K + 15) / 16 * 16;
+  const int64_t nbt = (B + TC_M - 1) / TC_M;
+  const int64_t j0 = (int64_t)blockIdx.z * tiles_per_split;
+  const int64_t j1 = min(nbt, j0 + tiles_per_split);
+  if (w == 0) tc::tmem_alloc(&tbase, 512);
+  if (t == 0) {
+    tc::mbar_init(&bars[0], 1);
+    tc::mbar_init(&bars[1], 1);
+    tc::mbar_init(&bars[2], 1);
+    tc::mbar_fence_init();
+    tc::mbar_arrive_expect_tx(&bars[0], (uint32_t)tile_bytes);
+    tc::bulk_g2s(wt, tiles + ((int64_t)l * ng + g) * tile_bytes, (uint32_t)tile_bytes, &bars[0]);
+  }
+  const float *EAl = EA + (int64_t)l * ws.bc * K;
+  const float *EBl = EB + (int64_t)l * ws.bc * K;
+  auto build = [&](int buf, int64_t jt) {
+    const int64_t b = jt * TC_M + t;
+    float *ahi = abuf + buf * 2 * TC_M * K;
+    float *alo = ahi + TC_M * K;
+    const float4 *src = (const float4 *)(EBl + (b < B ? b : 0) * K);
+#pragma unroll
+    for (int q = 0; q < K / 4; ++q) {
+      float4 v = b < B ? src[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t o = tc::kmaj_off(t, 4 * q, TC_M) / 4;
+      store_split4(ahi + o, alo + o, v);
+    }
+  };
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+  if (j0 < j1) build(0, j0);
+  int it = 0;
+  for (int64_t jt = j0; jt < j1; ++jt, ++it) {
+    const int buf = it & 1;
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (t == 0) {
+      if (it == 0) tc::mbar_wait(&bars[0], 0);
+      const uint32_t ah = tc::smem_u32(abuf + buf * 2 * TC_M * K);
+      const uint32_t bh = tc::smem_u32(wt);
+      mma_3xtf32(tm + buf * 256, ah, ah + TC_M * K * 4, TC_M, bh, bh + rows_tile * K * 4,
+                 rows_tile, nmma, K / 8, false);
+      tc::mma_commit(&bars[1 + buf]);
+    }
+    if (jt + 1 < j1) build(buf ^ 1, jt + 1);
+    tc::mbar_wait(&bars[1 + buf], (it >> 1) & 1);
+    tc::fence_after();
+    const int64_t b = jt * TC_M + t;
+    const bool live = b < B;
+    float ea[K];
+    {
+      const float4 *src = (const float4 *)(EAl + (live ? b : 0) * K);
+#pragma unroll
+      for (int q = 0; q < K / 4; ++q) {
+        const float4 v = live ? src[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        ea[4 * q] = v.x;
+        ea[4 * q + 1] = v.y;
+        ea[4 * q + 2] = v.z;
+        ea[4 * q + 3] = v.w;
+      }
+    }
+    const uint32_t ta = tm + buf * 256 + ((uint32_t)(32 * w) << 16);
+    float *o = slab_off(ws, out_slab[l], live ? b : 0);
+    for (int kl = 0; kl < nk; ++kl) {
+      float v[K];
+#pragma unroll
+      for (int q = 0; q < K / 8; ++q) {
+        float c8[8];
+        tc::tmem_ld8(ta + kl * K + 8 * q, c8);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[8 * q + u] = c8[u];
+      }
+      tc::tmem_wait_ld();
+      float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < K; i += 2) {
+        acc0 = fmaf(v[i], ea[i], acc0);
+        acc1 = fmaf(v[i + 1], ea[i + 1], acc1);
+      }
+      const float acc = acc0 + acc1;
+      if (live) o[g * kg + kl] = acc > 0.f ? logf(acc) : -CUDART_INF_F;
+    }
+  }
+  if (t == 0 && it == 0) tc::mbar_wait(&bars[0], 0);  // never exit with the copy in flight
+  tc::fence_before();
+  __syncthreads();
+  if (w == 0) tc::tmem_dealloc(tm, 512);
+}
+
+// ---- child responsibilities: U[b,(il,j)] = sum_k RT[b,k] W[k,i,j];
+//      left[b,i] = EA_i sum_j U EB_j, right[b,j] = EB_j sum_i U EA_i
+// grid (ceil(B/128), L), block 128; weight tiles double-buffered by bulk copies.
+template <int K>
+__global__ void __launch_bounds__(128, 1) k_einsum_childrho_tc(
+    const float *__restrict__ EA, const float *__restrict__ EB, const float *__restrict__ RT,
+    WsView ws, const int *__restrict__ slot_left, const int *__restrict__ slot_right,
+    const uint8_t *__restrict__ tiles, int64_t tile_bytes, int ni, int ig, int rows_tile,
+    int ko8, int Ko, int64_t B) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t wbar[2], mbar[2];
+  __shared__ uint32_t tbase;
+  const int l = blockIdx.y;
+  const int t = threadIdx.x, w = t >> 5;
+  float *ahi = (float *)sm;
+  float *alo = ahi + TC_M * ko8;
+  uint8_t *wbuf = sm + 2LL * TC_M * ko8 * 4;
+  const int64_t b = (int64_t)blockIdx.x * TC_M + t;
+  const bool live = b < B;
+  const int64_t row = (int64_t)l * ws.bc + (live ? b : 0);
+  const uint8_t *ltiles = tiles + (int64_t)l * ni * tile_bytes;
+  if (w == 0) tc::tmem_alloc(&tbase, 512);
+  if (t == 0) {
+    for (int q = 0; q < 2; ++q) {
+      tc::mbar_init(&wbar[q], 1);
+      tc::mbar_init(&mbar[q], 1);
+    }
+    tc::mbar_fence_init();
+    for (int h = 0; h < min(2, ni); ++h) {
+      tc::mbar_arrive_expect_tx(&wbar[h], (uint32_t)tile_bytes);
+      tc::bulk_g2s(wbuf + h * tile_bytes, ltiles + h * tile_bytes, (uint32_t)tile_bytes,
+                   &wbar[h]);
+    }
+  }
+  // A operand: the sample's rho/r row (K dim = k, padded to ko8)
+  for (int q = 0; q < ko8 / 4; ++q) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) {
+      const float *src = RT + row * ws.ks + 4 * q;
+      v.x = 4 * q + 0 < Ko ? src[0] : 0.f;
+      v.y = 4 * q + 1 < Ko ? src[1] : 0.f;
+      v.z = 4 * q + 2 < Ko ? src[2] : 0.f;
+      v.w = 4 * q + 3 < Ko ? src[3] : 0.f;
+    }
+    const uint32_t o = tc::kmaj_off(t, 4 * q, TC_M) / 4;
+    store_split4(ahi + o, alo + o, v);
+  }
+  float eb[K], right[K];
+  {
+    const float4 *src = (const float4 *)(EB + row * K);
+#pragma unroll
+    for (int q = 0; q < K / 4; ++q) {
+      const float4 v = live ? src[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      eb[4 * q] = v.x;
+      eb[4 * q + 1] = v.y;
+      eb[4 * q + 2] = v.z;
+      eb[4 * q + 3] = v.w;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) right[j] = 0.f;
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+  const uint32_t a_hi = tc::smem_u32(ahi), a_lo = tc::smem_u32(alo);
+  auto issue = [&](int h) {
+    const int hb = h & 1;
+    const int nil = min(ig, K - h * ig);
+    const int nmma = (nil * K + 15) / 16 * 16;
+    tc::mbar_wait(&wbar[hb], (h >> 1) & 1);
+    const uint32_t bh = tc::smem_u32(wbuf + hb * tile_bytes);
+    mma_3xtf32(tm + hb * 256, a_hi, a_lo, TC_M, bh, bh + rows_tile * ko8 * 4, rows_tile, nmma,
+               ko8 / 8, false);
+    tc::mma_commit(&mbar[hb]);
+  };
+  if (t == 0) issue(0);
+  float *dl = slot_ptr(ws, slot_left[l], live ? b : 0);
+  const float *earow = EA + row * K;
+  for (int h = 0; h < ni; ++h) {
+    const int hb = h & 1;
+    tc::mbar_wait(&mbar[hb], (h >> 1) & 1);
+    if (t == 0) {
+      if (h + 2 < ni) {
+        tc::mbar_arrive_expect_tx(&wbar[hb], (uint32_t)tile_bytes);
+        tc::bulk_g2s(wbuf + hb * tile_bytes, ltiles + (h + 2) * tile_bytes,
+                     (uint32_t)tile_bytes, &wbar[hb]);
+      }
+      if (h + 1 < ni) issue(h + 1);
+    }
+    tc::fence_after();
+    const int nil = min(ig, K - h * ig);
+    const uint32_t ta = tm + hb * 256 + ((uint32_t)(32 * w) << 16);
+    for (int il = 0; il < nil; ++il) {
+      const int i = h * ig + il;
+      float v[K];
+#pragma unroll
+      for (int q = 0; q < K / 8; ++q) {
+        float c8[8];
+        tc::tmem_ld8(ta + il * K + 8 * q, c8);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[8 * q + u] = c8[u];
+      }
+      tc::tmem_wait_ld();
+      const float eai = live ? earow[i] : 0.f;
+      float lacc = 0.f;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        lacc = fmaf(v[j], eb[j], lacc);
+        right[j] = fmaf(v[j], eai, right[j]);
+      }
+      if (live) dl[i] = eai * lacc;
+    }
+    tc::fence_before();
+    __syncthreads();
+  }
+  if (live) {
+    float *dr = slot_ptr(ws, slot_right[l], b);
+#pragma unroll
+    for (int j = 0; j < K; ++j) dr[j] = eb[j] * right[j];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (w == 0) tc::tmem_dealloc(tm, 512);
+}
+
+// ---- W statistics: S[(i,j), k] = sum_b EA[b,i] EB[b,j] RT[b,k] (M = (i,j) rows) ----
+// A = outer-product tile generated in smem, B = RT^T tile; TMEM accumulates
+// WS_DRAIN stages (256 samples) before each fp64 drain. grid (ceil(K^2/128), L, bsplit).
+__global__ void __launch_bounds__(128, 1) k_einsum_wstats_tc(
+    const float *__restrict__ EA, const float *__restrict__ EB, const float *__restrict__ RT,
+    int64_t Bc, int ks, int K, int Ko, int nn, int64_t B, int bsplit, double *wpart, int L) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t mbar[2];
+  __shared__ uint32_t tbase;
+  const int mt = blockIdx.x, l = blockIdx.y, split = blockIdx.z;
+  const int t = threadIdx.x, w = t >> 5;
+  const int KK = K * K;
+  const int m = mt * TC_M + t;
+  const bool mvalid = m < KK;
+  const int mi = mvalid ? m / K : 0, mj = mvalid ? m % K : 0;
+  float *abuf = (float *)sm;                                   // [2][hi|lo][128 x 32]
+  float *bbuf = abuf + 2 * 2 * TC_M * WS_STAGE;                // [2][hi|lo][nn x 32]
+  float *eas = bbuf + 2 * 2 * nn * WS_STAGE;                   // [32][K]
+  float *ebs = eas + WS_STAGE * K;                             // [32][K]
+  double *red = (double *)(ebs + WS_STAGE * K);                // [128][nn]
+  const int64_t per = (B + bsplit - 1) / bsplit;
+  const int64_t bb = split * per, be = min(B, bb + per);
+  const int nstages = (int)((be - bb + WS_STAGE - 1) / WS_STAGE);
+  const float *EAl = EA + (int64_t)l * Bc * K, *EBl = EB + (int64_t)l * Bc * K;
+  const float *RTl = RT + (int64_t)l * Bc * ks;
+  if (w == 0) tc::tmem_alloc(&tbase, nn <= 32 ? 32 : 64);
+  if (t == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::mbar_fence_init();
+  }
+  for (int n = 0; n < nn; ++n) red[t * nn + n] = 0.0;
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+  for (int q = 0; q < nstages; ++q) {
+    const int qb = q & 1;
+    const int64_t b0 = bb + (int64_t)q * WS_STAGE;
+    const int nb = (int)min((int64_t)WS_STAGE, be - b0);
+    if (q >= 2) tc::mbar_wait(&mbar[qb], ((q - 2) >> 1) & 1);
+    // stage EA/EB rows of the 32 samples
+    for (int e = t; e < WS_STAGE * K / 4; e += TC_M) {
+      const int r = e / (K / 4), c4 = e % (K / 4);
+      float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
+      if (r < nb) {
+        va = ((const float4 *)(EAl + (b0 + r) * K))[c4];
+        vb = ((const float4 *)(EBl + (b0 + r) * K))[c4];
+      }
+      ((float4 *)eas)[e] = va;
+      ((float4 *)ebs)[e] = vb;
+    }
+    __syncthreads();
+    // A: outer products of row m over the 32 samples
+    float *ahi = abuf + qb * 2 * TC_M * WS_STAGE, *alo = ahi + TC_M * WS_STAGE;
+#pragma unroll
+    for (int c = 0; c < WS_STAGE / 4; ++c) {
+      float4 v;
+      v.x = mvalid ? eas[(4 * c + 0) * K + mi] * ebs[(4 * c + 0) * K + mj] : 0.f;
+      v.y = mvalid ? eas[(4 * c + 1) * K + mi] * ebs[(4 * c + 1) * K + mj] : 0.f;
+      v.z = mvalid ? eas[(4 * c + 2) * K + mi] * ebs[(4 * c + 2) * K + mj] : 0.f;
+      v.w = mvalid ? eas[(4 * c + 3) * K + mi] * ebs[(4 * c + 3) * K + mj] : 0.f;
+      const uint32_t o = tc::kmaj_off(t, 4 * c, TC_M) / 4;
+      store_split4(ahi + o, alo + o, v);
+    }
+    // B: RT^T tile (n = k, K dim = sample)
+    float *bhi = bbuf + qb * 2 * nn * WS_STAGE, *blo = bhi + nn * WS_STAGE;
+    for (int e = t; e < nn * (WS_STAGE / 4); e += TC_M) {
+      const int n = e / (WS_STAGE / 4), c = e % (WS_STAGE / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (n < Ko) {
+        const int r0 = 4 * c;
+        v.x = r0 + 0 < nb ? RTl[(b0 + r0 + 0) * ks + n] : 0.f;
+        v.y = r0 + 1 < nb ? RTl[(b0 + r0 + 1) * ks + n] : 0.f;
+        v.z = r0 + 2 < nb ? RTl[(b0 + r0 + 2) * ks + n] : 0.f;
+        v.w = r0 + 3 < nb ? RTl[(b0 + r0 + 3) * ks + n] : 0.f;
+      }
+      const uint32_t o = tc::kmaj_off(n, 4 * c, nn) / 4;
+      store_split4(bhi + o, blo + o, v);
+    }
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (t == 0) {
+      const uint32_t ah = tc::smem_u32(ahi), bh = tc::smem_u32(bhi);
+      mma_3xtf32(tm, ah, ah + TC_M * WS_STAGE * 4, TC_M, bh, bh + nn * WS_STAGE * 4, nn, nn,
+                 WS_STAGE / 8, (q % WS_DRAIN) != 0);
+      tc::mma_commit(&mbar[qb]);
+    }
+    if ((q % WS_DRAIN) == WS_DRAIN - 1 || q == nstages - 1) {
+      tc::mbar_wait(&mbar[qb], (q >> 1) & 1);
+      tc::fence_after();
+      const uint32_t ta = tm + ((uint32_t)(32 * w) << 16);
+      for (int c = 0; c < nn; c += 16) {
+        float v[16];
+        tc::tmem_ld16(ta + c, v);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) red[t * nn + c + u] += (double)v[u];
+      }
+      tc::fence_before();
+    }
+  }
+  if (mvalid) {
+    for (int k = 0; k < Ko; ++k)
+      wpart[(((int64_t)split * L + l) * Ko + k) * KK + m] = red[t * nn + k];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (w == 0) tc::tmem_dealloc(tm, nn <= 32 ? 32 : 64);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+template <int K>
+static int fwd_tc(Plan &p, const LayerPlan &L, const uint8_t *compute, const float *EA,
+                  const float *EB, WsView &w, int64_t B, cudaStream_t st) {
+  const int64_t smem = fwd_smem(L.fw_rows, K);
+  cudaFuncSetAttribute(k_einsum_fwd_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  const int64_t nbt = (B + TC_M - 1) / TC_M;
+  const int64_t ctas = (int64_t)L.ng * L.rows;
+  int bs = (int)std::max<int64_t>(1, std::min<int64_t>(nbt, (p.num_sms + ctas - 1) / ctas));
+  const int per = (int)((nbt + bs - 1) / bs);
+  bs = (int)((nbt + per - 1) / per);
+  dim3 grid(L.ng, L.rows, bs);
+  k_einsum_fwd_tc<K><<<grid, 128, smem, st>>>(EA, EB, w, L.d_out_slab, compute + L.fw_off,
+                                              L.fw_tile, L.ng, L.kg, L.fw_rows, L.k_out, B, per);
+  return check_cuda(cudaGetLastError(), "einsum fwd tc");
+}
+
+template <int K>
+static int cr_tc(Plan &p, const LayerPlan &L, const uint8_t *compute, const float *EA,
+                 const float *EB, WsView &w, int64_t B, cudaStream_t st) {
+  (void)p;
+  const int64_t smem = cr_smem(L.uw_rows, L.ko8);
+  cudaFuncSetAttribute(k_einsum_childrho_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  dim3 grid(ceil_div(B, TC_M), L.rows);
+  k_einsum_childrho_tc<K><<<grid, 128, smem, st>>>(
+      EA, EB, w.rt, w, L.d_slot_left, L.d_slot_right, compute + L.uw_off, L.uw_tile, L.ni,
+      L.ig, L.uw_rows, L.ko8, L.k_out, B);
+  return check_cuda(cudaGetLastError(), "einsum child-rho tc");
+}
+
+#define EINET_TC_DISPATCH(FN, ...)                         \
+  switch (p.k) {                                           \
+    case 8: return FN<8>(__VA_ARGS__);                     \
+    case 16: return FN<16>(__VA_ARGS__);                   \
+    case 24: return FN<24>(__VA_ARGS__);                   \
+    case 32: return FN<32>(__VA_ARGS__);                   \
+    case 40: return FN<40>(__VA_ARGS__);                   \
+    case 48: return FN<48>(__VA_ARGS__);                   \
+    case 56: return FN<56>(__VA_ARGS__);                   \
+    case 64: return FN<64>(__VA_ARGS__);                   \
+    default: return fail(EINET_ERR_USAGE, "tc path: unsupported k"); \
+  }
+
+int launch_einsum_fwd_tc(Plan &p, const LayerPlan &L, const uint8_t *compute, const float *EA,
+                         const float *EB, WsView &w, int64_t B, cudaStream_t st) {
+  EINET_TC_DISPATCH(fwd_tc, p, L, compute, EA, EB, w, B, st)
+}
+
+int launch_einsum_childrho_tc(Plan &p, const LayerPlan &L, const uint8_t *compute,
+                              const float *EA, const float *EB, WsView &w, int64_t B,
+                              cudaStream_t st) {
+  EINET_TC_DISPATCH(cr_tc, p, L, compute, EA, EB, w, B, st)
+}
+
+int launch_einsum_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB,
+                            WsView &w, int64_t B, int *bsplit, cudaStream_t st) {
+  const int K = p.k;
+  const int mtiles = ceil_div((int64_t)K * K, TC_M);
+  const int64_t ctas = (int64_t)mtiles * L.rows;
+  const int64_t nst = (B + WS_STAGE - 1) / WS_STAGE;
+  int bs = (int)std::max<int64_t>(1, std::min<int64_t>((p.num_sms + ctas - 1) / ctas,
+                                                        std::min<int64_t>(nst, kMaxBSplit)));
+  const int64_t smem = ws_smem(K, L.nn);
+  cudaFuncSetAttribute(k_einsum_wstats_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  dim3 grid(mtiles, L.rows, bs);
+  k_einsum_wstats_tc<<<grid, 128, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, K, L.k_out, L.nn, B, bs,
+                                              w.wpart, L.rows);
+  *bsplit = bs;
+  return check_cuda(cudaGetLastError(), "einsum wstats tc");
+}
+
 }  // namespace einet

@@ -38,9 +38,9 @@ __global__ void k_prepare_active(const uint8_t *mask, uint8_t *active, int D) {
   if (d < D) active[d] = mask ? (mask[d] ? 0 : 1) : 1;
 }
 
-// phi (D,K,R,2) = (mean, second moment) -> (sa, -mu*sa) and centre mu, [r][d][k]
+// phi (D,K,R,2) = (mean, second moment) -> fp64 (sa, -mu*sa), [r][d][k]
 __global__ void k_prepare_gauss(const double *__restrict__ phi, const uint8_t *active,
-                                float2 *lp, float *center, int D, int K, int R) {
+                                double2 *lp, float *center, int D, int K, int R) {
   int64_t n = (int64_t)R * D * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -51,14 +51,14 @@ __global__ void k_prepare_gauss(const double *__restrict__ phi, const uint8_t *a
     double mu = ph[0];
     double var = ph[1] - mu * mu;
     double sa = sqrt(0.5 / var);
-    float2 v = make_float2(0.f, 0.f);
-    if (active[d]) v = make_float2((float)sa, (float)(-mu * sa));
+    double2 v = make_double2(0.0, 0.0);
+    if (active[d]) v = make_double2(sa, -mu * sa);
     lp[e] = v;
   }
 }
 
 // categorical: log phi per state, [r][d][k][s]; masked variables -> 0
-__global__ void k_prepare_cat(const double *__restrict__ phi, const uint8_t *active, float *lp,
+__global__ void k_prepare_cat(const double *__restrict__ phi, const uint8_t *active, double *lp,
                               int D, int K, int R, int S) {
   int64_t n = (int64_t)R * D * K * S;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -69,13 +69,13 @@ __global__ void k_prepare_cat(const double *__restrict__ phi, const uint8_t *act
     int d = (int)((q / K) % D);
     int r = (int)(q / ((int64_t)K * D));
     double p = phi[(((int64_t)d * K + k) * R + r) * S + s];
-    lp[e] = active[d] ? (float)log(p) : 0.f;
+    lp[e] = active[d] ? log(p) : 0.0;
   }
 }
 
 // binomial: (theta, A) with log p(x) = log h(x) + x*theta + A
 __global__ void k_prepare_binom(const double *__restrict__ phi, const uint8_t *active,
-                                float2 *lp, int D, int K, int R, int n_trials) {
+                                double2 *lp, int D, int K, int R, int n_trials) {
   int64_t n = (int64_t)R * D * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -84,8 +84,8 @@ __global__ void k_prepare_binom(const double *__restrict__ phi, const uint8_t *a
     int r = (int)(e / ((int64_t)K * D));
     double p = phi[((int64_t)d * K + k) * R + r] / (double)n_trials;
     double l1 = log1p(-p);
-    float2 v = make_float2(0.f, 0.f);
-    if (active[d]) v = make_float2((float)(log(p) - l1), (float)(n_trials * l1));
+    double2 v = make_double2(0.0, 0.0);
+    if (active[d]) v = make_double2(log(p) - l1, n_trials * l1);
     lp[e] = v;
   }
 }
@@ -151,13 +151,13 @@ int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_
   k_prepare_active<<<ceil_div(D, 256), 256, 0, st>>>(mask, c.active, D);
   const int64_t rdk = (int64_t)R * D * K;
   if (p.family == EINET_FAMILY_GAUSSIAN) {
-    k_prepare_gauss<<<grid_for(rdk), 256, 0, st>>>(phi, c.active, (float2 *)c.leafp,
+    k_prepare_gauss<<<grid_for(rdk), 256, 0, st>>>(phi, c.active, (double2 *)c.leafp,
                                                    c.center, D, K, R);
   } else if (p.family == EINET_FAMILY_CATEGORICAL) {
-    k_prepare_cat<<<grid_for(rdk * p.num_states), 256, 0, st>>>(phi, c.active, (float *)c.leafp,
+    k_prepare_cat<<<grid_for(rdk * p.num_states), 256, 0, st>>>(phi, c.active, (double *)c.leafp,
                                                                D, K, R, p.num_states);
   } else {
-    k_prepare_binom<<<grid_for(rdk), 256, 0, st>>>(phi, c.active, (float2 *)c.leafp, D, K, R,
+    k_prepare_binom<<<grid_for(rdk), 256, 0, st>>>(phi, c.active, (double2 *)c.leafp, D, K, R,
                                                    p.n_trials);
     k_prepare_logh<<<ceil_div(p.n_trials + 1, 256), 256, 0, st>>>(c.logh, p.n_trials);
     count_launch();
@@ -170,6 +170,8 @@ int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_
     count_launch();
   }
   count_launch((p.n_w ? 1 : 0) + (p.n_mix ? 1 : 0) + 3);
+  int rc = launch_prepare_tc_tiles(p, compute, st);
+  if (rc) return rc;
   return check_cuda(cudaGetLastError(), "prepare kernels");
 }
 
@@ -185,20 +187,26 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Gaussian: Q[b,l,k] = sum_{d in scope} (x_bd*sa_dk + nmsa_dk)^2 (fp32 chunks -> fp64).
+// Gaussian: Q[b,l,k] = sum_{d in scope} (x_bd*sa_dk + nmsa_dk)^2 with two fp64 FMAs
+// per term (B200 FP64 runs at half the FP32 rate): the leaf rows, whose
+// differences drive every posterior, stay exact to ~1e-12 even at |log p| ~ 1e4.
 // grid (ceil(B/128), n_leaf, dsplit*nkc), block 32*KG threads (KG = ceil(K/8) <= 8).
 // Chunks of 32 scope variables are gathered with cp.async into a double buffer
-// so the next chunk's loads overlap the current chunk's FFMAs.
+// so the next chunk's loads overlap the current chunk's FMAs.
 __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
     const float *__restrict__ x, int64_t B, int D, int K, int R,
     const int *__restrict__ scope_off, const int *__restrict__ scope_vars,
-    const int *__restrict__ leaf_rep, const float2 *__restrict__ lp,
+    const int *__restrict__ leaf_rep, const double2 *__restrict__ lp,
     const uint8_t *__restrict__ active, double *__restrict__ part, int64_t Bc, int n_leaf,
     int dsplit, int32_t *status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -206,7 +214,7 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
   const int KP = KG * LF_KPT;
   constexpr int XS = LF_VC * (LF_TB + 1);                      // floats per x buffer
   float *xs = (float *)smem_raw;                               // [2][VC][TB+1]
-  float2 *ps = (float2 *)(smem_raw + ((2 * XS * 4 + 15) & ~15));  // [2][VC][KP]
+  double2 *ps = (double2 *)(smem_raw + ((2 * XS * 4 + 15) & ~15));  // [2][VC][KP]
   const int nkc = gridDim.z / dsplit;  // k chunks of KP entries
   const int leaf = blockIdx.y, split = blockIdx.z / nkc;
   const int kbase = (blockIdx.z % nkc) * KP;
@@ -233,13 +241,13 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
     } else {
       for (int bl = kq; bl < LF_TB; bl += KG) xb[v * (LF_TB + 1) + bl] = 0.f;
     }
-    float2 *pb = ps + buf * LF_VC * KP;
+    double2 *pb = ps + buf * LF_VC * KP;
     for (int e = threadIdx.x; e < LF_VC * KP; e += blockDim.x) {
       const int vv = e / KP, k = e % KP;
       if (vv < nv && kbase + k < K)
-        cp_async8(pb + e, lp + ((int64_t)r * D + scope_vars[sbeg + c0 + vv]) * K + kbase + k);
+        cp_async16(pb + e, lp + ((int64_t)r * D + scope_vars[sbeg + c0 + vv]) * K + kbase + k);
       else
-        pb[e] = make_float2(0.f, 0.f);
+        pb[e] = make_double2(0.0, 0.0);
     }
     cp_async_commit();
   };
@@ -260,15 +268,11 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
     }
   };
 
-  float acc[LF_NS][LF_KPT];
   double tot[LF_NS][LF_KPT];
 #pragma unroll
   for (int s = 0; s < LF_NS; ++s)
 #pragma unroll
-    for (int j = 0; j < LF_KPT; ++j) {
-      acc[s][j] = 0.f;
-      tot[s][j] = 0.0;
-    }
+    for (int j = 0; j < LF_KPT; ++j) tot[s][j] = 0.0;
 
   if (vbeg < vend) stage(0, vbeg);
   int it = 0;
@@ -284,31 +288,22 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
     fixup(buf, c0);
     __syncthreads();
     const float *xb = xs + buf * XS;
-    const float2 *pb = ps + buf * LF_VC * KP;
+    const double2 *pb = ps + buf * LF_VC * KP;
     for (int v = 0; v < nv; ++v) {
-      float xv[LF_NS];
+      double xv[LF_NS];
 #pragma unroll
-      for (int s = 0; s < LF_NS; ++s) xv[s] = xb[v * (LF_TB + 1) + lane + 32 * s];
-      const float4 *pp = (const float4 *)(pb + v * KP + kq * LF_KPT);
+      for (int s = 0; s < LF_NS; ++s) xv[s] = (double)xb[v * (LF_TB + 1) + lane + 32 * s];
+      const double2 *pp = pb + v * KP + kq * LF_KPT;
 #pragma unroll
-      for (int j2 = 0; j2 < LF_KPT / 2; ++j2) {
-        const float4 q = pp[j2];
+      for (int j = 0; j < LF_KPT; ++j) {
+        const double2 q = pp[j];
 #pragma unroll
         for (int s = 0; s < LF_NS; ++s) {
-          float t0 = fmaf(xv[s], q.x, q.y);
-          float t1 = fmaf(xv[s], q.z, q.w);
-          acc[s][2 * j2] = fmaf(t0, t0, acc[s][2 * j2]);
-          acc[s][2 * j2 + 1] = fmaf(t1, t1, acc[s][2 * j2 + 1]);
+          const double t = fma(xv[s], q.x, q.y);
+          tot[s][j] = fma(t, t, tot[s][j]);
         }
       }
     }
-#pragma unroll
-    for (int s = 0; s < LF_NS; ++s)
-#pragma unroll
-      for (int j = 0; j < LF_KPT; ++j) {
-        tot[s][j] += (double)acc[s][j];
-        acc[s][j] = 0.f;
-      }
     __syncthreads();
   }
 #pragma unroll
@@ -340,14 +335,9 @@ __global__ void __launch_bounds__(1024) k_leaf_fwd_discrete(
   const int64_t b = (int64_t)blockIdx.x * 32 + lane;
   const bool live = b < B;
   const int top = family == EINET_FAMILY_CATEGORICAL ? S - 1 : n_trials;
-  float acc[LF_KPT];
   double tot[LF_KPT];
 #pragma unroll
-  for (int j = 0; j < LF_KPT; ++j) {
-    acc[j] = 0.f;
-    tot[j] = 0.0;
-  }
-  int cnt = 0;
+  for (int j = 0; j < LF_KPT; ++j) tot[j] = 0.0;
   for (int q = vbeg; q < vend; ++q) {
     const int d = scope_vars[sbeg + q];
     if (!active[d] || !live) continue;
@@ -357,31 +347,23 @@ __global__ void __launch_bounds__(1024) k_leaf_fwd_discrete(
     const int xi = ok ? (int)xv : 0;
     const int64_t base = ((int64_t)r * D + d) * K;
     if (family == EINET_FAMILY_CATEGORICAL) {
-      const float *lp = (const float *)lpv;
+      const double *lp = (const double *)lpv;
 #pragma unroll
       for (int j = 0; j < LF_KPT; ++j) {
         const int k = kq * LF_KPT + j;
-        if (k < K) acc[j] += lp[(base + k) * S + xi];
+        if (k < K) tot[j] += lp[(base + k) * S + xi];
       }
     } else {
-      const float2 *lp = (const float2 *)lpv;
-      const float h = (float)logh[xi];
-      const float xf = (float)xi;
+      const double2 *lp = (const double2 *)lpv;
+      const double h = logh[xi];
+      const double xf = (double)xi;
 #pragma unroll
       for (int j = 0; j < LF_KPT; ++j) {
         const int k = kq * LF_KPT + j;
         if (k < K) {
-          const float2 t = lp[base + k];
-          acc[j] += fmaf(xf, t.x, t.y) + h;
+          const double2 t = lp[base + k];
+          tot[j] += fma(xf, t.x, t.y) + h;
         }
-      }
-    }
-    if (++cnt == LF_VC) {
-      cnt = 0;
-#pragma unroll
-      for (int j = 0; j < LF_KPT; ++j) {
-        tot[j] += (double)acc[j];
-        acc[j] = 0.f;
       }
     }
   }
@@ -390,7 +372,7 @@ __global__ void __launch_bounds__(1024) k_leaf_fwd_discrete(
 #pragma unroll
   for (int j = 0; j < LF_KPT; ++j) {
     const int k = kq * LF_KPT + j;
-    if (k < K) dst[k] = tot[j] + (double)acc[j];
+    if (k < K) dst[k] = tot[j];
   }
 }
 
@@ -439,14 +421,14 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
     const int threads = 32 * kg;
     ds = leaf_dsplit(p, B, LF_TB);
     const size_t smem = ((2 * LF_VC * (LF_TB + 1) * sizeof(float) + 15) & ~(size_t)15) +
-                        2 * sizeof(float2) * LF_VC * kg * LF_KPT;
+                        2 * sizeof(double2) * LF_VC * kg * LF_KPT;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_leaf_fwd_gauss, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
     dim3 grid(ceil_div(B, LF_TB), p.n_leaf, ds * nkc);
     k_leaf_fwd_gauss<<<grid, threads, smem, st>>>(
         x, B, p.d_vars, p.k, p.num_replicas, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
-        (const float2 *)c.leafp, c.active, w.leafpart, w.bc, p.n_leaf, ds, status);
+        (const double2 *)c.leafp, c.active, w.leafpart, w.bc, p.n_leaf, ds, status);
   } else {
     const int threads = 32 * KG;
     if (threads > 1024) return fail(EINET_ERR_USAGE, "k too large for the leaf kernel (k <= 256)");

@@ -226,12 +226,4 @@ int launch_status_reset(int32_t *status, cudaStream_t st) {
   return check_cuda(cudaGetLastError(), "status reset");
 }
 
-// Tensor-core EinsumLayer path: not enabled in this build; the CUDA-core
-// kernels handle every layer.
-int launch_einsum_tc_forward(Plan &, const LayerPlan &, const float *, WsView &, int64_t,
-                             int32_t *, cudaStream_t, bool *handled) {
-  *handled = false;
-  return EINET_OK;
-}
-
 }  // namespace einet

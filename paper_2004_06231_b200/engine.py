@@ -186,6 +186,11 @@ class _Engine:
             except Exception:
                 pass
 
+    def set_tensor_cores(self, enabled: bool):
+        """Route eligible EinsumLayers to the tcgen05 kernels (default) or not."""
+        _native.check(self._lib.einet_plan_set_tensor_cores(self.handle, 1 if enabled else 0),
+                      "einet_plan_set_tensor_cores")
+
     # -- buffers ---------------------------------------------------------
     def new_workspace(self):
         return torch.empty(int(self.sizes.workspace_bytes), dtype=torch.uint8,

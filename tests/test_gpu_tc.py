@@ -24,3 +24,76 @@ def test_selftest_tf32_gemm(n, k):
     want = a.double() @ b.double().T
     err = ((d.double() - want).abs() / want.abs().clamp_min(1e-30)).max().item()
     assert err < 2e-6, err
+
+
+import numpy as np
+
+import paper_2004_06231_b200 as E
+from paper_2004_06231_b200 import engine, trainer
+from paper_2004_06231_b200.structures import StructureConfig
+from oracle import einet_oracle as O
+from tests.helpers import close
+
+
+def _pd_model(k, seed=0, both=True):
+    rg = E.lift_channels(E.poon_domingos(8, 8, StructureConfig(
+        deltas=(4,), axes="both" if both else "vertical")), 3)
+    fam = E.GaussianFamily(var_max=1e-2)
+    rng = np.random.default_rng(seed)
+    x = np.round(np.clip(rng.normal(0.5, 0.2, (300, rg.d_vars)) + rng.normal(0, 0.15, (300, 1)),
+                         0, 1) * 255) / 255
+    x = x.astype(np.float32).astype(np.float64)
+    circuit = E.compile_graph(rg, k)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=seed, data=x)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    op = O.OracleParams({i: f32(w) for i, w in ein.items()}, {i: f32(w) for i, w in mix.items()},
+                        f32(phi))
+    return circuit, fam, x, op
+
+
+def _run(circuit, fam, x, op, tc):
+    eng = engine.get_engine(circuit, fam, len(x))
+    eng.set_tensor_cores(tc)
+    p = engine.Parameters.from_numpy(circuit, fam, op.einsum, op.mixing, op.phi)
+    tr = engine.forward(circuit, p, fam, x)
+    st = engine.backward(circuit, p, fam, tr)
+    return tr.log_likelihood, st
+
+
+@pytest.mark.parametrize("k", [8, 16, 24, 32, 40, 48, 64])
+def test_tensor_core_einsum_matches_simt_and_oracle(k):
+    circuit, fam, x, op = _pd_model(k, seed=k)
+    assert any(getattr(L, "k_out", 0) for L in circuit.layers[1:])
+    ll_tc, st_tc = _run(circuit, fam, x, op, True)
+    ll_s, st_s = _run(circuit, fam, x, op, False)
+    otr = O.forward(circuit, op, fam.to_dict(), x)
+    ost = O.backward(circuit, op, fam.to_dict(), otr)
+    want = otr.log_likelihood
+    assert np.all(np.abs(ll_tc - want) <= 1e-4 * np.maximum(np.abs(want), 1))
+    assert np.all(np.abs(ll_tc - ll_s) <= 2e-6 * np.maximum(np.abs(ll_s), 1))
+    B = len(x)
+    for i in ost.einsum:
+        close(st_tc.einsum[i], ost.einsum[i], 1e-4, 1e-6 * B)
+        close(st_tc.einsum[i], st_s.einsum[i], 1e-5, 1e-8 * B)
+    for i in ost.mixing:
+        close(st_tc.mixing[i], ost.mixing[i], 1e-4, 1e-6 * B)
+    close(st_tc.acc_p, ost.acc_p, 1e-4, 1e-6 * B)
+    close(st_tc.acc_pt, ost.acc_pt, 1e-4, 1e-6 * B)
+
+
+def test_tensor_core_em_step_matches_oracle():
+    circuit, fam, x, op = _pd_model(40, seed=3, both=False)
+    eng = engine.get_engine(circuit, fam, len(x))
+    eng.set_tensor_cores(True)
+    model = E.EinetModel(circuit, engine.Parameters.from_numpy(circuit, fam, op.einsum,
+                                                               op.mixing, op.phi), fam)
+    for _ in range(3):
+        want_ll, op = O.em_step(circuit, op, fam.to_dict(), x, 0.5)
+        ll = trainer.em_stochastic_step(model, x, 0.5)
+        assert abs(ll - want_ll) <= 1e-4 * abs(want_ll)
+    e2, m2, phi2 = model.params.to_numpy()
+    for i in e2:
+        close(e2[i], op.einsum[i], 1e-4, 1e-9)
+    for i in m2:
+        close(m2[i], op.mixing[i], 1e-4, 1e-9)
+    close(phi2, op.phi, 1e-4, 1e-9)
