@@ -172,7 +172,8 @@ int einet_log_einsum_exp(const double *left, const double *right, const double *
                          double *out, void *stream);
 
 /* Diagnostic: D[128 x N] = A[128 x K] B[N x K]^T (fp32, row-major, device) on
- * one CTA with tcgen05 3xTF32 MMAs; validates the tensor-core plumbing. */
+ * one CTA with tcgen05 3xTF32 MMAs; validates the tensor-core plumbing.
+ * Passing -N stages A in tensor memory (tcgen05.st) instead of shared memory. */
 int einet_selftest_tf32_gemm(const float *A, const float *B, float *D, int32_t N, int32_t K,
                              void *stream);
 

@@ -313,7 +313,8 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   }
   z.compute_bytes = off;
 
-  const int64_t Bc = max_chunk, KS = p->ks;
+  p->bc = align_up(max_chunk, 32);  // per-sample arrays use 32-sample blocks
+  const int64_t Bc = p->bc, KS = p->ks;
   off = 0;
   p->w_off = seg(4 * (int64_t)p->num_slabs * Bc * KS);
   p->w_shift = seg(8 * (int64_t)p->num_slabs * Bc);
@@ -332,7 +333,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
                                    std::min<int64_t>(kMaxBSplit, (Bc + 63) / 64));
     // tensor-core W statistics split their batch as well (einsum_tc.cu)
     int64_t tc_blocks = (int64_t)((K * K + 127) / 128) * L.rows;
-    int64_t tc_bs = std::max<int64_t>(1, std::min<int64_t>((p->num_sms + tc_blocks - 1) / tc_blocks,
+    int64_t tc_bs = std::max<int64_t>(1, std::min<int64_t>((2 * p->num_sms + tc_blocks - 1) / tc_blocks,
                                                           std::min<int64_t>((Bc + 31) / 32,
                                                                             kMaxBSplit)));
     wpart = std::max(wpart, std::max(bs, tc_bs) * lw);
@@ -344,6 +345,8 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   p->w_ppart = seg(8 * (int64_t)ceil_div(Bc, 128) * p->n_leaf * K);
   p->w_mixpart = seg(8 * (int64_t)ceil_div(Bc, 64) * std::max<int64_t>(p->n_mix, 1));
   p->w_llpart = seg(8 * (int64_t)ceil_div(Bc, 256));
+  p->w_tmp_s = seg(8 * p->n_phi);
+  p->w_tmp_p = seg(8 * (int64_t)p->n_leaf * K);
   p->w_scratch_end = off;
   z.workspace_bytes = off;
 

@@ -84,8 +84,9 @@ struct Plan {
   // workspace segments (byte offsets)
   int64_t w_off = 0, w_shift = 0, w_slots = 0, w_leafpart = 0, w_ea = 0, w_eb = 0,
           w_rt = 0, w_wpart = 0, w_rho = 0, w_lspart = 0, w_ppart = 0, w_mixpart = 0,
-          w_llpart = 0, w_scratch_end = 0;
+          w_llpart = 0, w_tmp_s = 0, w_tmp_p = 0, w_scratch_end = 0;
   int64_t max_chunk = 0;
+  int64_t bc = 0;                  // per-chunk sample stride (max_chunk rounded to 32)
   int num_sms = 148;
   int max_lsplit = 1;              // leaf-statistics batch split allocated
   int n_erows = 0;                 // einsum rows over all layers
@@ -156,6 +157,12 @@ int launch_log_einsum_exp(const double *left, const double *right, const double 
 // deterministic reduction: dst[i] += (scale ? scale[i] : 1) * sum_p part[p*stride+i]
 void launch_reduce_partials(double *dst, const double *part, int nparts, int64_t n,
                             int64_t stride, const double *scale, cudaStream_t st);
+// same, overwriting: dst[i] = sum_p part[p*stride+i]
+void launch_reduce_partials_store(double *dst, const double *part, int nparts, int64_t n,
+                                  int64_t stride, cudaStream_t st);
+bool leaf_tc_supported(const Plan &p);
+int launch_leaf_stats_tc(Plan &p, const uint8_t *compute, const float *x, int64_t B,
+                         uint8_t *wsb, double *stats, const double *Pcall, cudaStream_t st);
 
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

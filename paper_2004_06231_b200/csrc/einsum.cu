@@ -44,7 +44,6 @@ __global__ void k_einsum_prep_fwd(WsView ws, const int *__restrict__ left_slab,
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const int64_t row = (int64_t)l * ws.bc + b;
   bool nan = false, dead = false;
   double shift = 0.0;
   for (int side = 0; side < 2; ++side) {
@@ -61,8 +60,8 @@ __global__ void k_einsum_prep_fwd(WsView ws, const int *__restrict__ left_slab,
     const bool d = s == -CUDART_INF || mx == -CUDART_INF_F;
     dead |= d;
     shift += s + (double)mx;
-    float *dst = (side ? EB : EA) + row * K;
-    for (int i = 0; i < K; ++i) dst[i] = d ? 0.f : expf(o[i] - mx);
+    float *dst = side ? EB : EA;
+    for (int i = 0; i < K; ++i) dst[tb_idx(l, b, i, ws.bc, K)] = d ? 0.f : expf(o[i] - mx);
   }
   if (nan) atomicMin(&status[1], layer_index);
   slab_shift(ws, out_slab[l])[b] = dead ? -CUDART_INF : shift;
@@ -110,12 +109,12 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const float *__
   stage_w(wsm, W + (int64_t)l * Ko * K * K, k0, nk, K, KT);
   const int64_t b = (int64_t)blockIdx.x * EF_TB + threadIdx.x;
   const bool live = b < B;
-  const int64_t row = (int64_t)l * ws.bc + (live ? b : 0);
+  const int64_t bb = live ? b : 0;
   float ea[KT], eb[KT];
 #pragma unroll
   for (int i = 0; i < KT; ++i) {
-    ea[i] = (live && i < K) ? EA[row * K + i] : 0.f;
-    eb[i] = (live && i < K) ? EB[row * K + i] : 0.f;
+    ea[i] = (live && i < K) ? EA[tb_idx(l, bb, i, ws.bc, K)] : 0.f;
+    eb[i] = (live && i < K) ? EB[tb_idx(l, bb, i, ws.bc, K)] : 0.f;
   }
   __syncthreads();
   if (!live) return;
@@ -137,16 +136,15 @@ __global__ void k_einsum_fwd_generic(WsView ws, const float *__restrict__ EA,
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const int64_t row = (int64_t)l * ws.bc + b;
-  const float *ea = EA + row * K, *eb = EB + row * K;
   float *o = slab_off(ws, out_slab[l], b);
   const float *Wl = W + (int64_t)l * Ko * K * K;
   for (int k = 0; k < Ko; ++k) {
     float acc = 0.f;
     for (int i = 0; i < K; ++i) {
       float t = 0.f;
-      for (int j = 0; j < K; ++j) t = fmaf(Wl[((int64_t)k * K + i) * K + j], eb[j], t);
-      acc = fmaf(ea[i], t, acc);
+      for (int j = 0; j < K; ++j)
+        t = fmaf(Wl[((int64_t)k * K + i) * K + j], EB[tb_idx(l, b, j, ws.bc, K)], t);
+      acc = fmaf(EA[tb_idx(l, b, i, ws.bc, K)], t, acc);
     }
     o[k] = acc > 0.f ? logf(acc) : -CUDART_INF_F;
   }
@@ -259,15 +257,13 @@ __global__ void k_einsum_bwd_rt(WsView ws, const int *out_slab, const int *csr_o
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const int64_t row = (int64_t)l * ws.bc + b;
   const int os = out_slab[l];
   const double so = slab_shift(ws, os)[b];
   const float *oo = slab_off(ws, os, b);
-  float *rt = RT + row * ws.ks;
   for (int k = 0; k < Ko; ++k) {
     const float r = so == -CUDART_INF ? 0.f : expf(oo[k]);
     const float rho = gather_rho(ws, csr_off, csr_slot, ones, os, b, k);
-    rt[k] = r > 0.f ? rho / r : 0.f;
+    RT[tb_idx(l, b, k, ws.bc, ws.ks)] = r > 0.f ? rho / r : 0.f;
   }
 }
 
@@ -305,12 +301,11 @@ __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__res
     for (int e = threadIdx.x; e < WS_BT * KP; e += blockDim.x) {
       const int bl = e / KP, i = e % KP;
       const bool ok = bl < nb && i < K;
-      const int64_t row = (int64_t)l * Bc + t + bl;
-      ea_s[e] = ok ? EA[row * K + i] : 0.f;
-      eb_s[e] = ok ? EB[row * K + i] : 0.f;
+      ea_s[e] = ok ? EA[tb_idx(l, t + bl, i, Bc, K)] : 0.f;
+      eb_s[e] = ok ? EB[tb_idx(l, t + bl, i, Bc, K)] : 0.f;
     }
     for (int e = threadIdx.x; e < WS_BT; e += blockDim.x)
-      rt_s[e] = e < nb ? RT[((int64_t)l * Bc + t + e) * ks + k] : 0.f;
+      rt_s[e] = e < nb ? RT[tb_idx(l, t + e, k, Bc, ks)] : 0.f;
     __syncthreads();
     for (int bl = 0; bl < nb; ++bl) {
       const float r = rt_s[bl];
@@ -351,12 +346,12 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_childrho(
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * EF_TB + threadIdx.x;
   const bool live = b < B;
-  const int64_t row = (int64_t)l * ws.bc + (live ? b : 0);
+  const int64_t bb = live ? b : 0;
   float ea[KT], eb[KT], left[KT], right[KT];
 #pragma unroll
   for (int i = 0; i < KT; ++i) {
-    ea[i] = (live && i < K) ? EA[row * K + i] : 0.f;
-    eb[i] = (live && i < K) ? EB[row * K + i] : 0.f;
+    ea[i] = (live && i < K) ? EA[tb_idx(l, bb, i, ws.bc, K)] : 0.f;
+    eb[i] = (live && i < K) ? EB[tb_idx(l, bb, i, ws.bc, K)] : 0.f;
     left[i] = 0.f;
     right[i] = 0.f;
   }
@@ -368,7 +363,7 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_childrho(
     __syncthreads();
     if (!live) continue;
     for (int kk = 0; kk < nk; ++kk) {
-      const float rt = RT[row * ws.ks + k0 + kk];
+      const float rt = RT[tb_idx(l, bb, k0 + kk, ws.bc, ws.ks)];
       if (rt == 0.f) continue;
       const float *wk = wsm + kk * K * KT;
 #pragma unroll
@@ -408,27 +403,28 @@ __global__ void k_einsum_childrho_generic(const float *__restrict__ EA,
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const int64_t row = (int64_t)l * ws.bc + b;
-  const float *ea = EA + row * K, *eb = EB + row * K, *rt = RT + row * ws.ks;
+  auto ea = [&](int i) { return EA[tb_idx(l, b, i, ws.bc, K)]; };
+  auto eb = [&](int i) { return EB[tb_idx(l, b, i, ws.bc, K)]; };
+  auto rt = [&](int k) { return RT[tb_idx(l, b, k, ws.bc, ws.ks)]; };
   const float *Wl = W + (int64_t)l * Ko * K * K;
   float *dl = slot_ptr(ws, slot_left[l], b), *dr = slot_ptr(ws, slot_right[l], b);
   for (int i = 0; i < K; ++i) {
     float acc = 0.f;
     for (int k = 0; k < Ko; ++k) {
       float t = 0.f;
-      for (int j = 0; j < K; ++j) t = fmaf(Wl[((int64_t)k * K + i) * K + j], eb[j], t);
-      acc = fmaf(rt[k], t, acc);
+      for (int j = 0; j < K; ++j) t = fmaf(Wl[((int64_t)k * K + i) * K + j], eb(j), t);
+      acc = fmaf(rt(k), t, acc);
     }
-    dl[i] = ea[i] * acc;
+    dl[i] = ea(i) * acc;
   }
   for (int j = 0; j < K; ++j) {
     float acc = 0.f;
     for (int k = 0; k < Ko; ++k) {
       float t = 0.f;
-      for (int i = 0; i < K; ++i) t = fmaf(Wl[((int64_t)k * K + i) * K + j], ea[i], t);
-      acc = fmaf(rt[k], t, acc);
+      for (int i = 0; i < K; ++i) t = fmaf(Wl[((int64_t)k * K + i) * K + j], ea(i), t);
+      acc = fmaf(rt(k), t, acc);
     }
-    dr[j] = eb[j] * acc;
+    dr[j] = eb(j) * acc;
   }
 }
 

@@ -18,7 +18,7 @@ namespace einet {
 __global__ void __launch_bounds__(128) k_selftest_gemm(const float *__restrict__ A,
                                                        const float *__restrict__ B,
                                                        float *__restrict__ D, int N, int K,
-                                                       uint32_t tcols) {
+                                                       uint32_t tcols, int a_in_tmem) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
@@ -50,7 +50,34 @@ __global__ void __launch_bounds__(128) k_selftest_gemm(const float *__restrict__
   __syncthreads();
   tc::fence_after();
   const uint32_t tm = tbase;
-  if (t == 0) {
+  if (a_in_tmem) {
+    // A_hi at columns [256, 256+K), A_lo at [256+K, 256+2K) (lane = row)
+    const uint32_t ta = tm + 256 + ((uint32_t)(32 * (t >> 5)) << 16);
+    for (int c = 0; c < K; c += 16) {
+      float h[16], l[16];
+      for (int u = 0; u < 16; ++u) {
+        const float v = c + u < K ? A[t * K + c + u] : 0.f;
+        tc::split_tf32(v, h[u], l[u]);
+      }
+      tc::tmem_st16(ta + c, h);
+      tc::tmem_st16(ta + K + c, l);
+    }
+    tc::tmem_wait_st();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (t == 0) {
+      const uint32_t id = tc::idesc_tf32(128, N);
+      const uint32_t sb = tc::smem_u32(bhi), sbl = tc::smem_u32(blo);
+      for (int s = 0; s < K / 8; ++s) {
+        const uint32_t ah = tm + 256 + 8 * s, al = tm + 256 + K + 8 * s;
+        tc::mma_tf32_ts(tm, ah, tc::kstep_desc(sb, N, s), id, s > 0);
+        tc::mma_tf32_ts(tm, ah, tc::kstep_desc(sbl, N, s), id, 1);
+        tc::mma_tf32_ts(tm, al, tc::kstep_desc(sb, N, s), id, 1);
+      }
+      tc::mma_commit(&bar);
+    }
+  } else if (t == 0) {
     const uint32_t id = tc::idesc_tf32(128, N);
     const uint32_t sa = tc::smem_u32(ahi), sl = tc::smem_u32(alo);
     const uint32_t sb = tc::smem_u32(bhi), sbl = tc::smem_u32(blo);
@@ -80,13 +107,15 @@ __global__ void __launch_bounds__(128) k_selftest_gemm(const float *__restrict__
 
 int launch_selftest_gemm(const float *A, const float *B, float *D, int N, int K,
                          cudaStream_t st) {
-  if (N < 16 || N > 256 || N % 16 || K < 8 || K % 8)
+  const int a_tmem = N < 0;
+  if (a_tmem) N = -N;
+  if (N < 16 || N > 256 || N % 16 || K < 8 || K % 8 || (a_tmem && 2 * K > 256))
     return fail(EINET_ERR_USAGE, "selftest gemm: N in [16,256] multiple of 16, K multiple of 8");
-  uint32_t cols = 32;
+  uint32_t cols = a_tmem ? 512 : 32;
   while (cols < (uint32_t)N) cols *= 2;
   const size_t smem = sizeof(float) * 2 * (128 + N) * K;
   cudaFuncSetAttribute(k_selftest_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_selftest_gemm<<<1, 128, smem, st>>>(A, B, D, N, K, cols);
+  k_selftest_gemm<<<1, 128, smem, st>>>(A, B, D, N, K, cols, a_tmem);
   count_launch();
   return check_cuda(cudaGetLastError(), "selftest gemm");
 }
@@ -108,9 +137,8 @@ static int64_t fwd_smem(int rows_tile, int K) {
 static int64_t cr_smem(int rows_tile, int ko8) {
   return 2LL * TC_M * ko8 * 4 + 2LL * (2LL * rows_tile * ko8 * 4);
 }
-static int64_t ws_smem(int K, int nn) {
-  return 2LL * 2 * TC_M * WS_STAGE * 4 + 2LL * 2 * nn * WS_STAGE * 4 + 2LL * WS_STAGE * K * 4 +
-         (int64_t)TC_M * nn * 8;
+static int64_t ws_smem(int K, int nn) {  // W-statistics kernel (staging + B tiles)
+  return 2LL * (2 * K + nn) * WS_STAGE * 4 + 2LL * 2 * nn * WS_STAGE * 4;
 }
 
 void plan_tc_tiling(Plan &p) {
@@ -118,7 +146,7 @@ void plan_tc_tiling(Plan &p) {
   for (auto &L : p.layers) {
     L.tc = 0;
     if (L.kind != EINET_LAYER_EINSUM) continue;
-    if (K % 8 != 0 || K < 8 || K > 64) continue;
+    if (K % 8 != 0 || K < 8 || K > 64 || p.ks % 4 != 0) continue;
     const int Ko = L.k_out;
     int kg = std::max(1, std::min(Ko, 256 / K));
     while (kg > 1 && fwd_smem(round_up(kg * K, 16), K) > TC_SMEM_MAX) --kg;
@@ -248,16 +276,17 @@ __global__ void __launch_bounds__(128, 1) k_einsum_fwd_tc(
     tc::mbar_arrive_expect_tx(&bars[0], (uint32_t)tile_bytes);
     tc::bulk_g2s(wt, tiles + ((int64_t)l * ng + g) * tile_bytes, (uint32_t)tile_bytes, &bars[0]);
   }
-  const float *EAl = EA + (int64_t)l * ws.bc * K;
-  const float *EBl = EB + (int64_t)l * ws.bc * K;
   auto build = [&](int buf, int64_t jt) {
     const int64_t b = jt * TC_M + t;
+    const bool ok = b < B;
+    const float *src = EB + tb_idx(l, ok ? b : 0, 0, ws.bc, K);
     float *ahi = abuf + buf * 2 * TC_M * K;
     float *alo = ahi + TC_M * K;
-    const float4 *src = (const float4 *)(EBl + (b < B ? b : 0) * K);
 #pragma unroll
     for (int q = 0; q < K / 4; ++q) {
-      float4 v = b < B ? src[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok) v = make_float4(src[(4 * q) * 32], src[(4 * q + 1) * 32], src[(4 * q + 2) * 32],
+                              src[(4 * q + 3) * 32]);
       const uint32_t o = tc::kmaj_off(t, 4 * q, TC_M) / 4;
       store_split4(ahi + o, alo + o, v);
     }
@@ -289,15 +318,9 @@ __global__ void __launch_bounds__(128, 1) k_einsum_fwd_tc(
     const bool live = b < B;
     float ea[K];
     {
-      const float4 *src = (const float4 *)(EAl + (live ? b : 0) * K);
+      const float *src = EA + tb_idx(l, live ? b : 0, 0, ws.bc, K);
 #pragma unroll
-      for (int q = 0; q < K / 4; ++q) {
-        const float4 v = live ? src[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-        ea[4 * q] = v.x;
-        ea[4 * q + 1] = v.y;
-        ea[4 * q + 2] = v.z;
-        ea[4 * q + 3] = v.w;
-      }
+      for (int i = 0; i < K; ++i) ea[i] = live ? src[i * 32] : 0.f;
     }
     const uint32_t ta = tm + buf * 256 + ((uint32_t)(32 * w) << 16);
     float *o = slab_off(ws, out_slab[l], live ? b : 0);
@@ -346,7 +369,7 @@ __global__ void __launch_bounds__(128, 1) k_einsum_childrho_tc(
   uint8_t *wbuf = sm + 2LL * TC_M * ko8 * 4;
   const int64_t b = (int64_t)blockIdx.x * TC_M + t;
   const bool live = b < B;
-  const int64_t row = (int64_t)l * ws.bc + (live ? b : 0);
+  const int64_t bsafe = live ? b : 0;
   const uint8_t *ltiles = tiles + (int64_t)l * ni * tile_bytes;
   if (w == 0) tc::tmem_alloc(&tbase, 512);
   if (t == 0) {
@@ -365,26 +388,20 @@ __global__ void __launch_bounds__(128, 1) k_einsum_childrho_tc(
   for (int q = 0; q < ko8 / 4; ++q) {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (live) {
-      const float *src = RT + row * ws.ks + 4 * q;
+      const float *src = RT + tb_idx(l, b, 4 * q, ws.bc, ws.ks);
       v.x = 4 * q + 0 < Ko ? src[0] : 0.f;
-      v.y = 4 * q + 1 < Ko ? src[1] : 0.f;
-      v.z = 4 * q + 2 < Ko ? src[2] : 0.f;
-      v.w = 4 * q + 3 < Ko ? src[3] : 0.f;
+      v.y = 4 * q + 1 < Ko ? src[32] : 0.f;
+      v.z = 4 * q + 2 < Ko ? src[64] : 0.f;
+      v.w = 4 * q + 3 < Ko ? src[96] : 0.f;
     }
     const uint32_t o = tc::kmaj_off(t, 4 * q, TC_M) / 4;
     store_split4(ahi + o, alo + o, v);
   }
   float eb[K], right[K];
   {
-    const float4 *src = (const float4 *)(EB + row * K);
+    const float *src = EB + tb_idx(l, bsafe, 0, ws.bc, K);
 #pragma unroll
-    for (int q = 0; q < K / 4; ++q) {
-      const float4 v = live ? src[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-      eb[4 * q] = v.x;
-      eb[4 * q + 1] = v.y;
-      eb[4 * q + 2] = v.z;
-      eb[4 * q + 3] = v.w;
-    }
+    for (int j = 0; j < K; ++j) eb[j] = live ? src[j * 32] : 0.f;
   }
 #pragma unroll
   for (int j = 0; j < K; ++j) right[j] = 0.f;
@@ -406,7 +423,7 @@ __global__ void __launch_bounds__(128, 1) k_einsum_childrho_tc(
   };
   if (t == 0) issue(0);
   float *dl = slot_ptr(ws, slot_left[l], live ? b : 0);
-  const float *earow = EA + row * K;
+  const float *earow = EA + tb_idx(l, bsafe, 0, ws.bc, K);
   for (int h = 0; h < ni; ++h) {
     const int hb = h & 1;
     tc::mbar_wait(&mbar[hb], (h >> 1) & 1);
@@ -432,7 +449,7 @@ __global__ void __launch_bounds__(128, 1) k_einsum_childrho_tc(
         for (int u = 0; u < 8; ++u) v[8 * q + u] = c8[u];
       }
       tc::tmem_wait_ld();
-      const float eai = live ? earow[i] : 0.f;
+      const float eai = live ? earow[i * 32] : 0.f;
       float lacc = 0.f;
 #pragma unroll
       for (int j = 0; j < K; ++j) {
@@ -455,116 +472,166 @@ __global__ void __launch_bounds__(128, 1) k_einsum_childrho_tc(
 }
 
 // ---- W statistics: S[(i,j), k] = sum_b EA[b,i] EB[b,j] RT[b,k] (M = (i,j) rows) ----
-// A = outer-product tile generated in smem, B = RT^T tile; TMEM accumulates
-// WS_DRAIN stages (256 samples) before each fp64 drain. grid (ceil(K^2/128), L, bsplit).
-__global__ void __launch_bounds__(128, 1) k_einsum_wstats_tc(
+// Per 32-sample block: EA/EB/RT blocks are prefetched with cp.async, the
+// outer-product A operand (128 (i,j) rows x 32 samples, hi/lo) is generated in
+// registers and written to TMEM with tcgen05.st, the RT^T B tile goes to smem;
+// 12 MMAs (4 K-steps x 3xTF32) accumulate in TMEM, drained to fp64 registers
+// every WS_DRAIN blocks. 8 warps: warp w and w+4 share TMEM lanes and split the
+// 32 samples / accumulator columns. grid (ceil(K^2/128), L, bsplit).
+__device__ __forceinline__ void cpa16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(smem)),
+               "l"(gmem));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+static int64_t ws_smem_v3(int K, int nn, int ko4) {
+  return 2LL * (2 * K + ko4) * WS_STAGE * 4 + 2LL * 2 * nn * WS_STAGE * 4;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256, 1) k_einsum_wstats_tc(
     const float *__restrict__ EA, const float *__restrict__ EB, const float *__restrict__ RT,
-    int64_t Bc, int ks, int K, int Ko, int nn, int64_t B, int bsplit, double *wpart, int L) {
+    int64_t Bc, int ks, int Ko, int nn, int64_t B, int bsplit, double *wpart, int L) {
+  constexpr int KK = K * K;
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t mbar[2];
   __shared__ uint32_t tbase;
   const int mt = blockIdx.x, l = blockIdx.y, split = blockIdx.z;
-  const int t = threadIdx.x, w = t >> 5;
-  const int KK = K * K;
-  const int m = mt * TC_M + t;
+  const int t = threadIdx.x, w = t >> 5, h = t >> 7, r = t & 127;
+  const int m = mt * TC_M + r;
   const bool mvalid = m < KK;
   const int mi = mvalid ? m / K : 0, mj = mvalid ? m % K : 0;
-  float *abuf = (float *)sm;                                   // [2][hi|lo][128 x 32]
-  float *bbuf = abuf + 2 * 2 * TC_M * WS_STAGE;                // [2][hi|lo][nn x 32]
-  float *eas = bbuf + 2 * 2 * nn * WS_STAGE;                   // [32][K]
-  float *ebs = eas + WS_STAGE * K;                             // [32][K]
-  double *red = (double *)(ebs + WS_STAGE * K);                // [128][nn]
-  const int64_t per = (B + bsplit - 1) / bsplit;
-  const int64_t bb = split * per, be = min(B, bb + per);
-  const int nstages = (int)((be - bb + WS_STAGE - 1) / WS_STAGE);
-  const float *EAl = EA + (int64_t)l * Bc * K, *EBl = EB + (int64_t)l * Bc * K;
-  const float *RTl = RT + (int64_t)l * Bc * ks;
-  if (w == 0) tc::tmem_alloc(&tbase, nn <= 32 ? 32 : 64);
+  const int ko4 = (Ko + 3) / 4 * 4;
+  const int sw = (2 * K + ko4) * WS_STAGE;                 // floats per staging buffer
+  float *stg = (float *)sm;                                // [2][EA | EB | RT rows][32]
+  float *bbuf = stg + 2 * sw;                              // [2][hi|lo][nn x 32]
+  const int64_t nblk = (B + WS_STAGE - 1) / WS_STAGE;
+  const int64_t per = (nblk + bsplit - 1) / bsplit;
+  const int64_t blk0 = split * per, blk1 = min(nblk, blk0 + per);
+  const int nstages = (int)max((int64_t)0, blk1 - blk0);
+  const int half = nn / 2;                                 // accumulator columns per half
+  if (w == 0) tc::tmem_alloc(&tbase, 256);
   if (t == 0) {
     tc::mbar_init(&mbar[0], 1);
     tc::mbar_init(&mbar[1], 1);
     tc::mbar_fence_init();
   }
-  for (int n = 0; n < nn; ++n) red[t * nn + n] = 0.0;
+  auto prefetch = [&](int q) {
+    float *sb = stg + (q & 1) * sw;
+    const int64_t b0 = (blk0 + q) * WS_STAGE;
+    const float *ga = EA + ((int64_t)l * Bc + b0) * K;
+    const float *gb = EB + ((int64_t)l * Bc + b0) * K;
+    const float *gr = RT + ((int64_t)l * Bc + b0) * ks;
+    const int nchunks = (2 * K + ko4) * (WS_STAGE / 4);
+    for (int e = t; e < nchunks; e += 256) {
+      const int row = e >> 3, c = (e & 7) * 4;
+      const float *src = row < K ? ga + row * 32 + c
+                         : row < 2 * K ? gb + (row - K) * 32 + c
+                                       : gr + (row - 2 * K) * 32 + c;
+      cpa16(sb + row * 32 + c, src);
+    }
+    cpa_commit();
+  };
+  if (nstages > 0) prefetch(0);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tm = tbase;
+  const uint32_t lane_base = (uint32_t)(32 * (w & 3)) << 16;
+  double red[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) red[c] = 0.0;
   for (int q = 0; q < nstages; ++q) {
     const int qb = q & 1;
-    const int64_t b0 = bb + (int64_t)q * WS_STAGE;
-    const int nb = (int)min((int64_t)WS_STAGE, be - b0);
-    if (q >= 2) tc::mbar_wait(&mbar[qb], ((q - 2) >> 1) & 1);
-    // stage EA/EB rows of the 32 samples
-    for (int e = t; e < WS_STAGE * K / 4; e += TC_M) {
-      const int r = e / (K / 4), c4 = e % (K / 4);
-      float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
-      if (r < nb) {
-        va = ((const float4 *)(EAl + (b0 + r) * K))[c4];
-        vb = ((const float4 *)(EBl + (b0 + r) * K))[c4];
-      }
-      ((float4 *)eas)[e] = va;
-      ((float4 *)ebs)[e] = vb;
+    const int nb = (int)min((int64_t)WS_STAGE, B - (blk0 + q) * WS_STAGE);
+    if (q + 1 < nstages) {
+      prefetch(q + 1);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
     }
     __syncthreads();
-    // A: outer products of row m over the 32 samples
-    float *ahi = abuf + qb * 2 * TC_M * WS_STAGE, *alo = ahi + TC_M * WS_STAGE;
+    if (q >= 2) tc::mbar_wait(&mbar[qb], ((q - 2) >> 1) & 1);
+    tc::fence_after();
+    const float *sb = stg + qb * sw;
+    // A: 16 samples of row m (this thread's half) -> TMEM columns
+    {
+      float hv[16], lv[16];
 #pragma unroll
-    for (int c = 0; c < WS_STAGE / 4; ++c) {
-      float4 v;
-      v.x = mvalid ? eas[(4 * c + 0) * K + mi] * ebs[(4 * c + 0) * K + mj] : 0.f;
-      v.y = mvalid ? eas[(4 * c + 1) * K + mi] * ebs[(4 * c + 1) * K + mj] : 0.f;
-      v.z = mvalid ? eas[(4 * c + 2) * K + mi] * ebs[(4 * c + 2) * K + mj] : 0.f;
-      v.w = mvalid ? eas[(4 * c + 3) * K + mi] * ebs[(4 * c + 3) * K + mj] : 0.f;
-      const uint32_t o = tc::kmaj_off(t, 4 * c, TC_M) / 4;
-      store_split4(ahi + o, alo + o, v);
+      for (int u = 0; u < 4; ++u) {
+        const int s0 = 16 * h + 4 * u;
+        const float4 a4 = *(const float4 *)(sb + mi * 32 + s0);
+        const float4 e4 = *(const float4 *)(sb + (K + mj) * 32 + s0);
+        float v[4] = {a4.x * e4.x, a4.y * e4.y, a4.z * e4.z, a4.w * e4.w};
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          if (!mvalid || s0 + z >= nb) v[z] = 0.f;
+          tc::split_tf32(v[z], hv[4 * u + z], lv[4 * u + z]);
+        }
+      }
+      const uint32_t acol = 64 + qb * 64 + 16 * h;
+      tc::tmem_st16(tm + lane_base + acol, hv);
+      tc::tmem_st16(tm + lane_base + acol + 32, lv);
     }
-    // B: RT^T tile (n = k, K dim = sample)
+    // B: RT^T tile (n = k, K dim = sample) in smem
     float *bhi = bbuf + qb * 2 * nn * WS_STAGE, *blo = bhi + nn * WS_STAGE;
-    for (int e = t; e < nn * (WS_STAGE / 4); e += TC_M) {
-      const int n = e / (WS_STAGE / 4), c = e % (WS_STAGE / 4);
+    for (int e = t; e < nn * (WS_STAGE / 4); e += 256) {
+      const int n = e >> 3, c = (e & 7) * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (n < Ko) {
-        const int r0 = 4 * c;
-        v.x = r0 + 0 < nb ? RTl[(b0 + r0 + 0) * ks + n] : 0.f;
-        v.y = r0 + 1 < nb ? RTl[(b0 + r0 + 1) * ks + n] : 0.f;
-        v.z = r0 + 2 < nb ? RTl[(b0 + r0 + 2) * ks + n] : 0.f;
-        v.w = r0 + 3 < nb ? RTl[(b0 + r0 + 3) * ks + n] : 0.f;
+        v = *(const float4 *)(sb + (2 * K + n) * 32 + c);
+        if (c + 0 >= nb) v.x = 0.f;
+        if (c + 1 >= nb) v.y = 0.f;
+        if (c + 2 >= nb) v.z = 0.f;
+        if (c + 3 >= nb) v.w = 0.f;
       }
-      const uint32_t o = tc::kmaj_off(n, 4 * c, nn) / 4;
+      const uint32_t o = tc::kmaj_off(n, c, nn) / 4;
       store_split4(bhi + o, blo + o, v);
     }
+    tc::tmem_wait_st();
     tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     if (t == 0) {
-      const uint32_t ah = tc::smem_u32(ahi), bh = tc::smem_u32(bhi);
-      mma_3xtf32(tm, ah, ah + TC_M * WS_STAGE * 4, TC_M, bh, bh + nn * WS_STAGE * 4, nn, nn,
-                 WS_STAGE / 8, (q % WS_DRAIN) != 0);
+      const uint32_t id = tc::idesc_tf32(TC_M, nn);
+      const uint32_t bh = tc::smem_u32(bhi), bl = tc::smem_u32(blo);
+      const uint32_t ah = tm + 64 + qb * 64;
+      const bool acc0 = (q % WS_DRAIN) != 0;
+#pragma unroll
+      for (int s = 0; s < WS_STAGE / 8; ++s) {
+        tc::mma_tf32_ts(tm, ah + 8 * s, tc::kstep_desc(bh, nn, s), id, (s > 0 || acc0) ? 1u : 0u);
+        tc::mma_tf32_ts(tm, ah + 8 * s, tc::kstep_desc(bl, nn, s), id, 1u);
+        tc::mma_tf32_ts(tm, ah + 32 + 8 * s, tc::kstep_desc(bh, nn, s), id, 1u);
+      }
       tc::mma_commit(&mbar[qb]);
     }
     if ((q % WS_DRAIN) == WS_DRAIN - 1 || q == nstages - 1) {
       tc::mbar_wait(&mbar[qb], (q >> 1) & 1);
       tc::fence_after();
-      const uint32_t ta = tm + ((uint32_t)(32 * w) << 16);
-      for (int c = 0; c < nn; c += 16) {
-        float v[16];
-        tc::tmem_ld16(ta + c, v);
+      for (int c = 0; c < half; c += 8) {
+        float v[8];
+        tc::tmem_ld8(tm + lane_base + h * half + c, v);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int u = 0; u < 16; ++u) red[t * nn + c + u] += (double)v[u];
+        for (int u = 0; u < 8; ++u) red[c + u] += (double)v[u];
       }
       tc::fence_before();
     }
   }
   if (mvalid) {
-    for (int k = 0; k < Ko; ++k)
-      wpart[(((int64_t)split * L + l) * Ko + k) * KK + m] = red[t * nn + k];
+    for (int c = 0; c < half; ++c) {
+      const int k = h * half + c;
+      if (k < Ko) wpart[(((int64_t)split * L + l) * Ko + k) * KK + m] = red[c];
+    }
   }
   tc::fence_before();
   __syncthreads();
-  if (w == 0) tc::tmem_dealloc(tm, nn <= 32 ? 32 : 64);
+  if (w == 0) tc::tmem_dealloc(tm, 256);
 }
 
 // ---------------------------------------------------------------------------
@@ -626,22 +693,29 @@ int launch_einsum_childrho_tc(Plan &p, const LayerPlan &L, const uint8_t *comput
   EINET_TC_DISPATCH(cr_tc, p, L, compute, EA, EB, w, B, st)
 }
 
-int launch_einsum_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB,
-                            WsView &w, int64_t B, int *bsplit, cudaStream_t st) {
-  const int K = p.k;
+template <int K>
+static int ws_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB, WsView &w,
+                 int64_t B, int *bsplit, cudaStream_t st) {
   const int mtiles = ceil_div((int64_t)K * K, TC_M);
   const int64_t ctas = (int64_t)mtiles * L.rows;
-  const int64_t nst = (B + WS_STAGE - 1) / WS_STAGE;
-  int bs = (int)std::max<int64_t>(1, std::min<int64_t>((p.num_sms + ctas - 1) / ctas,
-                                                        std::min<int64_t>(nst, kMaxBSplit)));
-  const int64_t smem = ws_smem(K, L.nn);
-  cudaFuncSetAttribute(k_einsum_wstats_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const int64_t nblk = (B + WS_STAGE - 1) / WS_STAGE;
+  int bs = (int)std::max<int64_t>(1, std::min<int64_t>((2 * p.num_sms + ctas - 1) / ctas,
+                                                        std::min<int64_t>(nblk, kMaxBSplit)));
+  const int64_t per = (nblk + bs - 1) / bs;
+  bs = (int)((nblk + per - 1) / per);
+  const int64_t smem = ws_smem_v3(K, L.nn, (L.k_out + 3) / 4 * 4);
+  cudaFuncSetAttribute(k_einsum_wstats_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   dim3 grid(mtiles, L.rows, bs);
-  k_einsum_wstats_tc<<<grid, 128, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, K, L.k_out, L.nn, B, bs,
-                                              w.wpart, L.rows);
+  k_einsum_wstats_tc<K><<<grid, 256, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, L.k_out, L.nn, B, bs,
+                                                 w.wpart, L.rows);
   *bsplit = bs;
   return check_cuda(cudaGetLastError(), "einsum wstats tc");
+}
+
+int launch_einsum_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB,
+                            WsView &w, int64_t B, int *bsplit, cudaStream_t st) {
+  EINET_TC_DISPATCH(ws_tc, p, L, EA, EB, w, B, bsplit, st)
 }
 
 }  // namespace einet

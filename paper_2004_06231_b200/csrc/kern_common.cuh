@@ -68,7 +68,7 @@ inline WsView ws_view(const Plan &p, const uint8_t *w) {
   v.ppart = (double *)(b + p.w_ppart);
   v.mixpart = (double *)(b + p.w_mixpart);
   v.llpart = (double *)(b + p.w_llpart);
-  v.bc = p.max_chunk;
+  v.bc = p.bc;
   v.ks = p.ks;
   return v;
 }
@@ -96,5 +96,14 @@ __device__ __forceinline__ float gather_rho(const WsView &w, const int *csr_off,
 }
 
 __device__ __forceinline__ bool is_nan_f(float v) { return v != v; }
+
+// Per-sample vectors EA, EB, RT and the leaf responsibilities live in 32-sample
+// transposed blocks: entry i of sample b in row l of a width-W array is at
+//   (l*bc + b - b%32)*W + i*32 + b%32      (bc is a multiple of 32)
+// so one block is a contiguous [W][32] tile (a batch-reduction GEMM stages it
+// with 16-byte copies) and per-sample loops read coalesced across a warp.
+__device__ __forceinline__ int64_t tb_idx(int64_t l, int64_t b, int i, int64_t bc, int W) {
+  return (l * bc + (b & ~31LL)) * W + (int64_t)i * 32 + (b & 31);
+}
 
 }  // namespace einet

@@ -472,12 +472,11 @@ __global__ void k_leaf_rho(WsView ws, const int *csr_off, const int *csr_slot,
   const int leaf = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * 128 + threadIdx.x;
   const int slab = leaf_slab[leaf];
-  float *rho = ws.rho + ((int64_t)leaf * ws.bc) * K;
   for (int k = 0; k < K; ++k) {
     float v = 0.f;
     if (b < B) {
       v = gather_rho(ws, csr_off, csr_slot, ones, slab, b, k);
-      rho[b * K + k] = v;
+      ws.rho[tb_idx(leaf, b, k, ws.bc, K)] = v;
     }
     float s = block_sum_128(v, red);
     if (threadIdx.x == 0) ppart[((int64_t)blockIdx.x * n_leaf + leaf) * K + k] = (double)s;
@@ -516,7 +515,6 @@ __global__ void __launch_bounds__(256) k_leaf_stats_gauss(
   const int r = leaf_rep[leaf];
   const int64_t per = (B + lsplit - 1) / lsplit;
   const int64_t bb = split * per, be = min(B, bb + per);
-  const float *rho = rho_all + (int64_t)leaf * Bc * K;
   const int tv = threadIdx.x % 16, tk = threadIdx.x / 16;
   for (int v = threadIdx.x; v < LS_VT; v += blockDim.x) {
     const int d = v < nv ? scope_vars[sbeg + v0 + v] : -1;
@@ -552,7 +550,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats_gauss(
     }
     for (int e = threadIdx.x; e < LS_BT * KPC; e += blockDim.x) {
       const int bl = e / KPC, k = kbase + e % KPC;
-      rs[e] = (bl < nb && k < K) ? rho[(t + bl) * K + k] : 0.f;
+      rs[e] = (bl < nb && k < K) ? rho_all[tb_idx(leaf, t + bl, k, Bc, K)] : 0.f;
     }
     __syncthreads();
 #pragma unroll
@@ -617,7 +615,6 @@ __global__ void __launch_bounds__(256) k_leaf_stats_discrete(
   const int r = leaf_rep[leaf];
   const int64_t per = (B + lsplit - 1) / lsplit;
   const int64_t bb = split * per, be = min(B, bb + per);
-  const float *rho = rho_all + (int64_t)leaf * Bc * K;
   const int64_t n_ent = (int64_t)nv * K * T;
   for (int64_t e = threadIdx.x; e < n_ent; e += blockDim.x) {
     const int t = (int)(e % T);
@@ -630,7 +627,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats_discrete(
       int cnt = 0;
       for (int64_t b = bb; b < be; ++b) {
         const float xv = x[b * D + d];
-        const float rr = rho[b * K + k];
+        const float rr = rho_all[tb_idx(leaf, b, k, Bc, K)];
         if (family == EINET_FAMILY_CATEGORICAL)
           run += ((int)xv == t && xv == floorf(xv)) ? rr : 0.f;
         else
@@ -660,14 +657,22 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
   WsView w = ws_view(p, wsb);
   const int K = p.k, D = p.d_vars, R = p.num_replicas, T = p.suff;
   const int nb = ceil_div(B, 128);
+  double *Pcall = (double *)(wsb + p.w_tmp_p);
   {
   ProfScope prof("leaf_rho", st);
   k_leaf_rho<<<dim3(nb, p.n_leaf), 128, 0, st>>>(w, p.d_csr_off, p.d_csr_slot, p.d_slab_ones,
                                                  p.d_leaf_slab, B, K, p.n_leaf, w.ppart);
-  launch_reduce_partials(stats + p.sizes.stats_p_offset, w.ppart, nb, (int64_t)p.n_leaf * K,
+  launch_reduce_partials_store(Pcall, w.ppart, nb, (int64_t)p.n_leaf * K,
+                               (int64_t)p.n_leaf * K, st);
+  launch_reduce_partials(stats + p.sizes.stats_p_offset, Pcall, 1, (int64_t)p.n_leaf * K,
                          (int64_t)p.n_leaf * K, nullptr, st);
   }
   ProfScope prof("leaf_stats", st);
+  if (leaf_tc_supported(p)) {
+    int rc = launch_leaf_stats_tc(p, compute, x, B, wsb, stats, Pcall, st);
+    count_launch(1);
+    return rc;
+  }
   const int ls = leaf_lsplit(p, B);
   const int64_t n_phi = p.n_phi;
   cudaMemsetAsync(w.lspart, 0, sizeof(double) * n_phi * ls, st);

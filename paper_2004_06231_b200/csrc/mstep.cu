@@ -19,6 +19,25 @@ __global__ void k_reduce_partials(double *__restrict__ dst, const double *__rest
   }
 }
 
+__global__ void k_reduce_partials_store(double *__restrict__ dst,
+                                        const double *__restrict__ part, int nparts, int64_t n,
+                                        int64_t stride) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * stride + i];
+    dst[i] = s;
+  }
+}
+
+void launch_reduce_partials_store(double *dst, const double *part, int nparts, int64_t n,
+                                  int64_t stride, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = (int)std::min<int64_t>((n + kReduceThreads - 1) / kReduceThreads, 8192);
+  k_reduce_partials_store<<<grid, kReduceThreads, 0, st>>>(dst, part, nparts, n, stride);
+  count_launch();
+}
+
 void launch_reduce_partials(double *dst, const double *part, int nparts, int64_t n,
                             int64_t stride, const double *scale, cudaStream_t st) {
   if (n <= 0) return;
