@@ -155,33 +155,42 @@ def _oracle_setup(config, n, seed):
     return circuit, fam.to_dict(), x, O.OracleParams(ein, mix, phi)
 
 
+_WORKER = {}
+
+
+def _oracle_worker_init(config, n, seed):
+    _WORKER["model"] = _oracle_setup(config, n, seed)
+
+
 def _oracle_shard(args):
-    config, n, seed, lo, hi = args
+    """E-step of one shard with the current parameters (engine.py:143-328)."""
+    params, lo, hi = args
     from oracle import einet_oracle as O
-    circuit, fam, x, p = _oracle_setup(config, n, seed)
-    tr = O.forward(circuit, p, fam, x[lo:hi])
-    return O.backward(circuit, p, fam, tr)
+    circuit, fam, x, _ = _WORKER["model"]
+    tr = O.forward(circuit, params, fam, x[lo:hi])
+    return O.backward(circuit, params, fam, tr)
 
 
 def cpu_reference_steps(config, n, steps, warmup, procs):
     """Reference EM step (trainer.py:99-117) restated in oracle/, sharded over
-    `procs` worker processes (merge = sum, engine.py:228-236)."""
+    `procs` worker processes that keep the model resident; the parent merges
+    the statistics (a sum, engine.py:228-236) and applies the M-step."""
     import multiprocessing as mp
     from oracle import einet_oracle as O
     circuit, fam, x, p = _oracle_setup(config, n, 0)
     bounds = np.linspace(0, n, procs + 1).astype(int)
-    jobs = [(config, n, 0, int(bounds[i]), int(bounds[i + 1])) for i in range(procs)
-            if bounds[i + 1] > bounds[i]]
+    spans = [(int(bounds[i]), int(bounds[i + 1])) for i in range(procs)
+             if bounds[i + 1] > bounds[i]]
     times = []
     ctx = mp.get_context("fork")
-    with ctx.Pool(len(jobs)) as pool:
+    with ctx.Pool(len(spans), initializer=_oracle_worker_init, initargs=(config, n, 0)) as pool:
         for it in range(warmup + steps):
             t0 = time.perf_counter()
-            parts = pool.map(_oracle_shard, jobs) if len(jobs) > 1 else [_oracle_shard(jobs[0])]
+            parts = pool.map(_oracle_shard, [(p, lo, hi) for lo, hi in spans])
             st = parts[0]
             for q in parts[1:]:
                 st.merge(q)
-            O.apply_update(circuit, p, fam, st, 0.5)
+            p = O.apply_update(circuit, p, fam, st, 0.5)
             dt = time.perf_counter() - t0
             if it >= warmup:
                 times.append(dt)
@@ -214,7 +223,7 @@ def run_reference(args):
     if rank != 0:
         return
     procs = max(1, len(os.sched_getaffinity(0)))
-    n = max(procs, args.cpu_sample)
+    n = max(procs * 32, args.cpu_sample)
     steps, warmup = max(1, min(args.steps, 3)), min(args.warmup, 1)
     times = cpu_reference_steps(args.config, n, steps, warmup, procs)
     sec = statistics.median(times)

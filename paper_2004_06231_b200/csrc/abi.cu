@@ -332,10 +332,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     int64_t bs = std::min<int64_t>(std::max<int64_t>(1, (2 * p->num_sms + blocks - 1) / blocks),
                                    std::min<int64_t>(kMaxBSplit, (Bc + 63) / 64));
     // tensor-core W statistics split their batch as well (einsum_tc.cu)
-    int64_t tc_blocks = (int64_t)((K * K + 127) / 128) * L.rows;
-    int64_t tc_bs = std::max<int64_t>(1, std::min<int64_t>((2 * p->num_sms + tc_blocks - 1) / tc_blocks,
-                                                          std::min<int64_t>((Bc + 31) / 32,
-                                                                            kMaxBSplit)));
+    int64_t tc_bs = L.tc ? wstats_tc_bsplit(*p, L, Bc, true) : 1;
     wpart = std::max(wpart, std::max(bs, tc_bs) * lw);
   }
   p->w_wpart = seg(8 * std::max<int64_t>(wpart, 1));

@@ -147,6 +147,7 @@ int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
                        cudaStream_t st);
 int launch_status_reset(int32_t *status, cudaStream_t st);
 void plan_tc_tiling(Plan &p);
+int wstats_tc_bsplit(const Plan &p, const LayerPlan &L, int64_t B, bool upper_bound);
 int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_selftest_gemm(const float *A, const float *B, float *D, int N, int K,
                          cudaStream_t st);

@@ -137,8 +137,8 @@ static int64_t fwd_smem(int rows_tile, int K) {
 static int64_t cr_smem(int rows_tile, int ko8) {
   return 2LL * TC_M * ko8 * 4 + 2LL * (2LL * rows_tile * ko8 * 4);
 }
-static int64_t ws_smem(int K, int nn) {  // W-statistics kernel (staging + B tiles)
-  return 2LL * (2 * K + nn) * WS_STAGE * 4 + 2LL * 2 * nn * WS_STAGE * 4;
+static int64_t ws_smem(int K, int nn) {  // W-statistics kernel (staging + B tile)
+  return 2LL * (2 * K + nn) * WS_STAGE * 4 + 2LL * nn * WS_STAGE * 4;
 }
 
 void plan_tc_tiling(Plan &p) {
@@ -489,35 +489,45 @@ __device__ __forceinline__ void cpa_wait() {
 }
 
 static int64_t ws_smem_v3(int K, int nn, int ko4) {
-  return 2LL * (2 * K + ko4) * WS_STAGE * 4 + 2LL * 2 * nn * WS_STAGE * 4;
+  return 2LL * (2 * K + ko4) * WS_STAGE * 4 + 2LL * nn * WS_STAGE * 4;
 }
 
+// hi = x with the low 13 mantissa bits cleared (exact TF32 value), lo = x - hi
+// (exact in fp32, |lo| < 2^-10 |x|, truncated to TF32 by the tensor core).
+__device__ __forceinline__ void split_trunc(float x, float &hi, float &lo) {
+  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  lo = x - hi;
+}
+
+constexpr int WS_MAX_SAMPLES = 4096;  // per CTA: fp32 TMEM accumulation, one drain
+
+// grid (ceil(ceil(K^2/128)/2), L, bsplit), block 256: warpgroup g (warps 4g..4g+3)
+// owns (i,j)-tile 2*blockIdx.x + g; both share the staged block and the B tile.
 template <int K>
-__global__ void __launch_bounds__(256, 1) k_einsum_wstats_tc(
+__global__ void __launch_bounds__(256, 2) k_einsum_wstats_tc(
     const float *__restrict__ EA, const float *__restrict__ EB, const float *__restrict__ RT,
     int64_t Bc, int ks, int Ko, int nn, int64_t B, int bsplit, double *wpart, int L) {
   constexpr int KK = K * K;
   extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ uint64_t mbar[2];
+  __shared__ uint64_t mbar;
   __shared__ uint32_t tbase;
-  const int mt = blockIdx.x, l = blockIdx.y, split = blockIdx.z;
-  const int t = threadIdx.x, w = t >> 5, h = t >> 7, r = t & 127;
-  const int m = mt * TC_M + r;
+  const int l = blockIdx.y, split = blockIdx.z;
+  const int t = threadIdx.x, w = t >> 5, g = t >> 7, r = t & 127;
+  const int m = (2 * blockIdx.x + g) * TC_M + r;
   const bool mvalid = m < KK;
   const int mi = mvalid ? m / K : 0, mj = mvalid ? m % K : 0;
   const int ko4 = (Ko + 3) / 4 * 4;
-  const int sw = (2 * K + ko4) * WS_STAGE;                 // floats per staging buffer
-  float *stg = (float *)sm;                                // [2][EA | EB | RT rows][32]
-  float *bbuf = stg + 2 * sw;                              // [2][hi|lo][nn x 32]
+  const int sw = (2 * K + ko4) * WS_STAGE;
+  float *stg = (float *)sm;                   // [2][EA | EB | RT rows][32]
+  float *bhi = stg + 2 * sw, *blo = bhi + nn * WS_STAGE;
   const int64_t nblk = (B + WS_STAGE - 1) / WS_STAGE;
   const int64_t per = (nblk + bsplit - 1) / bsplit;
   const int64_t blk0 = split * per, blk1 = min(nblk, blk0 + per);
   const int nstages = (int)max((int64_t)0, blk1 - blk0);
-  const int half = nn / 2;                                 // accumulator columns per half
+  // TMEM columns: acc tile g at [g*nn, (g+1)*nn), A(hi|lo) of warpgroup g at 128 + 64 g
   if (w == 0) tc::tmem_alloc(&tbase, 256);
   if (t == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
+    tc::mbar_init(&mbar, 1);
     tc::mbar_fence_init();
   }
   auto prefetch = [&](int q) {
@@ -542,9 +552,7 @@ __global__ void __launch_bounds__(256, 1) k_einsum_wstats_tc(
   tc::fence_after();
   const uint32_t tm = tbase;
   const uint32_t lane_base = (uint32_t)(32 * (w & 3)) << 16;
-  double red[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) red[c] = 0.0;
+  const uint32_t acol = 128 + 64 * g;
   for (int q = 0; q < nstages; ++q) {
     const int qb = q & 1;
     const int nb = (int)min((int64_t)WS_STAGE, B - (blk0 + q) * WS_STAGE);
@@ -554,43 +562,48 @@ __global__ void __launch_bounds__(256, 1) k_einsum_wstats_tc(
     } else {
       cpa_wait<0>();
     }
-    __syncthreads();
-    if (q >= 2) tc::mbar_wait(&mbar[qb], ((q - 2) >> 1) & 1);
-    tc::fence_after();
-    const float *sb = stg + qb * sw;
-    // A: 16 samples of row m (this thread's half) -> TMEM columns
-    {
-      float hv[16], lv[16];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int s0 = 16 * h + 4 * u;
-        const float4 a4 = *(const float4 *)(sb + mi * 32 + s0);
-        const float4 e4 = *(const float4 *)(sb + (K + mj) * 32 + s0);
-        float v[4] = {a4.x * e4.x, a4.y * e4.y, a4.z * e4.z, a4.w * e4.w};
-#pragma unroll
-        for (int z = 0; z < 4; ++z) {
-          if (!mvalid || s0 + z >= nb) v[z] = 0.f;
-          tc::split_tf32(v[z], hv[4 * u + z], lv[4 * u + z]);
-        }
-      }
-      const uint32_t acol = 64 + qb * 64 + 16 * h;
-      tc::tmem_st16(tm + lane_base + acol, hv);
-      tc::tmem_st16(tm + lane_base + acol + 32, lv);
+    float *sb = stg + qb * sw;
+    if (nb < WS_STAGE) {  // tail block: samples past the batch contribute exactly 0
+      __syncthreads();
+      for (int e = t; e < (2 * K + ko4) * WS_STAGE; e += 256)
+        if ((e & 31) >= nb) sb[e] = 0.f;
     }
-    // B: RT^T tile (n = k, K dim = sample) in smem
-    float *bhi = bbuf + qb * 2 * nn * WS_STAGE, *blo = bhi + nn * WS_STAGE;
+    __syncthreads();
+    // B tile (RT^T, n = k) shared by both (i,j) tiles; the previous stage's MMAs
+    // (which read B and the A columns) must have completed
+    if (q >= 1) tc::mbar_wait(&mbar, (q - 1) & 1);
+    tc::fence_after();
     for (int e = t; e < nn * (WS_STAGE / 4); e += 256) {
       const int n = e >> 3, c = (e & 7) * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (n < Ko) {
-        v = *(const float4 *)(sb + (2 * K + n) * 32 + c);
-        if (c + 0 >= nb) v.x = 0.f;
-        if (c + 1 >= nb) v.y = 0.f;
-        if (c + 2 >= nb) v.z = 0.f;
-        if (c + 3 >= nb) v.w = 0.f;
-      }
+      if (n < Ko) v = *(const float4 *)(sb + (2 * K + n) * 32 + c);
+      float4 h4, l4;
+      split_trunc(v.x, h4.x, l4.x);
+      split_trunc(v.y, h4.y, l4.y);
+      split_trunc(v.z, h4.z, l4.z);
+      split_trunc(v.w, h4.w, l4.w);
       const uint32_t o = tc::kmaj_off(n, c, nn) / 4;
-      store_split4(bhi + o, blo + o, v);
+      *(float4 *)(bhi + o) = h4;
+      *(float4 *)(blo + o) = l4;
+    }
+    // A: row m's 32 outer products -> TMEM (two 16-column halves, hi and lo)
+    {
+      const float *ea = sb + mi * 32, *eb = sb + (K + mj) * 32;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float hv[16], lv[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 a4 = *(const float4 *)(ea + 16 * half + 4 * u);
+          const float4 e4 = *(const float4 *)(eb + 16 * half + 4 * u);
+          split_trunc(a4.x * e4.x, hv[4 * u + 0], lv[4 * u + 0]);
+          split_trunc(a4.y * e4.y, hv[4 * u + 1], lv[4 * u + 1]);
+          split_trunc(a4.z * e4.z, hv[4 * u + 2], lv[4 * u + 2]);
+          split_trunc(a4.w * e4.w, hv[4 * u + 3], lv[4 * u + 3]);
+        }
+        tc::tmem_st16(tm + lane_base + acol + 16 * half, hv);
+        tc::tmem_st16(tm + lane_base + acol + 32 + 16 * half, lv);
+      }
     }
     tc::tmem_wait_st();
     tc::fence_async_smem();
@@ -600,35 +613,36 @@ __global__ void __launch_bounds__(256, 1) k_einsum_wstats_tc(
     if (t == 0) {
       const uint32_t id = tc::idesc_tf32(TC_M, nn);
       const uint32_t bh = tc::smem_u32(bhi), bl = tc::smem_u32(blo);
-      const uint32_t ah = tm + 64 + qb * 64;
-      const bool acc0 = (q % WS_DRAIN) != 0;
 #pragma unroll
-      for (int s = 0; s < WS_STAGE / 8; ++s) {
-        tc::mma_tf32_ts(tm, ah + 8 * s, tc::kstep_desc(bh, nn, s), id, (s > 0 || acc0) ? 1u : 0u);
-        tc::mma_tf32_ts(tm, ah + 8 * s, tc::kstep_desc(bl, nn, s), id, 1u);
-        tc::mma_tf32_ts(tm, ah + 32 + 8 * s, tc::kstep_desc(bh, nn, s), id, 1u);
-      }
-      tc::mma_commit(&mbar[qb]);
-    }
-    if ((q % WS_DRAIN) == WS_DRAIN - 1 || q == nstages - 1) {
-      tc::mbar_wait(&mbar[qb], (q >> 1) & 1);
-      tc::fence_after();
-      for (int c = 0; c < half; c += 8) {
-        float v[8];
-        tc::tmem_ld8(tm + lane_base + h * half + c, v);
-        tc::tmem_wait_ld();
+      for (int gg = 0; gg < 2; ++gg) {
+        const uint32_t d = tm + gg * nn, ah = tm + 128 + 64 * gg;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) red[c + u] += (double)v[u];
+        for (int s = 0; s < WS_STAGE / 8; ++s) {
+          tc::mma_tf32_ts(d, ah + 8 * s, tc::kstep_desc(bh, nn, s), id, (s > 0 || q > 0) ? 1u : 0u);
+          tc::mma_tf32_ts(d, ah + 8 * s, tc::kstep_desc(bl, nn, s), id, 1u);
+          tc::mma_tf32_ts(d, ah + 32 + 8 * s, tc::kstep_desc(bh, nn, s), id, 1u);
+        }
       }
-      tc::fence_before();
+      tc::mma_commit(&mbar);
     }
   }
-  if (mvalid) {
-    for (int c = 0; c < half; ++c) {
-      const int k = h * half + c;
-      if (k < Ko) wpart[(((int64_t)split * L + l) * Ko + k) * KK + m] = red[c];
+  if (nstages > 0) tc::mbar_wait(&mbar, (nstages - 1) & 1);
+  tc::fence_after();
+  // drain: warpgroup g reads its tile's accumulator rows (lane = row m)
+  for (int c = 0; c < nn; c += 8) {
+    float v[8];
+    tc::tmem_ld8(tm + lane_base + g * nn + c, v);
+    tc::tmem_wait_ld();
+    if (mvalid && nstages > 0) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = c + u;
+        if (k < Ko) wpart[(((int64_t)split * L + l) * Ko + k) * KK + m] = (double)v[u];
+      }
     }
   }
+  if (mvalid && nstages == 0)
+    for (int k = 0; k < Ko; ++k) wpart[(((int64_t)split * L + l) * Ko + k) * KK + m] = 0.0;
   tc::fence_before();
   __syncthreads();
   if (w == 0) tc::tmem_dealloc(tm, 256);
@@ -693,20 +707,31 @@ int launch_einsum_childrho_tc(Plan &p, const LayerPlan &L, const uint8_t *comput
   EINET_TC_DISPATCH(cr_tc, p, L, compute, EA, EB, w, B, st)
 }
 
+// Batch splits of the W-statistics kernel for a batch of B samples. With
+// upper_bound the pre-normalisation value is returned: it is monotone in B, so
+// the plan sizes the partial buffer with it (the normalised count is not).
+int wstats_tc_bsplit(const Plan &p, const LayerPlan &L, int64_t B, bool upper_bound) {
+  const int mpairs = ceil_div(ceil_div((int64_t)p.k * p.k, TC_M), 2);
+  const int64_t nblk = (B + WS_STAGE - 1) / WS_STAGE;
+  const int64_t per_max = WS_MAX_SAMPLES / WS_STAGE;
+  int bs = (int)std::min<int64_t>(kMaxBSplit, (nblk + per_max - 1) / per_max);
+  const int64_t ctas = (int64_t)mpairs * L.rows;
+  bs = (int)std::max<int64_t>(bs, std::min<int64_t>((2 * p.num_sms + ctas - 1) / ctas,
+                                                    std::min<int64_t>(nblk, kMaxBSplit)));
+  if (upper_bound) return bs;
+  const int64_t per = (nblk + bs - 1) / bs;
+  return (int)((nblk + per - 1) / per);
+}
+
 template <int K>
 static int ws_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB, WsView &w,
                  int64_t B, int *bsplit, cudaStream_t st) {
-  const int mtiles = ceil_div((int64_t)K * K, TC_M);
-  const int64_t ctas = (int64_t)mtiles * L.rows;
-  const int64_t nblk = (B + WS_STAGE - 1) / WS_STAGE;
-  int bs = (int)std::max<int64_t>(1, std::min<int64_t>((2 * p.num_sms + ctas - 1) / ctas,
-                                                        std::min<int64_t>(nblk, kMaxBSplit)));
-  const int64_t per = (nblk + bs - 1) / bs;
-  bs = (int)((nblk + per - 1) / per);
+  const int mpairs = ceil_div(ceil_div((int64_t)K * K, TC_M), 2);
+  const int bs = wstats_tc_bsplit(p, L, B, false);
   const int64_t smem = ws_smem_v3(K, L.nn, (L.k_out + 3) / 4 * 4);
   cudaFuncSetAttribute(k_einsum_wstats_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  dim3 grid(mtiles, L.rows, bs);
+  dim3 grid(mpairs, L.rows, bs);
   k_einsum_wstats_tc<K><<<grid, 256, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, L.k_out, L.nn, B, bs,
                                                  w.wpart, L.rows);
   *bsplit = bs;
