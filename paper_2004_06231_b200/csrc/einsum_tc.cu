@@ -334,13 +334,10 @@ __global__ void __launch_bounds__(128, 1) k_einsum_fwd_tc(
         for (int u = 0; u < 8; ++u) v[8 * q + u] = c8[u];
       }
       tc::tmem_wait_ld();
-      float acc0 = 0.f, acc1 = 0.f;
+      float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < K; i += 2) {
-        acc0 = fmaf(v[i], ea[i], acc0);
-        acc1 = fmaf(v[i + 1], ea[i + 1], acc1);
-      }
-      const float acc = acc0 + acc1;
+      for (int i = 0; i < K; ++i) a4[i & 3] = fmaf(v[i], ea[i], a4[i & 3]);
+      const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
       if (live) o[g * kg + kl] = acc > 0.f ? logf(acc) : -CUDART_INF_F;
     }
   }
@@ -450,13 +447,13 @@ __global__ void __launch_bounds__(128, 1) k_einsum_childrho_tc(
       }
       tc::tmem_wait_ld();
       const float eai = live ? earow[i * 32] : 0.f;
-      float lacc = 0.f;
+      float l4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        lacc = fmaf(v[j], eb[j], lacc);
+        l4[j & 3] = fmaf(v[j], eb[j], l4[j & 3]);
         right[j] = fmaf(v[j], eai, right[j]);
       }
-      if (live) dl[i] = eai * lacc;
+      if (live) dl[i] = eai * ((l4[0] + l4[1]) + (l4[2] + l4[3]));
     }
     tc::fence_before();
     __syncthreads();
@@ -488,8 +485,10 @@ __device__ __forceinline__ void cpa_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+constexpr int WS_ROW = WS_STAGE + 4;  // padded staging row (floats)
+
 static int64_t ws_smem_v3(int K, int nn, int ko4) {
-  return 2LL * (2 * K + ko4) * WS_STAGE * 4 + 2LL * nn * WS_STAGE * 4;
+  return 2LL * (2 * K + ko4) * WS_ROW * 4 + 2LL * nn * WS_STAGE * 4;
 }
 
 // hi = x with the low 13 mantissa bits cleared (exact TF32 value), lo = x - hi
@@ -517,8 +516,8 @@ __global__ void __launch_bounds__(256, 2) k_einsum_wstats_tc(
   const bool mvalid = m < KK;
   const int mi = mvalid ? m / K : 0, mj = mvalid ? m % K : 0;
   const int ko4 = (Ko + 3) / 4 * 4;
-  const int sw = (2 * K + ko4) * WS_STAGE;
-  float *stg = (float *)sm;                   // [2][EA | EB | RT rows][32]
+  const int sw = (2 * K + ko4) * WS_ROW;
+  float *stg = (float *)sm;                   // [2][EA | EB | RT rows][WS_ROW]
   float *bhi = stg + 2 * sw, *blo = bhi + nn * WS_STAGE;
   const int64_t nblk = (B + WS_STAGE - 1) / WS_STAGE;
   const int64_t per = (nblk + bsplit - 1) / bsplit;
@@ -542,7 +541,7 @@ __global__ void __launch_bounds__(256, 2) k_einsum_wstats_tc(
       const float *src = row < K ? ga + row * 32 + c
                          : row < 2 * K ? gb + (row - K) * 32 + c
                                        : gr + (row - 2 * K) * 32 + c;
-      cpa16(sb + row * 32 + c, src);
+      cpa16(sb + row * WS_ROW + c, src);
     }
     cpa_commit();
   };
@@ -566,7 +565,7 @@ __global__ void __launch_bounds__(256, 2) k_einsum_wstats_tc(
     if (nb < WS_STAGE) {  // tail block: samples past the batch contribute exactly 0
       __syncthreads();
       for (int e = t; e < (2 * K + ko4) * WS_STAGE; e += 256)
-        if ((e & 31) >= nb) sb[e] = 0.f;
+        if ((e & 31) >= nb) sb[(e >> 5) * WS_ROW + (e & 31)] = 0.f;
     }
     __syncthreads();
     // B tile (RT^T, n = k) shared by both (i,j) tiles; the previous stage's MMAs
@@ -576,7 +575,7 @@ __global__ void __launch_bounds__(256, 2) k_einsum_wstats_tc(
     for (int e = t; e < nn * (WS_STAGE / 4); e += 256) {
       const int n = e >> 3, c = (e & 7) * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (n < Ko) v = *(const float4 *)(sb + (2 * K + n) * 32 + c);
+      if (n < Ko) v = *(const float4 *)(sb + (2 * K + n) * WS_ROW + c);
       float4 h4, l4;
       split_trunc(v.x, h4.x, l4.x);
       split_trunc(v.y, h4.y, l4.y);
@@ -588,7 +587,7 @@ __global__ void __launch_bounds__(256, 2) k_einsum_wstats_tc(
     }
     // A: row m's 32 outer products -> TMEM (two 16-column halves, hi and lo)
     {
-      const float *ea = sb + mi * 32, *eb = sb + (K + mj) * 32;
+      const float *ea = sb + mi * WS_ROW, *eb = sb + (K + mj) * WS_ROW;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         float hv[16], lv[16];
