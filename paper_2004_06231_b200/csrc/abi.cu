@@ -32,6 +32,34 @@ int check_cuda(cudaError_t err, const char *what) {
 }
 void count_launch(int n) { g_launches += n; }
 
+int pick_split(int64_t per, int64_t slots, int lo, int hi) {
+  lo = std::max(lo, 1);
+  hi = std::max(hi, lo);
+  int best = lo;
+  double best_eff = -1.0;
+  for (int s = lo; s <= hi; ++s) {
+    const int64_t n = per * s;
+    const int64_t waves = (n + slots - 1) / slots;
+    const double eff = (double)n / (double)(waves * slots);
+    if (waves >= 2 && eff >= 0.85) return s;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
+int64_t device_slots(const void *kernel, int block, size_t smem, int num_sms) {
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return (int64_t)per_sm * num_sms;
+}
+
 static bool g_profiling = false;
 struct ProfClass {
   std::string name;

@@ -165,6 +165,13 @@ bool leaf_tc_supported(const Plan &p);
 int launch_leaf_stats_tc(Plan &p, const uint8_t *compute, const float *x, int64_t B,
                          uint8_t *wsb, double *stats, const double *Pcall, cudaStream_t st);
 
+// Split factor s in [lo, hi] for a grid of ctas_per_split * s CTAs on
+// `slots` concurrently resident CTAs: the smallest s whose last wave is at
+// least 85% full once there are >= 2 waves (or the best-filled single wave).
+int pick_split(int64_t ctas_per_split, int64_t slots, int lo, int hi);
+// resident CTAs of `kernel` on the whole device for the given block / smem
+int64_t device_slots(const void *kernel, int block, size_t smem, int num_sms);
+
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 

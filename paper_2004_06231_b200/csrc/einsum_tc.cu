@@ -659,7 +659,8 @@ static int fwd_tc(Plan &p, const LayerPlan &L, const uint8_t *compute, const flo
                        (int)smem);
   const int64_t nbt = (B + TC_M - 1) / TC_M;
   const int64_t ctas = (int64_t)L.ng * L.rows;
-  int bs = (int)std::max<int64_t>(1, std::min<int64_t>(nbt, (p.num_sms + ctas - 1) / ctas));
+  int bs = pick_split(ctas, device_slots((const void *)k_einsum_fwd_tc<K>, 128, smem, p.num_sms), 1,
+                      (int)std::min<int64_t>(nbt, 1024));
   const int per = (int)((nbt + bs - 1) / bs);
   bs = (int)((nbt + per - 1) / per);
   dim3 grid(L.ng, L.rows, bs);
@@ -706,18 +707,22 @@ int launch_einsum_childrho_tc(Plan &p, const LayerPlan &L, const uint8_t *comput
   EINET_TC_DISPATCH(cr_tc, p, L, compute, EA, EB, w, B, st)
 }
 
-// Batch splits of the W-statistics kernel for a batch of B samples. With
-// upper_bound the pre-normalisation value is returned: it is monotone in B, so
-// the plan sizes the partial buffer with it (the normalised count is not).
+// Batch splits of the W-statistics kernel for a batch of B samples: at most
+// WS_MAX_SAMPLES per CTA (one fp32 TMEM accumulation), full waves on the
+// resident slots (2 CTAs per SM). With upper_bound the cap of the search is
+// returned; it is monotone in B, so the plan sizes the partial buffer with it.
 int wstats_tc_bsplit(const Plan &p, const LayerPlan &L, int64_t B, bool upper_bound) {
   const int mpairs = ceil_div(ceil_div((int64_t)p.k * p.k, TC_M), 2);
   const int64_t nblk = (B + WS_STAGE - 1) / WS_STAGE;
-  const int64_t per_max = WS_MAX_SAMPLES / WS_STAGE;
-  int bs = (int)std::min<int64_t>(kMaxBSplit, (nblk + per_max - 1) / per_max);
   const int64_t ctas = (int64_t)mpairs * L.rows;
-  bs = (int)std::max<int64_t>(bs, std::min<int64_t>((2 * p.num_sms + ctas - 1) / ctas,
-                                                    std::min<int64_t>(nblk, kMaxBSplit)));
-  if (upper_bound) return bs;
+  const int64_t slots = 2LL * p.num_sms;
+  const int lo = (int)std::min<int64_t>(kMaxBSplit, (nblk + WS_MAX_SAMPLES / WS_STAGE - 1) /
+                                                        (WS_MAX_SAMPLES / WS_STAGE));
+  const int hi = (int)std::max<int64_t>(
+      lo, std::min<int64_t>(std::min<int64_t>(nblk, kMaxBSplit),
+                            std::max<int64_t>(4, (8 * slots + ctas - 1) / ctas)));
+  if (upper_bound) return hi;
+  int bs = pick_split(ctas, slots, lo, hi);
   const int64_t per = (nblk + bs - 1) / bs;
   return (int)((nblk + per - 1) / per);
 }

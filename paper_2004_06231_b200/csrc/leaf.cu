@@ -401,11 +401,10 @@ __global__ void k_leaf_finalize(const double *__restrict__ part, int dsplit,
   for (int k = 0; k < K; ++k) o[k] = (float)(value(k) - mx);
 }
 
-static int leaf_dsplit(const Plan &p, int64_t B, int tb) {
-  int64_t blocks = (int64_t)ceil_div(B, tb) * p.n_leaf;
-  int want = (int)std::max<int64_t>(1, (2 * p.num_sms + blocks - 1) / blocks);
-  int cap = std::max(1, std::min(kMaxDSplit, ceil_div(p.max_scope, LF_VC)));
-  return std::min(want, cap);
+static int leaf_dsplit(const Plan &p, int64_t B, int tb, int64_t slots, int nkc) {
+  const int64_t blocks = (int64_t)ceil_div(B, tb) * p.n_leaf * nkc;
+  const int cap = std::max(1, std::min(kMaxDSplit, ceil_div(p.max_scope, 4 * LF_VC)));
+  return pick_split(blocks, slots, 1, cap);
 }
 
 int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
@@ -419,12 +418,13 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
     const int kg = std::min(KG, 8);          // <= 64 k entries per CTA
     const int nkc = ceil_div(KG, kg);
     const int threads = 32 * kg;
-    ds = leaf_dsplit(p, B, LF_TB);
     const size_t smem = ((2 * LF_VC * (LF_TB + 1) * sizeof(float) + 15) & ~(size_t)15) +
                         2 * sizeof(double2) * LF_VC * kg * LF_KPT;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_leaf_fwd_gauss, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
+    ds = leaf_dsplit(p, B, LF_TB,
+                     device_slots((const void *)k_leaf_fwd_gauss, threads, smem, p.num_sms), nkc);
     dim3 grid(ceil_div(B, LF_TB), p.n_leaf, ds * nkc);
     k_leaf_fwd_gauss<<<grid, threads, smem, st>>>(
         x, B, p.d_vars, p.k, p.num_replicas, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
@@ -432,7 +432,7 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
   } else {
     const int threads = 32 * KG;
     if (threads > 1024) return fail(EINET_ERR_USAGE, "k too large for the leaf kernel (k <= 256)");
-    ds = leaf_dsplit(p, B, 32);
+    ds = leaf_dsplit(p, B, 32, 2LL * p.num_sms, 1);
     dim3 grid(ceil_div(B, 32), p.n_leaf, ds);
     k_leaf_fwd_discrete<<<grid, threads, 0, st>>>(
         x, B, p.d_vars, p.k, p.num_replicas, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
@@ -645,6 +645,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats_discrete(
 }
 
 int leaf_lsplit(const Plan &p, int64_t B) {
+  if (p.family == EINET_FAMILY_GAUSSIAN) return (int)std::max<int64_t>(1, std::min<int64_t>(16, (B + 255) / 256));
   int64_t blocks = (int64_t)ceil_div(p.max_scope, LS_VT) * p.n_leaf;
   int want = (int)std::max<int64_t>(1, (2 * p.num_sms + blocks - 1) / blocks);
   int cap = (int)std::max<int64_t>(1, std::min<int64_t>(8, (B + 255) / 256));

@@ -233,12 +233,12 @@ int launch_leaf_stats_tc(Plan &p, const uint8_t *compute, const float *x, int64_
   const int vchunks = ceil_div(p.max_scope, LT_VARS);
   const int64_t ctas = (int64_t)vchunks * p.n_leaf;
   const int64_t nblk = (B + LT_BLK - 1) / LT_BLK;
-  int ls = (int)std::max<int64_t>(1, std::min<int64_t>((2 * p.num_sms + ctas - 1) / ctas,
-                                                        std::min<int64_t>(nblk, p.max_lsplit)));
-  const int64_t per = (nblk + ls - 1) / ls;
-  ls = (int)((nblk + per - 1) / per);
   const int64_t smem = leaf_tc_smem(K, nn);
   cudaFuncSetAttribute(k_leaf_stats_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int ls = pick_split(ctas, device_slots((const void *)k_leaf_stats_tc, 256, smem, p.num_sms), 1,
+                      (int)std::min<int64_t>(nblk, p.max_lsplit));
+  const int64_t per = (nblk + ls - 1) / ls;
+  ls = (int)((nblk + per - 1) / per);
   dim3 grid(vchunks, p.n_leaf, ls);
   k_leaf_stats_tc<<<grid, 256, smem, st>>>(x, B, p.d_vars, K, p.num_replicas, nn, p.d_scope_off,
                                            p.d_scope_vars, p.d_leaf_rep, w.rho, w.bc, c.center,
