@@ -32,7 +32,7 @@ int check_cuda(cudaError_t err, const char *what) {
 }
 void count_launch(int n) { g_launches += n; }
 
-int pick_split(int64_t per, int64_t slots, int lo, int hi) {
+int pick_split(int64_t per, int64_t slots, int lo, int hi, double good) {
   lo = std::max(lo, 1);
   hi = std::max(hi, lo);
   int best = lo;
@@ -41,7 +41,7 @@ int pick_split(int64_t per, int64_t slots, int lo, int hi) {
     const int64_t n = per * s;
     const int64_t waves = (n + slots - 1) / slots;
     const double eff = (double)n / (double)(waves * slots);
-    if (waves >= 2 && eff >= 0.85) return s;
+    if (waves >= 2 && eff >= good) return s;
     if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best = s;
@@ -106,6 +106,7 @@ static void free_plan_memory(Plan *p) {
   f(p->d_leaf_rep);
   f(p->d_leaf_slab);
   f(p->d_leaf_of);
+  f(p->d_leaf_pvo);
   f(p->d_csr_off);
   f(p->d_csr_slot);
   f(p->d_slab_ones);
@@ -329,6 +330,15 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   p->c_const = seg(8 * (int64_t)p->n_leaf * K);
   p->c_active = seg(D);
   p->c_logh = seg(8 * (int64_t)(std::max(p->n_trials, 0) + 1));
+  p->leaf_dmma = p->family == EINET_FAMILY_GAUSSIAN && K % 8 == 0 && K <= 64;
+  if (p->leaf_dmma) {
+    p->h_leaf_pvo.assign(p->n_leaf + 1, 0);
+    for (int l = 0; l < p->n_leaf; ++l)
+      p->h_leaf_pvo[l + 1] =
+          p->h_leaf_pvo[l] + (int)align_up(p->h_scope_off[l + 1] - p->h_scope_off[l], 32);
+    p->c_leafimg = seg(16 * (int64_t)K * p->h_leaf_pvo.back());
+    p->c_cm2 = seg(8 * (int64_t)p->n_leaf * K);
+  }
   {
     const char *env = getenv("EINET_DISABLE_TC");
     p->use_tc = !(env && env[0] == '1');
@@ -382,6 +392,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   if ((rc = upload(&p->d_leaf_rep, p->h_leaf_rep))) return rc;
   if ((rc = upload(&p->d_leaf_slab, p->h_leaf_slab))) return rc;
   if ((rc = upload(&p->d_leaf_of, leaf_of))) return rc;
+  if (p->leaf_dmma && (rc = upload(&p->d_leaf_pvo, p->h_leaf_pvo))) return rc;
   if ((rc = upload(&p->d_csr_off, p->h_csr_off))) return rc;
   if ((rc = upload(&p->d_csr_slot, p->h_csr_slot))) return rc;
   if ((rc = upload(&p->d_slab_ones, p->h_slab_ones))) return rc;

@@ -80,7 +80,11 @@ struct Plan {
   einet_sizes sizes{};
   // compute segments (byte offsets)
   int64_t c_w32 = 0, c_mix32 = 0, c_leafp = 0, c_center = 0, c_const = 0, c_active = 0,
-          c_logh = 0;
+          c_logh = 0, c_leafimg = 0, c_cm2 = 0;
+  // FP64 tensor-core (DMMA) Gaussian leaf forward: scopes padded to 32 variables
+  int leaf_dmma = 0;               // eligible (Gaussian, K % 8 == 0, K <= 64)
+  std::vector<int> h_leaf_pvo;     // padded variable offset per leaf (n_leaf + 1)
+  int *d_leaf_pvo = nullptr;
   // workspace segments (byte offsets)
   int64_t w_off = 0, w_shift = 0, w_slots = 0, w_leafpart = 0, w_ea = 0, w_eb = 0,
           w_rt = 0, w_wpart = 0, w_rho = 0, w_lspart = 0, w_ppart = 0, w_mixpart = 0,
@@ -149,6 +153,11 @@ int launch_status_reset(int32_t *status, cudaStream_t st);
 void plan_tc_tiling(Plan &p);
 int wstats_tc_bsplit(const Plan &p, const LayerPlan &L, int64_t B, bool upper_bound);
 int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st);
+int launch_prepare_leaf_dmma(Plan &p, uint8_t *compute, cudaStream_t st);
+struct CompView;
+struct WsView;
+int launch_leaf_fwd_dmma(Plan &p, const CompView &c, const float *x, int64_t B, const WsView &w,
+                         int32_t *status, cudaStream_t st, int *ds_out);
 int launch_selftest_gemm(const float *A, const float *B, float *D, int N, int K,
                          cudaStream_t st);
 int leaf_lsplit(const Plan &p, int64_t B);
@@ -167,8 +176,8 @@ int launch_leaf_stats_tc(Plan &p, const uint8_t *compute, const float *x, int64_
 
 // Split factor s in [lo, hi] for a grid of ctas_per_split * s CTAs on
 // `slots` concurrently resident CTAs: the smallest s whose last wave is at
-// least 85% full once there are >= 2 waves (or the best-filled single wave).
-int pick_split(int64_t ctas_per_split, int64_t slots, int lo, int hi);
+// least `good` full once there are >= 2 waves (else the best-filled one).
+int pick_split(int64_t ctas_per_split, int64_t slots, int lo, int hi, double good = 0.85);
 // resident CTAs of `kernel` on the whole device for the given block / smem
 int64_t device_slots(const void *kernel, int block, size_t smem, int num_sms);
 

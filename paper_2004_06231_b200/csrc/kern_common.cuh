@@ -20,6 +20,8 @@ struct CompView {
   double *cnst;    // [n_leaf][K] fp64 scope constant
   uint8_t *active; // [D] 1 = not marginalised
   double *logh;    // binomial log base measure per count
+  double *leafimg; // DMMA leaf forward: B-fragment image [kstep][K/8][32] (padded scopes)
+  double *cm2;     // DMMA leaf forward: [n_leaf][K] sum of squared centred offsets
 };
 
 struct WsView {
@@ -49,6 +51,8 @@ inline CompView comp_view(const Plan &p, const uint8_t *c) {
   v.cnst = (double *)(b + p.c_const);
   v.active = (uint8_t *)(b + p.c_active);
   v.logh = (double *)(b + p.c_logh);
+  v.leafimg = (double *)(b + p.c_leafimg);
+  v.cm2 = (double *)(b + p.c_cm2);
   return v;
 }
 
@@ -104,6 +108,25 @@ __device__ __forceinline__ bool is_nan_f(float v) { return v != v; }
 // with 16-byte copies) and per-sample loops read coalesced across a warp.
 __device__ __forceinline__ int64_t tb_idx(int64_t l, int64_t b, int i, int64_t bc, int W) {
   return (l * bc + (b & ~31LL)) * W + (int64_t)i * 32 + (b & 31);
+}
+
+// cp.async (LDGSTS) helpers shared by the staged kernels
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
 }  // namespace einet

@@ -172,30 +172,13 @@ int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_
   count_launch((p.n_w ? 1 : 0) + (p.n_mix ? 1 : 0) + 3);
   int rc = launch_prepare_tc_tiles(p, compute, st);
   if (rc) return rc;
+  if ((rc = launch_prepare_leaf_dmma(p, compute, st))) return rc;
   return check_cuda(cudaGetLastError(), "prepare kernels");
 }
 
 // ---------------------------------------------------------------------------
 // leaf forward
 // ---------------------------------------------------------------------------
-
-__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 // Gaussian: Q[b,l,k] = sum_{d in scope} (x_bd*sa_dk + nmsa_dk)^2 with two fp64 FMAs
 // per term (B200 FP64 runs at half the FP32 rate): the leaf rows, whose
@@ -377,28 +360,39 @@ __global__ void __launch_bounds__(1024) k_leaf_fwd_discrete(
 }
 
 // value = cnst + sign * sum_split part  ->  slab (shift = max_k value, off = value - shift)
-__global__ void k_leaf_finalize(const double *__restrict__ part, int dsplit,
-                                const double *__restrict__ cnst, int64_t B, int K, int n_leaf,
-                                const int *leaf_slab, WsView ws, double sign) {
+// leaf row = cnst + sign * sum over splits, then the slab (shift, offsets).
+// grid (ceil(B/32), n_leaf), block 256; smem [32][K+1] doubles. The split sums
+// are read coalesced ([b][k] rows are contiguous per leaf), one warp per sample
+// takes the max over k and writes the sample's offsets contiguously.
+__global__ void __launch_bounds__(256) k_leaf_finalize(
+    const double *__restrict__ part, int dsplit, const double *__restrict__ cnst, int64_t B,
+    int K, int n_leaf, const int *leaf_slab, WsView ws, double sign) {
+  extern __shared__ double vals[];  // [32][K+1]
   const int leaf = blockIdx.y;
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
+  const int nb = (int)min((int64_t)32, B - b0);
   const int slab = leaf_slab[leaf];
-  auto value = [&](int k) {
+  for (int e = threadIdx.x; e < nb * K; e += 256) {
+    const int bl = e / K, k = e - bl * K;
+    const double *src = part + ((int64_t)leaf * ws.bc + b0) * K + e;
     double s = 0.0;
-    for (int q = 0; q < dsplit; ++q) s += part[(((int64_t)q * n_leaf + leaf) * ws.bc + b) * K + k];
-    return cnst[leaf * K + k] + sign * s;
-  };
-  double mx = -CUDART_INF;
-  for (int k = 0; k < K; ++k) mx = fmax(mx, value(k));
-  float *o = slab_off(ws, slab, b);
-  if (mx == -CUDART_INF) {
-    slab_shift(ws, slab)[b] = -CUDART_INF;
-    for (int k = 0; k < K; ++k) o[k] = 0.f;
-    return;
+    for (int q = 0; q < dsplit; ++q) s += src[(int64_t)q * n_leaf * ws.bc * K];
+    vals[bl * (K + 1) + k] = cnst[leaf * K + k] + sign * s;
   }
-  slab_shift(ws, slab)[b] = mx;
-  for (int k = 0; k < K; ++k) o[k] = (float)(value(k) - mx);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int bl = threadIdx.x >> 5; bl < nb; bl += 8) {
+    const double *v = vals + bl * (K + 1);
+    double mx = -CUDART_INF;
+    for (int k = lane; k < K; k += 32) mx = fmax(mx, v[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int64_t b = b0 + bl;
+    float *o = slab_off(ws, slab, b);
+    const bool dead = mx == -CUDART_INF;
+    if (lane == 0) slab_shift(ws, slab)[b] = mx;
+    for (int k = lane; k < K; k += 32) o[k] = dead ? 0.f : (float)(v[k] - mx);
+  }
 }
 
 static int leaf_dsplit(const Plan &p, int64_t B, int tb, int64_t slots, int nkc) {
@@ -414,7 +408,10 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
   WsView w = ws_view(p, wsb);
   const int KG = ceil_div(p.k, LF_KPT);
   int ds;
-  if (p.family == EINET_FAMILY_GAUSSIAN) {
+  if (p.leaf_dmma && p.use_tc) {
+    int rc = launch_leaf_fwd_dmma(p, c, x, B, w, status, st, &ds);
+    if (rc) return rc;
+  } else if (p.family == EINET_FAMILY_GAUSSIAN) {
     const int kg = std::min(KG, 8);          // <= 64 k entries per CTA
     const int nkc = ceil_div(KG, kg);
     const int threads = 32 * kg;
@@ -439,8 +436,12 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
         c.leafp, c.active, c.logh, p.family, p.num_states, p.n_trials, w.leafpart, w.bc,
         p.n_leaf, ds, status);
   }
-  dim3 g2(ceil_div(B, 128), p.n_leaf);
-  k_leaf_finalize<<<g2, 128, 0, st>>>(w.leafpart, ds, c.cnst, B, p.k, p.n_leaf, p.d_leaf_slab,
+  dim3 g2(ceil_div(B, 32), p.n_leaf);
+  const size_t fsmem = sizeof(double) * 32 * (p.k + 1);
+  if (fsmem > 48 * 1024)
+    cudaFuncSetAttribute(k_leaf_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fsmem);
+  k_leaf_finalize<<<g2, 256, fsmem, st>>>(w.leafpart, ds, c.cnst, B, p.k, p.n_leaf, p.d_leaf_slab,
                                       w, p.family == EINET_FAMILY_GAUSSIAN ? -1.0 : 1.0);
   count_launch(2);
   return check_cuda(cudaGetLastError(), "leaf forward kernels");
