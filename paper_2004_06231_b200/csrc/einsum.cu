@@ -31,40 +31,72 @@ int launch_einsum_childrho_tc(Plan &p, const LayerPlan &L, const uint8_t *comput
 constexpr int EF_TB = 128;  // samples per CTA, one per thread
 constexpr int EF_KC = 8;    // output entries (k) staged per W chunk
 
-// Forward prep (one thread per sample and row): normalised child exponentials
-// EA = exp(off_left - a), EB = exp(off_right - c) with a, c the fp32 maxima
-// (engine.py:99-104), kept per layer for the backward; the output shift
-// s_left + s_right + a + c (engine.py:108); NaN entering the layer -> status.
-// grid (ceil(B/128), L), block 128.
-__global__ void k_einsum_prep_fwd(WsView ws, const int *__restrict__ left_slab,
-                                  const int *__restrict__ right_slab,
-                                  const int *__restrict__ out_slab, int64_t B, int K,
-                                  float *__restrict__ EA, float *__restrict__ EB,
-                                  int layer_index, int32_t *status) {
-  const int l = blockIdx.y;
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  bool nan = false, dead = false;
-  double shift = 0.0;
-  for (int side = 0; side < 2; ++side) {
-    const int slab = side ? right_slab[l] : left_slab[l];
-    const float *o = slab_off(ws, slab, b);
-    const double s = slab_shift(ws, slab)[b];
-    float mx = -CUDART_INF_F;
-    for (int i = 0; i < K; ++i) {
-      const float v = o[i];
-      nan |= v != v;
-      mx = fmaxf(mx, v);
+// Forward prep: normalised child exponentials EA = exp(off_left - a),
+// EB = exp(off_right - c) with a, c the fp32 maxima (engine.py:99-104), kept
+// per layer for the backward; the output shift s_left + s_right + a + c
+// (engine.py:108); NaN entering the layer -> status.
+// One CTA per 32-sample block and row: the block's [K][32] slab tiles and the
+// EA/EB tiles are contiguous, so every pass is a coalesced elementwise sweep.
+// grid (ceil(B/32), L), block 128.
+__global__ void __launch_bounds__(128) k_einsum_prep_fwd(
+    WsView ws, const int *__restrict__ left_slab, const int *__restrict__ right_slab,
+    const int *__restrict__ out_slab, int64_t B, int K, float *__restrict__ EA,
+    float *__restrict__ EB, int layer_index, int32_t *status) {
+  __shared__ float mx[2][32];
+  __shared__ unsigned char dead[32];
+  const int l = blockIdx.y, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
+  const int nb = (int)min((int64_t)32, B - b0);
+  const int ls = left_slab[l], rs = right_slab[l];
+  if (wid < 2) {  // warp 0: left maxima, warp 1: right maxima (lane = sample)
+    const int slab = wid ? rs : ls;
+    const float *o = ws.off + tb_idx(slab, b0, 0, ws.bc, ws.ks) + lane;
+    float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F;
+    bool nan = false;
+    int k = 0;
+#pragma unroll 4
+    for (; k + 1 < K; k += 2) {
+      const float v0 = o[k * 32], v1 = o[(k + 1) * 32];
+      nan |= (v0 != v0) | (v1 != v1);
+      m0 = fmaxf(m0, v0);
+      m1 = fmaxf(m1, v1);
     }
-    nan |= s != s;
-    const bool d = s == -CUDART_INF || mx == -CUDART_INF_F;
-    dead |= d;
-    shift += s + (double)mx;
-    float *dst = side ? EB : EA;
-    for (int i = 0; i < K; ++i) dst[tb_idx(l, b, i, ws.bc, K)] = d ? 0.f : expf(o[i] - mx);
+    if (k < K) {
+      const float v = o[k * 32];
+      nan |= v != v;
+      m0 = fmaxf(m0, v);
+    }
+    const float m = fmaxf(m0, m1);
+    if (lane < nb) {
+      const double sh = slab_shift(ws, slab)[b0 + lane];
+      nan |= sh != sh;
+      if (nan) atomicMin(&status[1], layer_index);
+    }
+    mx[wid][lane] = m;
   }
-  if (nan) atomicMin(&status[1], layer_index);
-  slab_shift(ws, out_slab[l])[b] = dead ? -CUDART_INF : shift;
+  __syncthreads();
+  if (t < 32) {
+    const int64_t b = b0 + t;
+    bool d = true;
+    if (t < nb) {
+      const double sl = slab_shift(ws, ls)[b], sr = slab_shift(ws, rs)[b];
+      d = sl == -CUDART_INF || sr == -CUDART_INF || mx[0][t] == -CUDART_INF_F ||
+          mx[1][t] == -CUDART_INF_F;
+      slab_shift(ws, out_slab[l])[b] =
+          d ? -CUDART_INF : (sl + (double)mx[0][t]) + (sr + (double)mx[1][t]);
+    }
+    dead[t] = d;
+  }
+  __syncthreads();
+  const float *ol = ws.off + tb_idx(ls, b0, 0, ws.bc, ws.ks);
+  const float *orr = ws.off + tb_idx(rs, b0, 0, ws.bc, ws.ks);
+  float *ea = EA + tb_idx(l, b0, 0, ws.bc, K), *eb = EB + tb_idx(l, b0, 0, ws.bc, K);
+  for (int e = t; e < K * 32; e += 128) {
+    const int bl = e & 31;
+    const bool d = dead[bl];
+    ea[e] = d ? 0.f : expf(ol[e] - mx[0][bl]);
+    eb[e] = d ? 0.f : expf(orr[e] - mx[1][bl]);
+  }
 }
 
 template <int KT>
@@ -118,7 +150,7 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const float *__
   }
   __syncthreads();
   if (!live) return;
-  float *o = slab_off(ws, out_slab[l], b);
+  const Col32 o = slab_off(ws, out_slab[l], b);
   for (int kk = 0; kk < nk; ++kk) {
     const float *wk = wsm + kk * K * KT;
     float acc = 0.f;
@@ -136,7 +168,7 @@ __global__ void k_einsum_fwd_generic(WsView ws, const float *__restrict__ EA,
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  float *o = slab_off(ws, out_slab[l], b);
+  const Col32 o = slab_off(ws, out_slab[l], b);
   const float *Wl = W + (int64_t)l * Ko * K * K;
   for (int k = 0; k < Ko; ++k) {
     float acc = 0.f;
@@ -154,94 +186,127 @@ __global__ void k_einsum_fwd_generic(WsView ws, const float *__restrict__ EA,
 // mixing layers (engine.py:112-122, 268-293)
 // ---------------------------------------------------------------------------
 
-// grid (ceil(B/128), M), block 128
-__global__ void k_mixing_fwd(WsView ws, const int *__restrict__ src_slab,
-                             const uint8_t *__restrict__ mask, const int *__restrict__ out_slab,
-                             const float *__restrict__ w, int64_t B, int Ko, int dmax,
-                             int layer_index, int32_t *status) {
+// Mixing forward, elementwise over (sample, k) of a 32-sample block:
+// out = s + mk + log sum_c w_c exp(s_c - s + off_c - mk) with s = max_c s_c
+// (engine.py:112-122; masked children never contribute).
+// grid (ceil(B/32), M), block 128, smem: the row's (src slab, w) per child.
+__global__ void __launch_bounds__(128) k_mixing_fwd(
+    WsView ws, const int *__restrict__ src_slab, const uint8_t *__restrict__ mask,
+    const int *__restrict__ out_slab, const float *__restrict__ w, int64_t B, int Ko, int dmax,
+    int layer_index, int32_t *status) {
+  extern __shared__ int msm[];
+  int *src = msm;                        // [dmax], -1 = masked
+  float *wc = (float *)(msm + dmax);     // [dmax]
+  (void)layer_index;
+  (void)status;
   const int m = blockIdx.y;
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  double s = -CUDART_INF;
-  for (int c = 0; c < dmax; ++c) {
-    if (!mask[m * dmax + c]) continue;
-    const double sc = slab_shift(ws, src_slab[m * dmax + c])[b];
-    if (sc > s || sc != sc) s = sc;
+  for (int c = threadIdx.x; c < dmax; c += 128) {
+    src[c] = mask[m * dmax + c] ? src_slab[m * dmax + c] : -1;
+    wc[c] = w[m * dmax + c];
   }
+  __syncthreads();
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int os = out_slab[m];
-  float *o = slab_off(ws, os, b);
-  if (s == -CUDART_INF) {
-    slab_shift(ws, os)[b] = -CUDART_INF;
-    for (int k = 0; k < Ko; ++k) o[k] = 0.f;
-    return;
-  }
-  for (int k = 0; k < Ko; ++k) {
+  float *o = ws.off + tb_idx(os, b0, 0, ws.bc, ws.ks);
+  for (int e = threadIdx.x; e < Ko * 32; e += 128) {
+    const int bl = e & 31;
+    const int64_t b = b0 + bl;
+    if (b >= B) continue;
+    double sh = -CUDART_INF;
+    for (int c = 0; c < dmax; ++c) {
+      if (src[c] < 0) continue;
+      const double sc = slab_shift(ws, src[c])[b];
+      if (sc > sh || sc != sc) sh = sc;
+    }
+    if (e < 32) slab_shift(ws, os)[b] = sh;
+    if (sh == -CUDART_INF) {
+      o[e] = 0.f;
+      continue;
+    }
     float mk = -CUDART_INF_F;
     for (int c = 0; c < dmax; ++c) {
-      if (!mask[m * dmax + c]) continue;
-      const int sl = src_slab[m * dmax + c];
-      const double sc = slab_shift(ws, sl)[b];
+      if (src[c] < 0) continue;
+      const double sc = slab_shift(ws, src[c])[b];
       if (sc == -CUDART_INF) continue;
-      mk = fmaxf(mk, (float)(sc - s) + slab_off(ws, sl, b)[k]);
+      mk = fmaxf(mk, (float)(sc - sh) + ws.off[tb_idx(src[c], b0, 0, ws.bc, ws.ks) + e]);
     }
     float out = -CUDART_INF_F;
     if (mk != -CUDART_INF_F) {
       float sum = 0.f;
       for (int c = 0; c < dmax; ++c) {
-        if (!mask[m * dmax + c]) continue;
-        const int sl = src_slab[m * dmax + c];
-        const double sc = slab_shift(ws, sl)[b];
+        if (src[c] < 0) continue;
+        const double sc = slab_shift(ws, src[c])[b];
         if (sc == -CUDART_INF) continue;
-        const float dv = (float)(sc - s) + slab_off(ws, sl, b)[k];
-        sum = fmaf(w[m * dmax + c], expf(dv - mk), sum);
+        const float dv = (float)(sc - sh) + ws.off[tb_idx(src[c], b0, 0, ws.bc, ws.ks) + e];
+        sum = fmaf(wc[c], expf(dv - mk), sum);
       }
       if (sum > 0.f) out = mk + logf(sum);
     }
-    o[k] = out;
+    o[e] = out;
   }
-  slab_shift(ws, os)[b] = s;
 }
 
-// grid (ceil(B/64), M), block 64; per-CTA partials of the mixing statistics
-__global__ void k_mixing_bwd(WsView ws, const int *__restrict__ src_slab,
-                             const uint8_t *__restrict__ mask, const int *__restrict__ out_slab,
-                             const int *__restrict__ mix_slot, const float *__restrict__ w,
-                             const int *csr_off, const int *csr_slot, const uint8_t *ones,
-                             int64_t B, int Ko, int dmax, double *mixpart, int64_t mix_off,
-                             int64_t n_mix) {
-  __shared__ double red[2];
+// Responsibility of slab `slab` for element e (= k*32 + sample) of the
+// 32-sample block at b0: ordered sum over the slab's contribution slots.
+__device__ __forceinline__ float gather_rho_tile(const WsView &ws, int q0, int q1,
+                                                 const int *__restrict__ csr_slot, bool one,
+                                                 int64_t b0, int e) {
+  if (one) return 1.0f;
+  float acc = 0.0f;
+  for (int q = q0; q < q1; ++q) acc += ws.slots[tb_idx(csr_slot[q], b0, 0, ws.bc, ws.ks) + e];
+  return acc;
+}
+
+// Deterministic CTA sum of one double per thread (fixed tree, 4 warps).
+__device__ __forceinline__ double cta_sum128(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  const double s = (red[0] + red[1]) + (red[2] + red[3]);
+  __syncthreads();
+  return s;
+}
+
+// Mixing backward: contribution of child c to the responsibility of its slab
+// rho_c = rho * w_c * exp(s_c + off_c - s - off) (engine.py:268-293), written
+// to the child's slot; the mixing statistics get the per-CTA partial sums.
+// grid (ceil(B/32), M), block 128.
+__global__ void __launch_bounds__(128) k_mixing_bwd(
+    WsView ws, const int *__restrict__ src_slab, const uint8_t *__restrict__ mask,
+    const int *__restrict__ out_slab, const int *__restrict__ mix_slot,
+    const float *__restrict__ w, const int *csr_off, const int *__restrict__ csr_slot,
+    const uint8_t *ones, int64_t B, int Ko, int dmax, double *mixpart, int64_t mix_off,
+    int64_t n_mix) {
+  __shared__ double red[4];
   const int m = blockIdx.y;
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = b < B;
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int os = out_slab[m];
-  const double so = live ? slab_shift(ws, os)[b] : 0.0;
+  const int q0 = csr_off[os], q1 = csr_off[os + 1];
+  const bool one = ones[os] != 0;
+  const float *oo = ws.off + tb_idx(os, b0, 0, ws.bc, ws.ks);
   for (int c = 0; c < dmax; ++c) {
-    double part = 0.0;
-    if (live && mask[m * dmax + c]) {
+    float run = 0.f;
+    if (mask[m * dmax + c]) {
       const int sl = src_slab[m * dmax + c];
-      const double sc = slab_shift(ws, sl)[b];
-      const bool ok = so != -CUDART_INF && sc != -CUDART_INF;
-      const float delta = ok ? (float)(sc - so) : 0.f;
       const float wc = w[m * dmax + c];
-      float *dst = slot_ptr(ws, mix_slot[m * dmax + c], b);
-      const float *oc = slab_off(ws, sl, b), *oo = slab_off(ws, os, b);
-      float run = 0.f;
-      for (int k = 0; k < Ko; ++k) {
-        const float dk = delta + oc[k] - oo[k];
+      const float *oc = ws.off + tb_idx(sl, b0, 0, ws.bc, ws.ks);
+      float *dst = ws.slots + tb_idx(mix_slot[m * dmax + c], b0, 0, ws.bc, ws.ks);
+      for (int e = threadIdx.x; e < Ko * 32; e += 128) {
+        const int64_t b = b0 + (e & 31);
+        if (b >= B) continue;
+        const double so = slab_shift(ws, os)[b], sc = slab_shift(ws, sl)[b];
+        const bool ok = so != -CUDART_INF && sc != -CUDART_INF;
+        const float dk = (ok ? (float)(sc - so) : 0.f) + oc[e] - oo[e];
         const float ratio = (ok && isfinite(dk)) ? expf(dk) : 0.f;
-        const float contrib = gather_rho(ws, csr_off, csr_slot, ones, os, b, k) * wc * ratio;
-        dst[k] = contrib;
+        const float contrib = gather_rho_tile(ws, q0, q1, csr_slot, one, b0, e) * wc * ratio;
+        dst[e] = contrib;
         run += contrib;
       }
-      part = (double)run;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
-    __syncthreads();
+    const double tot = cta_sum128((double)run, red);
     if (threadIdx.x == 0)
-      mixpart[(int64_t)blockIdx.x * n_mix + mix_off + (int64_t)m * dmax + c] = red[0] + red[1];
-    __syncthreads();
+      mixpart[(int64_t)blockIdx.x * n_mix + mix_off + (int64_t)m * dmax + c] = tot;
   }
 }
 
@@ -250,20 +315,24 @@ __global__ void k_mixing_bwd(WsView ws, const int *__restrict__ src_slab,
 // ---------------------------------------------------------------------------
 
 // RT = rho / r per row and sample (engine.py:310-311), r = exp(log r) from the
-// forward offsets. grid (ceil(B/128), L), block 128
-__global__ void k_einsum_bwd_rt(WsView ws, const int *out_slab, const int *csr_off,
-                                const int *csr_slot, const uint8_t *ones, int64_t B, int Ko,
-                                float *RT) {
+// forward offsets; elementwise over a 32-sample block (contiguous tiles).
+// grid (ceil(B/32), L), block 128
+__global__ void __launch_bounds__(128) k_einsum_bwd_rt(
+    WsView ws, const int *out_slab, const int *csr_off, const int *__restrict__ csr_slot,
+    const uint8_t *ones, int64_t B, int Ko, float *RT) {
   const int l = blockIdx.y;
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int os = out_slab[l];
-  const double so = slab_shift(ws, os)[b];
-  const float *oo = slab_off(ws, os, b);
-  for (int k = 0; k < Ko; ++k) {
-    const float r = so == -CUDART_INF ? 0.f : expf(oo[k]);
-    const float rho = gather_rho(ws, csr_off, csr_slot, ones, os, b, k);
-    RT[tb_idx(l, b, k, ws.bc, ws.ks)] = r > 0.f ? rho / r : 0.f;
+  const int q0 = csr_off[os], q1 = csr_off[os + 1];
+  const bool one = ones[os] != 0;
+  const float *oo = ws.off + tb_idx(os, b0, 0, ws.bc, ws.ks);
+  float *rt = RT + tb_idx(l, b0, 0, ws.bc, ws.ks);
+  for (int e = threadIdx.x; e < Ko * 32; e += 128) {
+    const int64_t b = b0 + (e & 31);
+    if (b >= B) continue;
+    const float r = slab_shift(ws, os)[b] == -CUDART_INF ? 0.f : expf(oo[e]);
+    const float rho = gather_rho_tile(ws, q0, q1, csr_slot, one, b0, e);
+    rt[e] = r > 0.f ? rho / r : 0.f;
   }
 }
 
@@ -385,7 +454,7 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_childrho(
     }
   }
   if (!live) return;
-  float *dl = slot_ptr(ws, slot_left[l], b), *dr = slot_ptr(ws, slot_right[l], b);
+  const Col32 dl = slot_ptr(ws, slot_left[l], b), dr = slot_ptr(ws, slot_right[l], b);
 #pragma unroll
   for (int i = 0; i < KT; ++i)
     if (i < K) {
@@ -407,7 +476,7 @@ __global__ void k_einsum_childrho_generic(const float *__restrict__ EA,
   auto eb = [&](int i) { return EB[tb_idx(l, b, i, ws.bc, K)]; };
   auto rt = [&](int k) { return RT[tb_idx(l, b, k, ws.bc, ws.ks)]; };
   const float *Wl = W + (int64_t)l * Ko * K * K;
-  float *dl = slot_ptr(ws, slot_left[l], b), *dr = slot_ptr(ws, slot_right[l], b);
+  const Col32 dl = slot_ptr(ws, slot_left[l], b), dr = slot_ptr(ws, slot_right[l], b);
   for (int i = 0; i < K; ++i) {
     float acc = 0.f;
     for (int k = 0; k < Ko; ++k) {
@@ -552,7 +621,7 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
       float *EA = (float *)layer_ea(p, w, L), *EB = (float *)layer_eb(p, w, L);
       {
         ProfScope prof("einsum_prep", st);
-        dim3 grid(ceil_div(B, 128), L.rows);
+        dim3 grid(ceil_div(B, 32), L.rows);
         k_einsum_prep_fwd<<<grid, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
                                                 B, p.k, EA, EB, L.index, status);
       }
@@ -565,8 +634,8 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
       count_launch(2);
     } else {
       ProfScope prof("mixing_fwd", st);
-      dim3 grid(ceil_div(B, 128), L.rows);
-      k_mixing_fwd<<<grid, 128, 0, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
+      dim3 grid(ceil_div(B, 32), L.rows);
+      k_mixing_fwd<<<grid, 128, 8 * L.dmax, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
                                          c.mix32 + L.mix_off, B, L.k_out, L.dmax, L.index,
                                          status);
       count_launch();
@@ -603,9 +672,9 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
     const LayerPlan &L = p.layers[li];
     if (L.kind == EINET_LAYER_MIXING) {
       ProfScope prof("mixing_bwd", st);
-      const int nb = ceil_div(B, 64);
+      const int nb = ceil_div(B, 32);
       dim3 grid(nb, L.rows);
-      k_mixing_bwd<<<grid, 64, 0, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
+      k_mixing_bwd<<<grid, 128, 0, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
                                         L.d_mix_slot, c.mix32 + L.mix_off, p.d_csr_off,
                                         p.d_csr_slot, p.d_slab_ones, B, L.k_out, L.dmax,
                                         w.mixpart, L.mix_off, p.n_mix);
@@ -617,7 +686,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
     const float *EA = layer_ea(p, w, L), *EB = layer_eb(p, w, L);
     {
       ProfScope prof("einsum_bwd_rt", st);
-      dim3 g1(ceil_div(B, 128), L.rows);
+      dim3 g1(ceil_div(B, 32), L.rows);
       k_einsum_bwd_rt<<<g1, 128, 0, st>>>(w, L.d_out_slab, p.d_csr_off, p.d_csr_slot,
                                           p.d_slab_ones, B, L.k_out, w.rt);
     }

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(128, 1) k_einsum_fwd_tc(
       for (int i = 0; i < K; ++i) ea[i] = live ? src[i * 32] : 0.f;
     }
     const uint32_t ta = tm + buf * 256 + ((uint32_t)(32 * w) << 16);
-    float *o = slab_off(ws, out_slab[l], live ? b : 0);
+    const Col32 o = slab_off(ws, out_slab[l], live ? b : 0);
     for (int kl = 0; kl < nk; ++kl) {
       float v[K];
 #pragma unroll
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(128, 1) k_einsum_childrho_tc(
     tc::mma_commit(&mbar[hb]);
   };
   if (t == 0) issue(0);
-  float *dl = slot_ptr(ws, slot_left[l], live ? b : 0);
+  const Col32 dl = slot_ptr(ws, slot_left[l], live ? b : 0);
   const float *earow = EA + tb_idx(l, bsafe, 0, ws.bc, K);
   for (int h = 0; h < ni; ++h) {
     const int hb = h & 1;
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(128, 1) k_einsum_childrho_tc(
     __syncthreads();
   }
   if (live) {
-    float *dr = slot_ptr(ws, slot_right[l], b);
+    const Col32 dr = slot_ptr(ws, slot_right[l], b);
 #pragma unroll
     for (int j = 0; j < K; ++j) dr[j] = eb[j] * right[j];
   }

@@ -25,9 +25,9 @@ struct CompView {
 };
 
 struct WsView {
-  float *off;      // [slab][Bc][KS]
+  float *off;      // [slab][Bc/32][KS][32] (32-sample transposed blocks, tb_idx)
   double *shift;   // [slab][Bc]
-  float *slots;    // [slot][Bc][KS]
+  float *slots;    // [slot][Bc/32][KS][32]
   double *leafpart;
   float *ea, *eb;  // [row][Bc][K]
   float *rt;       // [row][Bc][KS]
@@ -77,14 +77,30 @@ inline WsView ws_view(const Plan &p, const uint8_t *w) {
   return v;
 }
 
-__device__ __forceinline__ float *slab_off(const WsView &w, int slab, int64_t b) {
-  return w.off + ((int64_t)slab * w.bc + b) * w.ks;
+// Per-sample vectors EA, EB, RT and the leaf responsibilities live in 32-sample
+// transposed blocks: entry i of sample b in row l of a width-W array is at
+//   (l*bc + b - b%32)*W + i*32 + b%32      (bc is a multiple of 32)
+// so one block is a contiguous [W][32] tile (a batch-reduction GEMM stages it
+// with 16-byte copies) and per-sample loops read coalesced across a warp.
+__device__ __forceinline__ int64_t tb_idx(int64_t l, int64_t b, int i, int64_t bc, int W) {
+  return (l * bc + (b & ~31LL)) * W + (int64_t)i * 32 + (b & 31);
+}
+
+// One sample's entries of a slab or slot: entry k of sample b lives at
+// tb_idx(slab, b, k, bc, ks), i.e. stride 32 floats, so a warp of consecutive
+// samples touching entry k reads or writes one contiguous 128-byte line.
+struct Col32 {
+  float *p;
+  __device__ __forceinline__ float &operator[](int k) const { return p[(int64_t)k * 32]; }
+};
+__device__ __forceinline__ Col32 slab_off(const WsView &w, int slab, int64_t b) {
+  return Col32{w.off + tb_idx(slab, b, 0, w.bc, w.ks)};
 }
 __device__ __forceinline__ double *slab_shift(const WsView &w, int slab) {
   return w.shift + (int64_t)slab * w.bc;
 }
-__device__ __forceinline__ float *slot_ptr(const WsView &w, int slot, int64_t b) {
-  return w.slots + ((int64_t)slot * w.bc + b) * w.ks;
+__device__ __forceinline__ Col32 slot_ptr(const WsView &w, int slot, int64_t b) {
+  return Col32{w.slots + tb_idx(slot, b, 0, w.bc, w.ks)};
 }
 
 // Responsibility of slab `slab` for sample b, entry k: ordered sum of its
@@ -100,15 +116,6 @@ __device__ __forceinline__ float gather_rho(const WsView &w, const int *csr_off,
 }
 
 __device__ __forceinline__ bool is_nan_f(float v) { return v != v; }
-
-// Per-sample vectors EA, EB, RT and the leaf responsibilities live in 32-sample
-// transposed blocks: entry i of sample b in row l of a width-W array is at
-//   (l*bc + b - b%32)*W + i*32 + b%32      (bc is a multiple of 32)
-// so one block is a contiguous [W][32] tile (a batch-reduction GEMM stages it
-// with 16-byte copies) and per-sample loops read coalesced across a warp.
-__device__ __forceinline__ int64_t tb_idx(int64_t l, int64_t b, int i, int64_t bc, int W) {
-  return (l * bc + (b & ~31LL)) * W + (int64_t)i * 32 + (b & 31);
-}
 
 // cp.async (LDGSTS) helpers shared by the staged kernels
 __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {

@@ -359,15 +359,17 @@ __global__ void __launch_bounds__(1024) k_leaf_fwd_discrete(
   }
 }
 
-// value = cnst + sign * sum_split part  ->  slab (shift = max_k value, off = value - shift)
-// leaf row = cnst + sign * sum over splits, then the slab (shift, offsets).
-// grid (ceil(B/32), n_leaf), block 256; smem [32][K+1] doubles. The split sums
-// are read coalesced ([b][k] rows are contiguous per leaf), one warp per sample
-// takes the max over k and writes the sample's offsets contiguously.
+// leaf row = cnst + sign * sum over splits, then the slab (shift = max_k value,
+// offsets = value - shift). grid (ceil(B/32), n_leaf), block 256; smem
+// [32][K+1] doubles. The split sums are read coalesced ([b][k] rows are
+// contiguous per leaf), one warp per sample takes the max over k, and the
+// block's [K][32] slab tile (contiguous in the 32-sample transposed layout) is
+// written coalesced.
 __global__ void __launch_bounds__(256) k_leaf_finalize(
     const double *__restrict__ part, int dsplit, const double *__restrict__ cnst, int64_t B,
     int K, int n_leaf, const int *leaf_slab, WsView ws, double sign) {
   extern __shared__ double vals[];  // [32][K+1]
+  __shared__ double mxs[32];
   const int leaf = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int nb = (int)min((int64_t)32, B - b0);
@@ -387,11 +389,18 @@ __global__ void __launch_bounds__(256) k_leaf_finalize(
     for (int k = lane; k < K; k += 32) mx = fmax(mx, v[k]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int64_t b = b0 + bl;
-    float *o = slab_off(ws, slab, b);
-    const bool dead = mx == -CUDART_INF;
-    if (lane == 0) slab_shift(ws, slab)[b] = mx;
-    for (int k = lane; k < K; k += 32) o[k] = dead ? 0.f : (float)(v[k] - mx);
+    if (lane == 0) {
+      mxs[bl] = mx;
+      slab_shift(ws, slab)[b0 + bl] = mx;
+    }
+  }
+  __syncthreads();
+  float *tile = ws.off + tb_idx(slab, b0, 0, ws.bc, ws.ks);
+  for (int e = threadIdx.x; e < K * 32; e += 256) {
+    const int k = e >> 5, bl = e & 31;
+    if (bl >= nb) continue;
+    const double mx = mxs[bl];
+    tile[e] = mx == -CUDART_INF ? 0.f : (float)(vals[bl * (K + 1) + k] - mx);
   }
 }
 
@@ -451,36 +460,33 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
 // leaf responsibilities and statistics (engine.py:318-327)
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ float block_sum_128(float v, float *red) {
-  // deterministic: fixed shuffle tree then fixed-order sum of 4 warp results
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  const int wid = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) red[wid] = v;
-  __syncthreads();
-  float s = 0.f;
-  if (threadIdx.x == 0) s = (red[0] + red[1]) + (red[2] + red[3]);
-  __syncthreads();
-  return s;
-}
-
-// rho_leaf[b,l,k] from the slot CSR; per-CTA partial of P[l,k] = sum_b rho.
-// grid (ceil(B/128), n_leaf), block 128.
-__global__ void k_leaf_rho(WsView ws, const int *csr_off, const int *csr_slot,
-                           const uint8_t *ones, const int *leaf_slab, int64_t B, int K,
-                           int n_leaf, double *ppart) {
-  __shared__ float red[4];
+// rho_leaf[b,l,k] from the slot CSR (elementwise over a 32-sample block) and
+// the block's partial of P[l,k] = sum_b rho: a warp covers one k for the 32
+// samples, reduced with a fixed shuffle tree.
+// grid (ceil(B/32), n_leaf), block 128.
+__global__ void __launch_bounds__(128) k_leaf_rho(WsView ws, const int *csr_off,
+                                                  const int *__restrict__ csr_slot,
+                                                  const uint8_t *ones, const int *leaf_slab,
+                                                  int64_t B, int K, int n_leaf, double *ppart) {
   const int leaf = blockIdx.y;
-  const int64_t b = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int slab = leaf_slab[leaf];
-  for (int k = 0; k < K; ++k) {
+  const int q0 = csr_off[slab], q1 = csr_off[slab + 1];
+  const bool one = ones[slab] != 0;
+  float *rho = ws.rho + tb_idx(leaf, b0, 0, ws.bc, K);
+  for (int e = threadIdx.x; e < K * 32; e += 128) {
     float v = 0.f;
-    if (b < B) {
-      v = gather_rho(ws, csr_off, csr_slot, ones, slab, b, k);
-      ws.rho[tb_idx(leaf, b, k, ws.bc, K)] = v;
+    if (b0 + (e & 31) < B) {
+      if (one) {
+        v = 1.f;
+      } else {
+        for (int q = q0; q < q1; ++q) v += ws.slots[tb_idx(csr_slot[q], b0, 0, ws.bc, ws.ks) + e];
+      }
+      rho[e] = v;
     }
-    float s = block_sum_128(v, red);
-    if (threadIdx.x == 0) ppart[((int64_t)blockIdx.x * n_leaf + leaf) * K + k] = (double)s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((e & 31) == 0) ppart[((int64_t)blockIdx.x * n_leaf + leaf) * K + (e >> 5)] = (double)v;
   }
 }
 
@@ -658,7 +664,7 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
   CompView c = comp_view(p, compute);
   WsView w = ws_view(p, wsb);
   const int K = p.k, D = p.d_vars, R = p.num_replicas, T = p.suff;
-  const int nb = ceil_div(B, 128);
+  const int nb = ceil_div(B, 32);
   double *Pcall = (double *)(wsb + p.w_tmp_p);
   {
   ProfScope prof("leaf_rho", st);

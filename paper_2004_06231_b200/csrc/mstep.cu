@@ -8,42 +8,61 @@
 
 namespace einet {
 
+// dst[i] (+)= scale[i] * sum_p part[p*stride + i]. Few partials: one thread per
+// output, loads unrolled. Many partials over few outputs: one CTA per output,
+// threads stride over the partials, fixed shuffle tree. Both fixed-order.
 __global__ void k_reduce_partials(double *__restrict__ dst, const double *__restrict__ part,
                                   int nparts, int64_t n, int64_t stride,
-                                  const double *__restrict__ scale) {
+                                  const double *__restrict__ scale, int store) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
+#pragma unroll 8
     for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * stride + i];
-    dst[i] += scale ? scale[i] * s : s;
+    if (scale) s *= scale[i];
+    dst[i] = store ? s : dst[i] + s;
   }
 }
 
-__global__ void k_reduce_partials_store(double *__restrict__ dst,
-                                        const double *__restrict__ part, int nparts, int64_t n,
-                                        int64_t stride) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * stride + i];
-    dst[i] = s;
+__global__ void __launch_bounds__(256) k_reduce_partials_cta(
+    double *__restrict__ dst, const double *__restrict__ part, int nparts, int64_t stride,
+    const double *__restrict__ scale, int store) {
+  __shared__ double red[8];
+  const int64_t i = blockIdx.x;
+  double s = 0.0;
+  for (int p = threadIdx.x; p < nparts; p += 256) s += part[(int64_t)p * stride + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
+    if (scale) t *= scale[i];
+    dst[i] = store ? t : dst[i] + t;
   }
+}
+
+static void reduce_partials(double *dst, const double *part, int nparts, int64_t n,
+                            int64_t stride, const double *scale, int store, cudaStream_t st) {
+  if (n <= 0) return;
+  if (nparts >= 64 && n <= 65536) {
+    k_reduce_partials_cta<<<(unsigned)n, 256, 0, st>>>(dst, part, nparts, stride, scale, store);
+  } else {
+    const int grid = (int)std::min<int64_t>((n + kReduceThreads - 1) / kReduceThreads, 8192);
+    k_reduce_partials<<<grid, kReduceThreads, 0, st>>>(dst, part, nparts, n, stride, scale,
+                                                       store);
+  }
+  count_launch();
 }
 
 void launch_reduce_partials_store(double *dst, const double *part, int nparts, int64_t n,
                                   int64_t stride, cudaStream_t st) {
-  if (n <= 0) return;
-  const int grid = (int)std::min<int64_t>((n + kReduceThreads - 1) / kReduceThreads, 8192);
-  k_reduce_partials_store<<<grid, kReduceThreads, 0, st>>>(dst, part, nparts, n, stride);
-  count_launch();
+  reduce_partials(dst, part, nparts, n, stride, nullptr, 1, st);
 }
 
 void launch_reduce_partials(double *dst, const double *part, int nparts, int64_t n,
                             int64_t stride, const double *scale, cudaStream_t st) {
-  if (n <= 0) return;
-  const int grid = (int)std::min<int64_t>((n + kReduceThreads - 1) / kReduceThreads, 8192);
-  k_reduce_partials<<<grid, kReduceThreads, 0, st>>>(dst, part, nparts, n, stride, scale);
-  count_launch();
+  reduce_partials(dst, part, nparts, n, stride, scale, 0, st);
 }
 
 __device__ __forceinline__ bool step_failed(const int32_t *status) {
