@@ -348,18 +348,19 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     if (!L.tc) continue;
     L.fw_off = seg(L.fw_tile * L.rows * L.ng);
     L.uw_off = seg(L.uw_tile * L.rows * L.ni);
+    L.vw_off = seg(std::max(L.uw_tile * L.ni, L.rw_tile) * L.rows);
   }
   z.compute_bytes = off;
 
-  p->bc = align_up(max_chunk, 32);  // per-sample arrays use 32-sample blocks
+  p->bc = align_up(max_chunk, 128);  // 32-sample blocks, 128-sample tensor-core tiles
   const int64_t Bc = p->bc, KS = p->ks;
   off = 0;
   p->w_off = seg(4 * (int64_t)p->num_slabs * Bc * KS);
   p->w_shift = seg(8 * (int64_t)p->num_slabs * Bc);
   p->w_slots = seg(4 * (int64_t)std::max(p->num_slots, 1) * Bc * KS);
   p->w_leafpart = seg(8 * (int64_t)kMaxDSplit * p->n_leaf * Bc * K);
-  p->w_ea = seg(4 * (int64_t)p->n_erows * Bc * K);
-  p->w_eb = seg(4 * (int64_t)p->n_erows * Bc * K);
+  p->w_ea = seg(4 * (int64_t)p->n_erows * (Bc / 32) * K * EV_ROW);
+  p->w_eb = seg(4 * (int64_t)p->n_erows * (Bc / 32) * K * EV_ROW);
   p->w_rt = seg(4 * p->max_rows * Bc * KS);
   // W-stat partials: bsplit chosen per layer by the launcher, bounded here
   int64_t wpart = 0;
@@ -369,9 +370,9 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     int64_t blocks = (int64_t)L.rows * L.k_out;
     int64_t bs = std::min<int64_t>(std::max<int64_t>(1, (2 * p->num_sms + blocks - 1) / blocks),
                                    std::min<int64_t>(kMaxBSplit, (Bc + 63) / 64));
-    // tensor-core W statistics split their batch as well (einsum_tc.cu)
-    int64_t tc_bs = L.tc ? wstats_tc_bsplit(*p, L, Bc, true) : 1;
-    wpart = std::max(wpart, std::max(bs, tc_bs) * lw);
+    // tensor-core W statistics: fp32 partials per (segment, slot) (wstats_tc.cu)
+    int64_t tc_slots = L.tc ? wstats_tc_slots(*p, L, Bc) : 0;
+    wpart = std::max(wpart, std::max(bs * lw, (tc_slots * lw + 1) / 2));
   }
   p->w_wpart = seg(8 * std::max<int64_t>(wpart, 1));
   p->w_rho = seg(4 * (int64_t)p->n_leaf * Bc * K);
@@ -382,6 +383,22 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   p->w_llpart = seg(8 * (int64_t)ceil_div(Bc, 256));
   p->w_tmp_s = seg(8 * p->n_phi);
   p->w_tmp_p = seg(8 * (int64_t)p->n_leaf * K);
+  {
+    int ko8max = 0;
+    bool any_tc = false;
+    for (auto &L : p->layers)
+      if (L.tc) {
+        any_tc = true;
+        ko8max = std::max(ko8max, L.ko8);
+      }
+    p->w_ebm = seg(any_tc ? 8 * (int64_t)p->n_erows * Bc * K : 0);
+    p->w_eam = seg(any_tc ? 8 * (int64_t)p->n_erows * Bc * K : 0);
+    p->w_rtm = seg(any_tc ? 8 * p->max_rows * Bc * ko8max : 0);
+    int nnmax = 0;
+    for (auto &L : p->layers)
+      if (L.tc) nnmax = std::max(nnmax, L.nn);
+    p->w_rtb = seg(any_tc ? 8 * p->max_rows * Bc * nnmax : 0);
+  }
   p->w_scratch_end = off;
   z.workspace_bytes = off;
 

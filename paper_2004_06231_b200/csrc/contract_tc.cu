@@ -1,0 +1,395 @@
+// Warp-specialised tcgen05 contraction kernel shared by the EinsumLayer
+// forward and the two child-responsibility passes (3xTF32).
+//
+// All three are, per einsum row l and 128-sample tile, a GEMM against a
+// stationary chunk of that row's weights followed by a per-sample contraction
+// of the accumulator with one of the layer's normalised child vectors:
+//
+//   forward (engine.py:91-109):  T[b,(kl,i)] = sum_j EB[b,j] W[k,i,j]
+//                                out[b,k]    = log sum_i EA[b,i] T        -> slab offsets
+//   left    (engine.py:312-313): U[b,(il,j)] = sum_k RT[b,k] W[k,i,j]
+//                                left[b,i]   = EA[b,i] sum_j EB[b,j] U    -> left slot
+//   right   (engine.py:314-315): V[b,(jl,i)] = sum_k RT[b,k] W[k,i,j]
+//                                right[b,j]  = EB[b,j] sum_i EA[b,i] V    -> right slot
+//
+// The A operand (EB or RT = rho / r) is written by its producer kernel in the
+// K-major core-matrix layout of a 128-sample tile, split into a truncated TF32
+// part and the fp32 remainder, so it reaches shared memory with one bulk copy.
+// The weight chunk (<= 256 accumulator columns: `og` outputs x K) is a
+// pre-tiled image (einsum_tc.cu, k_build_tiles) and stays resident while the
+// CTA walks its run of (row, chunk, tile) jobs; it is reloaded only when the
+// run crosses into the next (row, chunk).
+//
+// Roles (320 threads): warp 0 = bulk-copy producer, warp 1 = TMEM owner and
+// single-thread MMA issuer, warps 2..9 = epilogue (warp w reads TMEM lanes
+// 32*(w%4)..+31, one sample per thread; the two warps of a lane quarter take
+// alternate outputs). Pipelines: A stages (full/empty), the epilogue's
+// contraction-vector tiles (bulk copies of four [K][32] blocks, full/empty),
+// two TMEM accumulators (full/empty) and the weight chunk (full/empty). The
+// per-output scales (left/right) are loaded from global memory one job ahead.
+// Every job re-reads its A and contraction-vector tiles from L2 (once per
+// weight chunk), which makes the kernel L2-bandwidth bound at K = 40
+// (profiles/r01_s2_profile.md).
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+
+#include "kern_common.cuh"
+#include "tc_common.cuh"
+
+namespace einet {
+
+constexpr int CT_STAGES = 3;
+constexpr int CT_EPI_WARPS = 8;                 // two per TMEM lane quarter
+constexpr int CT_THREADS = 64 + 32 * CT_EPI_WARPS;
+
+struct ContractArgs {
+  const float *a_ops;     // A operand tiles of the layer's first row
+  int64_t a_row_stride;   // floats per row (ntl * 2 * 128 * ka)
+  int ka;                 // MMA K dimension (multiple of 8)
+  const float *e1;        // contraction vector, 32-sample transposed, width K
+  const float *sv;        // per-output scale vector (left/right), width K; null = forward
+  const uint8_t *tiles;   // weight chunk images [row][chunk]
+  int64_t tile_bytes;
+  int nchunk, og, rows_tile, n_out;
+  const int *dst;         // per row: output slab (forward) or slot (left/right)
+  int64_t B, ntl;
+  int L;
+  int stages;             // A-operand ring depth (2 or 3, by shared-memory fit)
+  int direct;             // K_out == 1 child-rho: out[o] = e1[o] * rt * acc[o] (no contraction)
+  int sv_w;               // transposed-block width of sv
+  int debug;              // EINET_CT_DEBUG (timing experiments only): 1 no epilogue math, 2 no MMA
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+template <int K>
+__global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, WsView ws) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar_wf, bar_we, bar_af[CT_STAGES], bar_ae[CT_STAGES], bar_cf[2], bar_ce[2],
+      bar_ef[2], bar_ee[2];
+  __shared__ uint32_t tbase;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int64_t J = (int64_t)a.L * a.nchunk * a.ntl;
+  const int64_t j0 = (int64_t)blockIdx.x * J / gridDim.x;
+  const int64_t j1 = (int64_t)(blockIdx.x + 1) * J / gridDim.x;
+  const int64_t wbytes = (a.tile_bytes + 1023) / 1024 * 1024;
+  const uint32_t abytes = (uint32_t)(2 * 128 * a.ka * 4);
+  const uint32_t ebytes = (uint32_t)(4 * K * EV_ROW * 4);
+  uint8_t *wsm = sm;
+  uint8_t *abuf = sm + wbytes;
+  float *ebuf = (float *)(abuf + (int64_t)a.stages * abytes);  // [2][128 x K] contraction vector
+  if (w == 1) tc::tmem_alloc(&tbase, 512);
+  if (t == 0) {
+    tc::mbar_init(&bar_wf, 1);
+    tc::mbar_init(&bar_we, 1);
+    for (int s = 0; s < CT_STAGES; ++s) {
+      tc::mbar_init(&bar_af[s], 1);
+      tc::mbar_init(&bar_ae[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&bar_cf[s], 1);
+      tc::mbar_init(&bar_ce[s], CT_EPI_WARPS);
+      tc::mbar_init(&bar_ef[s], 1);
+      tc::mbar_init(&bar_ee[s], CT_EPI_WARPS);
+    }
+    tc::mbar_fence_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+
+  if (w == 0) {
+    // ---- producer ----
+    if (lane == 0) {
+      int64_t prev = -1;
+      int q = -1, it = 0;
+      for (int64_t j = j0; j < j1; ++j, ++it) {
+        const int64_t pair = j / a.ntl, jt = j % a.ntl;
+        if (pair != prev) {
+          ++q;
+          if (q > 0) tc::mbar_wait(&bar_we, (q - 1) & 1);
+          tc::mbar_arrive_expect_tx(&bar_wf, (uint32_t)a.tile_bytes);
+          tc::bulk_g2s(wsm, a.tiles + pair * a.tile_bytes, (uint32_t)a.tile_bytes, &bar_wf);
+          prev = pair;
+        }
+        const int s = it % a.stages, ph = (it / a.stages) & 1;
+        tc::mbar_wait(&bar_ae[s], ph ^ 1);
+        const int l = (int)(pair / a.nchunk);
+        tc::mbar_arrive_expect_tx(&bar_af[s], abytes);
+        tc::bulk_g2s(abuf + (int64_t)s * abytes,
+                     a.a_ops + l * a.a_row_stride + jt * (2LL * 128 * a.ka), abytes, &bar_af[s]);
+        // the tile's contraction vector: 4 contiguous [K][32] blocks
+        const int se = it & 1, eph = (it >> 1) & 1;
+        tc::mbar_wait(&bar_ee[se], eph ^ 1);
+        tc::mbar_arrive_expect_tx(&bar_ef[se], ebytes);
+        tc::bulk_g2s(ebuf + se * 4 * K * EV_ROW, a.e1 + ev_idx(l, jt * 128, 0, ws.bc, K), ebytes,
+                     &bar_ef[se]);
+      }
+    }
+  } else if (w == 1) {
+    // ---- MMA issuer: the whole warp runs the loop (uniform registers), one
+    // elected lane issues; descriptors advance by adding to their 14-bit
+    // start-address field (16-byte units) ----
+    const uint64_t a_desc0 = tc::smem_desc(tc::smem_u32(abuf), 128 * 16, 128u);
+    const uint64_t b_desc0 = tc::smem_desc(tc::smem_u32(wsm), (uint32_t)(a.rows_tile * 16), 128u);
+    const uint32_t a_lo_units = 128 * a.ka * 4 / 16, b_lo_units = a.rows_tile * a.ka * 4 / 16;
+    const uint32_t a_ks_units = 2 * 128, b_ks_units = 2 * a.rows_tile;
+    const int nks = (a.debug & 2) ? 0 : a.ka / 8;
+    int64_t pair = j0 / a.ntl, jt = j0 % a.ntl;
+    int q = 0, it = 0;
+    if (j0 < j1) tc::mbar_wait(&bar_wf, 0);
+    for (int64_t j = j0; j < j1; ++j, ++it) {
+      const int c = (int)(pair % a.nchunk);
+      const int nol = min(a.og, a.n_out - c * a.og);
+      const int nmma = a.direct ? (K + 15) / 16 * 16 : (nol * K + 15) / 16 * 16;
+      const int s = it % a.stages, ph = (it / a.stages) & 1;
+      const int buf = it & 1, bph = (it >> 1) & 1;
+      tc::mbar_wait(&bar_af[s], ph);
+      tc::mbar_wait(&bar_ce[buf], bph ^ 1);
+      tc::fence_after();
+      const bool last_of_pair = j + 1 == j1 || jt + 1 == a.ntl;
+      if (tc::elect_one()) {
+        const uint32_t id = tc::idesc_tf32(128, nmma);
+        const uint32_t d = tm + (uint32_t)(buf * 256);
+        uint64_t ah = a_desc0 + (uint64_t)(s * (abytes >> 4));
+        uint64_t al = ah + a_lo_units;
+        uint64_t bh = b_desc0, bl = b_desc0 + b_lo_units;
+        for (int ks = 0; ks < nks; ++ks) {
+          tc::mma_tf32(d, ah, bh, id, ks > 0 ? 1u : 0u);
+          tc::mma_tf32(d, ah, bl, id, 1u);
+          tc::mma_tf32(d, al, bh, id, 1u);
+          ah += a_ks_units;
+          al += a_ks_units;
+          bh += b_ks_units;
+          bl += b_ks_units;
+        }
+        tc::mma_commit(&bar_ae[s]);
+        tc::mma_commit(&bar_cf[buf]);
+        if (last_of_pair) tc::mma_commit(&bar_we);
+      }
+      __syncwarp();
+      if (++jt == a.ntl) {
+        jt = 0;
+        ++pair;
+        if (j + 1 < j1) tc::mbar_wait(&bar_wf, (++q) & 1);
+      }
+    }
+  } else {
+    // ---- epilogue: one sample per thread ----
+    constexpr int OGM = 256 / K;  // outputs per chunk (accumulator columns / K)
+    const int quarter = w & 3, half = (w - 2) >> 2;  // the two warps of a quarter split the outputs
+    const int r = 32 * quarter + lane;
+    const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+    const bool fwd = a.sv == nullptr;
+    // per-output scales of the next job, loaded one job ahead
+    float sv_next[OGM];
+    auto load_next = [&](int64_t j) {
+      if (fwd || j >= j1) return;
+      const int64_t pair = j / a.ntl, jt = j % a.ntl;
+      const int l = (int)(pair / a.nchunk), c = (int)(pair % a.nchunk);
+      const int nol = min(a.og, a.n_out - c * a.og);
+      const int64_t b = min(jt * 128 + r, a.B - 1);
+      if (a.direct) {
+        sv_next[0] = a.sv[tb_idx(l, b, 0, ws.bc, a.sv_w)];
+        return;
+      }
+      const float *svp = a.sv + ev_idx(l, b, c * a.og, ws.bc, K);
+#pragma unroll
+      for (int u = 0; u < OGM; ++u)
+        if (u < nol) sv_next[u] = svp[u * EV_ROW];
+    };
+    load_next(j0);
+    int it = 0;
+    for (int64_t j = j0; j < j1; ++j, ++it) {
+      const int64_t pair = j / a.ntl, jt = j % a.ntl;
+      const int l = (int)(pair / a.nchunk), c = (int)(pair % a.nchunk);
+      const int nol = min(a.og, a.n_out - c * a.og);
+      const int64_t b = jt * 128 + r;
+      const bool live = b < a.B;
+      const int64_t bs = live ? b : 0;
+      float sv[OGM];
+#pragma unroll
+      for (int u = 0; u < OGM; ++u) sv[u] = sv_next[u];
+      load_next(j + 1);
+      const int se = it & 1, eph = (it >> 1) & 1;
+      tc::mbar_wait(&bar_ef[se], eph);
+      float e1[K];
+      {
+        const float *src = ebuf + se * 4 * K * EV_ROW + (r >> 5) * (K * EV_ROW) + lane;
+#pragma unroll
+        for (int i = 0; i < K; ++i) e1[i] = src[i * EV_ROW];
+      }
+      const int buf = it & 1, bph = (it >> 1) & 1;
+      tc::mbar_wait(&bar_cf[buf], bph);
+      tc::fence_after();
+      const uint32_t ta = tm + lane_off + (uint32_t)(buf * 256);
+      float *out = (fwd ? ws.off : ws.slots) + tb_idx(a.dst[l], bs, 0, ws.bc, ws.ks);
+      if (a.direct) {
+        float v[K];
+        int u = 0;
+#pragma unroll
+        for (; u + 16 <= K; u += 16) {
+          float c16[16];
+          tc::tmem_ld16(ta + u, c16);
+#pragma unroll
+          for (int z = 0; z < 16; ++z) v[u + z] = c16[z];
+        }
+#pragma unroll
+        for (; u < K; u += 8) {
+          float c8[8];
+          tc::tmem_ld8(ta + u, c8);
+#pragma unroll
+          for (int z = 0; z < 8; ++z) v[u + z] = c8[z];
+        }
+        tc::tmem_wait_ld();
+        const float rt = sv[0];
+        if (live) {
+#pragma unroll
+          for (int o = 0; o < K; ++o)
+            if ((o & 1) == half) out[o * 32] = e1[o] * (rt * v[o]);
+        }
+      }
+#pragma unroll 1
+      for (int ol = half; ol < ((a.direct || (a.debug & 1)) ? 0 : nol); ol += 2) {
+        float v[K];
+        int u = 0;
+#pragma unroll
+        for (; u + 16 <= K; u += 16) {
+          float c16[16];
+          tc::tmem_ld16(ta + ol * K + u, c16);
+#pragma unroll
+          for (int z = 0; z < 16; ++z) v[u + z] = c16[z];
+        }
+#pragma unroll
+        for (; u < K; u += 8) {
+          float c8[8];
+          tc::tmem_ld8(ta + ol * K + u, c8);
+#pragma unroll
+          for (int z = 0; z < 8; ++z) v[u + z] = c8[z];
+        }
+        tc::tmem_wait_ld();
+        float a4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < K; ++i) a4[i & 3] = fmaf(v[i], e1[i], a4[i & 3]);
+        const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        float scale = 1.f;
+#pragma unroll
+        for (int z = 0; z < OGM; ++z)
+          if (z == ol) scale = sv[z];
+        const int o = c * a.og + ol;
+        if (live) out[o * 32] = fwd ? (acc > 0.f ? logf(acc) : -CUDART_INF_F) : scale * acc;
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bar_ce[buf]);
+        mbar_arrive(&bar_ee[se]);
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (w == 1) tc::tmem_dealloc(tm, 512);
+}
+
+constexpr size_t CT_SMEM_MAX = 220 * 1024;
+
+size_t contract_smem(int64_t tile_bytes, int ka, int stages, int K) {
+  return (size_t)((tile_bytes + 1023) / 1024 * 1024) + (size_t)stages * 2 * 128 * ka * 4 +
+         2 * 4 * (size_t)K * EV_ROW * 4;
+}
+
+template <int K>
+static int contract_t(Plan &p, ContractArgs &a, const WsView &w, cudaStream_t st) {
+  a.stages = CT_STAGES;
+  while (a.stages > 2 && contract_smem(a.tile_bytes, a.ka, a.stages, K) > CT_SMEM_MAX) --a.stages;
+  const size_t smem = contract_smem(a.tile_bytes, a.ka, a.stages, K);
+  if (smem > CT_SMEM_MAX) return fail(EINET_ERR_UNSUPPORTED, "contraction tile exceeds shared memory");
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_contract_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = smem;
+  }
+  const int64_t J = (int64_t)a.L * a.nchunk * a.ntl;
+  const int grid = (int)std::min<int64_t>(J, p.num_sms);
+  k_contract_tc<K><<<grid, CT_THREADS, smem, st>>>(a, w);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "einsum contraction (tcgen05)");
+}
+
+// mode 0: forward, 1: left child responsibilities, 2: right
+int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *compute,
+                       const float *EA, const float *EB, const WsView &w, int64_t B,
+                       cudaStream_t st) {
+  ContractArgs a;
+  const int K = p.k;
+  a.B = B;
+  a.ntl = (B + 127) / 128;
+  a.L = L.rows;
+  a.direct = 0;
+  a.sv_w = K;
+  {
+    const char *env = getenv("EINET_CT_DEBUG");
+    a.debug = env ? atoi(env) : 0;
+  }
+  if (mode != 0 && L.direct) {
+    a.direct = 1;
+    a.a_ops = (mode == 1 ? w.ebm : w.eam) + (int64_t)L.erow_base * w.bc * 2 * K;
+    a.a_row_stride = w.bc * 2 * K;
+    a.ka = K;
+    a.e1 = mode == 1 ? EA : EB;
+    a.sv = w.rt;
+    a.sv_w = w.ks;
+    a.tiles = compute + (mode == 1 ? L.fw_off : L.vw_off);
+    a.tile_bytes = mode == 1 ? L.fw_tile : L.rw_tile;
+    a.nchunk = 1;
+    a.og = K;
+    a.rows_tile = mode == 1 ? L.fw_rows : L.rw_rows;
+    a.n_out = K;
+    a.dst = mode == 1 ? L.d_slot_left : L.d_slot_right;
+  } else if (mode == 0) {
+    a.a_ops = w.ebm + (int64_t)L.erow_base * (w.bc / 128) * 2 * 128 * K;
+    a.a_row_stride = (w.bc / 128) * 2 * 128 * K;
+    a.ka = K;
+    a.e1 = EA;
+    a.sv = nullptr;
+    a.tiles = compute + L.fw_off;
+    a.tile_bytes = L.fw_tile;
+    a.nchunk = L.ng;
+    a.og = L.kg;
+    a.rows_tile = L.fw_rows;
+    a.n_out = L.k_out;
+    a.dst = L.d_out_slab;
+  } else {
+    a.a_ops = w.rtm;
+    a.a_row_stride = (w.bc / 128) * 2 * 128 * L.ko8;
+    a.ka = L.ko8;
+    a.e1 = mode == 1 ? EB : EA;
+    a.sv = mode == 1 ? EA : EB;
+    a.tiles = compute + (mode == 1 ? L.uw_off : L.vw_off);
+    a.tile_bytes = L.uw_tile;
+    a.nchunk = L.ni;
+    a.og = L.ig;
+    a.rows_tile = L.uw_rows;
+    a.n_out = K;
+    a.dst = mode == 1 ? L.d_slot_left : L.d_slot_right;
+  }
+  switch (K) {
+    case 8: return contract_t<8>(p, a, w, st);
+    case 16: return contract_t<16>(p, a, w, st);
+    case 24: return contract_t<24>(p, a, w, st);
+    case 32: return contract_t<32>(p, a, w, st);
+    case 40: return contract_t<40>(p, a, w, st);
+    case 48: return contract_t<48>(p, a, w, st);
+    case 56: return contract_t<56>(p, a, w, st);
+    case 64: return contract_t<64>(p, a, w, st);
+    default: return fail(EINET_ERR_USAGE, "tc path: unsupported k");
+  }
+}
+
+}  // namespace einet

@@ -23,6 +23,7 @@ namespace einet {
 constexpr int kMaxDSplit = 16;     // leaf forward split of a scope across CTAs
 constexpr int kMaxBSplit = 64;     // batch split of statistic reductions
 constexpr int kReduceThreads = 256;
+constexpr int EV_ROW = 36;         // padded row of the EA / EB 32-sample blocks (kern_common.cuh)
 
 struct LayerPlan {
   int kind = 0;        // EINET_LAYER_*
@@ -48,7 +49,12 @@ struct LayerPlan {
   int ko8 = 0;                      // K_out padded to 8 (child-rho MMA K dimension)
   int nn = 0;                       // W-stats MMA N: K_out padded to 16
   int64_t fw_off = 0, fw_tile = 0;  // compute byte offset, bytes per forward tile
-  int64_t uw_off = 0, uw_tile = 0;  // compute byte offset, bytes per child-rho tile
+  int64_t uw_off = 0, uw_tile = 0;  // compute byte offset, bytes per child-rho tile (left)
+  int64_t vw_off = 0;               // right child-rho tiles (rows (jl, i)), uw_tile bytes each
+  // K_out == 1 (root): child responsibilities as one direct GEMM per side,
+  // left = EA * rt * (EB W0^T) (forward tile), right = EB * rt * (EA W0) (rw tile at vw_off)
+  int direct = 0, rw_rows = 0;
+  int64_t rw_tile = 0;
   std::vector<int> h_out_slab;
   std::vector<int> h_src;          // mixing local src
   std::vector<uint8_t> h_mask;
@@ -88,7 +94,7 @@ struct Plan {
   // workspace segments (byte offsets)
   int64_t w_off = 0, w_shift = 0, w_slots = 0, w_leafpart = 0, w_ea = 0, w_eb = 0,
           w_rt = 0, w_wpart = 0, w_rho = 0, w_lspart = 0, w_ppart = 0, w_mixpart = 0,
-          w_llpart = 0, w_tmp_s = 0, w_tmp_p = 0, w_scratch_end = 0;
+          w_llpart = 0, w_tmp_s = 0, w_tmp_p = 0, w_ebm = 0, w_eam = 0, w_rtm = 0, w_rtb = 0, w_scratch_end = 0;
   int64_t max_chunk = 0;
   int64_t bc = 0;                  // per-chunk sample stride (max_chunk rounded to 32)
   int num_sms = 148;
@@ -132,6 +138,8 @@ struct ProfScope {
 };
 
 // ---- launchers (implemented in the .cu files) -------------------------------
+struct CompView;
+struct WsView;
 int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_t *mask,
                    const double *leaf_offset, cudaStream_t st);
 int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
@@ -151,13 +159,18 @@ int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
                        cudaStream_t st);
 int launch_status_reset(int32_t *status, cudaStream_t st);
 void plan_tc_tiling(Plan &p);
-int wstats_tc_bsplit(const Plan &p, const LayerPlan &L, int64_t B, bool upper_bound);
+int64_t wstats_tc_slots(const Plan &p, const LayerPlan &L, int64_t B);
+int launch_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB, WsView &w,
+                     int64_t B, const double *Wl, double *stats, cudaStream_t st);
 int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_prepare_leaf_dmma(Plan &p, uint8_t *compute, cudaStream_t st);
 struct CompView;
 struct WsView;
 int launch_leaf_fwd_dmma(Plan &p, const CompView &c, const float *x, int64_t B, const WsView &w,
                          int32_t *status, cudaStream_t st, int *ds_out);
+int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *compute,
+                       const float *EA, const float *EB, const WsView &w, int64_t B,
+                       cudaStream_t st);
 int launch_selftest_gemm(const float *A, const float *B, float *D, int N, int K,
                          cudaStream_t st);
 int leaf_lsplit(const Plan &p, int64_t B);

@@ -20,13 +20,8 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
                         uint8_t *wsb, int32_t *status, cudaStream_t st);
 int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
                          uint8_t *wsb, double *stats, cudaStream_t st);
-int launch_einsum_fwd_tc(Plan &p, const LayerPlan &L, const uint8_t *compute, const float *EA,
-                         const float *EB, WsView &w, int64_t B, cudaStream_t st);
 int launch_einsum_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB,
                             WsView &w, int64_t B, int *bsplit, cudaStream_t st);
-int launch_einsum_childrho_tc(Plan &p, const LayerPlan &L, const uint8_t *compute,
-                              const float *EA, const float *EB, WsView &w, int64_t B,
-                              cudaStream_t st);
 
 constexpr int EF_TB = 128;  // samples per CTA, one per thread
 constexpr int EF_KC = 8;    // output entries (k) staged per W chunk
@@ -41,7 +36,8 @@ constexpr int EF_KC = 8;    // output entries (k) staged per W chunk
 __global__ void __launch_bounds__(128) k_einsum_prep_fwd(
     WsView ws, const int *__restrict__ left_slab, const int *__restrict__ right_slab,
     const int *__restrict__ out_slab, int64_t B, int K, float *__restrict__ EA,
-    float *__restrict__ EB, int layer_index, int32_t *status) {
+    float *__restrict__ EB, float *__restrict__ EBM, float *__restrict__ EAM, int layer_index,
+    int32_t *status) {
   __shared__ float mx[2][32];
   __shared__ unsigned char dead[32];
   const int l = blockIdx.y, t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -90,12 +86,33 @@ __global__ void __launch_bounds__(128) k_einsum_prep_fwd(
   __syncthreads();
   const float *ol = ws.off + tb_idx(ls, b0, 0, ws.bc, ws.ks);
   const float *orr = ws.off + tb_idx(rs, b0, 0, ws.bc, ws.ks);
-  float *ea = EA + tb_idx(l, b0, 0, ws.bc, K), *eb = EB + tb_idx(l, b0, 0, ws.bc, K);
-  for (int e = t; e < K * 32; e += 128) {
-    const int bl = e & 31;
+  float *ea = EA + ev_idx(l, b0, 0, ws.bc, K), *eb = EB + ev_idx(l, b0, 0, ws.bc, K);
+  if (EBM == nullptr) {
+    for (int e = t; e < K * 32; e += 128) {
+      const int bl = e & 31, x = (e >> 5) * EV_ROW + bl;
+      const bool d = dead[bl];
+      ea[x] = d ? 0.f : expf(ol[e] - mx[0][bl]);
+      eb[x] = d ? 0.f : expf(orr[e] - mx[1][bl]);
+    }
+    return;
+  }
+  // tensor-core path (K % 8 == 0): also the EB A-operand tile (hi | lo)
+  const int64_t ntl = ws.bc / 128;
+  for (int e = t; e < (K / 4) * 32; e += 128) {
+    const int bl = e & 31, q = e >> 5;
     const bool d = dead[bl];
-    ea[e] = d ? 0.f : expf(ol[e] - mx[0][bl]);
-    eb[e] = d ? 0.f : expf(orr[e] - mx[1][bl]);
+    float va[4], vb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int x = (4 * q + u) * 32 + bl, xe = (4 * q + u) * EV_ROW + bl;
+      va[u] = d ? 0.f : expf(ol[x] - mx[0][bl]);
+      vb[u] = d ? 0.f : expf(orr[x] - mx[1][bl]);
+      ea[xe] = va[u];
+      eb[xe] = vb[u];
+    }
+    store_hilo4(EBM + mt_idx(l, b0 + bl, q, ntl, K), K, make_float4(vb[0], vb[1], vb[2], vb[3]));
+    if (EAM)
+      store_hilo4(EAM + mt_idx(l, b0 + bl, q, ntl, K), K, make_float4(va[0], va[1], va[2], va[3]));
   }
 }
 
@@ -145,8 +162,8 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const float *__
   float ea[KT], eb[KT];
 #pragma unroll
   for (int i = 0; i < KT; ++i) {
-    ea[i] = (live && i < K) ? EA[tb_idx(l, bb, i, ws.bc, K)] : 0.f;
-    eb[i] = (live && i < K) ? EB[tb_idx(l, bb, i, ws.bc, K)] : 0.f;
+    ea[i] = (live && i < K) ? EA[ev_idx(l, bb, i, ws.bc, K)] : 0.f;
+    eb[i] = (live && i < K) ? EB[ev_idx(l, bb, i, ws.bc, K)] : 0.f;
   }
   __syncthreads();
   if (!live) return;
@@ -175,8 +192,8 @@ __global__ void k_einsum_fwd_generic(WsView ws, const float *__restrict__ EA,
     for (int i = 0; i < K; ++i) {
       float t = 0.f;
       for (int j = 0; j < K; ++j)
-        t = fmaf(Wl[((int64_t)k * K + i) * K + j], EB[tb_idx(l, b, j, ws.bc, K)], t);
-      acc = fmaf(EA[tb_idx(l, b, i, ws.bc, K)], t, acc);
+        t = fmaf(Wl[((int64_t)k * K + i) * K + j], EB[ev_idx(l, b, j, ws.bc, K)], t);
+      acc = fmaf(EA[ev_idx(l, b, i, ws.bc, K)], t, acc);
     }
     o[k] = acc > 0.f ? logf(acc) : -CUDART_INF_F;
   }
@@ -314,12 +331,27 @@ __global__ void __launch_bounds__(128) k_mixing_bwd(
 // einsum backward
 // ---------------------------------------------------------------------------
 
+// The block's RT^T as the W-statistics B operand (rows k < nn, 32 samples;
+// hi | lo, K-major core matrices), read back from the block's RT tile after
+// the CTA wrote it. Rows k >= Ko are zero.
+__device__ __forceinline__ void rtb_tile(const float *rt, float *RTB, int l, int64_t b0, int Ko,
+                                         int nn, int64_t bc) {
+  __syncthreads();
+  float *dst = RTB + ((int64_t)l * (bc / 32) + b0 / 32) * (2 * nn * 32);
+  for (int e = threadIdx.x; e < nn * 8; e += blockDim.x) {
+    const int n = e >> 3, q = e & 7;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n < Ko) v = *(const float4 *)(rt + n * 32 + 4 * q);
+    store_hilo4_at(dst + q * (nn * 4) + (n >> 3) * 32 + (n & 7) * 4, nn * 32, v);
+  }
+}
+
 // RT = rho / r per row and sample (engine.py:310-311), r = exp(log r) from the
 // forward offsets; elementwise over a 32-sample block (contiguous tiles).
 // grid (ceil(B/32), L), block 128
 __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
     WsView ws, const int *out_slab, const int *csr_off, const int *__restrict__ csr_slot,
-    const uint8_t *ones, int64_t B, int Ko, float *RT) {
+    const uint8_t *ones, int64_t B, int Ko, float *RT, float *RTM, int ko8, float *RTB, int nn) {
   const int l = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int os = out_slab[l];
@@ -327,13 +359,42 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
   const bool one = ones[os] != 0;
   const float *oo = ws.off + tb_idx(os, b0, 0, ws.bc, ws.ks);
   float *rt = RT + tb_idx(l, b0, 0, ws.bc, ws.ks);
-  for (int e = threadIdx.x; e < Ko * 32; e += 128) {
-    const int64_t b = b0 + (e & 31);
-    if (b >= B) continue;
-    const float r = slab_shift(ws, os)[b] == -CUDART_INF ? 0.f : expf(oo[e]);
-    const float rho = gather_rho_tile(ws, q0, q1, csr_slot, one, b0, e);
-    rt[e] = r > 0.f ? rho / r : 0.f;
+  if (RTM == nullptr) {
+    for (int e = threadIdx.x; e < Ko * 32; e += 128) {
+      const int64_t b = b0 + (e & 31);
+      float v = 0.f;
+      if (b < B) {
+        const float r = slab_shift(ws, os)[b] == -CUDART_INF ? 0.f : expf(oo[e]);
+        const float rho = gather_rho_tile(ws, q0, q1, csr_slot, one, b0, e);
+        v = r > 0.f ? rho / r : 0.f;
+      }
+      rt[e] = v;  // samples past the batch hold 0 (the W statistics sum whole blocks)
+    }
+    if (RTB) rtb_tile(rt, RTB, l, b0, Ko, nn, ws.bc);
+    return;
   }
+  // tensor-core path: also the RT A-operand tile (width ko8, zero padded)
+  const int64_t ntl = ws.bc / 128;
+  for (int e = threadIdx.x; e < (ko8 / 4) * 32; e += 128) {
+    const int bl = e & 31, q = e >> 5;
+    const int64_t b = b0 + bl;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    const bool live = b < B && slab_shift(ws, os)[b] != -CUDART_INF;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = 4 * q + u;
+      if (k >= Ko) continue;
+      const int x = k * 32 + bl;
+      if (b < B) {
+        const float r = live ? expf(oo[x]) : 0.f;
+        const float rho = gather_rho_tile(ws, q0, q1, csr_slot, one, b0, x);
+        v[u] = r > 0.f ? rho / r : 0.f;
+      }
+      rt[x] = v[u];
+    }
+    store_hilo4(RTM + mt_idx(l, b, q, ntl, ko8), ko8, make_float4(v[0], v[1], v[2], v[3]));
+  }
+  if (RTB) rtb_tile(rt, RTB, l, b0, Ko, nn, ws.bc);
 }
 
 constexpr int WS_BT = 32;  // samples per fp32 run of the W statistics
@@ -370,8 +431,8 @@ __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__res
     for (int e = threadIdx.x; e < WS_BT * KP; e += blockDim.x) {
       const int bl = e / KP, i = e % KP;
       const bool ok = bl < nb && i < K;
-      ea_s[e] = ok ? EA[tb_idx(l, t + bl, i, Bc, K)] : 0.f;
-      eb_s[e] = ok ? EB[tb_idx(l, t + bl, i, Bc, K)] : 0.f;
+      ea_s[e] = ok ? EA[ev_idx(l, t + bl, i, Bc, K)] : 0.f;
+      eb_s[e] = ok ? EB[ev_idx(l, t + bl, i, Bc, K)] : 0.f;
     }
     for (int e = threadIdx.x; e < WS_BT; e += blockDim.x)
       rt_s[e] = e < nb ? RT[tb_idx(l, t + e, k, Bc, ks)] : 0.f;
@@ -419,8 +480,8 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_childrho(
   float ea[KT], eb[KT], left[KT], right[KT];
 #pragma unroll
   for (int i = 0; i < KT; ++i) {
-    ea[i] = (live && i < K) ? EA[tb_idx(l, bb, i, ws.bc, K)] : 0.f;
-    eb[i] = (live && i < K) ? EB[tb_idx(l, bb, i, ws.bc, K)] : 0.f;
+    ea[i] = (live && i < K) ? EA[ev_idx(l, bb, i, ws.bc, K)] : 0.f;
+    eb[i] = (live && i < K) ? EB[ev_idx(l, bb, i, ws.bc, K)] : 0.f;
     left[i] = 0.f;
     right[i] = 0.f;
   }
@@ -472,8 +533,8 @@ __global__ void k_einsum_childrho_generic(const float *__restrict__ EA,
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  auto ea = [&](int i) { return EA[tb_idx(l, b, i, ws.bc, K)]; };
-  auto eb = [&](int i) { return EB[tb_idx(l, b, i, ws.bc, K)]; };
+  auto ea = [&](int i) { return EA[ev_idx(l, b, i, ws.bc, K)]; };
+  auto eb = [&](int i) { return EB[ev_idx(l, b, i, ws.bc, K)]; };
   auto rt = [&](int k) { return RT[tb_idx(l, b, k, ws.bc, ws.ks)]; };
   const float *Wl = W + (int64_t)l * Ko * K * K;
   const Col32 dl = slot_ptr(ws, slot_left[l], b), dr = slot_ptr(ws, slot_right[l], b);
@@ -604,10 +665,10 @@ static void einsum_childrho_simt(const LayerPlan &L, const float *w32, const flo
 }
 
 static inline const float *layer_ea(const Plan &p, const WsView &w, const LayerPlan &L) {
-  return w.ea + (int64_t)L.erow_base * w.bc * p.k;
+  return w.ea + (int64_t)L.erow_base * (w.bc / 32) * p.k * EV_ROW;
 }
 static inline const float *layer_eb(const Plan &p, const WsView &w, const LayerPlan &L) {
-  return w.eb + (int64_t)L.erow_base * w.bc * p.k;
+  return w.eb + (int64_t)L.erow_base * (w.bc / 32) * p.k * EV_ROW;
 }
 
 int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, uint8_t *wsb,
@@ -622,12 +683,15 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
       {
         ProfScope prof("einsum_prep", st);
         dim3 grid(ceil_div(B, 32), L.rows);
+        const bool tcl = p.use_tc && L.tc;
+        float *EBM = tcl ? w.ebm + (int64_t)L.erow_base * w.bc * 2 * p.k : nullptr;
+        float *EAM = tcl && L.direct ? w.eam + (int64_t)L.erow_base * w.bc * 2 * p.k : nullptr;
         k_einsum_prep_fwd<<<grid, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
-                                                B, p.k, EA, EB, L.index, status);
+                                                B, p.k, EA, EB, EBM, EAM, L.index, status);
       }
       ProfScope prof("einsum_fwd", st);
       if (p.use_tc && L.tc)
-        rc = launch_einsum_fwd_tc(p, L, compute, EA, EB, w, B, st);
+        rc = launch_contract_tc(p, L, 0, compute, EA, EB, w, B, st);
       else
         einsum_forward_simt(L, c.w32, EA, EB, w, B, p.k, st);
       if (rc) return rc;
@@ -687,30 +751,33 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
     {
       ProfScope prof("einsum_bwd_rt", st);
       dim3 g1(ceil_div(B, 32), L.rows);
+      const bool tcl = p.use_tc && L.tc;
       k_einsum_bwd_rt<<<g1, 128, 0, st>>>(w, L.d_out_slab, p.d_csr_off, p.d_csr_slot,
-                                          p.d_slab_ones, B, L.k_out, w.rt);
+                                          p.d_slab_ones, B, L.k_out, w.rt,
+                                          tcl && !L.direct ? w.rtm : nullptr, L.ko8,
+                                          tcl ? w.rtb : nullptr, L.nn);
     }
     const int64_t lw = (int64_t)L.rows * L.k_out * K * K;
     {
       ProfScope prof("einsum_wstats", st);
-      int bs;
       if (p.use_tc && L.tc) {
-        int rc = launch_einsum_wstats_tc(p, L, EA, EB, w, B, &bs, st);
+        int rc = launch_wstats_tc(p, L, EA, EB, w, B, params + L.w_off, stats + L.w_off, st);
         if (rc) return rc;
       } else {
-        bs = wstats_bsplit(p, L, B);
+        const int bs = wstats_bsplit(p, L, B);
         const int K4 = (K + 3) / 4;
         const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT);
         dim3 g2(L.rows * L.k_out, bs);
         k_einsum_wstats<<<g2, K4 * K4, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K, L.k_out,
                                                    L.rows, bs, w.wpart);
+        launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);
       }
-      launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);
     }
     {
       ProfScope prof("einsum_childrho", st);
       if (p.use_tc && L.tc) {
-        int rc = launch_einsum_childrho_tc(p, L, compute, EA, EB, w, B, st);
+        int rc = launch_contract_tc(p, L, 1, compute, EA, EB, w, B, st);
+        if (!rc) rc = launch_contract_tc(p, L, 2, compute, EA, EB, w, B, st);
         if (rc) return rc;
       } else {
         einsum_childrho_simt(L, c.w32, EA, EB, w, B, K, st);

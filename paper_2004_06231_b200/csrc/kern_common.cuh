@@ -30,7 +30,11 @@ struct WsView {
   float *slots;    // [slot][Bc/32][KS][32]
   double *leafpart;
   float *ea, *eb;  // [row][Bc][K]
-  float *rt;       // [row][Bc][KS]
+  float *rt;       // [row][Bc/32][KS][32]
+  float *ebm;      // tcgen05 A operand EB: [einsum row][Bc/128][hi|lo][128 x K] (K-major core matrices)
+  float *rtb;      // tcgen05 B operand RT^T of the W statistics: [row][Bc/32][hi|lo][nn x 32]
+  float *eam;      // tcgen05 A operand EA (direct child-rho of K_out == 1 rows), as ebm
+  float *rtm;      // tcgen05 A operand RT: [row][Bc/128][hi|lo][128 x ko8]
   double *wpart;
   float *rho;      // [leaf][Bc][K]
   double *lspart;
@@ -66,6 +70,10 @@ inline WsView ws_view(const Plan &p, const uint8_t *w) {
   v.ea = (float *)(b + p.w_ea);
   v.eb = (float *)(b + p.w_eb);
   v.rt = (float *)(b + p.w_rt);
+  v.ebm = (float *)(b + p.w_ebm);
+  v.rtm = (float *)(b + p.w_rtm);
+  v.eam = (float *)(b + p.w_eam);
+  v.rtb = (float *)(b + p.w_rtb);
   v.wpart = (double *)(b + p.w_wpart);
   v.rho = (float *)(b + p.w_rho);
   v.lspart = (double *)(b + p.w_lspart);
@@ -84,6 +92,14 @@ inline WsView ws_view(const Plan &p, const uint8_t *w) {
 // with 16-byte copies) and per-sample loops read coalesced across a warp.
 __device__ __forceinline__ int64_t tb_idx(int64_t l, int64_t b, int i, int64_t bc, int W) {
   return (l * bc + (b & ~31LL)) * W + (int64_t)i * 32 + (b & 31);
+}
+
+// The normalised child exponentials EA / EB use the same 32-sample blocks with
+// each entry row padded to EV_ROW floats: a block [K][EV_ROW] is contiguous, so
+// one bulk copy lands it in shared memory where 32 threads reading one 16-byte
+// chunk of 32 consecutive rows hit 8 distinct bank groups.
+__device__ __host__ __forceinline__ int64_t ev_idx(int64_t l, int64_t b, int i, int64_t bc, int K) {
+  return (l * (bc >> 5) + (b >> 5)) * ((int64_t)K * EV_ROW) + (int64_t)i * EV_ROW + (b & 31);
 }
 
 // One sample's entries of a slab or slot: entry k of sample b lives at
@@ -116,6 +132,42 @@ __device__ __forceinline__ float gather_rho(const WsView &w, const int *csr_off,
 }
 
 __device__ __forceinline__ bool is_nan_f(float v) { return v != v; }
+
+// tcgen05 A-operand tiles of per-sample vectors (width W, multiple of 4):
+// 128-sample tile t holds the truncated-TF32 part then the fp32 remainder,
+// each 128 x W in the K-major no-swizzle core-matrix layout (8 samples x 4
+// entries = 128 contiguous bytes). Float index of (sample b, entries 4q..4q+3)
+// in the hi part; the lo part is + 128 * W.
+__device__ __forceinline__ int64_t mt_idx(int64_t row, int64_t b, int q, int64_t ntl, int W) {
+  const int r = (int)(b & 127);
+  return ((row * ntl + (b >> 7)) * 2) * (128LL * W) + q * 512 + (r >> 3) * 32 + (r & 7) * 4;
+}
+__device__ __forceinline__ void store_hilo4_at(float *hi, int64_t lo_off, float4 v) {
+  float4 h, l;
+  h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+  h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+  h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+  h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  l.x = v.x - h.x;
+  l.y = v.y - h.y;
+  l.z = v.z - h.z;
+  l.w = v.w - h.w;
+  *(float4 *)hi = h;
+  *(float4 *)(hi + lo_off) = l;
+}
+__device__ __forceinline__ void store_hilo4(float *hi, int W, float4 v) {
+  float4 h, l;
+  h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+  h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+  h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+  h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  l.x = v.x - h.x;
+  l.y = v.y - h.y;
+  l.z = v.z - h.z;
+  l.w = v.w - h.w;
+  *(float4 *)hi = h;
+  *(float4 *)(hi + 128 * W) = l;
+}
 
 // cp.async (LDGSTS) helpers shared by the staged kernels
 __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {

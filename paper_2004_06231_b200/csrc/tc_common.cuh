@@ -174,6 +174,19 @@ __device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gsrc, uint3
       : "memory");
 }
 
+// One lane of a converged warp (elect.sync): the whole warp runs an issue loop
+// with warp-uniform values (kept in uniform registers by the compiler) and the
+// elected lane issues the tcgen05 instruction.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // fp32 -> (hi, lo) with hi = tf32(x) (round to nearest) and lo = x - hi.
 __device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
   uint32_t h;

@@ -8,10 +8,11 @@ WHAT=${*:-tests bench launches full}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/gpu.txt 2>&1
+make -q -C paper_2004_06231_b200/csrc > /dev/null 2>&1 || echo "WARNING: libeinet_b200.so older than its sources" >> $OUT/status.txt
 for w in $WHAT; do
 case $w in
 tests)
-  timeout 900 python -m pytest tests -m gpu -x -q > $OUT/tests.log 2>&1; echo "tests rc=$?" >> $OUT/status.txt ;;
+  timeout ${TEST_TIMEOUT:-400} python -m pytest tests -m gpu -x -q > $OUT/tests.log 2>&1; echo "tests rc=$?" >> $OUT/status.txt ;;
 bench)
   timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/status.txt ;;
 ref)
