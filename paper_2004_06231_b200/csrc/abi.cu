@@ -106,6 +106,10 @@ static void free_plan_memory(Plan *p) {
   f(p->d_leaf_rep);
   f(p->d_leaf_slab);
   f(p->d_leaf_of);
+  f(p->d_lseg_leaf);
+  f(p->d_lseg_v0);
+  f(p->d_lseg_vec);
+  f(p->d_phi_seg);
   f(p->d_leaf_pvo);
   f(p->d_csr_off);
   f(p->d_csr_slot);
@@ -186,6 +190,28 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
       leaf_of[(size_t)r * D + v] = l;
     }
   }
+
+  // ---- leaf-statistics segments (128 scope positions; leaf_tc.cu) ------------
+  std::vector<int> lseg_leaf, lseg_v0, phi_seg((size_t)R * D, -1);
+  std::vector<uint8_t> lseg_vec;
+  for (int l = 0; l < d->n_leaf; ++l) {
+    const int sb = p->h_scope_off[l], slen = p->h_scope_off[l + 1] - sb;
+    for (int v0 = 0; v0 < slen; v0 += 128) {
+      const int nv = std::min(128, slen - v0);
+      bool vec = nv % 4 == 0;
+      for (int g = 0; vec && g < nv; g += 4) {
+        const int d0 = p->h_scope_vars[sb + v0 + g];
+        vec = d0 % 4 == 0;
+        for (int u = 1; vec && u < 4; ++u) vec = p->h_scope_vars[sb + v0 + g + u] == d0 + u;
+      }
+      for (int q = 0; q < nv; ++q)
+        phi_seg[(size_t)p->h_leaf_rep[l] * D + p->h_scope_vars[sb + v0 + q]] = (int)lseg_leaf.size();
+      lseg_leaf.push_back(l);
+      lseg_v0.push_back(v0);
+      lseg_vec.push_back(vec ? 1 : 0);
+    }
+  }
+  p->n_lseg = (int)lseg_leaf.size();
 
   // ---- layers, slabs -------------------------------------------------------
   int next_slab = p->nbr;
@@ -377,7 +403,8 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   p->w_wpart = seg(8 * std::max<int64_t>(wpart, 1));
   p->w_rho = seg(4 * (int64_t)p->n_leaf * Bc * K);
   p->max_lsplit = leaf_lsplit(*p, Bc);
-  p->w_lspart = seg(8 * (int64_t)p->max_lsplit * p->n_phi);
+  p->w_lspart = seg(std::max(8 * (int64_t)p->max_lsplit * p->n_phi,
+                             4 * leaf_stats_slots(*p, Bc) * p->n_phi));
   p->w_ppart = seg(8 * (int64_t)ceil_div(Bc, 32) * p->n_leaf * K);
   p->w_mixpart = seg(8 * (int64_t)ceil_div(Bc, 32) * std::max<int64_t>(p->n_mix, 1));
   p->w_llpart = seg(8 * (int64_t)ceil_div(Bc, 256));
@@ -398,6 +425,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     for (auto &L : p->layers)
       if (L.tc) nnmax = std::max(nnmax, L.nn);
     p->w_rtb = seg(any_tc ? 8 * p->max_rows * Bc * nnmax : 0);
+    p->w_rhob = seg(8 * (int64_t)p->n_leaf * Bc * ((K + 15) / 16 * 16));
   }
   p->w_scratch_end = off;
   z.workspace_bytes = off;
@@ -409,6 +437,10 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   if ((rc = upload(&p->d_leaf_rep, p->h_leaf_rep))) return rc;
   if ((rc = upload(&p->d_leaf_slab, p->h_leaf_slab))) return rc;
   if ((rc = upload(&p->d_leaf_of, leaf_of))) return rc;
+  if ((rc = upload(&p->d_lseg_leaf, lseg_leaf))) return rc;
+  if ((rc = upload(&p->d_lseg_v0, lseg_v0))) return rc;
+  if ((rc = upload(&p->d_lseg_vec, lseg_vec))) return rc;
+  if ((rc = upload(&p->d_phi_seg, phi_seg))) return rc;
   if (p->leaf_dmma && (rc = upload(&p->d_leaf_pvo, p->h_leaf_pvo))) return rc;
   if ((rc = upload(&p->d_csr_off, p->h_csr_off))) return rc;
   if ((rc = upload(&p->d_csr_slot, p->h_csr_slot))) return rc;

@@ -71,6 +71,10 @@ struct Plan {
   int *d_scope_off = nullptr, *d_scope_vars = nullptr, *d_leaf_rep = nullptr,
       *d_leaf_slab = nullptr;
   int *d_leaf_of = nullptr;        // (R, D): leaf index covering (d, r) or -1
+  // leaf-statistics segments (leaf_tc.cu): 128 scope positions each
+  int n_lseg = 0;
+  int *d_lseg_leaf = nullptr, *d_lseg_v0 = nullptr, *d_phi_seg = nullptr;
+  uint8_t *d_lseg_vec = nullptr;
   std::vector<LayerPlan> layers;   // einsum / mixing layers in circuit order
   int root_mix_row = -1;
   // slabs & slots
@@ -94,7 +98,7 @@ struct Plan {
   // workspace segments (byte offsets)
   int64_t w_off = 0, w_shift = 0, w_slots = 0, w_leafpart = 0, w_ea = 0, w_eb = 0,
           w_rt = 0, w_wpart = 0, w_rho = 0, w_lspart = 0, w_ppart = 0, w_mixpart = 0,
-          w_llpart = 0, w_tmp_s = 0, w_tmp_p = 0, w_ebm = 0, w_eam = 0, w_rtm = 0, w_rtb = 0, w_scratch_end = 0;
+          w_llpart = 0, w_tmp_s = 0, w_tmp_p = 0, w_ebm = 0, w_eam = 0, w_rtm = 0, w_rtb = 0, w_rhob = 0, w_scratch_end = 0;
   int64_t max_chunk = 0;
   int64_t bc = 0;                  // per-chunk sample stride (max_chunk rounded to 32)
   int num_sms = 148;
@@ -184,6 +188,7 @@ void launch_reduce_partials(double *dst, const double *part, int nparts, int64_t
 void launch_reduce_partials_store(double *dst, const double *part, int nparts, int64_t n,
                                   int64_t stride, cudaStream_t st);
 bool leaf_tc_supported(const Plan &p);
+int64_t leaf_stats_slots(const Plan &p, int64_t B);
 int launch_leaf_stats_tc(Plan &p, const uint8_t *compute, const float *x, int64_t B,
                          uint8_t *wsb, double *stats, const double *Pcall, cudaStream_t st);
 

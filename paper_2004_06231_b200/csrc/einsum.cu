@@ -331,21 +331,6 @@ __global__ void __launch_bounds__(128) k_mixing_bwd(
 // einsum backward
 // ---------------------------------------------------------------------------
 
-// The block's RT^T as the W-statistics B operand (rows k < nn, 32 samples;
-// hi | lo, K-major core matrices), read back from the block's RT tile after
-// the CTA wrote it. Rows k >= Ko are zero.
-__device__ __forceinline__ void rtb_tile(const float *rt, float *RTB, int l, int64_t b0, int Ko,
-                                         int nn, int64_t bc) {
-  __syncthreads();
-  float *dst = RTB + ((int64_t)l * (bc / 32) + b0 / 32) * (2 * nn * 32);
-  for (int e = threadIdx.x; e < nn * 8; e += blockDim.x) {
-    const int n = e >> 3, q = e & 7;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (n < Ko) v = *(const float4 *)(rt + n * 32 + 4 * q);
-    store_hilo4_at(dst + q * (nn * 4) + (n >> 3) * 32 + (n & 7) * 4, nn * 32, v);
-  }
-}
-
 // RT = rho / r per row and sample (engine.py:310-311), r = exp(log r) from the
 // forward offsets; elementwise over a 32-sample block (contiguous tiles).
 // grid (ceil(B/32), L), block 128
@@ -370,7 +355,10 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
       }
       rt[e] = v;  // samples past the batch hold 0 (the W statistics sum whole blocks)
     }
-    if (RTB) rtb_tile(rt, RTB, l, b0, Ko, nn, ws.bc);
+    if (RTB) {
+      __syncthreads();
+      bt_tile(rt, RTB + ((int64_t)l * (ws.bc / 32) + b0 / 32) * (2 * nn * 32), Ko, nn);
+    }
     return;
   }
   // tensor-core path: also the RT A-operand tile (width ko8, zero padded)
@@ -394,7 +382,10 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
     }
     store_hilo4(RTM + mt_idx(l, b, q, ntl, ko8), ko8, make_float4(v[0], v[1], v[2], v[3]));
   }
-  if (RTB) rtb_tile(rt, RTB, l, b0, Ko, nn, ws.bc);
+  if (RTB) {
+    __syncthreads();
+    bt_tile(rt, RTB + ((int64_t)l * (ws.bc / 32) + b0 / 32) * (2 * nn * 32), Ko, nn);
+  }
 }
 
 constexpr int WS_BT = 32;  // samples per fp32 run of the W statistics

@@ -32,6 +32,7 @@ struct WsView {
   float *ea, *eb;  // [row][Bc][K]
   float *rt;       // [row][Bc/32][KS][32]
   float *ebm;      // tcgen05 A operand EB: [einsum row][Bc/128][hi|lo][128 x K] (K-major core matrices)
+  float *rhob;     // tcgen05 B operand rho^T of the leaf statistics: [leaf][Bc/32][hi|lo][nn x 32]
   float *rtb;      // tcgen05 B operand RT^T of the W statistics: [row][Bc/32][hi|lo][nn x 32]
   float *eam;      // tcgen05 A operand EA (direct child-rho of K_out == 1 rows), as ebm
   float *rtm;      // tcgen05 A operand RT: [row][Bc/128][hi|lo][128 x ko8]
@@ -74,6 +75,7 @@ inline WsView ws_view(const Plan &p, const uint8_t *w) {
   v.rtm = (float *)(b + p.w_rtm);
   v.eam = (float *)(b + p.w_eam);
   v.rtb = (float *)(b + p.w_rtb);
+  v.rhob = (float *)(b + p.w_rhob);
   v.wpart = (double *)(b + p.w_wpart);
   v.rho = (float *)(b + p.w_rho);
   v.lspart = (double *)(b + p.w_lspart);
@@ -142,12 +144,23 @@ __device__ __forceinline__ int64_t mt_idx(int64_t row, int64_t b, int q, int64_t
   const int r = (int)(b & 127);
   return ((row * ntl + (b >> 7)) * 2) * (128LL * W) + q * 512 + (r >> 3) * 32 + (r & 7) * 4;
 }
+// hi = tf32(x) rounded to nearest (cvt.rna), lo = x - hi (exact in fp32; the
+// tensor core truncates it to TF32). Round-to-nearest keeps the sign of lo
+// random, so the truncation errors of the lo products do not accumulate with
+// one sign over long batch reductions (a truncated hi would make every lo
+// positive: a 2^-20 relative bias that the leaf statistics' un-centring
+// exposes as an absolute error, profiles/r01_s2_profile.md).
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  return __uint_as_float(h);
+}
 __device__ __forceinline__ void store_hilo4_at(float *hi, int64_t lo_off, float4 v) {
   float4 h, l;
-  h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-  h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-  h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-  h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  h.x = tf32_rn(v.x);
+  h.y = tf32_rn(v.y);
+  h.z = tf32_rn(v.z);
+  h.w = tf32_rn(v.w);
   l.x = v.x - h.x;
   l.y = v.y - h.y;
   l.z = v.z - h.z;
@@ -156,17 +169,19 @@ __device__ __forceinline__ void store_hilo4_at(float *hi, int64_t lo_off, float4
   *(float4 *)(hi + lo_off) = l;
 }
 __device__ __forceinline__ void store_hilo4(float *hi, int W, float4 v) {
-  float4 h, l;
-  h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-  h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-  h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-  h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-  l.x = v.x - h.x;
-  l.y = v.y - h.y;
-  l.z = v.z - h.z;
-  l.w = v.w - h.w;
-  *(float4 *)hi = h;
-  *(float4 *)(hi + 128 * W) = l;
+  store_hilo4_at(hi, 128LL * W, v);
+}
+
+// A 32-sample block [n][32] (rows n < nvalid, written by this CTA before a
+// __syncthreads) as a tcgen05 B operand: rows n < nn, K = 32 samples, hi | lo,
+// K-major core matrices. Rows n >= nvalid are zero.
+__device__ __forceinline__ void bt_tile(const float *src, float *dst, int nvalid, int nn) {
+  for (int e = threadIdx.x; e < nn * 8; e += blockDim.x) {
+    const int n = e >> 3, q = e & 7;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n < nvalid) v = *(const float4 *)(src + n * 32 + 4 * q);
+    store_hilo4_at(dst + q * (nn * 4) + (n >> 3) * 32 + (n & 7) * 4, nn * 32, v);
+  }
 }
 
 // cp.async (LDGSTS) helpers shared by the staged kernels

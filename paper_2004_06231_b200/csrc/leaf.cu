@@ -467,7 +467,8 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
 __global__ void __launch_bounds__(128) k_leaf_rho(WsView ws, const int *csr_off,
                                                   const int *__restrict__ csr_slot,
                                                   const uint8_t *ones, const int *leaf_slab,
-                                                  int64_t B, int K, int n_leaf, double *ppart) {
+                                                  int64_t B, int K, int n_leaf, double *ppart,
+                                                  int nn) {
   const int leaf = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int slab = leaf_slab[leaf];
@@ -482,11 +483,15 @@ __global__ void __launch_bounds__(128) k_leaf_rho(WsView ws, const int *csr_off,
       } else {
         for (int q = q0; q < q1; ++q) v += ws.slots[tb_idx(csr_slot[q], b0, 0, ws.bc, ws.ks) + e];
       }
-      rho[e] = v;
     }
+    rho[e] = v;  // samples past the batch hold 0 (the statistics sum whole blocks)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if ((e & 31) == 0) ppart[((int64_t)blockIdx.x * n_leaf + leaf) * K + (e >> 5)] = (double)v;
+  }
+  if (nn > 0) {  // tensor-core leaf statistics: the block's rho^T B operand
+    __syncthreads();
+    bt_tile(rho, ws.rhob + ((int64_t)leaf * (ws.bc / 32) + b0 / 32) * (2 * nn * 32), K, nn);
   }
 }
 
@@ -669,7 +674,8 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
   {
   ProfScope prof("leaf_rho", st);
   k_leaf_rho<<<dim3(nb, p.n_leaf), 128, 0, st>>>(w, p.d_csr_off, p.d_csr_slot, p.d_slab_ones,
-                                                 p.d_leaf_slab, B, K, p.n_leaf, w.ppart);
+                                                 p.d_leaf_slab, B, K, p.n_leaf, w.ppart,
+                                                 leaf_tc_supported(p) ? (K + 15) / 16 * 16 : 0);
   launch_reduce_partials_store(Pcall, w.ppart, nb, (int64_t)p.n_leaf * K,
                                (int64_t)p.n_leaf * K, st);
   launch_reduce_partials(stats + p.sizes.stats_p_offset, Pcall, 1, (int64_t)p.n_leaf * K,
