@@ -315,10 +315,17 @@ def run_ours(args):
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item())
 
+    # kernels per step: counted on one uncaptured step (the timed steps replay
+    # the CUDA graph of exactly this launch sequence)
+    os.environ["EINET_CUDA_GRAPHS"] = "0"
     launches0 = _native.launch_count()
+    step(x_dev)
+    launches = _native.launch_count() - launches0
+    os.environ.pop("EINET_CUDA_GRAPHS")
+    step(x_dev)
+    torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
         ms = timed(lambda: step(x_dev), args.steps)
-    launches = (_native.launch_count() - launches0) // args.steps
 
     # end to end: pinned host batch -> device each step, mean LL read back
     e2e_steps = max(3, args.steps // 4)

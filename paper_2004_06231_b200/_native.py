@@ -140,8 +140,13 @@ def launch_count() -> int:
     return int(load().einet_launch_count())
 
 
+PROFILING = False
+
+
 def profile_enable(on: bool = True):
+    global PROFILING
     load().einet_profile_enable(1 if on else 0)
+    PROFILING = bool(on)
 
 
 def profile_read() -> dict:

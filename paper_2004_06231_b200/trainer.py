@@ -4,17 +4,23 @@ One EM step = for each chunk: forward + responsibility back-pass (statistics
 accumulate in one fp64 device buffer) -> optional all-reduce of that buffer
 across ranks -> one fused M-step kernel sequence. The host synchronises once
 per step, to read the log-likelihood sum and the error words.
+
+On a single device the whole step (statistics reset, every chunk's forward and
+back-pass, M-step) is captured once into a CUDA graph per (batch buffer,
+shape, lambda, chunk) and replayed, removing the per-kernel launch gaps
+(EINET_CUDA_GRAPHS=0 disables it).
 """
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
-from . import engine
+from . import _native, engine
 from .model import EinetModel
 
 EPS_COUNT = 1e-12
@@ -70,6 +76,36 @@ def accumulate(model: EinetModel, batch: torch.Tensor, chunk: int):
     return eng, stats, status, compute
 
 
+_GRAPH_CACHE_SIZE = 4
+
+
+def _graphs_enabled() -> bool:
+    return os.environ.get("EINET_CUDA_GRAPHS", "1") != "0" and not _native.PROFILING
+
+
+def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk):
+    """Replay (capturing on first use) the CUDA graph of one EM step on the
+    device batch ``xd``; returns (engine, stats, status)."""
+    n = xd.shape[0]
+    eng, ws, stats, status, root = model.step_buffers(min(chunk, max(n, 1)))
+    compute = model.params.compute_for(eng)  # prepares outside the graph if stale
+    key = (xd.data_ptr(), tuple(xd.shape), float(lam), float(eps_w), int(chunk),
+           model.params.flat.data_ptr(), ws.data_ptr(), compute.data_ptr())
+    cache = model.__dict__.setdefault("_graphs", {})
+    g = cache.get(key)
+    if g is None:
+        if len(cache) >= _GRAPH_CACHE_SIZE:
+            cache.pop(next(iter(cache)))
+        torch.cuda.current_stream().synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            accumulate(model, xd, chunk)
+            eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
+        cache[key] = g
+    g.replay()
+    return eng, stats, status
+
+
 def em_stochastic_step(model: EinetModel, batch, lam, eps_w=engine.EPS_W, chunk=4096,
                        process_group=None) -> float:
     """One gliding-average EM update; returns the pre-update mean LL of the
@@ -83,13 +119,16 @@ def em_stochastic_step(model: EinetModel, batch, lam, eps_w=engine.EPS_W, chunk=
     xd = engine.as_device_batch(batch)
     if xd.shape[0] == 0:
         raise ValueError("empty batch")
-    eng, stats, status, compute = accumulate(model, xd, chunk)
-    if process_group is not None:
-        import torch.distributed as dist
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=process_group)
-        dist.all_reduce(status, op=dist.ReduceOp.MIN, group=process_group)
-    if lam != 0.0:
-        eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
+    if lam != 0.0 and process_group is None and xd.is_cuda and _graphs_enabled():
+        eng, stats, status = _graph_step(model, xd, lam, eps_w, chunk)
+    else:
+        eng, stats, status, compute = accumulate(model, xd, chunk)
+        if process_group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=process_group)
+            dist.all_reduce(status, op=dist.ReduceOp.MIN, group=process_group)
+        if lam != 0.0:
+            eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
     ll_off = int(eng.sizes.stats_ll_offset)
     info = torch.cat([stats[ll_off:ll_off + 2], status.to(torch.float64)]).cpu().tolist()
     engine._raise_words([int(v) for v in info[2:]], model.family)
