@@ -85,7 +85,7 @@ static void profile_clear() {
 }
 
 template <typename T>
-static int upload(T **dst, const std::vector<T> &src) {
+int upload(T **dst, const std::vector<T> &src) {
   *dst = nullptr;
   size_t n = std::max<size_t>(src.size(), 1);
   int rc = check_cuda(cudaMalloc((void **)dst, n * sizeof(T)), "cudaMalloc(plan)");
@@ -95,6 +95,37 @@ static int upload(T **dst, const std::vector<T> &src) {
                                cudaMemcpyHostToDevice),
                     "cudaMemcpy(plan)");
   return rc;
+}
+
+int upload_tiledesc(Plan &p) {
+  std::vector<int64_t> td;
+  const int64_t KK = (int64_t)p.k * p.k;
+  for (auto &L : p.layers) {
+    if (L.kind != EINET_LAYER_EINSUM) continue;
+    int64_t w[TD_WORDS] = {0};
+    w[TD_SLICE0] = L.w_off / KK;
+    w[TD_ROWS] = L.rows;
+    w[TD_KO] = L.k_out;
+    w[TD_TC] = L.tc;
+    w[TD_DIRECT] = L.direct;
+    w[TD_KG] = L.kg;
+    w[TD_NG] = L.ng;
+    w[TD_FW_ROWS] = L.fw_rows;
+    w[TD_IG] = L.ig;
+    w[TD_NI] = L.ni;
+    w[TD_UW_ROWS] = L.uw_rows;
+    w[TD_KO8] = L.ko8;
+    w[TD_RW_ROWS] = L.rw_rows;
+    w[TD_FW_OFF] = L.fw_off;
+    w[TD_FW_TILE] = L.fw_tile;
+    w[TD_UW_OFF] = L.uw_off;
+    w[TD_UW_TILE] = L.uw_tile;
+    w[TD_VW_OFF] = L.vw_off;
+    w[TD_RW_TILE] = L.rw_tile;
+    td.insert(td.end(), w, w + TD_WORDS);
+  }
+  p.n_tiledesc = (int)(td.size() / TD_WORDS);
+  return upload(&p.d_tiledesc, td);
 }
 
 static void free_plan_memory(Plan *p) {
@@ -111,6 +142,8 @@ static void free_plan_memory(Plan *p) {
   f(p->d_lseg_vec);
   f(p->d_phi_seg);
   f(p->d_leaf_pvo);
+  f(p->d_scope_pos);
+  f(p->d_tiledesc);
   f(p->d_csr_off);
   f(p->d_csr_slot);
   f(p->d_slab_ones);
@@ -376,6 +409,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     L.uw_off = seg(L.uw_tile * L.rows * L.ni);
     L.vw_off = seg(std::max(L.uw_tile * L.ni, L.rw_tile) * L.rows);
   }
+  p->c_mtmp = seg(16 * (int64_t)R * D * K);
   z.compute_bytes = off;
 
   p->bc = align_up(max_chunk, 128);  // 32-sample blocks, 128-sample tensor-core tiles
@@ -442,6 +476,14 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   if ((rc = upload(&p->d_lseg_vec, lseg_vec))) return rc;
   if ((rc = upload(&p->d_phi_seg, phi_seg))) return rc;
   if (p->leaf_dmma && (rc = upload(&p->d_leaf_pvo, p->h_leaf_pvo))) return rc;
+  {
+    std::vector<int> pos((size_t)R * D, -1);
+    for (int l = 0; l < d->n_leaf; ++l)
+      for (int q = p->h_scope_off[l]; q < p->h_scope_off[l + 1]; ++q)
+        pos[(size_t)p->h_leaf_rep[l] * D + p->h_scope_vars[q]] = q - p->h_scope_off[l];
+    if ((rc = upload(&p->d_scope_pos, pos))) return rc;
+  }
+  if ((rc = upload_tiledesc(*p))) return rc;
   if ((rc = upload(&p->d_csr_off, p->h_csr_off))) return rc;
   if ((rc = upload(&p->d_csr_slot, p->h_csr_slot))) return rc;
   if ((rc = upload(&p->d_slab_ones, p->h_slab_ones))) return rc;

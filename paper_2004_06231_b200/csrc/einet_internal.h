@@ -23,6 +23,12 @@ namespace einet {
 constexpr int kMaxDSplit = 16;     // leaf forward split of a scope across CTAs
 constexpr int kMaxBSplit = 64;     // batch split of statistic reductions
 constexpr int kReduceThreads = 256;
+// per-einsum-layer tile descriptor for the fused M-step (int64 words)
+enum TileDescWord {
+  TD_SLICE0, TD_ROWS, TD_KO, TD_TC, TD_DIRECT, TD_KG, TD_NG, TD_FW_ROWS, TD_IG, TD_NI,
+  TD_UW_ROWS, TD_KO8, TD_RW_ROWS, TD_FW_OFF, TD_FW_TILE, TD_UW_OFF, TD_UW_TILE, TD_VW_OFF,
+  TD_RW_TILE, TD_WORDS
+};
 constexpr int EV_ROW = 36;         // padded row of the EA / EB 32-sample blocks (kern_common.cuh)
 
 struct LayerPlan {
@@ -95,6 +101,11 @@ struct Plan {
   int leaf_dmma = 0;               // eligible (Gaussian, K % 8 == 0, K <= 64)
   std::vector<int> h_leaf_pvo;     // padded variable offset per leaf (n_leaf + 1)
   int *d_leaf_pvo = nullptr;
+  int *d_scope_pos = nullptr;      // (R, D): position of d in its leaf's scope, or -1
+  // fused M-step (mstep.cu): per-einsum-layer tile geometry, temp leaf terms
+  int64_t *d_tiledesc = nullptr;   // einsum layers x TD_WORDS (mstep.cu)
+  int n_tiledesc = 0;
+  int64_t c_mtmp = 0;              // compute segment: 2 x R*D*K doubles
   // workspace segments (byte offsets)
   int64_t w_off = 0, w_shift = 0, w_slots = 0, w_leafpart = 0, w_ea = 0, w_eb = 0,
           w_rt = 0, w_wpart = 0, w_rho = 0, w_lspart = 0, w_ppart = 0, w_mixpart = 0,
@@ -153,6 +164,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
                     cudaStream_t st);
 int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
                  double lam, double eps_w, const int32_t *status, cudaStream_t st);
+int upload_tiledesc(Plan &p);
 int launch_expand_acc_p(Plan &p, const double *stats, double *acc_p, cudaStream_t st);
 int launch_export_buffer(Plan &p, const uint8_t *ws, int64_t B, double *out,
                          cudaStream_t st);

@@ -5,6 +5,7 @@
 #include <cmath>
 
 #include "kern_common.cuh"
+#include "tc_common.cuh"
 
 namespace einet {
 
@@ -87,9 +88,12 @@ __device__ __forceinline__ double block_sum_256(double v, double *red) {
 // engine.py:46-49.
 __global__ void __launch_bounds__(256) k_mstep_einsum(double *__restrict__ W,
                                                       float *__restrict__ w32,
-                                                      const double *__restrict__ n, int KK,
+                                                      const double *__restrict__ n, int K,
                                                       double lam, double eps,
-                                                      const int32_t *status) {
+                                                      const int32_t *status,
+                                                      const int64_t *__restrict__ tiledesc,
+                                                      int ntd, uint8_t *compute) {
+  const int KK = K * K;
   __shared__ double red[8];
   if (step_failed(status)) return;
   const int64_t base = (int64_t)blockIdx.x * KK;
@@ -106,10 +110,56 @@ __global__ void __launch_bounds__(256) k_mstep_einsum(double *__restrict__ W,
     s2 += v;
   }
   const double tot = block_sum_256(s2, red);
+  // tensor-core weight images of this (l, k) slice (einsum_tc.cu k_build_tiles
+  // layouts; padding entries were zeroed by the first prepare)
+  const int64_t *td = nullptr;
+  int64_t l = 0, k = 0;
+  if (tiledesc) {
+    for (int q = 0; q < ntd; ++q) {
+      const int64_t *c = tiledesc + (int64_t)q * TD_WORDS;
+      const int64_t rel = (int64_t)blockIdx.x - c[TD_SLICE0];
+      if (rel >= 0 && rel < c[TD_ROWS] * c[TD_KO]) {
+        if (c[TD_TC]) td = c;
+        l = rel / c[TD_KO];
+        k = rel % c[TD_KO];
+        break;
+      }
+    }
+  }
   for (int e = threadIdx.x; e < KK; e += 256) {
     const double v = W[base + e] / tot;
     W[base + e] = v;
     w32[base + e] = (float)v;
+    if (td) {
+      const int i = e / K, j = e - (e / K) * K;
+      float h, lo;
+      tc::split_tf32((float)v, h, lo);
+      {  // forward tile: rows kl*K + i, K dim j
+        const int64_t kg = td[TD_KG], rows = td[TD_FW_ROWS];
+        const int64_t tile = l * td[TD_NG] + k / kg;
+        float *t = (float *)(compute + td[TD_FW_OFF] + tile * td[TD_FW_TILE]);
+        const int64_t o = tc::kmaj_off((int)((k % kg) * K + i), j, (int)rows) / 4;
+        t[o] = h;
+        t[o + rows * K] = lo;
+      }
+      if (td[TD_DIRECT]) {  // K_out == 1: right tile rows j, K dim i
+        const int64_t rows = td[TD_RW_ROWS];
+        float *t = (float *)(compute + td[TD_VW_OFF] + l * td[TD_RW_TILE]);
+        const int64_t o = tc::kmaj_off(j, i, (int)rows) / 4;
+        t[o] = h;
+        t[o + rows * K] = lo;
+      } else {  // left (rows il*K + j) and right (rows jl*K + i) tiles, K dim k
+        const int64_t ig = td[TD_IG], rows = td[TD_UW_ROWS], ko8 = td[TD_KO8];
+        float *tl = (float *)(compute + td[TD_UW_OFF] + (l * td[TD_NI] + i / ig) * td[TD_UW_TILE]);
+        const int64_t ol = tc::kmaj_off((int)((i % ig) * K + j), (int)k, (int)rows) / 4;
+        tl[ol] = h;
+        tl[ol + rows * ko8] = lo;
+        float *tr = (float *)(compute + td[TD_VW_OFF] + (l * td[TD_NI] + j / ig) * td[TD_UW_TILE]);
+        const int64_t orr = tc::kmaj_off((int)((j % ig) * K + i), (int)k, (int)rows) / 4;
+        tr[orr] = h;
+        tr[orr + rows * ko8] = lo;
+      }
+    }
   }
 }
 
@@ -184,15 +234,127 @@ __global__ void k_mstep_leaf(double *__restrict__ phi, const double *__restrict_
   }
 }
 
+// Gaussian leaves, one warp per (r, d), lanes over k: the M-step update
+// (trainer.py:82-85, 114, 96; expfam.py GaussianFamily.project) followed by the
+// per-variable compute tensors the forward and the statistics read (leaf.cu
+// k_prepare_gauss / k_prepare_center, leaf_dmma.cu k_prepare_leaf_img) and the
+// per-(variable, k) terms of the leaf constants (reduced by k_leaf_consts).
+// Masked variables never reach a cached compute buffer (marginal queries build
+// their own), so every covered variable is active here.
+__global__ void __launch_bounds__(256) k_mstep_leaf_gauss(
+    double *__restrict__ phi, const double *__restrict__ acc_pt, const double *__restrict__ P,
+    const int *__restrict__ leaf_of, const int *__restrict__ scope_pos,
+    const int *__restrict__ pvo, int D, int K, int R, double lam, double var_min,
+    double var_max, const int32_t *status, CompView c, int dmma, double *__restrict__ mtmp) {
+  if (step_failed(status)) return;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= R * D) return;
+  const int r = wid / D, d = wid - r * D;
+  const int l = leaf_of[(int64_t)r * D + d];
+  double mu[2] = {0.0, 0.0}, var[2] = {1.0, 1.0};
+  double csum = 0.0;
+  for (int u = 0; u < 2; ++u) {
+    const int k = lane + 32 * u;
+    if (k >= K) continue;
+    const int64_t e = ((int64_t)d * K + k) * R + r;
+    double *ph = phi + e * 2;
+    double m = ph[0], s2 = ph[1];
+    if (l >= 0) {
+      const double p = P[(int64_t)l * K + k];
+      const bool keep = p <= kEpsCount;
+      const double t0 = keep ? m : acc_pt[e * 2] / p;
+      const double t1 = keep ? s2 : acc_pt[e * 2 + 1] / p;
+      const double mn = (1.0 - lam) * m + lam * t0;
+      const double sn = (1.0 - lam) * s2 + lam * t1;
+      const double v = fmin(fmax(sn - mn * mn, var_min), var_max);
+      m = mn;
+      s2 = v + mn * mn;
+      ph[0] = m;
+      ph[1] = s2;
+    }
+    mu[u] = m;
+    var[u] = s2 - m * m;
+    csum += m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+  const float cen = (float)(csum / K);
+  if (lane == 0) c.center[(int64_t)r * D + d] = cen;
+  const int pos = scope_pos[(int64_t)r * D + d];
+  double2 *lp = (double2 *)c.leafp;
+  for (int u = 0; u < 2; ++u) {
+    const int k = lane + 32 * u;
+    if (k >= K) continue;
+    const double sa = sqrt(0.5 / var[u]);
+    lp[((int64_t)r * D + d) * K + k] = make_double2(sa, -mu[u] * sa);
+    const double m = -(-mu[u] * sa + (double)cen * sa);
+    if (l >= 0) {
+      double *t = mtmp + (((int64_t)r * D + d) * K + k) * 2;
+      t[0] = -0.5 * (kLog2Pi + log(var[u]));
+      t[1] = m * m;
+      if (dmma) {
+        const int pv = pvo[l] + pos;
+        double *img = c.leafimg + ((int64_t)(pv >> 1) * (K / 8) + k / 8) * 32 + (k % 8) * 4 +
+                      (pv & 1) * 2;
+        img[0] = sa * sa;
+        img[1] = -2.0 * sa * m;
+      }
+    }
+  }
+}
+
+// per (leaf, k): scope sums of the per-variable terms (fixed-order tree):
+// cnst = sum -0.5 (log 2 pi + log var), cm2 = sum m^2. grid (n_leaf, K).
+__global__ void __launch_bounds__(256) k_leaf_consts(const double *__restrict__ mtmp,
+                                                     const int *scope_off, const int *scope_vars,
+                                                     const int *leaf_rep, int D, int K,
+                                                     double *cnst, double *cm2,
+                                                     const int32_t *status) {
+  __shared__ double red[2][8];
+  if (step_failed(status)) return;
+  const int leaf = blockIdx.x, k = blockIdx.y, r = leaf_rep[leaf];
+  double a = 0.0, b = 0.0;
+  for (int q = scope_off[leaf] + threadIdx.x; q < scope_off[leaf + 1]; q += 256) {
+    const double *t = mtmp + (((int64_t)r * D + scope_vars[q]) * K + k) * 2;
+    a += t[0];
+    b += t[1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a;
+    red[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      sa += red[0][w];
+      sb += red[1][w];
+    }
+    cnst[leaf * K + k] = sa;
+    if (cm2) cm2[leaf * K + k] = sb;
+  }
+}
+
 int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats, double lam,
                  double eps_w, const int32_t *status, cudaStream_t st) {
   CompView c = comp_view(p, compute);
   const int K = p.k;
   const int KK = K * K;
   ProfScope prof("mstep", st);
+  // fused path (Gaussian leaves): the M-step kernels also re-derive every compute
+  // tensor of the cached, unmasked training compute (tensor-core weight images
+  // for tc-capable layers, DMMA leaf image), replacing launch_prepare
+  const bool fused = p.family == EINET_FAMILY_GAUSSIAN && p.k <= 64;
   if (p.n_w) {
     const int nslices = (int)(p.n_w / KK);
-    k_mstep_einsum<<<nslices, 256, 0, st>>>(params, c.w32, stats, KK, lam, eps_w, status);
+    k_mstep_einsum<<<nslices, 256, 0, st>>>(params, c.w32, stats, K, lam, eps_w, status,
+                                            fused ? p.d_tiledesc : nullptr,
+                                            p.n_tiledesc, compute);
     count_launch();
   }
   if (p.n_mixrows) {
@@ -200,6 +362,19 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
         params + p.n_w, c.mix32, stats + p.n_w, p.d_mixrow_off, p.d_mixrow_len,
         p.d_mix_mask_all, p.n_mixrows, lam, eps_w, status);
     count_launch();
+  }
+  if (fused) {
+    const int64_t warps = (int64_t)p.num_replicas * p.d_vars;
+    double *mtmp = (double *)(compute + p.c_mtmp);
+    k_mstep_leaf_gauss<<<(int)((warps + 7) / 8), 256, 0, st>>>(
+        params + p.sizes.phi_offset, stats + p.sizes.stats_acc_pt_offset,
+        stats + p.sizes.stats_p_offset, p.d_leaf_of, p.d_scope_pos, p.d_leaf_pvo, p.d_vars, K,
+        p.num_replicas, lam, p.var_min, p.var_max, status, c, p.leaf_dmma, mtmp);
+    k_leaf_consts<<<dim3(p.n_leaf, K), 256, 0, st>>>(mtmp, p.d_scope_off, p.d_scope_vars,
+                                                     p.d_leaf_rep, p.d_vars, K, c.cnst,
+                                                     p.leaf_dmma ? c.cm2 : nullptr, status);
+    count_launch(2);
+    return check_cuda(cudaGetLastError(), "fused mstep kernels");
   }
   const int64_t n = (int64_t)p.d_vars * K * p.num_replicas;
   k_mstep_leaf<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(

@@ -83,6 +83,27 @@ def _graphs_enabled() -> bool:
     return os.environ.get("EINET_CUDA_GRAPHS", "1") != "0" and not _native.PROFILING
 
 
+def _stage_batch(model: EinetModel, batch) -> torch.Tensor:
+    """Device batch for the graph path. Device fp32 tensors are used in place;
+    host data is copied (asynchronously when pinned) into a persistent
+    per-model staging buffer, so the captured graph's input address is stable
+    across steps."""
+    if isinstance(batch, torch.Tensor) and batch.is_cuda:
+        return engine.as_device_batch(batch)
+    t = batch if isinstance(batch, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(batch, dtype=np.float64), dtype=np.float32))
+    if t.dim() == 1:
+        t = t[None, :]
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        t = t.to(torch.float32).contiguous()
+    st = model.__dict__.get("_staging")
+    if st is None or st.shape != t.shape:
+        st = torch.empty(t.shape, dtype=torch.float32, device=model.params.flat.device)
+        model.__dict__["_staging"] = st
+    st.copy_(t, non_blocking=t.is_pinned())
+    return st
+
+
 def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk):
     """Replay (capturing on first use) the CUDA graph of one EM step on the
     device batch ``xd``; returns (engine, stats, status)."""
@@ -116,10 +137,11 @@ def em_stochastic_step(model: EinetModel, batch, lam, eps_w=engine.EPS_W, chunk=
     all-reduce of the packed buffer) and every rank applies the identical
     M-step; the returned mean LL is then the global one.
     """
-    xd = engine.as_device_batch(batch)
+    use_graph = lam != 0.0 and process_group is None and _graphs_enabled()
+    xd = _stage_batch(model, batch) if use_graph else engine.as_device_batch(batch)
     if xd.shape[0] == 0:
         raise ValueError("empty batch")
-    if lam != 0.0 and process_group is None and xd.is_cuda and _graphs_enabled():
+    if use_graph:
         eng, stats, status = _graph_step(model, xd, lam, eps_w, chunk)
     else:
         eng, stats, status, compute = accumulate(model, xd, chunk)
