@@ -387,7 +387,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     p->c_leafp = seg(16 * RDK);
   p->c_center = seg(4 * RDK);
   p->c_const = seg(8 * (int64_t)p->n_leaf * K);
-  p->c_active = seg(D);
+  p->c_active = seg(D + 1);
   p->c_logh = seg(8 * (int64_t)(std::max(p->n_trials, 0) + 1));
   p->leaf_dmma = p->family == EINET_FAMILY_GAUSSIAN && K % 8 == 0 && K <= 64;
   if (p->leaf_dmma) {

@@ -33,9 +33,12 @@ __global__ void k_to_f32(const double *__restrict__ src, float *__restrict__ dst
     dst[i] = (float)src[i];
 }
 
+// active[d] = not marginalised; active[D] = 1 when a mask was given (the DMMA
+// leaf forward then zeroes masked / non-finite x before the contraction).
 __global__ void k_prepare_active(const uint8_t *mask, uint8_t *active, int D) {
   int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d < D) active[d] = mask ? (mask[d] ? 0 : 1) : 1;
+  if (d == 0) active[D] = mask ? 1 : 0;
 }
 
 // phi (D,K,R,2) = (mean, second moment) -> fp64 (sa, -mu*sa), [r][d][k]
@@ -367,20 +370,23 @@ __global__ void __launch_bounds__(1024) k_leaf_fwd_discrete(
 // written coalesced.
 __global__ void __launch_bounds__(256) k_leaf_finalize(
     const double *__restrict__ part, int dsplit, const double *__restrict__ cnst, int64_t B,
-    int K, int n_leaf, const int *leaf_slab, WsView ws, double sign) {
+    int K, int n_leaf, const int *leaf_slab, WsView ws, double sign, int32_t *status) {
   extern __shared__ double vals[];  // [32][K+1]
   __shared__ double mxs[32];
   const int leaf = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int nb = (int)min((int64_t)32, B - b0);
   const int slab = leaf_slab[leaf];
+  bool bad = false;
   for (int e = threadIdx.x; e < nb * K; e += 256) {
     const int bl = e / K, k = e - bl * K;
     const double *src = part + ((int64_t)leaf * ws.bc + b0) * K + e;
     double s = 0.0;
     for (int q = 0; q < dsplit; ++q) s += src[(int64_t)q * n_leaf * ws.bc * K];
     vals[bl * (K + 1) + k] = cnst[leaf * K + k] + sign * s;
+    bad |= !isfinite(s);
   }
+  if (bad && status) atomicMin(&status[2], 0);  // non-finite x reached a leaf row
   __syncthreads();
   const int lane = threadIdx.x & 31;
   for (int bl = threadIdx.x >> 5; bl < nb; bl += 8) {
@@ -401,6 +407,20 @@ __global__ void __launch_bounds__(256) k_leaf_finalize(
     if (bl >= nb) continue;
     const double mx = mxs[bl];
     tile[e] = mx == -CUDART_INF ? 0.f : (float)(vals[bl * (K + 1) + k] - mx);
+  }
+}
+
+// Reference support check (expfam.py:278-294) for the unmasked DMMA path:
+// only when a leaf row came out non-finite, report the lowest active variable
+// holding a non-finite value (atomicMin, like the gathering kernels).
+__global__ void k_leaf_check(const float *__restrict__ x, int64_t B, int D,
+                             const uint8_t *__restrict__ active, int32_t *status) {
+  if (status[2] == INT_MAX) return;
+  const int64_t n = B * D;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int d = (int)(e % D);
+    if (active[d] && !isfinite(x[e])) atomicMin(&status[0], d);
   }
 }
 
@@ -451,8 +471,13 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
     cudaFuncSetAttribute(k_leaf_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)fsmem);
   k_leaf_finalize<<<g2, 256, fsmem, st>>>(w.leafpart, ds, c.cnst, B, p.k, p.n_leaf, p.d_leaf_slab,
-                                      w, p.family == EINET_FAMILY_GAUSSIAN ? -1.0 : 1.0);
+                                      w, p.family == EINET_FAMILY_GAUSSIAN ? -1.0 : 1.0,
+                                      status);
   count_launch(2);
+  if (p.leaf_dmma && p.use_tc) {
+    k_leaf_check<<<2 * p.num_sms, 256, 0, st>>>(x, B, p.d_vars, c.active, status);
+    count_launch();
+  }
   return check_cuda(cudaGetLastError(), "leaf forward kernels");
 }
 

@@ -146,6 +146,9 @@ __global__ void __launch_bounds__(32 * WARPS, 8 / WARPS + 1) k_leaf_fwd_dmma(
   const int64_t b0 = (int64_t)blockIdx.x * TBS;
   const int nbl = (int)min((int64_t)TBS, B - b0);
   const double *limg = img + (int64_t)(pvo[leaf] / 2) * NT * 32;
+  // unmasked compute: x goes straight into the contraction; a non-finite value
+  // makes the leaf row non-finite, which k_leaf_finalize flags for k_leaf_check
+  const bool masked = active[D] != 0;
 
   auto stage = [&](int buf, int ch) {
     const int c0 = ch * LD_VC, nv = min(LD_VC, slen - c0);
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(32 * WARPS, 8 / WARPS + 1) k_leaf_fwd_dmma(
     } else {
       cp_async_wait<0>();
     }
-    fixup(buf, ch);
+    if (masked) fixup(buf, ch);
     __syncthreads();
     const double *ib = is + buf * IS;
     const float *xb = xs + buf * XS;

@@ -272,6 +272,28 @@ def test_unsupported_values_raise():
         mc.forward(np.array([[0.0, 3.0, 1.0]]))
 
 
+def test_unsupported_values_raise_dmma_path():
+    """K % 8 == 0 Gaussian leaves take the FP64 tensor-core forward, which has
+    no per-value check on unmasked data: the non-finite row flag must still
+    raise for the lowest offending variable, and the EM step must not update."""
+    rg = E.random_binary_tree(16, StructureConfig(depth=2, replicas=2, seed=3))
+    m = E.build_model(rg, E.GaussianFamily(), k=8, seed=2, data=np.zeros((4, 16)))
+    x = np.zeros((40, 16))
+    x[33, 11] = np.inf
+    x[7, 5] = np.nan
+    with pytest.raises(E.UnsupportedValueError, match="variable 5"):
+        m.forward(x)
+    before = m.params.flat.clone()
+    with pytest.raises(E.UnsupportedValueError, match="variable 5"):
+        trainer.em_stochastic_step(m, x, 0.5)
+    assert torch.equal(before, m.params.flat)
+    x[7, 5] = 0.0
+    with pytest.raises(E.UnsupportedValueError, match="variable 11"):
+        trainer.em_stochastic_step(m, x, 0.5)
+    x[33, 11] = 0.0
+    trainer.em_stochastic_step(m, x, 0.5)
+
+
 def test_shape_mismatch_raises():
     m = _gauss_model(11, data=np.zeros((4, 4)))
     with pytest.raises(E.EngineError):
