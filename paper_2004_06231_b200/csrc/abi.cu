@@ -114,7 +114,7 @@ int upload_tiledesc(Plan &p) {
     w[TD_IG] = L.ig;
     w[TD_NI] = L.ni;
     w[TD_UW_ROWS] = L.uw_rows;
-    w[TD_KO8] = L.ko8;
+    w[TD_KOB] = L.kob;
     w[TD_RW_ROWS] = L.rw_rows;
     w[TD_FW_OFF] = L.fw_off;
     w[TD_FW_TILE] = L.fw_tile;
@@ -445,16 +445,17 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   p->w_tmp_s = seg(8 * p->n_phi);
   p->w_tmp_p = seg(8 * (int64_t)p->n_leaf * K);
   {
-    int ko8max = 0;
+    int kobmax = 0;
     bool any_tc = false;
     for (auto &L : p->layers)
       if (L.tc) {
         any_tc = true;
-        ko8max = std::max(ko8max, L.ko8);
+        kobmax = std::max(kobmax, L.kob);
       }
-    p->w_ebm = seg(any_tc ? 8 * (int64_t)p->n_erows * Bc * K : 0);
-    p->w_eam = seg(any_tc ? 8 * (int64_t)p->n_erows * Bc * K : 0);
-    p->w_rtm = seg(any_tc ? 8 * p->max_rows * Bc * ko8max : 0);
+    // bf16 hi | lo A-operand tiles (contract_tc.cu)
+    p->w_ebm = seg(any_tc ? 4 * (int64_t)p->n_erows * Bc * p->kp : 0);
+    p->w_eam = seg(any_tc ? 4 * (int64_t)p->n_erows * Bc * p->kp : 0);
+    p->w_rtm = seg(any_tc ? 4 * p->max_rows * Bc * kobmax : 0);
     int nnmax = 0;
     for (auto &L : p->layers)
       if (L.tc) nnmax = std::max(nnmax, L.nn);

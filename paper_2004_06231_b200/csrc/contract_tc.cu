@@ -1,5 +1,7 @@
 // Warp-specialised tcgen05 contraction kernel shared by the EinsumLayer
-// forward and the two child-responsibility passes (3xTF32).
+// forward and the two child-responsibility passes (3xBF16: hi*hi + hi*lo +
+// lo*hi of round-to-nearest bf16 splits, fp32 accumulation; ~2^-17 relative
+// per product with random signs).
 //
 // All three are, per einsum row l and 128-sample tile, a GEMM against a
 // stationary chunk of that row's weights followed by a per-sample contraction
@@ -13,8 +15,8 @@
 //                                right[b,j]  = EB[b,j] sum_i EA[b,i] V    -> right slot
 //
 // The A operand (EB or RT = rho / r) is written by its producer kernel in the
-// K-major core-matrix layout of a 128-sample tile, split into a truncated TF32
-// part and the fp32 remainder, so it reaches shared memory with one bulk copy.
+// K-major core-matrix layout of a 128-sample tile as bf16 hi and lo parts, so
+// it reaches shared memory with one bulk copy.
 // The weight chunk (<= 256 accumulator columns: `og` outputs x K) is a
 // pre-tiled image (einsum_tc.cu, k_build_tiles) and stays resident while the
 // CTA walks its run of (row, chunk, tile) jobs; it is reloaded only when the
@@ -32,6 +34,7 @@
 // (profiles/r01_s2_profile.md).
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kern_common.cuh"
@@ -39,14 +42,14 @@
 
 namespace einet {
 
-constexpr int CT_STAGES = 3;
+constexpr int CT_STAGES = 4;
 constexpr int CT_EPI_WARPS = 8;                 // two per TMEM lane quarter
 constexpr int CT_THREADS = 64 + 32 * CT_EPI_WARPS;
 
 struct ContractArgs {
   const float *a_ops;     // A operand tiles of the layer's first row
-  int64_t a_row_stride;   // floats per row (ntl * 2 * 128 * ka)
-  int ka;                 // MMA K dimension (multiple of 8)
+  int64_t a_row_stride;   // bytes per row (ntl * 128 * ka * 4: bf16 hi | lo)
+  int ka;                 // MMA K dimension (multiple of 16)
   const float *e1;        // contraction vector, 32-sample transposed, width K
   const float *sv;        // per-output scale vector (left/right), width K; null = forward
   const uint8_t *tiles;   // weight chunk images [row][chunk]
@@ -59,7 +62,41 @@ struct ContractArgs {
   int direct;             // K_out == 1 child-rho: out[o] = e1[o] * rt * acc[o] (no contraction)
   int sv_w;               // transposed-block width of sv
   int debug;              // EINET_CT_DEBUG (timing experiments only): 1 no epilogue math, 2 no MMA
+  long long *trace;       // EINET_CT_TRACE (diagnostics): per-job timestamps of CTA 0
 };
+
+__device__ __forceinline__ long long ct_now() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// (pair = row * nchunk + chunk, 128-sample tile) of consecutive jobs, advanced
+// incrementally (64-bit division costs hundreds of cycles in the issue loops)
+struct JobCursor {
+  int pair, jt, l, c;
+  __device__ __forceinline__ void init(int64_t j, int64_t ntl, int nchunk) {
+    pair = (int)(j / ntl);
+    jt = (int)(j % ntl);
+    l = pair / nchunk;
+    c = pair % nchunk;
+  }
+  // returns true when the next job starts a new (row, chunk) pair
+  __device__ __forceinline__ bool next(int ntl, int nchunk) {
+    if (++jt < ntl) return false;
+    jt = 0;
+    ++pair;
+    if (++c == nchunk) {
+      c = 0;
+      ++l;
+    }
+    return true;
+  }
+};
+
+#define CT_TRACE(slot, it)                                                      \
+  do {                                                                          \
+    if (a.trace && blockIdx.x == 0 && (it) < 64) a.trace[(it) * 8 + (slot)] = ct_now(); \
+  } while (0)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
@@ -76,7 +113,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
   const int64_t j0 = (int64_t)blockIdx.x * J / gridDim.x;
   const int64_t j1 = (int64_t)(blockIdx.x + 1) * J / gridDim.x;
   const int64_t wbytes = (a.tile_bytes + 1023) / 1024 * 1024;
-  const uint32_t abytes = (uint32_t)(2 * 128 * a.ka * 4);
+  const uint32_t abytes = (uint32_t)(128 * a.ka * 4);  // bf16 hi | lo
   const uint32_t ebytes = (uint32_t)(4 * K * EV_ROW * 4);
   uint8_t *wsm = sm;
   uint8_t *abuf = sm + wbytes;
@@ -105,29 +142,37 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
   if (w == 0) {
     // ---- producer ----
     if (lane == 0) {
-      int64_t prev = -1;
-      int q = -1, it = 0;
+      const int ntl = (int)a.ntl;
+      JobCursor cur;
+      cur.init(j0, a.ntl, a.nchunk);
+      bool fresh = true;
+      int q = -1, it = 0, s = 0, ph = 0;
       for (int64_t j = j0; j < j1; ++j, ++it) {
-        const int64_t pair = j / a.ntl, jt = j % a.ntl;
-        if (pair != prev) {
+        const int pair = cur.pair, jt = cur.jt, l = cur.l;
+        if (fresh) {
           ++q;
           if (q > 0) tc::mbar_wait(&bar_we, (q - 1) & 1);
           tc::mbar_arrive_expect_tx(&bar_wf, (uint32_t)a.tile_bytes);
-          tc::bulk_g2s(wsm, a.tiles + pair * a.tile_bytes, (uint32_t)a.tile_bytes, &bar_wf);
-          prev = pair;
+          tc::bulk_g2s(wsm, a.tiles + (int64_t)pair * a.tile_bytes, (uint32_t)a.tile_bytes,
+                       &bar_wf);
         }
-        const int s = it % a.stages, ph = (it / a.stages) & 1;
         tc::mbar_wait(&bar_ae[s], ph ^ 1);
-        const int l = (int)(pair / a.nchunk);
+        CT_TRACE(0, it);
         tc::mbar_arrive_expect_tx(&bar_af[s], abytes);
         tc::bulk_g2s(abuf + (int64_t)s * abytes,
-                     a.a_ops + l * a.a_row_stride + jt * (2LL * 128 * a.ka), abytes, &bar_af[s]);
+                     (const uint8_t *)a.a_ops + l * a.a_row_stride + (int64_t)jt * abytes, abytes,
+                     &bar_af[s]);
         // the tile's contraction vector: 4 contiguous [K][32] blocks
         const int se = it & 1, eph = (it >> 1) & 1;
         tc::mbar_wait(&bar_ee[se], eph ^ 1);
         tc::mbar_arrive_expect_tx(&bar_ef[se], ebytes);
-        tc::bulk_g2s(ebuf + se * 4 * K * EV_ROW, a.e1 + ev_idx(l, jt * 128, 0, ws.bc, K), ebytes,
-                     &bar_ef[se]);
+        tc::bulk_g2s(ebuf + se * 4 * K * EV_ROW, a.e1 + ev_idx(l, (int64_t)jt * 128, 0, ws.bc, K),
+                     ebytes, &bar_ef[se]);
+        if (++s == a.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+        fresh = cur.next(ntl, a.nchunk);
       }
     }
   } else if (w == 1) {
@@ -136,32 +181,35 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
     // start-address field (16-byte units) ----
     const uint64_t a_desc0 = tc::smem_desc(tc::smem_u32(abuf), 128 * 16, 128u);
     const uint64_t b_desc0 = tc::smem_desc(tc::smem_u32(wsm), (uint32_t)(a.rows_tile * 16), 128u);
-    const uint32_t a_lo_units = 128 * a.ka * 4 / 16, b_lo_units = a.rows_tile * a.ka * 4 / 16;
+    const uint32_t a_lo_units = 128 * a.ka * 2 / 16, b_lo_units = a.rows_tile * a.ka * 2 / 16;
     const uint32_t a_ks_units = 2 * 128, b_ks_units = 2 * a.rows_tile;
-    const int nks = (a.debug & 2) ? 0 : a.ka / 8;
-    int64_t pair = j0 / a.ntl, jt = j0 % a.ntl;
-    int q = 0, it = 0;
+    const int nks = (a.debug & 2) ? 0 : a.ka / 16;
+    const int ntl = (int)a.ntl;
+    JobCursor cur;
+    cur.init(j0, a.ntl, a.nchunk);
+    int q = 0, it = 0, s = 0, ph = 0;
     if (j0 < j1) tc::mbar_wait(&bar_wf, 0);
     for (int64_t j = j0; j < j1; ++j, ++it) {
-      const int c = (int)(pair % a.nchunk);
+      const int c = cur.c, jt = cur.jt;
       const int nol = min(a.og, a.n_out - c * a.og);
       const int nmma = a.direct ? (K + 15) / 16 * 16 : (nol * K + 15) / 16 * 16;
-      const int s = it % a.stages, ph = (it / a.stages) & 1;
       const int buf = it & 1, bph = (it >> 1) & 1;
       tc::mbar_wait(&bar_af[s], ph);
+      if (lane == 0) CT_TRACE(1, it);
       tc::mbar_wait(&bar_ce[buf], bph ^ 1);
       tc::fence_after();
-      const bool last_of_pair = j + 1 == j1 || jt + 1 == a.ntl;
+      if (lane == 0) CT_TRACE(2, it);
+      const bool last_of_pair = j + 1 == j1 || jt + 1 == ntl;
       if (tc::elect_one()) {
-        const uint32_t id = tc::idesc_tf32(128, nmma);
+        const uint32_t id = tc::idesc_bf16(128, nmma);
         const uint32_t d = tm + (uint32_t)(buf * 256);
         uint64_t ah = a_desc0 + (uint64_t)(s * (abytes >> 4));
         uint64_t al = ah + a_lo_units;
         uint64_t bh = b_desc0, bl = b_desc0 + b_lo_units;
         for (int ks = 0; ks < nks; ++ks) {
-          tc::mma_tf32(d, ah, bh, id, ks > 0 ? 1u : 0u);
-          tc::mma_tf32(d, ah, bl, id, 1u);
-          tc::mma_tf32(d, al, bh, id, 1u);
+          tc::mma_bf16(d, ah, bh, id, ks > 0 ? 1u : 0u);
+          tc::mma_bf16(d, ah, bl, id, 1u);
+          tc::mma_bf16(d, al, bh, id, 1u);
           ah += a_ks_units;
           al += a_ks_units;
           bh += b_ks_units;
@@ -172,11 +220,11 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
         if (last_of_pair) tc::mma_commit(&bar_we);
       }
       __syncwarp();
-      if (++jt == a.ntl) {
-        jt = 0;
-        ++pair;
-        if (j + 1 < j1) tc::mbar_wait(&bar_wf, (++q) & 1);
+      if (++s == a.stages) {
+        s = 0;
+        ph ^= 1;
       }
+      if (cur.next(ntl, a.nchunk) && j + 1 < j1) tc::mbar_wait(&bar_wf, (++q) & 1);
     }
   } else {
     // ---- epilogue: one sample per thread ----
@@ -187,12 +235,15 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
     const bool fwd = a.sv == nullptr;
     // per-output scales of the next job, loaded one job ahead
     float sv_next[OGM];
+    const int ntl = (int)a.ntl;
+    JobCursor cur, nxt;
+    cur.init(j0, a.ntl, a.nchunk);
+    nxt = cur;
     auto load_next = [&](int64_t j) {
       if (fwd || j >= j1) return;
-      const int64_t pair = j / a.ntl, jt = j % a.ntl;
-      const int l = (int)(pair / a.nchunk), c = (int)(pair % a.nchunk);
+      const int l = nxt.l, c = nxt.c;
       const int nol = min(a.og, a.n_out - c * a.og);
-      const int64_t b = min(jt * 128 + r, a.B - 1);
+      const int64_t b = min((int64_t)nxt.jt * 128 + r, a.B - 1);
       if (a.direct) {
         sv_next[0] = a.sv[tb_idx(l, b, 0, ws.bc, a.sv_w)];
         return;
@@ -203,19 +254,22 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
         if (u < nol) sv_next[u] = svp[u * EV_ROW];
     };
     load_next(j0);
+    nxt.next(ntl, a.nchunk);
     int it = 0;
     for (int64_t j = j0; j < j1; ++j, ++it) {
-      const int64_t pair = j / a.ntl, jt = j % a.ntl;
-      const int l = (int)(pair / a.nchunk), c = (int)(pair % a.nchunk);
+      const int l = cur.l, c = cur.c;
       const int nol = min(a.og, a.n_out - c * a.og);
-      const int64_t b = jt * 128 + r;
+      const int64_t b = (int64_t)cur.jt * 128 + r;
       const bool live = b < a.B;
       const int64_t bs = live ? b : 0;
       float sv[OGM];
 #pragma unroll
       for (int u = 0; u < OGM; ++u) sv[u] = sv_next[u];
       load_next(j + 1);
+      nxt.next(ntl, a.nchunk);
+      cur.next(ntl, a.nchunk);
       const int se = it & 1, eph = (it >> 1) & 1;
+      if (w == 2 && lane == 0) CT_TRACE(6, it);
       tc::mbar_wait(&bar_ef[se], eph);
       float e1[K];
       {
@@ -224,7 +278,9 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
         for (int i = 0; i < K; ++i) e1[i] = src[i * EV_ROW];
       }
       const int buf = it & 1, bph = (it >> 1) & 1;
+      if (w == 2 && lane == 0) CT_TRACE(3, it);
       tc::mbar_wait(&bar_cf[buf], bph);
+      if (w == 2 && lane == 0) CT_TRACE(4, it);
       tc::fence_after();
       const uint32_t ta = tm + lane_off + (uint32_t)(buf * 256);
       float *out = (fwd ? ws.off : ws.slots) + tb_idx(a.dst[l], bs, 0, ws.bc, ws.ks);
@@ -253,40 +309,57 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
             if ((o & 1) == half) out[o * 32] = e1[o] * (rt * v[o]);
         }
       }
+      // this warp's outputs ol = half, half + 2, ...: the accumulator columns of
+      // up to OPW outputs are loaded with one tcgen05.wait, then contracted
+      constexpr int OPW = (96 / K) < 1 ? 1 : (96 / K);
+      const int nmine = (a.direct || (a.debug & 1)) ? 0 : (nol - half + 1) / 2;
 #pragma unroll 1
-      for (int ol = half; ol < ((a.direct || (a.debug & 1)) ? 0 : nol); ol += 2) {
-        float v[K];
-        int u = 0;
+      for (int g0 = 0; g0 < nmine; g0 += OPW) {
+        float v[OPW][K];
 #pragma unroll
-        for (; u + 16 <= K; u += 16) {
-          float c16[16];
-          tc::tmem_ld16(ta + ol * K + u, c16);
+        for (int gi = 0; gi < OPW; ++gi) {
+          if (g0 + gi >= nmine) break;
+          const int ol = half + 2 * (g0 + gi);
+          int u = 0;
 #pragma unroll
-          for (int z = 0; z < 16; ++z) v[u + z] = c16[z];
-        }
+          for (; u + 32 <= K; u += 32) tc::tmem_ld32(ta + ol * K + u, &v[gi][u]);
 #pragma unroll
-        for (; u < K; u += 8) {
-          float c8[8];
-          tc::tmem_ld8(ta + ol * K + u, c8);
+          for (; u + 16 <= K; u += 16) {
+            float c16[16];
+            tc::tmem_ld16(ta + ol * K + u, c16);
 #pragma unroll
-          for (int z = 0; z < 8; ++z) v[u + z] = c8[z];
+            for (int z = 0; z < 16; ++z) v[gi][u + z] = c16[z];
+          }
+#pragma unroll
+          for (; u < K; u += 8) {
+            float c8[8];
+            tc::tmem_ld8(ta + ol * K + u, c8);
+#pragma unroll
+            for (int z = 0; z < 8; ++z) v[gi][u + z] = c8[z];
+          }
         }
         tc::tmem_wait_ld();
-        float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int i = 0; i < K; ++i) a4[i & 3] = fmaf(v[i], e1[i], a4[i & 3]);
-        const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-        float scale = 1.f;
+        for (int gi = 0; gi < OPW; ++gi) {
+          if (g0 + gi >= nmine) break;
+          const int ol = half + 2 * (g0 + gi);
+          float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int z = 0; z < OGM; ++z)
-          if (z == ol) scale = sv[z];
-        const int o = c * a.og + ol;
-        if (live) out[o * 32] = fwd ? (acc > 0.f ? logf(acc) : -CUDART_INF_F) : scale * acc;
+          for (int i = 0; i < K; ++i) a4[i & 3] = fmaf(v[gi][i], e1[i], a4[i & 3]);
+          const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+          float scale = 1.f;
+#pragma unroll
+          for (int z = 0; z < OGM; ++z)
+            if (z == ol) scale = sv[z];
+          const int o = c * a.og + ol;
+          if (live) out[o * 32] = fwd ? (acc > 0.f ? logf(acc) : -CUDART_INF_F) : scale * acc;
+        }
       }
       tc::fence_before();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&bar_ce[buf]);
+        if (w == 2) CT_TRACE(5, it);
         mbar_arrive(&bar_ee[se]);
       }
     }
@@ -299,7 +372,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
 constexpr size_t CT_SMEM_MAX = 220 * 1024;
 
 size_t contract_smem(int64_t tile_bytes, int ka, int stages, int K) {
-  return (size_t)((tile_bytes + 1023) / 1024 * 1024) + (size_t)stages * 2 * 128 * ka * 4 +
+  return (size_t)((tile_bytes + 1023) / 1024 * 1024) + (size_t)stages * 128 * ka * 4 +
          2 * 4 * (size_t)K * EV_ROW * 4;
 }
 
@@ -317,7 +390,26 @@ static int contract_t(Plan &p, ContractArgs &a, const WsView &w, cudaStream_t st
   }
   const int64_t J = (int64_t)a.L * a.nchunk * a.ntl;
   const int grid = (int)std::min<int64_t>(J, p.num_sms);
+  static long long *trace_buf = nullptr;
+  a.trace = nullptr;
+  const bool tracing = getenv("EINET_CT_TRACE") != nullptr;
+  if (tracing) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 64 * 8 * sizeof(long long));
+    cudaMemsetAsync(trace_buf, 0, 64 * 8 * sizeof(long long), st);
+    a.trace = trace_buf;
+  }
   k_contract_tc<K><<<grid, CT_THREADS, smem, st>>>(a, w);
+  if (tracing) {
+    long long h[64 * 8];
+    cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "contract trace L=%d nchunk=%d ka=%d direct=%d stages=%d\n", a.L, a.nchunk,
+            a.ka, a.direct, a.stages);
+    for (int i = 0; i < 12; ++i)
+      fprintf(stderr, "  it %2d prod %6lld a_full %6lld acc_free %6lld | e_wait %6lld e_ok %6lld acc_full %6lld epi_done %6lld\n",
+              i, h[i * 8] - h[0], h[i * 8 + 1] - h[0], h[i * 8 + 2] - h[0], h[i * 8 + 6] - h[0],
+              h[i * 8 + 3] - h[0], h[i * 8 + 4] - h[0], h[i * 8 + 5] - h[0]);
+  }
   count_launch();
   return check_cuda(cudaGetLastError(), "einsum contraction (tcgen05)");
 }
@@ -339,9 +431,9 @@ int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *com
   }
   if (mode != 0 && L.direct) {
     a.direct = 1;
-    a.a_ops = (mode == 1 ? w.ebm : w.eam) + (int64_t)L.erow_base * w.bc * 2 * K;
-    a.a_row_stride = w.bc * 2 * K;
-    a.ka = K;
+    a.a_ops = (mode == 1 ? w.ebm : w.eam) + (int64_t)L.erow_base * w.bc * p.kp;
+    a.a_row_stride = w.bc * p.kp * 4;
+    a.ka = p.kp;
     a.e1 = mode == 1 ? EA : EB;
     a.sv = w.rt;
     a.sv_w = w.ks;
@@ -353,9 +445,9 @@ int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *com
     a.n_out = K;
     a.dst = mode == 1 ? L.d_slot_left : L.d_slot_right;
   } else if (mode == 0) {
-    a.a_ops = w.ebm + (int64_t)L.erow_base * (w.bc / 128) * 2 * 128 * K;
-    a.a_row_stride = (w.bc / 128) * 2 * 128 * K;
-    a.ka = K;
+    a.a_ops = w.ebm + (int64_t)L.erow_base * w.bc * p.kp;
+    a.a_row_stride = w.bc * p.kp * 4;
+    a.ka = p.kp;
     a.e1 = EA;
     a.sv = nullptr;
     a.tiles = compute + L.fw_off;
@@ -367,8 +459,8 @@ int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *com
     a.dst = L.d_out_slab;
   } else {
     a.a_ops = w.rtm;
-    a.a_row_stride = (w.bc / 128) * 2 * 128 * L.ko8;
-    a.ka = L.ko8;
+    a.a_row_stride = w.bc * L.kob * 4;
+    a.ka = L.kob;
     a.e1 = mode == 1 ? EB : EA;
     a.sv = mode == 1 ? EA : EB;
     a.tiles = compute + (mode == 1 ? L.uw_off : L.vw_off);

@@ -26,7 +26,7 @@ constexpr int kReduceThreads = 256;
 // per-einsum-layer tile descriptor for the fused M-step (int64 words)
 enum TileDescWord {
   TD_SLICE0, TD_ROWS, TD_KO, TD_TC, TD_DIRECT, TD_KG, TD_NG, TD_FW_ROWS, TD_IG, TD_NI,
-  TD_UW_ROWS, TD_KO8, TD_RW_ROWS, TD_FW_OFF, TD_FW_TILE, TD_UW_OFF, TD_UW_TILE, TD_VW_OFF,
+  TD_UW_ROWS, TD_KOB, TD_RW_ROWS, TD_FW_OFF, TD_FW_TILE, TD_UW_OFF, TD_UW_TILE, TD_VW_OFF,
   TD_RW_TILE, TD_WORDS
 };
 constexpr int EV_ROW = 36;         // padded row of the EA / EB 32-sample blocks (kern_common.cuh)
@@ -52,7 +52,7 @@ struct LayerPlan {
   int tc = 0;
   int kg = 0, ng = 0, fw_rows = 0;  // forward: k per N tile, #tiles, tile rows (N_max)
   int ig = 0, ni = 0, uw_rows = 0;  // child-rho: i per N tile, #tiles, tile rows
-  int ko8 = 0;                      // K_out padded to 8 (child-rho MMA K dimension)
+  int kob = 0;                      // K_out padded to 16 (child-rho bf16 MMA K dimension)
   int nn = 0;                       // W-stats MMA N: K_out padded to 16
   int64_t fw_off = 0, fw_tile = 0;  // compute byte offset, bytes per forward tile
   int64_t uw_off = 0, uw_tile = 0;  // compute byte offset, bytes per child-rho tile (left)
@@ -116,6 +116,7 @@ struct Plan {
   int max_lsplit = 1;              // leaf-statistics batch split allocated
   int n_erows = 0;                 // einsum rows over all layers
   int use_tc = 1;                  // tcgen05 EinsumLayer path enabled
+  int kp = 0;                      // K padded to 16 (forward bf16 MMA K dimension)
   // mixing rows flattened over layers for the M-step
   int n_mixrows = 0;
   int *d_mixrow_off = nullptr, *d_mixrow_len = nullptr;

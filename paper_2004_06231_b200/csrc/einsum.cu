@@ -36,8 +36,8 @@ constexpr int EF_KC = 8;    // output entries (k) staged per W chunk
 __global__ void __launch_bounds__(128) k_einsum_prep_fwd(
     WsView ws, const int *__restrict__ left_slab, const int *__restrict__ right_slab,
     const int *__restrict__ out_slab, int64_t B, int K, float *__restrict__ EA,
-    float *__restrict__ EB, float *__restrict__ EBM, float *__restrict__ EAM, int layer_index,
-    int32_t *status) {
+    float *__restrict__ EB, float *__restrict__ EBM, float *__restrict__ EAM, int kp,
+    int layer_index, int32_t *status) {
   __shared__ float mx[2][32];
   __shared__ unsigned char dead[32];
   const int l = blockIdx.y, t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -96,23 +96,25 @@ __global__ void __launch_bounds__(128) k_einsum_prep_fwd(
     }
     return;
   }
-  // tensor-core path (K % 8 == 0): also the EB A-operand tile (hi | lo)
+  // tensor-core path (K % 8 == 0): also the EB (and for direct child-rho rows
+  // EA) bf16 A-operand tiles, width kp (entries K..kp-1 are zero)
   const int64_t ntl = ws.bc / 128;
-  for (int e = t; e < (K / 4) * 32; e += 128) {
+  for (int e = t; e < (kp / 4) * 32; e += 128) {
     const int bl = e & 31, q = e >> 5;
     const bool d = dead[bl];
-    float va[4], vb[4];
+    float va[4] = {0.f, 0.f, 0.f, 0.f}, vb[4] = {0.f, 0.f, 0.f, 0.f};
+    if (4 * q < K) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int x = (4 * q + u) * 32 + bl, xe = (4 * q + u) * EV_ROW + bl;
-      va[u] = d ? 0.f : expf(ol[x] - mx[0][bl]);
-      vb[u] = d ? 0.f : expf(orr[x] - mx[1][bl]);
-      ea[xe] = va[u];
-      eb[xe] = vb[u];
+      for (int u = 0; u < 4; ++u) {
+        const int x = (4 * q + u) * 32 + bl, xe = (4 * q + u) * EV_ROW + bl;
+        va[u] = d ? 0.f : expf(ol[x] - mx[0][bl]);
+        vb[u] = d ? 0.f : expf(orr[x] - mx[1][bl]);
+        ea[xe] = va[u];
+        eb[xe] = vb[u];
+      }
     }
-    store_hilo4(EBM + mt_idx(l, b0 + bl, q, ntl, K), K, make_float4(vb[0], vb[1], vb[2], vb[3]));
-    if (EAM)
-      store_hilo4(EAM + mt_idx(l, b0 + bl, q, ntl, K), K, make_float4(va[0], va[1], va[2], va[3]));
+    store_bf16_quad(EBM, l, b0 + bl, q, ntl, kp, make_float4(vb[0], vb[1], vb[2], vb[3]));
+    if (EAM) store_bf16_quad(EAM, l, b0 + bl, q, ntl, kp, make_float4(va[0], va[1], va[2], va[3]));
   }
 }
 
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(128) k_mixing_bwd(
 // grid (ceil(B/32), L), block 128
 __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
     WsView ws, const int *out_slab, const int *csr_off, const int *__restrict__ csr_slot,
-    const uint8_t *ones, int64_t B, int Ko, float *RT, float *RTM, int ko8, float *RTB, int nn) {
+    const uint8_t *ones, int64_t B, int Ko, float *RT, float *RTM, int kob, float *RTB, int nn) {
   const int l = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int os = out_slab[l];
@@ -361,9 +363,9 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
     }
     return;
   }
-  // tensor-core path: also the RT A-operand tile (width ko8, zero padded)
+  // tensor-core path: also the RT bf16 A-operand tile (width kob, zero padded)
   const int64_t ntl = ws.bc / 128;
-  for (int e = threadIdx.x; e < (ko8 / 4) * 32; e += 128) {
+  for (int e = threadIdx.x; e < (kob / 4) * 32; e += 128) {
     const int bl = e & 31, q = e >> 5;
     const int64_t b = b0 + bl;
     float v[4] = {0.f, 0.f, 0.f, 0.f};
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
       }
       rt[x] = v[u];
     }
-    store_hilo4(RTM + mt_idx(l, b, q, ntl, ko8), ko8, make_float4(v[0], v[1], v[2], v[3]));
+    store_bf16_quad(RTM, l, b, q, ntl, kob, make_float4(v[0], v[1], v[2], v[3]));
   }
   if (RTB) {
     __syncthreads();
@@ -675,10 +677,10 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
         ProfScope prof("einsum_prep", st);
         dim3 grid(ceil_div(B, 32), L.rows);
         const bool tcl = p.use_tc && L.tc;
-        float *EBM = tcl ? w.ebm + (int64_t)L.erow_base * w.bc * 2 * p.k : nullptr;
-        float *EAM = tcl && L.direct ? w.eam + (int64_t)L.erow_base * w.bc * 2 * p.k : nullptr;
+        float *EBM = tcl ? w.ebm + (int64_t)L.erow_base * w.bc * p.kp : nullptr;
+        float *EAM = tcl && L.direct ? w.eam + (int64_t)L.erow_base * w.bc * p.kp : nullptr;
         k_einsum_prep_fwd<<<grid, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
-                                                B, p.k, EA, EB, EBM, EAM, L.index, status);
+                                                B, p.k, EA, EB, EBM, EAM, p.kp, L.index, status);
       }
       ProfScope prof("einsum_fwd", st);
       if (p.use_tc && L.tc)
@@ -745,7 +747,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
       const bool tcl = p.use_tc && L.tc;
       k_einsum_bwd_rt<<<g1, 128, 0, st>>>(w, L.d_out_slab, p.d_csr_off, p.d_csr_slot,
                                           p.d_slab_ones, B, L.k_out, w.rt,
-                                          tcl && !L.direct ? w.rtm : nullptr, L.ko8,
+                                          tcl && !L.direct ? w.rtm : nullptr, L.kob,
                                           tcl ? w.rtb : nullptr, L.nn);
     }
     const int64_t lw = (int64_t)L.rows * L.k_out * K * K;

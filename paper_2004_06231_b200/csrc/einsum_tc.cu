@@ -129,43 +129,45 @@ constexpr int64_t TC_SMEM_MAX = 220 * 1024;  // dynamic smem budget per CTA
 
 static inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
-// contraction kernel (contract_tc.cu): resident weight chunk, two A stages and
-// two contraction-vector stages
-static int64_t fwd_smem(int rows_tile, int K) {
-  return 2LL * rows_tile * K * 4 + 2LL * 2 * TC_M * K * 4 + 2LL * 4 * K * EV_ROW * 4 + 1024;
+// contraction kernel (contract_tc.cu, 3xBF16): resident weight chunk (bf16
+// hi | lo), at least two A stages and two contraction-vector stages
+static int64_t fwd_smem(int rows_tile, int K, int kp) {
+  return 4LL * rows_tile * kp + 2LL * 4 * TC_M * kp + 2LL * 4 * K * EV_ROW * 4 + 1024;
 }
-static int64_t cr_smem(int rows_tile, int ko8, int K) {
-  return 2LL * rows_tile * ko8 * 4 + 2LL * (2LL * TC_M * ko8 * 4) + 2LL * 4 * K * EV_ROW * 4 + 1024;
+static int64_t cr_smem(int rows_tile, int kob, int K) {
+  return 4LL * rows_tile * kob + 2LL * 4 * TC_M * kob + 2LL * 4 * K * EV_ROW * 4 + 1024;
 }
 size_t wstats_smem(int K, int nn);  // wstats_tc.cu
 static int64_t ws_smem(int K, int nn) { return (int64_t)wstats_smem(K, nn); }
 
 void plan_tc_tiling(Plan &p) {
   const int K = p.k;
+  p.kp = round_up(K, 16);
+  const int kp = p.kp;
   for (auto &L : p.layers) {
     L.tc = 0;
     if (L.kind != EINET_LAYER_EINSUM) continue;
     if (K % 8 != 0 || K < 8 || K > 64 || p.ks % 4 != 0) continue;
     const int Ko = L.k_out;
     int kg = std::max(1, std::min(Ko, 256 / K));
-    while (kg > 1 && fwd_smem(round_up(kg * K, 16), K) > TC_SMEM_MAX) --kg;
+    while (kg > 1 && fwd_smem(round_up(kg * K, 16), K, kp) > TC_SMEM_MAX) --kg;
     L.kg = kg;
     L.ng = ceil_div(Ko, kg);
     L.fw_rows = round_up(kg * K, 16);
-    L.fw_tile = 2LL * L.fw_rows * K * 4;
-    L.ko8 = round_up(Ko, 8);
+    L.fw_tile = 4LL * L.fw_rows * kp;
+    L.kob = round_up(Ko, 16);
     int ig = std::max(1, std::min(K, 256 / K));
-    while (ig > 1 && cr_smem(round_up(ig * K, 16), L.ko8, K) > TC_SMEM_MAX) --ig;
+    while (ig > 1 && cr_smem(round_up(ig * K, 16), L.kob, K) > TC_SMEM_MAX) --ig;
     L.ig = ig;
     L.ni = ceil_div(K, ig);
     L.uw_rows = round_up(ig * K, 16);
-    L.uw_tile = 2LL * L.uw_rows * L.ko8 * 4;
+    L.uw_tile = 4LL * L.uw_rows * L.kob;
     L.nn = round_up(Ko, 16);
     L.direct = Ko == 1;
     L.rw_rows = round_up(K, 16);
-    L.rw_tile = 2LL * L.rw_rows * K * 4;
-    if (L.fw_rows > 256 || L.uw_rows > 256 || L.nn > 64 || L.ko8 > 256) continue;
-    if (fwd_smem(L.fw_rows, K) > TC_SMEM_MAX || cr_smem(L.uw_rows, L.ko8, K) > TC_SMEM_MAX ||
+    L.rw_tile = 4LL * L.rw_rows * kp;
+    if (L.fw_rows > 256 || L.uw_rows > 256 || L.nn > 64 || L.kob > 256) continue;
+    if (fwd_smem(L.fw_rows, K, kp) > TC_SMEM_MAX || cr_smem(L.uw_rows, L.kob, K) > TC_SMEM_MAX ||
         ws_smem(K, L.nn) > TC_SMEM_MAX)
       continue;
     L.tc = 1;
@@ -173,63 +175,62 @@ void plan_tc_tiling(Plan &p) {
 }
 
 // --- pre-tiled weight images (built by prepare after every parameter change) ---
-// forward tile g of row l: rows n = kl*K + i (k = g*kg + kl), K dim = j
-// child-rho tile h of row l: rows n = il*K + j (i = h*ig + il), K dim = k
+// bf16 hi | lo, K-major core matrices (kmaj_off16), K dims padded to 16 with zeros.
+// forward tile g of row l: rows n = kl*K + i (k = g*kg + kl), K dim = j (kp)
+// child-rho tile h of row l: rows n = il*K + j (i = h*ig + il), K dim = k (kob)
 // right child-rho tile h of row l: rows n = jl*K + i (j = h*ig + jl), K dim = k
+__device__ __forceinline__ void put_bf16_hilo(uint8_t *tile, int64_t lo_bytes, uint32_t off,
+                                              float v) {
+  __nv_bfloat16 h, l;
+  tc::split_bf16(v, h, l);
+  *(__nv_bfloat16 *)(tile + off) = h;
+  *(__nv_bfloat16 *)(tile + lo_bytes + off) = l;
+}
+
 __global__ void k_build_tiles(const float *__restrict__ W, uint8_t *fw, uint8_t *uw,
-                              uint8_t *vw, int L, int Ko, int K, int kg, int ng, int fw_rows,
-                              int ig, int ni, int uw_rows, int ko8) {
-  const int64_t n_fw = (int64_t)L * ng * fw_rows * K;
-  const int64_t n_uw = (int64_t)L * ni * uw_rows * ko8;
+                              uint8_t *vw, int L, int Ko, int K, int kp, int kg, int ng,
+                              int fw_rows, int ig, int ni, int uw_rows, int kob) {
+  const int64_t n_fw = (int64_t)L * ng * fw_rows * kp;
+  const int64_t n_uw = (int64_t)L * ni * uw_rows * kob;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_fw + 2 * n_uw;
        e += (int64_t)gridDim.x * blockDim.x) {
     float v = 0.f;
-    float *hi, *lo;
     if (e < n_fw) {
-      const int kk = (int)(e % K);
-      const int n = (int)((e / K) % fw_rows);
-      const int64_t tile = e / ((int64_t)K * fw_rows);  // l * ng + g
+      const int kk = (int)(e % kp);
+      const int n = (int)((e / kp) % fw_rows);
+      const int64_t tile = e / ((int64_t)kp * fw_rows);  // l * ng + g
       const int l = (int)(tile / ng), g = (int)(tile % ng);
       const int kl = n / K, i = n % K, k = g * kg + kl;
-      if (kl < kg && k < Ko) v = W[(((int64_t)l * Ko + k) * K + i) * K + kk];
-      float *base = (float *)(fw + tile * (2LL * fw_rows * K * 4));
-      hi = base + tc::kmaj_off(n, kk, fw_rows) / 4;
-      lo = hi + fw_rows * K;
+      if (kl < kg && k < Ko && kk < K) v = W[(((int64_t)l * Ko + k) * K + i) * K + kk];
+      put_bf16_hilo(fw + tile * (4LL * fw_rows * kp), 2LL * fw_rows * kp,
+                    tc::kmaj_off16(n, kk, fw_rows), v);
     } else {
       const bool right = e >= n_fw + n_uw;
       const int64_t q = e - n_fw - (right ? n_uw : 0);
-      const int kk = (int)(q % ko8);
-      const int n = (int)((q / ko8) % uw_rows);
-      const int64_t tile = q / ((int64_t)ko8 * uw_rows);  // l * ni + h
+      const int kk = (int)(q % kob);
+      const int n = (int)((q / kob) % uw_rows);
+      const int64_t tile = q / ((int64_t)kob * uw_rows);  // l * ni + h
       const int l = (int)(tile / ni), h = (int)(tile % ni);
       const int ol = n / K, in = n % K, o = h * ig + ol;
       const int i = right ? in : o, j = right ? o : in;
       if (ol < ig && o < K && kk < Ko) v = W[(((int64_t)l * Ko + kk) * K + i) * K + j];
-      float *base = (float *)((right ? vw : uw) + tile * (2LL * uw_rows * ko8 * 4));
-      hi = base + tc::kmaj_off(n, kk, uw_rows) / 4;
-      lo = hi + uw_rows * ko8;
+      put_bf16_hilo((right ? vw : uw) + tile * (4LL * uw_rows * kob), 2LL * uw_rows * kob,
+                    tc::kmaj_off16(n, kk, uw_rows), v);
     }
-    float h, l2;
-    tc::split_tf32(v, h, l2);
-    *hi = h;
-    *lo = l2;
   }
 }
 
-// direct right tile of a K_out == 1 row: rows n = j, K dim = i, value W[l,0,i,j]
-__global__ void k_build_rw(const float *__restrict__ W, uint8_t *rw, int L, int K, int rows) {
-  const int64_t n_rw = (int64_t)L * rows * K;
+// direct right tile of a K_out == 1 row: rows n = j, K dim = i (kp), value W[l,0,i,j]
+__global__ void k_build_rw(const float *__restrict__ W, uint8_t *rw, int L, int K, int kp,
+                           int rows) {
+  const int64_t n_rw = (int64_t)L * rows * kp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_rw;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e % K);
-    const int n = (int)((e / K) % rows);
-    const int l = (int)(e / ((int64_t)K * rows));
-    const float v = n < K ? W[((int64_t)l * K + i) * K + n] : 0.f;
-    float *hi = (float *)(rw + l * (2LL * rows * K * 4)) + tc::kmaj_off(n, i, rows) / 4;
-    float h, l2;
-    tc::split_tf32(v, h, l2);
-    hi[0] = h;
-    hi[rows * K] = l2;
+    const int i = (int)(e % kp);
+    const int n = (int)((e / kp) % rows);
+    const int l = (int)(e / ((int64_t)kp * rows));
+    const float v = (n < K && i < K) ? W[((int64_t)l * K + i) * K + n] : 0.f;
+    put_bf16_hilo(rw + l * (4LL * rows * kp), 2LL * rows * kp, tc::kmaj_off16(n, i, rows), v);
   }
 }
 
@@ -238,17 +239,16 @@ int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st) {
   for (auto &L : p.layers) {
     if (!L.tc) continue;
     if (L.direct) {
-      const int64_t n = (int64_t)L.rows * L.rw_rows * p.k;
+      const int64_t n = (int64_t)L.rows * L.rw_rows * p.kp;
       k_build_rw<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
-          c.w32 + L.w_off, compute + L.vw_off, L.rows, p.k, L.rw_rows);
+          c.w32 + L.w_off, compute + L.vw_off, L.rows, p.k, p.kp, L.rw_rows);
       count_launch();
     }
-    const int64_t n = (int64_t)L.rows * (L.ng * L.fw_rows * p.k +
-                                         (L.direct ? 0 : 2 * L.ni * L.uw_rows * L.ko8));
+    const int64_t n = (int64_t)L.rows * (L.ng * L.fw_rows * p.kp +
+                                         (L.direct ? 0 : 2 * L.ni * L.uw_rows * L.kob));
     k_build_tiles<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
         c.w32 + L.w_off, compute + L.fw_off, compute + L.uw_off, compute + L.vw_off, L.rows,
-        L.k_out, p.k, L.kg,
-        L.ng, L.fw_rows, L.ig, L.direct ? 0 : L.ni, L.uw_rows, L.ko8);
+        L.k_out, p.k, p.kp, L.kg, L.ng, L.fw_rows, L.ig, L.direct ? 0 : L.ni, L.uw_rows, L.kob);
     count_launch();
   }
   return check_cuda(cudaGetLastError(), "build tc tiles");

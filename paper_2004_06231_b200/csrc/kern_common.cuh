@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <math_constants.h>
 #include <stdint.h>
 
@@ -31,11 +32,11 @@ struct WsView {
   double *leafpart;
   float *ea, *eb;  // [row][Bc][K]
   float *rt;       // [row][Bc/32][KS][32]
-  float *ebm;      // tcgen05 A operand EB: [einsum row][Bc/128][hi|lo][128 x K] (K-major core matrices)
+  float *ebm;      // tcgen05 A operand EB: [einsum row][Bc/128][hi|lo][128 x kp] bf16 (K-major core matrices)
   float *rhob;     // tcgen05 B operand rho^T of the leaf statistics: [leaf][Bc/32][hi|lo][nn x 32]
   float *rtb;      // tcgen05 B operand RT^T of the W statistics: [row][Bc/32][hi|lo][nn x 32]
   float *eam;      // tcgen05 A operand EA (direct child-rho of K_out == 1 rows), as ebm
-  float *rtm;      // tcgen05 A operand RT: [row][Bc/128][hi|lo][128 x ko8]
+  float *rtm;      // tcgen05 A operand RT: [row][Bc/128][hi|lo][128 x kob] bf16
   double *wpart;
   float *rho;      // [leaf][Bc][K]
   double *lspart;
@@ -182,6 +183,27 @@ __device__ __forceinline__ void bt_tile(const float *src, float *dst, int nvalid
     if (n < nvalid) v = *(const float4 *)(src + n * 32 + 4 * q);
     store_hilo4_at(dst + q * (nn * 4) + (n >> 3) * 32 + (n & 7) * 4, nn * 32, v);
   }
+}
+
+// bf16 A-operand tiles of per-sample vectors (3xBF16 contraction kernels):
+// 128-sample tile t of row `row` holds the bf16 hi part then the lo part, each
+// 128 x W (W a multiple of 16) in K-major core matrices (tc::kmaj_off16).
+// Stores entries 4q..4q+3 of sample b (8 bytes per part).
+__device__ __forceinline__ void store_bf16_quad(void *base, int64_t row, int64_t b, int q,
+                                                int64_t ntl, int W, float4 v) {
+  uint8_t *tile = (uint8_t *)base + ((row * ntl + (b >> 7)) * 4) * (128LL * W);
+  const int r = (int)(b & 127), k = 4 * q;
+  const uint32_t off = (uint32_t)((k >> 3) * (128 * 16) + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+  const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y), h23 = __floats2bfloat162_rn(v.z, v.w);
+  const __nv_bfloat162 l01 = __floats2bfloat162_rn(v.x - __low2float(h01), v.y - __high2float(h01));
+  const __nv_bfloat162 l23 = __floats2bfloat162_rn(v.z - __low2float(h23), v.w - __high2float(h23));
+  uint2 hv, lv;
+  hv.x = *(const uint32_t *)&h01;
+  hv.y = *(const uint32_t *)&h23;
+  lv.x = *(const uint32_t *)&l01;
+  lv.y = *(const uint32_t *)&l23;
+  *(uint2 *)(tile + off) = hv;
+  *(uint2 *)(tile + 2LL * 128 * W + off) = lv;
 }
 
 // cp.async (LDGSTS) helpers shared by the staged kernels

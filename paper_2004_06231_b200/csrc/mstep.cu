@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) k_mstep_einsum(double *__restrict__ W,
                                                       double lam, double eps,
                                                       const int32_t *status,
                                                       const int64_t *__restrict__ tiledesc,
-                                                      int ntd, uint8_t *compute) {
+                                                      int ntd, uint8_t *compute, int kp) {
   const int KK = K * K;
   __shared__ double red[8];
   if (step_failed(status)) return;
@@ -132,32 +132,28 @@ __global__ void __launch_bounds__(256) k_mstep_einsum(double *__restrict__ W,
     w32[base + e] = (float)v;
     if (td) {
       const int i = e / K, j = e - (e / K) * K;
-      float h, lo;
-      tc::split_tf32((float)v, h, lo);
-      {  // forward tile: rows kl*K + i, K dim j
+      __nv_bfloat16 h, lo;
+      tc::split_bf16((float)v, h, lo);
+      auto put = [&](uint8_t *tile, int64_t lo_bytes, uint32_t off) {
+        *(__nv_bfloat16 *)(tile + off) = h;
+        *(__nv_bfloat16 *)(tile + lo_bytes + off) = lo;
+      };
+      {  // forward tile: rows kl*K + i, K dim j (kp)
         const int64_t kg = td[TD_KG], rows = td[TD_FW_ROWS];
         const int64_t tile = l * td[TD_NG] + k / kg;
-        float *t = (float *)(compute + td[TD_FW_OFF] + tile * td[TD_FW_TILE]);
-        const int64_t o = tc::kmaj_off((int)((k % kg) * K + i), j, (int)rows) / 4;
-        t[o] = h;
-        t[o + rows * K] = lo;
+        put(compute + td[TD_FW_OFF] + tile * td[TD_FW_TILE], 2 * rows * kp,
+            tc::kmaj_off16((int)((k % kg) * K + i), j, (int)rows));
       }
-      if (td[TD_DIRECT]) {  // K_out == 1: right tile rows j, K dim i
+      if (td[TD_DIRECT]) {  // K_out == 1: right tile rows j, K dim i (kp)
         const int64_t rows = td[TD_RW_ROWS];
-        float *t = (float *)(compute + td[TD_VW_OFF] + l * td[TD_RW_TILE]);
-        const int64_t o = tc::kmaj_off(j, i, (int)rows) / 4;
-        t[o] = h;
-        t[o + rows * K] = lo;
-      } else {  // left (rows il*K + j) and right (rows jl*K + i) tiles, K dim k
-        const int64_t ig = td[TD_IG], rows = td[TD_UW_ROWS], ko8 = td[TD_KO8];
-        float *tl = (float *)(compute + td[TD_UW_OFF] + (l * td[TD_NI] + i / ig) * td[TD_UW_TILE]);
-        const int64_t ol = tc::kmaj_off((int)((i % ig) * K + j), (int)k, (int)rows) / 4;
-        tl[ol] = h;
-        tl[ol + rows * ko8] = lo;
-        float *tr = (float *)(compute + td[TD_VW_OFF] + (l * td[TD_NI] + j / ig) * td[TD_UW_TILE]);
-        const int64_t orr = tc::kmaj_off((int)((j % ig) * K + i), (int)k, (int)rows) / 4;
-        tr[orr] = h;
-        tr[orr + rows * ko8] = lo;
+        put(compute + td[TD_VW_OFF] + l * td[TD_RW_TILE], 2 * rows * kp,
+            tc::kmaj_off16(j, i, (int)rows));
+      } else {  // left (rows il*K + j) and right (rows jl*K + i) tiles, K dim k (kob)
+        const int64_t ig = td[TD_IG], rows = td[TD_UW_ROWS], kob = td[TD_KOB];
+        put(compute + td[TD_UW_OFF] + (l * td[TD_NI] + i / ig) * td[TD_UW_TILE], 2 * rows * kob,
+            tc::kmaj_off16((int)((i % ig) * K + j), (int)k, (int)rows));
+        put(compute + td[TD_VW_OFF] + (l * td[TD_NI] + j / ig) * td[TD_UW_TILE], 2 * rows * kob,
+            tc::kmaj_off16((int)((j % ig) * K + i), (int)k, (int)rows));
       }
     }
   }
@@ -354,7 +350,7 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
     const int nslices = (int)(p.n_w / KK);
     k_mstep_einsum<<<nslices, 256, 0, st>>>(params, c.w32, stats, K, lam, eps_w, status,
                                             fused ? p.d_tiledesc : nullptr,
-                                            p.n_tiledesc, compute);
+                                            p.n_tiledesc, compute, p.kp);
     count_launch();
   }
   if (p.n_mixrows) {

@@ -14,6 +14,6 @@ circuit = compile_graph(rg, k)
 x = torch.from_numpy(gen(16384, seed=1).astype(np.float32)).cuda()
 ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=gen(2048, seed=7).astype(np.float64))
 model = EinetModel(circuit, engine.Parameters.from_numpy(circuit, fam, ein, mix, phi), fam)
-for _ in range(2):
+for _ in range(1):
     trainer.em_stochastic_step(model, x, 0.5, chunk=16384)
 torch.cuda.synchronize()
