@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
     }
     if (RTB) {
       __syncthreads();
-      bt_tile(rt, RTB + ((int64_t)l * (ws.bc / 32) + b0 / 32) * (2 * nn * 32), Ko, nn);
+      bt_tile16(rt, (uint8_t *)RTB + ((int64_t)l * (ws.bc / 32) + b0 / 32) * (nn * 128), Ko, nn);
     }
     return;
   }
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
   }
   if (RTB) {
     __syncthreads();
-    bt_tile(rt, RTB + ((int64_t)l * (ws.bc / 32) + b0 / 32) * (2 * nn * 32), Ko, nn);
+    bt_tile16(rt, (uint8_t *)RTB + ((int64_t)l * (ws.bc / 32) + b0 / 32) * (nn * 128), Ko, nn);
   }
 }
 

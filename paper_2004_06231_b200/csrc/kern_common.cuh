@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include "einet_internal.h"
+#include "tc_common.cuh"
 
 namespace einet {
 
@@ -204,6 +205,28 @@ __device__ __forceinline__ void store_bf16_quad(void *base, int64_t row, int64_t
   lv.y = *(const uint32_t *)&l23;
   *(uint2 *)(tile + off) = hv;
   *(uint2 *)(tile + 2LL * 128 * W + off) = lv;
+}
+
+// bf16 variant of bt_tile (the W-statistics B operand RT^T): rows n < nn,
+// K = 32 samples, bf16 hi | lo (tc::kmaj_off16 layout, 8 samples per 16-byte
+// core-matrix row); rows n >= nvalid are zero.
+__device__ __forceinline__ void bt_tile16(const float *src, uint8_t *dst, int nvalid, int nn) {
+  for (int e = threadIdx.x; e < nn * 4; e += blockDim.x) {
+    const int n = e >> 2, q = e & 3;  // samples 8q .. 8q+7
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (n < nvalid) {
+      const float4 a = *(const float4 *)(src + n * 32 + 8 * q);
+      const float4 b = *(const float4 *)(src + n * 32 + 8 * q + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tc::split_bf16x2(v[2 * u], v[2 * u + 1], h[u], l[u]);
+    const uint32_t off = (uint32_t)(q * (nn * 16) + (n >> 3) * 128 + (n & 7) * 16);
+    *(uint4 *)(dst + off) = make_uint4(h[0], h[1], h[2], h[3]);
+    *(uint4 *)(dst + nn * 64 + off) = make_uint4(l[0], l[1], l[2], l[3]);
+  }
 }
 
 // cp.async (LDGSTS) helpers shared by the staged kernels
