@@ -142,6 +142,29 @@ def work_per_sample(circuit):
     }
 
 
+# FP64 tensor-core (DMMA) peak of this pool's B200, measured by
+# scripts/peak_dmma.cu (m16n8k16, 8-16 warps per CTA): MEASURED_PEAKS.json has
+# no FP64 figure, and the Gaussian leaf forward runs on the FP64 tensor pipe.
+FP64_TENSOR_PEAK_TFLOPS = 37.1
+
+# ncu DRAM traffic (read + write bytes per launch) of the dominant kernels,
+# from the committed --set full capture
+KERNEL_TRAFFIC = {"leaf_fwd": "k_leaf_fwd_dmma<5, 4, 4>", "leaf_stats": "k_leaf_stats_tc",
+                  "einsum_wstats": "k_wstats_tc<40>", "einsum_childrho": "k_contract_tc<40>",
+                  "einsum_fwd": "k_contract_tc<40>"}
+
+
+def kernel_traffic(name):
+    path = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    try:
+        with open(path) as f:
+            doc = json.load(f)
+        v = doc[KERNEL_TRAFFIC[name]]["dram_bytes_per_launch"]
+        return max(v)
+    except Exception:
+        return None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -328,9 +351,15 @@ def run_ours(args):
         ms = timed(lambda: step(x_dev), args.steps)
 
     # end to end: the pinned host batch goes through the public API each step
-    # (host -> device copy inside em_stochastic_step), mean LL read back
+    # (host -> device copy inside trainer.em_stochastic_steps, overlapped with
+    # the previous step), every step's mean LL read back
     e2e_steps = max(3, args.steps // 4)
-    ms_e2e = timed(lambda: step(x_host), e2e_steps)  # the API stages the pinned batch
+    if group is None:
+        # the public multi-step API: batch i+1's host->device copy overlaps step i
+        ms_e2e = timed(lambda: trainer.em_stochastic_steps(model, [x_host] * e2e_steps, 0.5,
+                                                            chunk=args.chunk), 1)
+    else:
+        ms_e2e = timed(lambda: step(x_host), e2e_steps)  # the API stages the pinned batch
 
     # per-kernel-class device time of the same step (CUDA events, separate pass)
     _native.profile_enable(True)
@@ -370,12 +399,25 @@ def run_ours(args):
         roof = {"kernel": top, "bound": "tensor", "achieved": achieved, "peak": bf16,
                 "unit": "TFLOP/s", "frac": achieved / bf16,
                 "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json)"}
+    elif top == "leaf_fwd" and circuit.k % 8 == 0 and type(fam).__name__ == "GaussianFamily":
+        # FP64 DMMA leaf forward: 4 D K R algorithmic flops per sample (two
+        # features per variable and component)
+        achieved = tw["flops"] * B / groups / (per_launch_ms / 1e3) / 1e12
+        roof = {"kernel": top, "bound": "tensor", "achieved": achieved,
+                "peak": FP64_TENSOR_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_TENSOR_PEAK_TFLOPS,
+                "peak_source": "measured FP64 tensor-core (DMMA) peak, scripts/peak_dmma.cu "
+                               "(MEASURED_PEAKS.json has no FP64 figure)",
+                "hbm_gbs": tw["bytes"] * B / groups / (per_launch_ms / 1e3) / 1e9}
     else:
         achieved = tw["bytes"] * B / groups / (per_launch_ms / 1e3) / 1e9
         roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": hbm,
                 "unit": "GB/s", "frac": achieved / hbm,
                 "peak_source": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
-    roof["traffic"] = None
+    roof["traffic"] = kernel_traffic(top)
+    if roof["traffic"] is not None:
+        roof["traffic_source"] = "profiles/kernel_traffic.json (ncu dram read+write bytes/launch)"
+        roof["algorithmic_bytes"] = tw["bytes"] * B / groups
     roof["per_launch_ms"] = per_launch_ms
 
     cpu = None

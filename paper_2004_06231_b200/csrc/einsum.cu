@@ -208,7 +208,10 @@ __global__ void k_einsum_fwd_generic(WsView ws, const float *__restrict__ EA,
 // Mixing forward, elementwise over (sample, k) of a 32-sample block:
 // out = s + mk + log sum_c w_c exp(s_c - s + off_c - mk) with s = max_c s_c
 // (engine.py:112-122; masked children never contribute).
-// grid (ceil(B/32), M), block 128, smem: the row's (src slab, w) per child.
+// grid (ceil(B/32), M), block 128: a thread keeps one sample (lane) and walks
+// k = warp, warp + 4, ...; the sample's child shifts are loaded once, the
+// child offsets of one k are independent loads (MC children in registers).
+constexpr int MC = 8;  // children handled in registers; larger rows loop over groups
 __global__ void __launch_bounds__(128) k_mixing_fwd(
     WsView ws, const int *__restrict__ src_slab, const uint8_t *__restrict__ mask,
     const int *__restrict__ out_slab, const float *__restrict__ w, int64_t B, int Ko, int dmax,
@@ -218,26 +221,67 @@ __global__ void __launch_bounds__(128) k_mixing_fwd(
   float *wc = (float *)(msm + dmax);     // [dmax]
   (void)layer_index;
   (void)status;
-  const int m = blockIdx.y;
+  const int m = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int c = threadIdx.x; c < dmax; c += 128) {
     src[c] = mask[m * dmax + c] ? src_slab[m * dmax + c] : -1;
     wc[c] = w[m * dmax + c];
   }
   __syncthreads();
-  const int64_t b0 = (int64_t)blockIdx.x * 32;
+  const int64_t b0 = (int64_t)blockIdx.x * 32, b = b0 + lane;
+  if (b >= B) return;
   const int os = out_slab[m];
   float *o = ws.off + tb_idx(os, b0, 0, ws.bc, ws.ks);
-  for (int e = threadIdx.x; e < Ko * 32; e += 128) {
-    const int bl = e & 31;
-    const int64_t b = b0 + bl;
-    if (b >= B) continue;
+  if (dmax <= MC) {
+    double sc[MC];
+    const float *oc[MC];
     double sh = -CUDART_INF;
-    for (int c = 0; c < dmax; ++c) {
-      if (src[c] < 0) continue;
-      const double sc = slab_shift(ws, src[c])[b];
-      if (sc > sh || sc != sc) sh = sc;
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      sc[c] = -CUDART_INF;
+      oc[c] = nullptr;
+      if (c < dmax && src[c] >= 0) {
+        sc[c] = slab_shift(ws, src[c])[b];
+        oc[c] = ws.off + tb_idx(src[c], b0, 0, ws.bc, ws.ks);
+        if (sc[c] > sh || sc[c] != sc[c]) sh = sc[c];
+      }
     }
-    if (e < 32) slab_shift(ws, os)[b] = sh;
+    if (wid == 0) slab_shift(ws, os)[b] = sh;
+    for (int k = wid; k < Ko; k += 4) {
+      const int e = k * 32 + lane;
+      if (sh == -CUDART_INF) {
+        o[e] = 0.f;
+        continue;
+      }
+      float dv[MC];
+      float mk = -CUDART_INF_F;
+#pragma unroll
+      for (int c = 0; c < MC; ++c) {
+        dv[c] = -CUDART_INF_F;
+        if (oc[c] && sc[c] != -CUDART_INF) dv[c] = (float)(sc[c] - sh) + oc[c][e];
+        mk = fmaxf(mk, dv[c]);
+      }
+      float out = -CUDART_INF_F;
+      if (mk != -CUDART_INF_F) {
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < MC; ++c)
+          if (dv[c] != -CUDART_INF_F) sum = fmaf(wc[c < dmax ? c : 0], expf(dv[c] - mk), sum);
+        if (sum > 0.f) out = mk + logf(sum);
+      }
+      o[e] = out;
+    }
+    return;
+  }
+  // generic (many children)
+  double sh = -CUDART_INF;
+  for (int c = 0; c < dmax; ++c) {
+    if (src[c] < 0) continue;
+    const double scc = slab_shift(ws, src[c])[b];
+    if (scc > sh || scc != scc) sh = scc;
+  }
+  if (wid == 0) slab_shift(ws, os)[b] = sh;
+  for (int k = wid; k < Ko; k += 4) {
+    const int e = k * 32 + lane;
     if (sh == -CUDART_INF) {
       o[e] = 0.f;
       continue;
@@ -245,19 +289,19 @@ __global__ void __launch_bounds__(128) k_mixing_fwd(
     float mk = -CUDART_INF_F;
     for (int c = 0; c < dmax; ++c) {
       if (src[c] < 0) continue;
-      const double sc = slab_shift(ws, src[c])[b];
-      if (sc == -CUDART_INF) continue;
-      mk = fmaxf(mk, (float)(sc - sh) + ws.off[tb_idx(src[c], b0, 0, ws.bc, ws.ks) + e]);
+      const double scc = slab_shift(ws, src[c])[b];
+      if (scc == -CUDART_INF) continue;
+      mk = fmaxf(mk, (float)(scc - sh) + ws.off[tb_idx(src[c], b0, 0, ws.bc, ws.ks) + e]);
     }
     float out = -CUDART_INF_F;
     if (mk != -CUDART_INF_F) {
       float sum = 0.f;
       for (int c = 0; c < dmax; ++c) {
         if (src[c] < 0) continue;
-        const double sc = slab_shift(ws, src[c])[b];
-        if (sc == -CUDART_INF) continue;
-        const float dv = (float)(sc - sh) + ws.off[tb_idx(src[c], b0, 0, ws.bc, ws.ks) + e];
-        sum = fmaf(wc[c], expf(dv - mk), sum);
+        const double scc = slab_shift(ws, src[c])[b];
+        if (scc == -CUDART_INF) continue;
+        const float dvv = (float)(scc - sh) + ws.off[tb_idx(src[c], b0, 0, ws.bc, ws.ks) + e];
+        sum = fmaf(wc[c], expf(dvv - mk), sum);
       }
       if (sum > 0.f) out = mk + logf(sum);
     }

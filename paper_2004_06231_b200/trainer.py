@@ -151,12 +151,79 @@ def em_stochastic_step(model: EinetModel, batch, lam, eps_w=engine.EPS_W, chunk=
             dist.all_reduce(status, op=dist.ReduceOp.MIN, group=process_group)
         if lam != 0.0:
             eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
+    return _finish_step(model, eng, stats, status, lam)
+
+
+def _finish_step(model, eng, stats, status, lam) -> float:
+    """Read the LL sum and the error words (one device->host copy, syncs),
+    raise the reference exceptions, return the mean LL."""
     ll_off = int(eng.sizes.stats_ll_offset)
     info = torch.cat([stats[ll_off:ll_off + 2], status.to(torch.float64)]).cpu().tolist()
     engine._raise_words([int(v) for v in info[2:]], model.family)
     if lam != 0.0:
         model.params.mark_compute_current(eng)
     return info[0] / info[1]
+
+
+def _host_batch(batch) -> torch.Tensor:
+    t = batch if isinstance(batch, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(batch, dtype=np.float64), dtype=np.float32))
+    if t.dim() == 1:
+        t = t[None, :]
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        t = t.to(torch.float32).contiguous()
+    return t
+
+
+def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
+                        chunk=4096) -> list:
+    """Consecutive gliding-average EM steps over a sequence of host batches of
+    one shape (equivalent to calling ``em_stochastic_step`` on each): the
+    host->device copy of batch i+1 runs on a copy stream into the other half
+    of a double-buffered staging area while step i runs on the device. Every
+    step's LL (and error words) is read back after the step, as in
+    ``em_stochastic_step``; returns the list of mean LLs."""
+    hosts = [_host_batch(b) for b in batches]
+    if not hosts:
+        return []
+    if lam == 0.0 or not _graphs_enabled() or hosts[0].is_cuda:
+        return [em_stochastic_step(model, b, lam, eps_w, chunk) for b in hosts]
+    shape = tuple(hosts[0].shape)
+    if shape[0] == 0:
+        raise ValueError("empty batch")
+    dev = model.params.flat.device
+    copy = model.__dict__.get("_copy_stream")
+    if copy is None:
+        copy = torch.cuda.Stream(device=dev)
+        model.__dict__["_copy_stream"] = copy
+    bufs = model.__dict__.get("_stage2")
+    if bufs is None or tuple(bufs[0].shape) != shape:
+        bufs = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
+        model.__dict__["_stage2"] = bufs
+    cur = torch.cuda.current_stream(dev)
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+    used = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def issue_copy(i):
+        s = i & 1
+        copy.wait_stream(cur) if i < 2 else copy.wait_event(used[s])
+        with torch.cuda.stream(copy):
+            bufs[s].copy_(hosts[i], non_blocking=hosts[i].is_pinned())
+            copied[s].record(copy)
+
+    issue_copy(0)
+    out = []
+    for i, h in enumerate(hosts):
+        if tuple(h.shape) != shape:
+            raise ValueError("em_stochastic_steps needs batches of one shape")
+        s = i & 1
+        cur.wait_event(copied[s])
+        eng, stats, status = _graph_step(model, bufs[s], lam, eps_w, chunk)
+        used[s].record(cur)
+        if i + 1 < len(hosts):
+            issue_copy(i + 1)
+        out.append(_finish_step(model, eng, stats, status, lam))
+    return out
 
 
 def em_full_step(model: EinetModel, data, eps_w=engine.EPS_W, chunk=4096,

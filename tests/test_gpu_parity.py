@@ -294,6 +294,23 @@ def test_unsupported_values_raise_dmma_path():
     trainer.em_stochastic_step(m, x, 0.5)
 
 
+def test_pipelined_steps_equal_sequential_steps():
+    """trainer.em_stochastic_steps (copy of batch i+1 overlapping step i) is the
+    same computation as em_stochastic_step per batch: bitwise equal results."""
+    rng = np.random.default_rng(4)
+    batches = [torch.from_numpy(rng.normal(0.5, 0.2, (96, 16)).astype(np.float32)).pin_memory()
+               for _ in range(3)]
+    ms = []
+    for _ in range(2):
+        rg = E.random_binary_tree(16, StructureConfig(depth=2, replicas=2, seed=3))
+        ms.append(E.build_model(rg, E.GaussianFamily(), k=8, seed=2,
+                                data=batches[0].numpy().astype(np.float64)))
+    lls_a = trainer.em_stochastic_steps(ms[0], batches, 0.5, chunk=64)
+    lls_b = [trainer.em_stochastic_step(ms[1], b, 0.5, chunk=64) for b in batches]
+    assert lls_a == lls_b
+    assert torch.equal(ms[0].params.flat, ms[1].params.flat)
+
+
 def test_shape_mismatch_raises():
     m = _gauss_model(11, data=np.zeros((4, 4)))
     with pytest.raises(E.EngineError):
