@@ -83,6 +83,14 @@ def _graphs_enabled() -> bool:
     return os.environ.get("EINET_CUDA_GRAPHS", "1") != "0" and not _native.PROFILING
 
 
+def _nccl_group(group) -> bool:
+    try:
+        import torch.distributed as dist
+        return dist.get_backend(group) == "nccl"
+    except Exception:
+        return False
+
+
 def _stage_batch(model: EinetModel, batch) -> torch.Tensor:
     """Device batch for the graph path. Device fp32 tensors are used in place;
     host data is copied (asynchronously when pinned) into a persistent
@@ -104,26 +112,45 @@ def _stage_batch(model: EinetModel, batch) -> torch.Tensor:
     return st
 
 
-def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk):
+def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_group=None):
     """Replay (capturing on first use) the CUDA graph of one EM step on the
-    device batch ``xd``; returns (engine, stats, status)."""
+    device batch ``xd``; returns (engine, stats, status). With a process group
+    the step is two graphs (E-step, M-step) around the all-reduce of the
+    statistics and of the status words (NCCL, outside the graphs)."""
     n = xd.shape[0]
     eng, ws, stats, status, root = model.step_buffers(min(chunk, max(n, 1)))
     compute = model.params.compute_for(eng)  # prepares outside the graph if stale
     key = (xd.data_ptr(), tuple(xd.shape), float(lam), float(eps_w), int(chunk),
-           model.params.flat.data_ptr(), ws.data_ptr(), compute.data_ptr())
+           model.params.flat.data_ptr(), ws.data_ptr(), compute.data_ptr(),
+           process_group is not None)
     cache = model.__dict__.setdefault("_graphs", {})
-    g = cache.get(key)
-    if g is None:
+    gs = cache.get(key)
+    if gs is None:
         if len(cache) >= _GRAPH_CACHE_SIZE:
             cache.pop(next(iter(cache)))
         torch.cuda.current_stream().synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            accumulate(model, xd, chunk)
-            eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
-        cache[key] = g
-    g.replay()
+        if process_group is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                accumulate(model, xd, chunk)
+                eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
+            gs = (g,)
+        else:
+            ge, gm = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ge):
+                accumulate(model, xd, chunk)
+            with torch.cuda.graph(gm):
+                eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
+            gs = (ge, gm)
+        cache[key] = gs
+    if process_group is None:
+        gs[0].replay()
+    else:
+        import torch.distributed as dist
+        gs[0].replay()
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=process_group)
+        dist.all_reduce(status, op=dist.ReduceOp.MIN, group=process_group)
+        gs[1].replay()
     return eng, stats, status
 
 
@@ -137,12 +164,13 @@ def em_stochastic_step(model: EinetModel, batch, lam, eps_w=engine.EPS_W, chunk=
     all-reduce of the packed buffer) and every rank applies the identical
     M-step; the returned mean LL is then the global one.
     """
-    use_graph = lam != 0.0 and process_group is None and _graphs_enabled()
+    use_graph = (lam != 0.0 and _graphs_enabled() and
+                 (process_group is None or _nccl_group(process_group)))
     xd = _stage_batch(model, batch) if use_graph else engine.as_device_batch(batch)
     if xd.shape[0] == 0:
         raise ValueError("empty batch")
     if use_graph:
-        eng, stats, status = _graph_step(model, xd, lam, eps_w, chunk)
+        eng, stats, status = _graph_step(model, xd, lam, eps_w, chunk, process_group)
     else:
         eng, stats, status, compute = accumulate(model, xd, chunk)
         if process_group is not None:
