@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--chunk", type=int, default=16384)
     ap.add_argument("--config", default=CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--small-batch", type=int, default=1,
+                    help="also time the 4096-sample batch of SURVEY.md 8d (secondary field)")
     ap.add_argument("--cpu-sample", type=int, default=96,
                     help="samples per oracle EM step for the CPU legs")
     return ap.parse_args()
@@ -361,6 +363,18 @@ def run_ours(args):
     else:
         ms_e2e = timed(lambda: step(x_host), e2e_steps)  # the API stages the pinned batch
 
+    # secondary: the SURVEY.md 8d weak-scaling batch (4096 per GPU), same model
+    small = None
+    if args.batch > 4096 and args.small_batch:
+        xs = x_dev[:4096]
+        sstep = lambda: trainer.em_stochastic_step(model, xs, 0.5, chunk=4096, process_group=group)
+        for _ in range(3):
+            sstep()
+        ms_small = timed(sstep, args.steps)
+        small = {"batch_per_gpu": 4096, "chunk": 4096,
+                 "value": world * 4096 * args.steps / (ms_small / 1e3),
+                 "ms_per_step": ms_small / args.steps}
+
     # per-kernel-class device time of the same step (CUDA events, separate pass)
     _native.profile_enable(True)
     prof_steps = 3
@@ -444,6 +458,7 @@ def run_ours(args):
         "kernels": classes,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
+        "secondary_b4096": small,
     }
     print(json.dumps(line), flush=True)
     if group is not None:
