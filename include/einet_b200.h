@@ -167,6 +167,20 @@ int einet_ef_log_prob(einet_plan *plan, const double *params, const float *x,
 
 /* Standalone EinsumLayer contraction (engine.log_einsum_exp, engine.py:91-109):
  * left/right (B, L, K) fp64, w (L, K_out, K, K) fp64 -> out (B, L, K_out). */
+/* Batched ancestral sampling (engine.py:331-423, sample / conditional_sample).
+ * Writes n complete assignments to out (n, d_vars) fp64, deterministic in
+ * seed: every decision of sample b uses a Philox4x32-10 uniform keyed by
+ * (seed, b, decision site). conditional != 0: branch choices follow the
+ * posterior of the forward pass of x_e held in `workspace` (einet_forward
+ * with batch 1 and the evidence-marginalised compute), observed variables
+ * (evidence[d] != 0) are copied from x_e. scratch: einet_sample_scratch_bytes
+ * bytes. A sum node whose weights are all zero sets status word 3 (the slab)
+ * -> EngineError. Replaces the per-sample Python descent _descend. */
+int64_t einet_sample_scratch_bytes(const einet_plan *plan, int64_t n);
+int einet_sample(einet_plan *plan, const double *params, const void *workspace,
+                 int32_t conditional, const double *x_e, const uint8_t *evidence, int64_t n,
+                 uint64_t seed, void *scratch, double *out, int32_t *status, void *stream);
+
 int einet_log_einsum_exp(const double *left, const double *right, const double *w,
                          int64_t batch, int32_t rows, int32_t k, int32_t k_out,
                          double *out, void *stream);

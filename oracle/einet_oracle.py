@@ -424,3 +424,156 @@ def init_params(circuit, fam, seed=0, data=None, eps_w=EPS_W):
         p = 0.25 + 0.5 * rng.random(shape)
         phi = project_phi(fam, (p * float(fam["n_trials"]))[..., None])
     return OracleParams(einsum=ein, mixing=mix, phi=phi)
+
+
+# ----------------------------------------------------------------------------
+# sampling (engine.py:331-423) with the device's Philox4x32-10 uniforms
+# ----------------------------------------------------------------------------
+# The reference draws from per-sample numpy generators; the device kernels
+# (paper_2004_06231_b200/csrc/sample.cu) use a counter-based Philox4x32-10
+# stream keyed by (seed, sample b, decision site). This restatement performs
+# the reference descent (_descend: mixing draw, einsum (i, j) draw over the
+# flattened K x K weights, leaf draws) with those uniforms, so device samples
+# can be checked draw for draw; the reference's own sampler is matched
+# statistically (tests/golden/sampling.npz).
+
+_PHILOX_M0, _PHILOX_M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+_PHILOX_W0, _PHILOX_W1 = 0x9E3779B9, 0xBB67AE85
+
+
+def philox4x32_10(ctr, key):
+    """ctr (N, 4) uint32, key (k0, k1) -> (N, 4) uint32 (Random123 Philox4x32-10)."""
+    c = [np.asarray(ctr[:, i], dtype=np.uint64) for i in range(4)]
+    k0, k1 = int(key[0]) & 0xFFFFFFFF, int(key[1]) & 0xFFFFFFFF
+    mask = np.uint64(0xFFFFFFFF)
+    for _ in range(10):
+        p0 = _PHILOX_M0 * c[0]
+        p1 = _PHILOX_M1 * c[2]
+        hi0, lo0 = p0 >> np.uint64(32), p0 & mask
+        hi1, lo1 = p1 >> np.uint64(32), p1 & mask
+        c = [hi1 ^ c[1] ^ np.uint64(k0), lo1, hi0 ^ c[3] ^ np.uint64(k1), lo0]
+        k0 = (k0 + _PHILOX_W0) & 0xFFFFFFFF
+        k1 = (k1 + _PHILOX_W1) & 0xFFFFFFFF
+    return np.stack(c, axis=1).astype(np.uint64)
+
+
+def philox_uniforms(seed, b, site):
+    """(u0, u1) in [0, 1) with 53 bits each for samples b (array) at one site."""
+    b = np.asarray(b, dtype=np.uint64)
+    ctr = np.stack([b & np.uint64(0xFFFFFFFF), b >> np.uint64(32),
+                    np.full_like(b, np.uint64(site)), np.zeros_like(b)], axis=1)
+    seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    r = philox4x32_10(ctr, (seed & 0xFFFFFFFF, seed >> 32))
+    u0 = ((r[:, 0] >> np.uint64(5)).astype(np.float64) * 67108864.0 +
+          (r[:, 1] >> np.uint64(6)).astype(np.float64)) / 9007199254740992.0
+    u1 = ((r[:, 2] >> np.uint64(5)).astype(np.float64) * 67108864.0 +
+          (r[:, 3] >> np.uint64(6)).astype(np.float64)) / 9007199254740992.0
+    return u0, u1
+
+
+def slab_ids(circuit):
+    """Slab of every (layer, row) output, numbered like the device plan
+    (csrc/abi.cu build_plan): buffer rows first, then the unbuffered outputs
+    (out_rows == -1) in layer order."""
+    nxt = circuit.num_buffer_rows
+    out = {}
+    for i, layer in enumerate(circuit.layers[1:], start=1):
+        ids = []
+        for o in np.asarray(layer.out_rows):
+            if o >= 0:
+                ids.append(int(o))
+            else:
+                ids.append(nxt)
+                nxt += 1
+        out[i] = ids
+    return out, nxt
+
+
+def sample_philox(circuit, params, fam, n, seed=0, x_e=None, evidence=None, trace=None):
+    """Ancestral / conditional samples (engine.py:339-423) drawn with the
+    device uniforms; ``trace`` = ``forward`` of x_e with the evidence-
+    marginalised mask for conditional sampling."""
+    slabs, num_slabs = slab_ids(circuit)
+    layers = circuit.layers
+    k_sel = np.full((num_slabs, n), -1, dtype=np.int64)
+    last = len(layers) - 1
+    if _kind(layers[last]) == "mixing":
+        root_slab = slabs[last][list(layers[last].region_ids).index(circuit.rg.root)]
+    else:
+        root_slab = slabs[last][0]
+    k_sel[root_slab, :] = 0
+    bidx = np.arange(n)
+    for i in range(last, 0, -1):
+        layer = layers[i]
+        for row, os in enumerate(slabs[i]):
+            active = np.nonzero(k_sel[os] >= 0)[0]
+            if active.size == 0:
+                continue
+            u0, _ = philox_uniforms(seed, bidx[active], os)
+            for t, b in enumerate(active):
+                k = int(k_sel[os, b])
+                if _kind(layer) == "einsum":
+                    w = params.einsum[i][row, k]
+                    if trace is not None:
+                        log_n = trace.buffer[0, layer.left_src[row], :]
+                        log_np = trace.buffer[0, layer.right_src[row], :]
+                        log_s = trace.outputs[i][0, row, k]
+                        w = w * np.exp(log_n[:, None] + log_np[None, :] - log_s)
+                    c = np.cumsum(w.ravel())
+                    if c[-1] <= 0.0:
+                        raise RuntimeError("cannot sample from an all-zero weight vector")
+                    idx = int(np.searchsorted(c, u0[t] * c[-1], side="right"))
+                    idx = min(idx, c.size - 1)
+                    ii, jj = divmod(idx, circuit.k)
+                    k_sel[layer.left_src[row], b] = ii
+                    k_sel[layer.right_src[row], b] = jj
+                else:
+                    w = np.where(layer.mask[row], params.mixing[i][row], 0.0)
+                    if trace is not None:
+                        prev = trace.outputs[i - 1]
+                        diff = prev[0, layer.src[row], k] - trace.outputs[i][0, row, k]
+                        ok = layer.mask[row] & np.isfinite(diff)
+                        w = w * np.where(ok, np.exp(np.where(ok, diff, 0.0)), 0.0)
+                    c = np.cumsum(w)
+                    if c[-1] <= 0.0:
+                        raise RuntimeError("cannot sample from an all-zero weight vector")
+                    ci = min(int(np.searchsorted(c, u0[t] * c[-1], side="right")), c.size - 1)
+                    src_slab = slabs[i - 1][int(layer.src[row, ci])]
+                    k_sel[src_slab, b] = k
+    leaf = layers[0]
+    d_vars = circuit.d_vars
+    out = np.full((n, d_vars), np.nan)
+    ev = set() if evidence is None else set(evidence)
+    for li, scope in enumerate(leaf.scopes):
+        slab = int(leaf.out_rows[li])
+        rep = int(leaf.replica[li])
+        active = np.nonzero(k_sel[slab] >= 0)[0]
+        for dv in scope:
+            if dv in ev:
+                out[active, dv] = x_e[dv]
+                continue
+            u0, u1 = philox_uniforms(seed, bidx[active], num_slabs + dv)
+            for t, b in enumerate(active):
+                phi = params.phi[dv, int(k_sel[slab, b]), rep]
+                if fam["family"] == "gaussian":
+                    mu, var = phi[0], phi[1] - phi[0] * phi[0]
+                    z = math.sqrt(-2.0 * math.log(1.0 - u0[t])) * math.cos(
+                        6.283185307179586 * u1[t])
+                    out[b, dv] = mu + math.sqrt(var) * z
+                elif fam["family"] == "categorical":
+                    c = np.cumsum(phi)
+                    out[b, dv] = min(int(np.searchsorted(c, u0[t] * c[-1], side="right")),
+                                     c.size - 1)
+                else:
+                    nt = int(fam["n_trials"])
+                    pr = phi[0] / nt
+                    acc, pick = 0.0, nt
+                    for xv in range(nt + 1):
+                        acc += math.exp(math.lgamma(nt + 1.0) - math.lgamma(xv + 1.0) -
+                                        math.lgamma(nt - xv + 1.0) + xv * math.log(pr) +
+                                        (nt - xv) * math.log1p(-pr))
+                        if acc > u0[t]:
+                            pick = xv
+                            break
+                    out[b, dv] = pick
+    return out

@@ -75,6 +75,9 @@ EXPORTS = {
                                     c_void_p, c_void_p, c_void_p]),
     "einet_log_einsum_exp": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                        c_int32, c_int32, c_void_p, c_void_p]),
+    "einet_sample_scratch_bytes": (c_int64, [c_void_p, c_int64]),
+    "einet_sample": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_int64,
+                               ctypes.c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "einet_selftest_tf32_gemm": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32,
                                            c_void_p]),
     "einet_launch_count": (c_int64, []),

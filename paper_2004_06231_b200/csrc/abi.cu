@@ -655,6 +655,24 @@ int einet_log_einsum_exp(const double *left, const double *right, const double *
                                (cudaStream_t)stream);
 }
 
+int64_t einet_sample_scratch_bytes(const einet_plan *plan, int64_t n) {
+  if (!plan || n < 0) return -1;
+  return sample_scratch_bytes(plan->impl, n);
+}
+
+int einet_sample(einet_plan *plan, const double *params, const void *workspace,
+                 int32_t conditional, const double *x_e, const uint8_t *evidence, int64_t n,
+                 uint64_t seed, void *scratch, double *out, int32_t *status, void *stream) {
+  if (!plan || !params || !scratch || !out || !status)
+    return fail(EINET_ERR_USAGE, "null argument");
+  if (conditional && (!workspace || !x_e || !evidence))
+    return fail(EINET_ERR_USAGE, "conditional sampling needs the forward workspace, x_e and the evidence mask");
+  if (n < 0) return fail(EINET_ERR_USAGE, "n must be >= 0");
+  return launch_sample(plan->impl, params, (const uint8_t *)workspace, conditional, x_e,
+                       evidence, n, seed, (uint8_t *)scratch, out, status,
+                       (cudaStream_t)stream);
+}
+
 int einet_selftest_tf32_gemm(const float *A, const float *B, float *D, int32_t N, int32_t K,
                              void *stream) {
   if (!A || !B || !D) return fail(EINET_ERR_USAGE, "null argument");

@@ -188,6 +188,10 @@ int launch_leaf_fwd_dmma(Plan &p, const CompView &c, const float *x, int64_t B, 
 int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *compute,
                        const float *EA, const float *EB, const WsView &w, int64_t B,
                        cudaStream_t st);
+int64_t sample_scratch_bytes(const Plan &p, int64_t n);
+int launch_sample(Plan &p, const double *params, const uint8_t *wsb, int conditional,
+                  const double *x_e, const uint8_t *evidence, int64_t n, uint64_t seed,
+                  uint8_t *scratch, double *out, int32_t *status, cudaStream_t st);
 int launch_selftest_gemm(const float *A, const float *B, float *D, int N, int K,
                          cudaStream_t st);
 int leaf_lsplit(const Plan &p, int64_t B);

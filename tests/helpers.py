@@ -68,3 +68,41 @@ def close(a, b, rtol, atol):
         i = np.unravel_index(np.argmax(np.where(bad, err / np.maximum(bound, 1e-300), 0)), a.shape)
         raise AssertionError(f"{bad.sum()} of {a.size} entries differ; worst at {i}: "
                              f"got {a[i]!r} want {b[i]!r} (rtol {rtol}, atol {atol})")
+
+
+def sampling_cases():
+    """(index, Case, evidence list) of tests/golden/sampling.npz."""
+    g = dict(np.load(os.path.join(GOLDEN, "sampling.npz")))
+    return g, [(i, Case(str(g[f"case{i}_name"])), [int(v) for v in g[f"case{i}_evidence"]])
+               for i in range(int(g["num_cases"]))]
+
+
+def oracle_samples(case, evidence, n, seed):
+    """Philox-restated samples of the oracle (conditional when evidence)."""
+    p = case.params("init")
+    if not evidence:
+        return O.sample_philox(case.circuit, p, case.fam_doc, n, seed=seed)
+    mask = np.array([i not in evidence for i in range(case.circuit.d_vars)])
+    tr = O.forward(case.circuit, p, case.fam_doc, case.x[:1], mask)
+    return O.sample_philox(case.circuit, p, case.fam_doc, n, seed=seed, x_e=case.x[0],
+                           evidence=evidence, trace=tr)
+
+
+def moment_z(s, g, key):
+    """Largest |z| of the sample moments of s against the fixture's reference
+    moments (two-sample standard errors from s; constant columns such as
+    evidence must match to 1e-9)."""
+    n = s.shape[0]
+
+    def z(mine, ref, var):
+        se = np.sqrt(2.0 * var / n) + 1e-9 * (1.0 + np.abs(ref))
+        return np.abs(mine - ref) / se
+
+    prod = s[:, :, None] * s[:, None, :]
+    zs = [z(s.mean(axis=0), g[f"{key}_mean"], s.var(axis=0)),
+          z(prod.mean(axis=0), g[f"{key}_m2"], prod.var(axis=0))]
+    if f"{key}_freq" in g:
+        f = g[f"{key}_freq"]
+        mine = np.stack([(s == v).mean(axis=0) for v in range(f.shape[1])], axis=1)
+        zs.append(z(mine, f, np.maximum(mine * (1 - mine), 1.0 / n)))
+    return max(float(np.max(v)) for v in zs)
