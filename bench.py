@@ -10,6 +10,12 @@ N > 1, fused M-step) -- the reference ``trainer.em_stochastic_step``
 synthetic image data, a fixed per-GPU batch (weak scaling). Inputs are larger
 than L2 (16384 x 3072 fp32 = 201 MB > 126 MB), so no flush is needed.
 
+``e2e`` runs the same steps through the public ``trainer.em_stochastic_steps``
+from pinned host memory: the batch ships as the u8 pixels it was quantised
+from (x = k/255, the reference's EIND1 u8 dataset payload, modelio.py:145-166)
+and is decoded on the device (``einet_decode_u8``, bit-identical values);
+``e2e.fp32_host_input`` is the same leg fed the fp32 host array.
+
 ``--impl reference`` times the CPU restatement of the reference's EM step
 (oracle/einet_oracle.py; the Python reference itself cannot travel to the GPU
 box) on all host cores with a bounded sample per step.
@@ -307,7 +313,12 @@ def run_ours(args):
     rg, fam, k, gen = cfg(args.config)
     circuit = compile_graph(rg, k)
     B = args.batch
-    x_host = torch.from_numpy(gen(B, seed=1000 + rank).astype(np.float32)).pin_memory()
+    x64 = gen(B, seed=1000 + rank)
+    x_host = torch.from_numpy(x64.astype(np.float32)).pin_memory()
+    # the same batch as the image bytes it was quantised from (k / 255, an
+    # EIND1 u8 payload): the e2e leg ships these and decodes on the device
+    x_u8 = torch.from_numpy(np.rint(x64 * 255.0).astype(np.uint8)).pin_memory()
+    del x64
     x_dev = x_host.to(dev)
     init_x = gen(4096, seed=7).astype(np.float32).astype(np.float64)
     ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=init_x)
@@ -356,12 +367,22 @@ def run_ours(args):
     # (host -> device copy inside trainer.em_stochastic_steps, overlapped with
     # the previous step), every step's mean LL read back
     e2e_steps = max(3, args.steps // 4)
-    if group is None:
-        # the public multi-step API: batch i+1's host->device copy overlaps step i
-        ms_e2e = timed(lambda: trainer.em_stochastic_steps(model, [x_host] * e2e_steps, 0.5,
-                                                            chunk=args.chunk), 1)
-    else:
-        ms_e2e = timed(lambda: step(x_host), e2e_steps)  # the API stages the pinned batch
+
+    def e2e_leg(xh):
+        if group is None:
+            # the public multi-step API: batch i+1's host->device copy overlaps step i
+            return timed(lambda: trainer.em_stochastic_steps(model, [xh] * e2e_steps, 0.5,
+                                                              chunk=args.chunk), 1)
+        return timed(lambda: step(xh), e2e_steps)  # the API stages the pinned batch
+
+    # the u8 and fp32 host batches decode to the same device values
+    assert torch.equal(engine.as_device_batch(x_u8.to(dev)), x_dev)
+    for xh in (x_u8, x_host):  # staging buffers and their graphs exist before timing
+        trainer.em_stochastic_steps(model, [xh] * 2, 0.5, chunk=args.chunk)
+        if group is not None:
+            step(xh)
+    ms_e2e = e2e_leg(x_u8)
+    ms_e2e_f32 = e2e_leg(x_host)
 
     # secondary: the SURVEY.md 8d weak-scaling batch (4096 per GPU), same model
     small = None
@@ -391,6 +412,7 @@ def run_ours(args):
 
     value = world * B * args.steps / (ms / 1e3)
     e2e = world * B * e2e_steps / (ms_e2e / 1e3)
+    e2e_f32 = world * B * e2e_steps / (ms_e2e_f32 / 1e3)
     hbm, bf16, peak_kind = load_peaks()
     work = work_per_sample(circuit)
     classes = {}
@@ -451,8 +473,12 @@ def run_ours(args):
                    "batch_per_gpu": B, "global_batch": B * world, "chunk": args.chunk,
                    "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (B*3072*4 bytes per GPU > 126 MB)"},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(B * rg.d_vars * 4),
-                "d2h_bytes_per_step": 48},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(B * rg.d_vars),
+                "d2h_bytes_per_step": 48, "steps": e2e_steps,
+                "input": "pinned host u8 pixels (EIND1 payload, x = k/255), copied and "
+                         "decoded on the device inside trainer.em_stochastic_steps",
+                "fp32_host_input": {"value": e2e_f32,
+                                    "h2d_bytes_per_step": int(B * rg.d_vars * 4)}},
         "gpu_launches": int(launches),
         "roofline": roof,
         "kernels": classes,

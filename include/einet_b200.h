@@ -181,6 +181,14 @@ int einet_sample(einet_plan *plan, const double *params, const void *workspace,
                  int32_t conditional, const double *x_e, const uint8_t *evidence, int64_t n,
                  uint64_t seed, void *scratch, double *out, int32_t *status, void *stream);
 
+/* Dataset payload decode (modelio.py:145-166, load_dataset): dst[i] =
+ * (float)((double)src[i] / divisor) for count u8 values on the device
+ * (divisor 255 = the reference's default normalisation of EIND1 u8 payloads,
+ * 1 = raw counts). Lets callers ship image batches as bytes: the values are
+ * bit-identical to the fp32 staging of the reference's float64 array. */
+int einet_decode_u8(const uint8_t *src, int64_t count, double divisor, float *dst,
+                    void *stream);
+
 int einet_log_einsum_exp(const double *left, const double *right, const double *w,
                          int64_t batch, int32_t rows, int32_t k, int32_t k_out,
                          double *out, void *stream);

@@ -78,6 +78,7 @@ EXPORTS = {
     "einet_sample_scratch_bytes": (c_int64, [c_void_p, c_int64]),
     "einet_sample": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_int64,
                                ctypes.c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "einet_decode_u8": (c_int32, [c_void_p, c_int64, ctypes.c_double, c_void_p, c_void_p]),
     "einet_selftest_tf32_gemm": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32,
                                            c_void_p]),
     "einet_launch_count": (c_int64, []),

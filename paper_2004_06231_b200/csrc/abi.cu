@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -671,6 +672,15 @@ int einet_sample(einet_plan *plan, const double *params, const void *workspace,
   return launch_sample(plan->impl, params, (const uint8_t *)workspace, conditional, x_e,
                        evidence, n, seed, (uint8_t *)scratch, out, status,
                        (cudaStream_t)stream);
+}
+
+int einet_decode_u8(const uint8_t *src, int64_t count, double divisor, float *dst,
+                    void *stream) {
+  if (count < 0) return fail(EINET_ERR_USAGE, "count must be >= 0");
+  if (count > 0 && (!src || !dst)) return fail(EINET_ERR_USAGE, "null argument");
+  if (!(divisor > 0.0) || !std::isfinite(divisor))
+    return fail(EINET_ERR_USAGE, "divisor must be finite and > 0");
+  return launch_decode_u8(src, count, divisor, dst, (cudaStream_t)stream);
 }
 
 int einet_selftest_tf32_gemm(const float *A, const float *B, float *D, int32_t N, int32_t K,

@@ -189,6 +189,8 @@ int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *com
                        const float *EA, const float *EB, const WsView &w, int64_t B,
                        cudaStream_t st);
 int64_t sample_scratch_bytes(const Plan &p, int64_t n);
+int launch_decode_u8(const uint8_t *src, int64_t count, double divisor, float *dst,
+                     cudaStream_t st);
 int launch_sample(Plan &p, const double *params, const uint8_t *wsb, int conditional,
                   const double *x_e, const uint8_t *evidence, int64_t n, uint64_t seed,
                   uint8_t *scratch, double *out, int32_t *status, cudaStream_t st);

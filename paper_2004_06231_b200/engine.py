@@ -465,8 +465,41 @@ class AllocationTracker:
 # forward / backward
 # ---------------------------------------------------------------------------
 
-def as_device_batch(x, device=None) -> torch.Tensor:
-    """(B, D) fp32 contiguous CUDA tensor (zero-copy for such tensors)."""
+def _is_u8(x) -> bool:
+    return (x.dtype == torch.uint8) if isinstance(x, torch.Tensor) else \
+        (np.asarray(x).dtype == np.uint8)
+
+
+def _divisor(normalize) -> float:
+    """u8 payloads divide by 255 unless ``normalize`` is False (reference
+    ``modelio.py:150-166``: normalisation defaults on for u8 data)."""
+    return 1.0 if normalize is False else 255.0
+
+
+def decode_u8(src: torch.Tensor, normalize=None, out: torch.Tensor = None) -> torch.Tensor:
+    """fp32 values of a device u8 batch, decoded by the engine's kernel
+    (``einet_decode_u8``): ``float(float64(v) / 255)`` with the reference's
+    default normalisation, raw counts with ``normalize=False``."""
+    if not (src.is_cuda and src.dtype == torch.uint8):
+        raise TypeError("decode_u8 needs a CUDA uint8 tensor")
+    src = src.contiguous()
+    if out is None:
+        out = torch.empty(src.shape, dtype=torch.float32, device=src.device)
+    _native.check(_native.lib().einet_decode_u8(_ptr(src), src.numel(), _divisor(normalize),
+                                                _ptr(out), _stream()), "einet_decode_u8")
+    return out
+
+
+def as_device_batch(x, device=None, normalize=None) -> torch.Tensor:
+    """(B, D) fp32 contiguous CUDA tensor (zero-copy for such tensors). u8
+    batches (EIND1 payloads) travel as bytes and are decoded on the device."""
+    if _is_u8(x):
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+        if t.dim() == 1:
+            t = t[None, :]
+        if not t.is_cuda:
+            t = t.contiguous().to(device or "cuda", non_blocking=t.is_pinned())
+        return decode_u8(t, normalize)
     if isinstance(x, torch.Tensor):
         t = x
         if t.dim() == 1:

@@ -76,7 +76,7 @@ def accumulate(model: EinetModel, batch: torch.Tensor, chunk: int):
     return eng, stats, status, compute
 
 
-_GRAPH_CACHE_SIZE = 4
+_GRAPH_CACHE_SIZE = 8
 
 
 def _graphs_enabled() -> bool:
@@ -91,24 +91,26 @@ def _nccl_group(group) -> bool:
         return False
 
 
-def _stage_batch(model: EinetModel, batch) -> torch.Tensor:
+def _stage_batch(model: EinetModel, batch, normalize=None) -> torch.Tensor:
     """Device batch for the graph path. Device fp32 tensors are used in place;
     host data is copied (asynchronously when pinned) into a persistent
     per-model staging buffer, so the captured graph's input address is stable
-    across steps."""
-    if isinstance(batch, torch.Tensor) and batch.is_cuda:
+    across steps. u8 batches travel as bytes and are decoded on the device
+    into the fp32 staging buffer (``engine.decode_u8``)."""
+    if isinstance(batch, torch.Tensor) and batch.is_cuda and batch.dtype != torch.uint8:
         return engine.as_device_batch(batch)
-    t = batch if isinstance(batch, torch.Tensor) else torch.from_numpy(
-        np.ascontiguousarray(np.asarray(batch, dtype=np.float64), dtype=np.float32))
-    if t.dim() == 1:
-        t = t[None, :]
-    if t.dtype != torch.float32 or not t.is_contiguous():
-        t = t.to(torch.float32).contiguous()
+    t = _host_batch(batch)
+    dev = model.params.flat.device
     st = model.__dict__.get("_staging")
     if st is None or st.shape != t.shape:
-        st = torch.empty(t.shape, dtype=torch.float32, device=model.params.flat.device)
+        st = torch.empty(t.shape, dtype=torch.float32, device=dev)
         model.__dict__["_staging"] = st
-    st.copy_(t, non_blocking=t.is_pinned())
+    if t.dtype == torch.uint8:
+        if not t.is_cuda:
+            t = t.to(dev, non_blocking=t.is_pinned())
+        engine.decode_u8(t, normalize, out=st)
+    else:
+        st.copy_(t, non_blocking=t.is_pinned())
     return st
 
 
@@ -155,7 +157,7 @@ def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_
 
 
 def em_stochastic_step(model: EinetModel, batch, lam, eps_w=engine.EPS_W, chunk=4096,
-                       process_group=None) -> float:
+                       process_group=None, normalize=None) -> float:
     """One gliding-average EM update; returns the pre-update mean LL of the
     batch (reference ``trainer.py:99-117``). ``lam == 0`` leaves every
     parameter bitwise unchanged.
@@ -163,10 +165,15 @@ def em_stochastic_step(model: EinetModel, batch, lam, eps_w=engine.EPS_W, chunk=
     With ``process_group`` the statistics are summed across ranks (one NCCL
     all-reduce of the packed buffer) and every rank applies the identical
     M-step; the returned mean LL is then the global one.
+
+    A uint8 batch (an EIND1 payload, reference ``modelio.py:145-166``) is
+    copied as bytes and decoded on the device: divided by 255 unless
+    ``normalize`` is False, like the reference's ``load_dataset``.
     """
     use_graph = (lam != 0.0 and _graphs_enabled() and
                  (process_group is None or _nccl_group(process_group)))
-    xd = _stage_batch(model, batch) if use_graph else engine.as_device_batch(batch)
+    xd = (_stage_batch(model, batch, normalize) if use_graph
+          else engine.as_device_batch(batch, normalize=normalize))
     if xd.shape[0] == 0:
         raise ValueError("empty batch")
     if use_graph:
@@ -194,29 +201,38 @@ def _finish_step(model, eng, stats, status, lam) -> float:
 
 
 def _host_batch(batch) -> torch.Tensor:
-    t = batch if isinstance(batch, torch.Tensor) else torch.from_numpy(
-        np.ascontiguousarray(np.asarray(batch, dtype=np.float64), dtype=np.float32))
+    """(B, D) contiguous tensor: uint8 stays bytes, everything else fp32."""
+    if isinstance(batch, torch.Tensor):
+        t = batch
+    elif engine._is_u8(batch):
+        t = torch.from_numpy(np.ascontiguousarray(batch))
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(batch, dtype=np.float64),
+                                                  dtype=np.float32))
     if t.dim() == 1:
         t = t[None, :]
-    if t.dtype != torch.float32 or not t.is_contiguous():
-        t = t.to(torch.float32).contiguous()
-    return t
+    if t.dtype not in (torch.float32, torch.uint8):
+        t = t.to(torch.float32)
+    return t.contiguous()
 
 
 def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
-                        chunk=4096) -> list:
+                        chunk=4096, normalize=None) -> list:
     """Consecutive gliding-average EM steps over a sequence of host batches of
     one shape (equivalent to calling ``em_stochastic_step`` on each): the
     host->device copy of batch i+1 runs on a copy stream into the other half
     of a double-buffered staging area while step i runs on the device. Every
     step's LL (and error words) is read back after the step, as in
-    ``em_stochastic_step``; returns the list of mean LLs."""
+    ``em_stochastic_step``; returns the list of mean LLs. uint8 batches are
+    copied as bytes and decoded on the device (see ``em_stochastic_step``)."""
     hosts = [_host_batch(b) for b in batches]
     if not hosts:
         return []
     if lam == 0.0 or not _graphs_enabled() or hosts[0].is_cuda:
-        return [em_stochastic_step(model, b, lam, eps_w, chunk) for b in hosts]
+        return [em_stochastic_step(model, b, lam, eps_w, chunk, normalize=normalize)
+                for b in hosts]
     shape = tuple(hosts[0].shape)
+    dtype = hosts[0].dtype
     if shape[0] == 0:
         raise ValueError("empty batch")
     dev = model.params.flat.device
@@ -224,10 +240,17 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     if copy is None:
         copy = torch.cuda.Stream(device=dev)
         model.__dict__["_copy_stream"] = copy
-    bufs = model.__dict__.get("_stage2")
+    key = "_stage2_u8" if dtype == torch.uint8 else "_stage2_f32"
+    bufs = model.__dict__.get(key)
     if bufs is None or tuple(bufs[0].shape) != shape:
-        bufs = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
-        model.__dict__["_stage2"] = bufs
+        bufs = [torch.empty(shape, dtype=dtype, device=dev) for _ in range(2)]
+        model.__dict__[key] = bufs
+    u8 = dtype == torch.uint8
+    if u8:
+        xf = model.__dict__.get("_staging")
+        if xf is None or tuple(xf.shape) != shape:
+            xf = torch.empty(shape, dtype=torch.float32, device=dev)
+            model.__dict__["_staging"] = xf
     cur = torch.cuda.current_stream(dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     used = [torch.cuda.Event(), torch.cuda.Event()]
@@ -242,12 +265,17 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     issue_copy(0)
     out = []
     for i, h in enumerate(hosts):
-        if tuple(h.shape) != shape:
-            raise ValueError("em_stochastic_steps needs batches of one shape")
+        if tuple(h.shape) != shape or h.dtype != dtype:
+            raise ValueError("em_stochastic_steps needs batches of one shape and dtype")
         s = i & 1
         cur.wait_event(copied[s])
-        eng, stats, status = _graph_step(model, bufs[s], lam, eps_w, chunk)
-        used[s].record(cur)
+        if u8:
+            engine.decode_u8(bufs[s], normalize, out=xf)  # frees bufs[s] for batch i + 2
+            used[s].record(cur)
+            eng, stats, status = _graph_step(model, xf, lam, eps_w, chunk)
+        else:
+            eng, stats, status = _graph_step(model, bufs[s], lam, eps_w, chunk)
+            used[s].record(cur)
         if i + 1 < len(hosts):
             issue_copy(i + 1)
         out.append(_finish_step(model, eng, stats, status, lam))

@@ -349,3 +349,60 @@ def test_launch_counter_moves():
     data = np.random.default_rng(13).normal(size=(8, 4))
     _gauss_model(13, data=data).forward(data)
     assert _native.launch_count() > before
+
+
+def test_u8_batches_decode_like_the_reference_normalisation():
+    """EIND1 u8 payloads (modelio.py:145-166): x = float64(v) / 255 (or raw
+    with normalize=False); the device decode equals fp32 staging of that
+    array bit for bit, including odd lengths and unaligned slices."""
+    rng = np.random.default_rng(0)
+    for n in (1, 15, 16, 17, 4099, 1 << 20):
+        v = rng.integers(0, 256, n).astype(np.uint8)
+        dev = torch.from_numpy(v).cuda()
+        got = engine.decode_u8(dev).cpu().numpy()
+        assert np.array_equal(got, (v.astype(np.float64) / 255.0).astype(np.float32))
+        raw = engine.decode_u8(dev, normalize=False).cpu().numpy()
+        assert np.array_equal(raw, v.astype(np.float32))
+    big = torch.from_numpy(rng.integers(0, 256, 5000).astype(np.uint8)).cuda()
+    got = engine.decode_u8(big[3:4003]).cpu().numpy()
+    assert np.array_equal(got, (big[3:4003].cpu().numpy() / 255.0).astype(np.float32))
+
+
+def test_u8_em_steps_equal_float_steps():
+    """A u8 host batch through em_stochastic_step / em_stochastic_steps gives
+    bitwise the same parameters and LLs as its float64 normalisation."""
+    rg, fam, k, gen = config("C2")
+    x = gen(512, seed=3)
+    xu = np.rint(x * 255.0).astype(np.uint8)
+    assert np.array_equal(xu / 255.0, x)
+    circuit = E.compile_graph(rg, k)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=x)
+    ma = E.EinetModel(circuit, engine.Parameters.from_numpy(circuit, fam, ein, mix, phi), fam)
+    mb = E.EinetModel(circuit, engine.Parameters.from_numpy(circuit, fam, ein, mix, phi), fam)
+    la = [trainer.em_stochastic_step(ma, x, 0.5, chunk=256)]
+    lb = [trainer.em_stochastic_step(mb, torch.from_numpy(xu).pin_memory(), 0.5, chunk=256)]
+    la += trainer.em_stochastic_steps(ma, [x, x[::-1].copy()], 0.5, chunk=256)
+    lb += trainer.em_stochastic_steps(mb, [xu, xu[::-1].copy()], 0.5, chunk=256)
+    assert la == lb
+    assert torch.equal(ma.params.flat, mb.params.flat)
+
+
+@pytest.mark.parametrize("name,query,evidence", [
+    ("rat_gaussian", [1, 2], [0, 3, 5]),
+    ("rat_categorical4", [0], [1, 2, 6]),
+    ("rat_binomial", [2, 3, 4], []),
+    ("pd_lift_gaussian_image", list(range(0, 48, 5)), list(range(1, 48, 5)))])
+def test_conditional_log_density_matches_oracle(name, query, evidence):
+    """log p(x_q | x_e) (engine.py:198-215) = two marginalised forwards."""
+    case = Case(name)
+    p = device_params(case)
+    got = E.conditional_log_density(case.circuit, p, case.family, case.x, query, evidence)
+    d = case.circuit.d_vars
+    num = np.array([i not in query and i not in evidence for i in range(d)])
+    den = np.array([i not in evidence for i in range(d)])
+    op = case.params()
+    want = (O.forward(case.circuit, op, case.fam_doc, case.x, num).root[:, 0] -
+            O.forward(case.circuit, op, case.fam_doc, case.x, den).root[:, 0])
+    ll_close(got, want)
+    with pytest.raises(ValueError):
+        E.conditional_log_density(case.circuit, p, case.family, case.x, [0], [0])
