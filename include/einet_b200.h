@@ -189,6 +189,27 @@ int einet_sample(einet_plan *plan, const double *params, const void *workspace,
 int einet_decode_u8(const uint8_t *src, int64_t count, double divisor, float *dst,
                     void *stream);
 
+/* EINM1 model files (modelio.py:55-134, save_model / load_model) on the
+ * device. The host parses the magic, the JSON header and the tensor manifest;
+ * the blob section (per tensor: u32 ndim, u32 dims, f64 payload) lives in
+ * device memory.
+ * einet_crc32: *crc (device) = zlib CRC32 of data[0, len) (the checksum that
+ *   closes the file, modelio.py:83 / :100-102).
+ * einet_params_from_blob: table (device, int64 [n_tensors][8] = blob offset
+ *   of the tensor's u32 ndim, ndim, d0..d3, parameter offset (< 0: check
+ *   only), element count)
+ *   -> checks each embedded ndim/dims against the table and copies the
+ *   payloads into params; *bad (device, caller-initialised to INT32_MAX) =
+ *   the first tensor whose embedded shape differs or whose payload runs past
+ *   blob_len (ShapeError, modelio.py:106-117). max_count = largest count.
+ * einet_params_to_blob: the inverse (writes ndim, dims and payloads). */
+int einet_crc32(const uint8_t *data, int64_t len, uint32_t *crc, void *stream);
+int einet_params_from_blob(const uint8_t *blob, int64_t blob_len, const int64_t *table,
+                           int32_t n_tensors, int64_t max_count, double *params, int32_t *bad,
+                           void *stream);
+int einet_params_to_blob(const double *params, const int64_t *table, int32_t n_tensors,
+                         int64_t max_count, uint8_t *blob, void *stream);
+
 int einet_log_einsum_exp(const double *left, const double *right, const double *w,
                          int64_t batch, int32_t rows, int32_t k, int32_t k_out,
                          double *out, void *stream);

@@ -683,6 +683,32 @@ int einet_decode_u8(const uint8_t *src, int64_t count, double divisor, float *ds
   return launch_decode_u8(src, count, divisor, dst, (cudaStream_t)stream);
 }
 
+int einet_crc32(const uint8_t *data, int64_t len, uint32_t *crc, void *stream) {
+  if (len < 0) return fail(EINET_ERR_USAGE, "len must be >= 0");
+  if (!crc || (len > 0 && !data)) return fail(EINET_ERR_USAGE, "null argument");
+  return launch_crc32(data, len, crc, (cudaStream_t)stream);
+}
+
+int einet_params_from_blob(const uint8_t *blob, int64_t blob_len, const int64_t *table,
+                           int32_t n_tensors, int64_t max_count, double *params, int32_t *bad,
+                           void *stream) {
+  if (n_tensors < 0 || blob_len < 0 || max_count < 0)
+    return fail(EINET_ERR_USAGE, "sizes must be >= 0");
+  if (n_tensors > 0 && (!blob || !table || !params || !bad))
+    return fail(EINET_ERR_USAGE, "null argument");
+  return launch_blob_to_params(blob, blob_len, table, n_tensors, max_count, params, bad,
+                               (cudaStream_t)stream);
+}
+
+int einet_params_to_blob(const double *params, const int64_t *table, int32_t n_tensors,
+                         int64_t max_count, uint8_t *blob, void *stream) {
+  if (n_tensors < 0 || max_count < 0) return fail(EINET_ERR_USAGE, "sizes must be >= 0");
+  if (n_tensors > 0 && (!blob || !table || !params))
+    return fail(EINET_ERR_USAGE, "null argument");
+  return launch_params_to_blob(params, table, n_tensors, max_count, blob,
+                               (cudaStream_t)stream);
+}
+
 int einet_selftest_tf32_gemm(const float *A, const float *B, float *D, int32_t N, int32_t K,
                              void *stream) {
   if (!A || !B || !D) return fail(EINET_ERR_USAGE, "null argument");

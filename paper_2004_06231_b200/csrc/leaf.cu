@@ -132,14 +132,22 @@ __global__ void __launch_bounds__(256) k_prepare_const(
 
 // Gaussian statistics centre per (r, d): mean over k of the component means.
 // Centring the fp32 batch partial sums keeps E[x^2] - E[x]^2 well conditioned.
-__global__ void k_prepare_center(const double *__restrict__ phi, float *center, int D, int K,
-                                 int R) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= (int64_t)R * D) return;
-  const int d = (int)(e % D), r = (int)(e / D);
+// Gaussian statistics centre per (r, d): mean over k of the component means.
+// Centring the fp32 batch partial sums keeps E[x^2] - E[x]^2 well conditioned.
+// One warp per (r, d), lanes over k, xor-butterfly: the summation order of the
+// fused M-step (mstep.cu k_mstep_leaf_gauss), so a re-prepared compute buffer
+// equals the one the M-step left behind bit for bit.
+__global__ void __launch_bounds__(256) k_prepare_center(const double *__restrict__ phi,
+                                                        float *center, int D, int K, int R) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (int64_t)R * D) return;
+  const int d = (int)(w % D), r = (int)(w / D);
   double s = 0.0;
-  for (int k = 0; k < K; ++k) s += phi[(((int64_t)d * K + k) * R + r) * 2];
-  center[e] = (float)(s / K);
+  for (int k = lane; k < K; k += 32) s += phi[(((int64_t)d * K + k) * R + r) * 2];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) center[w] = (float)(s / K);
 }
 
 int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_t *mask,
@@ -169,7 +177,7 @@ int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_
                                                      p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
                                                      c.cnst, D, K, R, p.family);
   if (p.family == EINET_FAMILY_GAUSSIAN) {
-    k_prepare_center<<<ceil_div((int64_t)R * D, 256), 256, 0, st>>>(phi, c.center, D, K, R);
+    k_prepare_center<<<ceil_div((int64_t)R * D * 32, 256), 256, 0, st>>>(phi, c.center, D, K, R);
     count_launch();
   }
   count_launch((p.n_w ? 1 : 0) + (p.n_mix ? 1 : 0) + 3);

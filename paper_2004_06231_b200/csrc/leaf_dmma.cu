@@ -61,7 +61,7 @@ __global__ void k_prepare_leaf_img(const double2 *__restrict__ lp, const float *
       const int d = scope_vars[scope_off[leaf] + v], r = leaf_rep[leaf];
       const int k = nt * 8 + (lane >> 2);
       const double2 q = lp[((int64_t)r * D + d) * K + k];
-      const double sa = q.x, m = -(q.y + (double)center[(int64_t)r * D + d] * sa);
+      const double sa = q.x, m = -fma((double)center[(int64_t)r * D + d], sa, q.y);
       val = (lane & 1) ? -2.0 * sa * m : sa * sa;
     }
     img[e] = val;
@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(256) k_prepare_cm2(const double2 *__restrict__
   for (int q = scope_off[leaf] + threadIdx.x; q < scope_off[leaf + 1]; q += 256) {
     const int d = scope_vars[q];
     const double2 p = lp[((int64_t)r * D + d) * K + k];
-    const double m = -(p.y + (double)center[(int64_t)r * D + d] * p.x);
-    acc = fma(m, m, acc);
+    const double m = -fma((double)center[(int64_t)r * D + d], p.x, p.y);
+    acc += __dmul_rn(m, m);  // rounded square: the fused M-step's order (mstep.cu)
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);

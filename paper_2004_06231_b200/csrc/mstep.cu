@@ -282,12 +282,14 @@ __global__ void __launch_bounds__(256) k_mstep_leaf_gauss(
     const int k = lane + 32 * u;
     if (k >= K) continue;
     const double sa = sqrt(0.5 / var[u]);
-    lp[((int64_t)r * D + d) * K + k] = make_double2(sa, -mu[u] * sa);
-    const double m = -(-mu[u] * sa + (double)cen * sa);
+    const double nmsa = -mu[u] * sa;
+    lp[((int64_t)r * D + d) * K + k] = make_double2(sa, nmsa);
+    // same roundings as the prepare path (leaf_dmma.cu k_prepare_leaf_img / _cm2)
+    const double m = -fma((double)cen, sa, nmsa);
     if (l >= 0) {
       double *t = mtmp + (((int64_t)r * D + d) * K + k) * 2;
       t[0] = -0.5 * (kLog2Pi + log(var[u]));
-      t[1] = m * m;
+      t[1] = __dmul_rn(m, m);
       if (dmma) {
         const int pv = pvo[l] + pos;
         double *img = c.leafimg + ((int64_t)(pv >> 1) * (K / 8) + k / 8) * 32 + (k % 8) * 4 +

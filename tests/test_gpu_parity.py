@@ -406,3 +406,18 @@ def test_conditional_log_density_matches_oracle(name, query, evidence):
     ll_close(got, want)
     with pytest.raises(ValueError):
         E.conditional_log_density(case.circuit, p, case.family, case.x, [0], [0])
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_reprepared_compute_equals_fused_mstep(cfg):
+    """The fused M-step rewrites the compute copies in place; preparing them
+    again from the master parameters (a reloaded model) gives the same LLs
+    bit for bit."""
+    rg, fam, k, gen = config(cfg)
+    x = gen(128, seed=5)
+    m = E.build_model(rg, fam, k=k, seed=0, data=x)
+    trainer.em_stochastic_step(m, x, 0.5)
+    a = m.log_likelihood(x)
+    m.params.touch()
+    b = m.log_likelihood(x)
+    assert np.array_equal(a, b)
