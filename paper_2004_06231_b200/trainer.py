@@ -295,29 +295,268 @@ def _check_finite(model, epoch, batch_idx):
             f"non-finite parameters after epoch {epoch}, batch {batch_idx}")
 
 
+def _enqueue_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk):
+    """One EM step on a device batch, enqueued on the current stream without
+    a host sync (the caller reads the status words later). Returns the
+    device status words."""
+    if lam != 0.0 and _graphs_enabled():
+        eng, stats, status = _graph_step(model, xd, lam, eps_w, chunk)
+    else:
+        eng, stats, status, compute = accumulate(model, xd, chunk)
+        if lam != 0.0:
+            eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
+    if lam != 0.0:
+        model.params.mark_compute_current(eng)
+    return status
+
+
+def _ll_pass(model, eng, ws, root, status, compute, xd, out):
+    eng.status_reset(status)
+    step = eng.max_chunk
+    for lo in range(0, xd.shape[0], step):
+        b = min(step, xd.shape[0] - lo)
+        eng.forward(compute, xd[lo:lo + b], b, ws, root, status)
+        out[lo:lo + b].copy_(root[:b, 0])
+
+
+def _enqueue_ll(model: EinetModel, xd: torch.Tensor, chunk):
+    """Per-sample log-likelihoods of the device dataset on the current stream,
+    in chunks of the EM step's engine (``chunk`` = the step's chunk) with its
+    workspace; the chunk loop is one CUDA graph per (model, dataset).
+    Returns (device LLs, device status words), both owned by the model."""
+    n = xd.shape[0]
+    eng, ws, stats, status, root = model.step_buffers(chunk)
+    if root.shape[1] != 1:
+        raise engine.EngineError("root vector length != 1 has no scalar density")
+    compute = model.params.compute_for(eng)
+    key = (xd.data_ptr(), tuple(xd.shape), ws.data_ptr(), compute.data_ptr(),
+           model.params.flat.data_ptr())
+    cache = model.__dict__.setdefault("_ll_graphs", {})
+    ent = cache.get(key)
+    if ent is None:
+        out = torch.empty(n, dtype=torch.float64, device=xd.device)
+        if not _graphs_enabled():
+            _ll_pass(model, eng, ws, root, status, compute, xd, out)
+            return out, status
+        if len(cache) >= 4:
+            cache.pop(next(iter(cache)))
+        torch.cuda.current_stream().synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            _ll_pass(model, eng, ws, root, status, compute, xd, out)
+        ent = cache[key] = (g, out)
+    ent[0].replay()
+    return ent[1], status
+
+
+def _pinned(shape, dtype):
+    t = torch.empty(shape, dtype=dtype)
+    return t.pin_memory() if torch.cuda.is_available() else t
+
+
 def train(model: EinetModel, data, cfg: TrainerConfig, valid=None) -> list:
     """Seeded epoch loop (reference ``trainer.py:137-162``); the dataset is
     uploaded once and batches are gathered on the device."""
-    host = np.atleast_2d(np.asarray(data, dtype=np.float64))
-    if len(host) == 0:
-        raise ValueError("training dataset is empty")
-    xd = engine.as_device_batch(host)
-    vd = None if valid is None else engine.as_device_batch(valid)
-    rng = np.random.default_rng(cfg.seed)
-    metrics = []
+    return train_many([model], [data], cfg, None if valid is None else [valid])[0]
+
+
+def train_many(models, datasets, cfg: TrainerConfig, valids=None, streams=16) -> list:
+    """Train each model on its own dataset exactly like ``train`` (reference
+    ``trainer.py:137-162``: seeded permutation per epoch, one
+    ``em_stochastic_step`` per batch, or ``em_full_step``; epoch metrics),
+    all models at once: model c's steps are CUDA-graph replays on stream
+    c mod ``streams``, its batches are gathered on the device, and the host
+    synchronises once per epoch to read every step's error words, the
+    parameter-finiteness checks and the epoch log-likelihoods. Every model
+    ends bitwise where a sequential ``train`` would leave it; errors raise
+    the reference exceptions for the first failing (model, batch) in
+    sequential order. Returns one metrics list per model; ``wall_seconds``
+    is the epoch time of the whole group."""
+    models = list(models)
+    datasets = list(datasets)
+    if len(datasets) != len(models):
+        raise ValueError("one dataset per model")
+    for d in datasets:
+        if (d.shape[0] if isinstance(d, torch.Tensor) else len(np.atleast_2d(d))) == 0:
+            raise ValueError("training dataset is empty")
+    valids = list(valids) if valids is not None else [None] * len(models)
+    if not models:
+        return []
+    dev = models[0].params.flat.device
+    cur = torch.cuda.current_stream(dev)
+    # datasets stay resident on the device (device fp32 tensors are used in place)
+    xds = [engine.as_device_batch(d, device=dev) for d in datasets]
+    vds = [None if v is None else engine.as_device_batch(v, device=dev) for v in valids]
+    hosts = xds
+    if len(models) == 1:
+        pool = [cur]
+    else:
+        pool = [torch.cuda.Stream(device=dev) for _ in range(min(len(models), max(1, streams)))]
+        for s in pool:
+            s.wait_stream(cur)
+    rngs = [np.random.default_rng(cfg.seed) for _ in models]
+    full = cfg.mode == "full"
+    nbs = [1 if full else -(-len(h) // cfg.batch_size) for h in hosts]
+    # epoch LLs run on the engine of the training steps (same workspace)
+    evc = [min(cfg.chunk, len(h) if full else min(cfg.batch_size, len(h))) for h in hosts]
+    metrics = [[] for _ in models]
     for epoch in range(cfg.epochs):
         t0 = time.perf_counter()
-        if cfg.mode == "full":
-            em_full_step(model, xd, eps_w=cfg.eps_w, chunk=cfg.chunk)
-            _check_finite(model, epoch, 0)
-        else:
-            order = torch.from_numpy(rng.permutation(len(host))).to(xd.device)
-            for bi, lo in enumerate(range(0, len(host), cfg.batch_size)):
-                em_stochastic_step(model, xd.index_select(0, order[lo:lo + cfg.batch_size]),
-                                   cfg.step_size, eps_w=cfg.eps_w, chunk=cfg.chunk)
-                _check_finite(model, epoch, bi)
-        train_ll = model.mean_log_likelihood(xd)
-        valid_ll = model.mean_log_likelihood(vd) if vd is not None else float("nan")
-        metrics.append(EpochMetrics(epoch=epoch, train_ll=train_ll, valid_ll=valid_ll,
-                                    wall_seconds=time.perf_counter() - t0))
+        logs = [torch.empty((nb, _native.STATUS_WORDS), dtype=torch.int32, device=dev)
+                for nb in nbs]
+        sums = [torch.empty(nb, dtype=torch.float64, device=dev) for nb in nbs]
+        orders, keep = [], []
+        for c, m in enumerate(models):
+            if full:
+                orders.append(None)
+                continue
+            perm = torch.from_numpy(rngs[c].permutation(len(hosts[c])))
+            if torch.cuda.is_available():
+                perm = perm.pin_memory()
+            keep.append(perm)
+            with torch.cuda.stream(pool[c % len(pool)]):
+                orders.append(perm.to(dev, non_blocking=True))
+        for bi in range(max(nbs)):
+            for c, m in enumerate(models):
+                if bi >= nbs[c]:
+                    continue
+                with torch.cuda.stream(pool[c % len(pool)]):
+                    if full:
+                        status = _enqueue_step(m, xds[c], 1.0, cfg.eps_w, cfg.chunk)
+                    else:
+                        lo = bi * cfg.batch_size
+                        idx = orders[c][lo:lo + cfg.batch_size]
+                        stage = m.__dict__.setdefault("_train_stage", {})
+                        key = (idx.shape[0], xds[c].shape[1])
+                        xb = stage.get(key)
+                        if xb is None:
+                            xb = stage[key] = torch.empty(key, dtype=torch.float32, device=dev)
+                        torch.index_select(xds[c], 0, idx, out=xb)
+                        status = _enqueue_step(m, xb, cfg.step_size, cfg.eps_w, cfg.chunk)
+                    logs[c][bi].copy_(status)
+                    sums[c][bi] = m.params.flat.sum()
+        lls, vlls, lstat, vstat = [], [], [], []
+        for c, m in enumerate(models):
+            with torch.cuda.stream(pool[c % len(pool)]):
+                out, st = _enqueue_ll(m, xds[c], evc[c])
+                lstat.append(st.clone())
+                h = _pinned(out.shape, torch.float64)
+                h.copy_(out, non_blocking=True)
+                lls.append(h)
+                if vds[c] is not None:
+                    vo, st = _enqueue_ll(m, vds[c], evc[c])
+                    vstat.append(st.clone())
+                    hv = _pinned(vo.shape, torch.float64)
+                    hv.copy_(vo, non_blocking=True)
+                    vlls.append(hv)
+                else:
+                    vstat.append(None)
+                    vlls.append(None)
+        for s in pool:
+            s.synchronize()
+        for c, m in enumerate(models):
+            words = logs[c].cpu().tolist()
+            fin = np.isfinite(sums[c].cpu().numpy())
+            for bi in range(nbs[c]):
+                engine._raise_words(words[bi], m.family)
+                if not fin[bi]:
+                    raise TrainingDiverged(
+                        f"non-finite parameters after epoch {epoch}, batch {bi}")
+            engine._raise_words(lstat[c].cpu().tolist(), m.family)
+            if vstat[c] is not None:
+                engine._raise_words(vstat[c].cpu().tolist(), m.family)
+        wall = time.perf_counter() - t0
+        for c in range(len(models)):
+            valid_ll = float(np.mean(vlls[c].numpy())) if vlls[c] is not None else float("nan")
+            metrics[c].append(EpochMetrics(epoch=epoch, train_ll=float(np.mean(lls[c].numpy())),
+                                           valid_ll=valid_ll, wall_seconds=wall))
+    for s in pool:
+        cur.wait_stream(s)
     return metrics
+
+
+# ---------------------------------------------------------------------------
+# cluster-then-mix pipeline (reference trainer.py:165-228, paper section 4.2)
+# ---------------------------------------------------------------------------
+
+def _sq_dists(data, centers, rows=None):
+    """Squared distances data x centers with the reference's arithmetic
+    (elementwise difference, square, sum over the variable axis), computed in
+    row blocks so SVHN-sized data never materialises an (n, k, d) array."""
+    n, k = len(data), len(centers)
+    d2 = np.empty((n, k))
+    step = rows or max(1, int(2 ** 25 // max(1, k * data.shape[1])))
+    for lo in range(0, n, step):
+        blk = data[lo:lo + step]
+        d2[lo:lo + step] = ((blk[:, None, :] - centers[None, :, :]) ** 2).sum(axis=2)
+    return d2
+
+
+def kmeans(data, k, seed=0, max_iter=50, block_rows=None):
+    """Lloyd's algorithm; an empty cluster is re-seeded to the point farthest
+    from its nearest centre (reference ``trainer.py:165-190``, identical
+    labels and centres). Returns (labels, centers)."""
+    data = np.asarray(data)
+    if k < 1:
+        raise ValueError("need at least one cluster")
+    if k > len(data):
+        raise ValueError("more clusters than samples")
+    rng = np.random.default_rng(seed)
+    centers = data[rng.choice(len(data), size=k, replace=False)].astype(float)
+    labels = np.zeros(len(data), dtype=np.int64)
+    for _ in range(max_iter):
+        d2 = _sq_dists(data, centers, rows=block_rows)
+        assign = d2.argmin(axis=1)
+        nearest = None
+        for c in range(k):
+            members = assign == c
+            if members.any():
+                centers[c] = data[members].mean(axis=0)
+                continue
+            if nearest is None:
+                nearest = d2.min(axis=1)
+            far = nearest.argmax()
+            centers[c] = data[far]
+            assign[far] = c
+        if np.array_equal(assign, labels):
+            break
+        labels = assign
+    return labels, centers
+
+
+@dataclass
+class MixtureModel:
+    """Convex mixture of trained models (reference ``trainer.py:193-209``)."""
+
+    components: list
+    log_pi: np.ndarray
+
+    @property
+    def weights(self):
+        return np.exp(self.log_pi)
+
+    def log_likelihood(self, x) -> np.ndarray:
+        from scipy.special import logsumexp
+        xd = engine.as_device_batch(x)
+        parts = np.stack([m.log_likelihood(xd) for m in self.components])
+        return logsumexp(parts + self.log_pi[:, None], axis=0)
+
+    def mean_log_likelihood(self, x) -> float:
+        return float(np.mean(self.log_likelihood(x)))
+
+
+def train_mixture(data, n_clusters, model_factory, cfg: TrainerConfig, seed=0,
+                  streams=16) -> MixtureModel:
+    """Cluster the data (``kmeans``), train one model per cluster, mix by
+    cluster proportion (reference ``trainer.py:212-228``).
+    ``model_factory(cluster_index, cluster_data)`` returns a fresh untrained
+    EinetModel. The component trainings run concurrently on the device
+    (``train_many``), each bitwise equal to training it alone."""
+    data = np.atleast_2d(np.asarray(data, dtype=np.float64))
+    labels, _ = kmeans(data, n_clusters, seed=seed)
+    subsets = [data[labels == c] for c in range(n_clusters)]
+    components = [model_factory(c, s) for c, s in enumerate(subsets)]
+    train_many(components, subsets, cfg, streams=streams)
+    pi = np.asarray([len(s) for s in subsets], dtype=np.float64)
+    pi /= pi.sum()
+    return MixtureModel(components=components, log_pi=np.log(pi))
