@@ -182,7 +182,12 @@ class _Engine:
         h = getattr(self, "handle", None)
         if h is not None and h.value:
             try:
-                self._lib.einet_plan_destroy(h)
+                if torch.cuda.is_current_stream_capturing():
+                    # the garbage collector may run inside a CUDA graph capture;
+                    # cudaFree there would invalidate the capture
+                    _DEFERRED_PLANS.append((self._lib, h))
+                else:
+                    self._lib.einet_plan_destroy(h)
             except Exception:
                 pass
 
@@ -238,8 +243,20 @@ def _bucket(batch: int) -> int:
     return b
 
 
+_DEFERRED_PLANS = []
+
+
+def _release_deferred_plans():
+    """Destroy plans whose owners were collected during a graph capture."""
+    if _DEFERRED_PLANS and not torch.cuda.is_current_stream_capturing():
+        while _DEFERRED_PLANS:
+            lib, h = _DEFERRED_PLANS.pop()
+            lib.einet_plan_destroy(h)
+
+
 def get_engine(circuit, family, batch: int = 256) -> _Engine:
     """Cached native plan whose max_chunk covers ``batch``."""
+    _release_deferred_plans()
     cache = circuit.__dict__.setdefault("_einet_b200_engines", {})
     key = (family.key(), _bucket(max(int(batch), 1)))
     eng = cache.get(key)

@@ -354,6 +354,117 @@ def _pinned(shape, dtype):
     return t.pin_memory() if torch.cuda.is_available() else t
 
 
+class _EpochPlan:
+    """One model's training epoch on one device dataset as a single enqueue
+    (a CUDA graph when graphs are enabled and lam != 0): for every batch the
+    gather ``x[order[lo:hi]]`` from the persistent permutation buffer, the EM
+    step (statistics reset, chunked forward + back-pass, M-step), a copy of
+    the step's error words and the sum of the parameters (the finiteness
+    check of ``_check_finite``); then the epoch log-likelihood pass. The
+    host sends the epoch's permutation and reads the logs back once."""
+
+    def __init__(self, model, xd, cfg):
+        dev = xd.device
+        self.full = cfg.mode == "full"
+        self.n = xd.shape[0]
+        self.xd = xd
+        self.lam = 1.0 if self.full else cfg.step_size
+        self.eps_w, self.chunk = cfg.eps_w, cfg.chunk
+        self.bs = self.n if self.full else cfg.batch_size
+        self.nb = -(-self.n // self.bs)
+        self.ll_chunk = min(cfg.chunk, self.bs, self.n)
+        self.order = None if self.full else torch.empty(self.n, dtype=torch.int64, device=dev)
+        self.logs = torch.empty((self.nb, _native.STATUS_WORDS), dtype=torch.int32, device=dev)
+        self.sums = torch.empty(self.nb, dtype=torch.float64, device=dev)
+        self.lstat = torch.empty(_native.STATUS_WORDS, dtype=torch.int32, device=dev)
+        self.stage = {}
+        if not self.full:
+            for b in {min(self.bs, self.n - lo) for lo in range(0, self.n, self.bs)}:
+                self.stage[b] = torch.empty((b, xd.shape[1]), dtype=torch.float32, device=dev)
+        self.h_perm = _pinned((self.n,), torch.int64)
+        self.h_logs = _pinned(tuple(self.logs.shape), torch.int32)
+        self.h_sums = _pinned((self.nb,), torch.float64)
+        self.h_lstat = _pinned((_native.STATUS_WORDS,), torch.int32)
+        self.h_ll = _pinned((self.n,), torch.float64)
+        self.graph = None
+        self.ll = None
+        self.engines = []
+        self.valid_host = None
+
+    @staticmethod
+    def get(model, xd, cfg):
+        key = (xd.data_ptr(), tuple(xd.shape), cfg.mode, cfg.batch_size, cfg.step_size,
+               cfg.eps_w, cfg.chunk, model.params.flat.data_ptr())
+        cache = model.__dict__.setdefault("_epoch_plans", {})
+        ep = cache.get(key)
+        if ep is None:
+            if len(cache) >= 2:
+                cache.pop(next(iter(cache)))
+            ep = cache[key] = _EpochPlan(model, xd, cfg)
+        return ep
+
+    def _body(self, model):
+        for bi in range(self.nb):
+            lo = bi * self.bs
+            if self.full:
+                xb = self.xd
+            else:
+                idx = self.order[lo:lo + self.bs]
+                xb = self.stage[idx.shape[0]]
+                torch.index_select(self.xd, 0, idx, out=xb)
+            eng, stats, status, compute = accumulate(model, xb, self.chunk)
+            if self.lam != 0.0:
+                eng.mstep(model.params.flat, compute, stats, self.lam, self.eps_w, status)
+            self.logs[bi].copy_(status)
+            self.sums[bi].copy_(model.params.flat.sum())
+        eng, ws, stats, status, root = model.step_buffers(self.ll_chunk)
+        if root.shape[1] != 1:
+            raise engine.EngineError("root vector length != 1 has no scalar density")
+        if self.ll is None:
+            self.ll = torch.empty(self.n, dtype=torch.float64, device=self.xd.device)
+        _ll_pass(model, eng, ws, root, status, model.params.compute_for(eng), self.xd, self.ll)
+        self.lstat.copy_(status)
+        return eng
+
+    def run(self, model, perm):
+        """Enqueue one epoch on the current stream (no host sync)."""
+        if perm is not None:
+            self.h_perm.copy_(torch.from_numpy(perm))
+            self.order.copy_(self.h_perm, non_blocking=True)
+        use_graph = self.lam != 0.0 and _graphs_enabled()
+        if use_graph and self.graph is not None and self.graph[1] != self._buffer_key(model):
+            self.graph = None  # buffers moved (e.g. evicted workspace): capture again
+        if use_graph and self.graph is None:
+            # buffers and compute copies exist before capture (nothing is
+            # allocated for the engine inside the graph)
+            sizes = {min(self.chunk, b) for b in
+                     ([self.n] if self.full else list(self.stage))} | {self.ll_chunk}
+            for s in sizes:
+                model.params.compute_for(model.step_buffers(s)[0])
+            torch.cuda.current_stream().synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode=os.environ.get("EINET_CAPTURE_MODE",
+                                                                        "global")):
+                eng = self._body(model)
+            self.graph = (g, self._buffer_key(model), eng)
+        if use_graph:
+            self.graph[0].replay()
+            eng = self.graph[2]
+        else:
+            eng = self._body(model)
+        if self.lam != 0.0:
+            model.params.mark_compute_current(eng)
+        self.h_logs.copy_(self.logs, non_blocking=True)
+        self.h_sums.copy_(self.sums, non_blocking=True)
+        self.h_lstat.copy_(self.lstat, non_blocking=True)
+        self.h_ll.copy_(self.ll, non_blocking=True)
+
+    def _buffer_key(self, model):
+        return tuple(sorted((k, b[1].data_ptr(), b[2].data_ptr())
+                            for k, b in model._buffers.items())) + (
+            model.params._compute.data_ptr() if model.params._compute is not None else 0,)
+
+
 def train(model: EinetModel, data, cfg: TrainerConfig, valid=None) -> list:
     """Seeded epoch loop (reference ``trainer.py:137-162``); the dataset is
     uploaded once and batches are gathered on the device."""
@@ -387,7 +498,6 @@ def train_many(models, datasets, cfg: TrainerConfig, valids=None, streams=16) ->
     # datasets stay resident on the device (device fp32 tensors are used in place)
     xds = [engine.as_device_batch(d, device=dev) for d in datasets]
     vds = [None if v is None else engine.as_device_batch(v, device=dev) for v in valids]
-    hosts = xds
     if len(models) == 1:
         pool = [cur]
     else:
@@ -395,80 +505,36 @@ def train_many(models, datasets, cfg: TrainerConfig, valids=None, streams=16) ->
         for s in pool:
             s.wait_stream(cur)
     rngs = [np.random.default_rng(cfg.seed) for _ in models]
-    full = cfg.mode == "full"
-    nbs = [1 if full else -(-len(h) // cfg.batch_size) for h in hosts]
-    # epoch LLs run on the engine of the training steps (same workspace)
-    evc = [min(cfg.chunk, len(h) if full else min(cfg.batch_size, len(h))) for h in hosts]
+    plans = [_EpochPlan.get(m, xd, cfg) for m, xd in zip(models, xds)]
     metrics = [[] for _ in models]
     for epoch in range(cfg.epochs):
         t0 = time.perf_counter()
-        logs = [torch.empty((nb, _native.STATUS_WORDS), dtype=torch.int32, device=dev)
-                for nb in nbs]
-        sums = [torch.empty(nb, dtype=torch.float64, device=dev) for nb in nbs]
-        orders, keep = [], []
-        for c, m in enumerate(models):
-            if full:
-                orders.append(None)
-                continue
-            perm = torch.from_numpy(rngs[c].permutation(len(hosts[c])))
-            if torch.cuda.is_available():
-                perm = perm.pin_memory()
-            keep.append(perm)
+        for c, (m, ep) in enumerate(zip(models, plans)):
+            perm = None if ep.full else rngs[c].permutation(ep.n)
             with torch.cuda.stream(pool[c % len(pool)]):
-                orders.append(perm.to(dev, non_blocking=True))
-        for bi in range(max(nbs)):
-            for c, m in enumerate(models):
-                if bi >= nbs[c]:
-                    continue
-                with torch.cuda.stream(pool[c % len(pool)]):
-                    if full:
-                        status = _enqueue_step(m, xds[c], 1.0, cfg.eps_w, cfg.chunk)
-                    else:
-                        lo = bi * cfg.batch_size
-                        idx = orders[c][lo:lo + cfg.batch_size]
-                        stage = m.__dict__.setdefault("_train_stage", {})
-                        key = (idx.shape[0], xds[c].shape[1])
-                        xb = stage.get(key)
-                        if xb is None:
-                            xb = stage[key] = torch.empty(key, dtype=torch.float32, device=dev)
-                        torch.index_select(xds[c], 0, idx, out=xb)
-                        status = _enqueue_step(m, xb, cfg.step_size, cfg.eps_w, cfg.chunk)
-                    logs[c][bi].copy_(status)
-                    sums[c][bi] = m.params.flat.sum()
-        lls, vlls, lstat, vstat = [], [], [], []
-        for c, m in enumerate(models):
-            with torch.cuda.stream(pool[c % len(pool)]):
-                out, st = _enqueue_ll(m, xds[c], evc[c])
-                lstat.append(st.clone())
-                h = _pinned(out.shape, torch.float64)
-                h.copy_(out, non_blocking=True)
-                lls.append(h)
+                ep.run(m, perm)
                 if vds[c] is not None:
-                    vo, st = _enqueue_ll(m, vds[c], evc[c])
-                    vstat.append(st.clone())
-                    hv = _pinned(vo.shape, torch.float64)
-                    hv.copy_(vo, non_blocking=True)
-                    vlls.append(hv)
-                else:
-                    vstat.append(None)
-                    vlls.append(None)
+                    vo, st = _enqueue_ll(m, vds[c], ep.ll_chunk)
+                    ep.valid_host = (_pinned(vo.shape, torch.float64), st.clone())
+                    ep.valid_host[0].copy_(vo, non_blocking=True)
         for s in pool:
             s.synchronize()
-        for c, m in enumerate(models):
-            words = logs[c].cpu().tolist()
-            fin = np.isfinite(sums[c].cpu().numpy())
-            for bi in range(nbs[c]):
+        for c, (m, ep) in enumerate(zip(models, plans)):
+            words = ep.h_logs.tolist()
+            fin = np.isfinite(ep.h_sums.numpy())
+            for bi in range(ep.nb):
                 engine._raise_words(words[bi], m.family)
                 if not fin[bi]:
                     raise TrainingDiverged(
                         f"non-finite parameters after epoch {epoch}, batch {bi}")
-            engine._raise_words(lstat[c].cpu().tolist(), m.family)
-            if vstat[c] is not None:
-                engine._raise_words(vstat[c].cpu().tolist(), m.family)
+            engine._raise_words(ep.h_lstat.tolist(), m.family)
+            if vds[c] is not None:
+                engine._raise_words(ep.valid_host[1].cpu().tolist(), m.family)
         wall = time.perf_counter() - t0
-        for c in range(len(models)):
-            valid_ll = float(np.mean(vlls[c].numpy())) if vlls[c] is not None else float("nan")
-            metrics[c].append(EpochMetrics(epoch=epoch, train_ll=float(np.mean(lls[c].numpy())),
+        for c, ep in enumerate(plans):
+            valid_ll = (float(np.mean(ep.valid_host[0].numpy())) if vds[c] is not None
+                        else float("nan"))
+            metrics[c].append(EpochMetrics(epoch=epoch, train_ll=float(np.mean(ep.h_ll.numpy())),
                                            valid_ll=valid_ll, wall_seconds=wall))
     for s in pool:
         cur.wait_stream(s)
