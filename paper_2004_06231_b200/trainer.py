@@ -59,14 +59,17 @@ class EpochMetrics:
     wall_seconds: float
 
 
-def accumulate(model: EinetModel, batch: torch.Tensor, chunk: int):
+def accumulate(model: EinetModel, batch: torch.Tensor, chunk: int, reset_status=True):
     """E-step over a device batch into the model's stats buffer
-    (reference ``trainer.py:57-66``). Returns (engine, stats, status)."""
+    (reference ``trainer.py:57-66``). Returns (engine, stats, status).
+    ``reset_status=False`` keeps earlier error words (a pipelined sequence of
+    steps: once a step fails, every later M-step is skipped)."""
     n = batch.shape[0]
     eng, ws, stats, status, root = model.step_buffers(min(chunk, max(n, 1)))
     compute = model.params.compute_for(eng)
     stats.zero_()
-    eng.status_reset(status)
+    if reset_status:
+        eng.status_reset(status)
     step = eng.max_chunk if chunk >= eng.max_chunk else chunk
     for lo in range(0, n, step):
         xb = batch[lo:lo + step]
@@ -114,17 +117,19 @@ def _stage_batch(model: EinetModel, batch, normalize=None) -> torch.Tensor:
     return st
 
 
-def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_group=None):
+def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_group=None,
+                sticky=False):
     """Replay (capturing on first use) the CUDA graph of one EM step on the
     device batch ``xd``; returns (engine, stats, status). With a process group
     the step is two graphs (E-step, M-step) around the all-reduce of the
-    statistics and of the status words (NCCL, outside the graphs)."""
+    statistics and of the status words (NCCL, outside the graphs).
+    ``sticky``: the graph does not reset the status words."""
     n = xd.shape[0]
     eng, ws, stats, status, root = model.step_buffers(min(chunk, max(n, 1)))
     compute = model.params.compute_for(eng)  # prepares outside the graph if stale
     key = (xd.data_ptr(), tuple(xd.shape), float(lam), float(eps_w), int(chunk),
            model.params.flat.data_ptr(), ws.data_ptr(), compute.data_ptr(),
-           process_group is not None)
+           process_group is not None, bool(sticky))
     cache = model.__dict__.setdefault("_graphs", {})
     gs = cache.get(key)
     if gs is None:
@@ -134,7 +139,7 @@ def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_
         if process_group is None:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                accumulate(model, xd, chunk)
+                accumulate(model, xd, chunk, reset_status=not sticky)
                 eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
             gs = (g,)
         else:
@@ -221,10 +226,15 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     """Consecutive gliding-average EM steps over a sequence of host batches of
     one shape (equivalent to calling ``em_stochastic_step`` on each): the
     host->device copy of batch i+1 runs on a copy stream into the other half
-    of a double-buffered staging area while step i runs on the device. Every
-    step's LL (and error words) is read back after the step, as in
-    ``em_stochastic_step``; returns the list of mean LLs. uint8 batches are
-    copied as bytes and decoded on the device (see ``em_stochastic_step``)."""
+    of a double-buffered staging area while step i runs on the device, and
+    the host does not wait between steps: each step's LL sum and error words
+    are logged on the device and read once at the end. The error words stay
+    set across the sequence, so after a failing step every later M-step is a
+    no-op: the first failing step raises its reference exception with the
+    parameters left as after the steps before it, as a loop of
+    ``em_stochastic_step`` would. Returns the list of mean LLs. uint8 batches
+    are copied as bytes and decoded on the device (see
+    ``em_stochastic_step``)."""
     hosts = [_host_batch(b) for b in batches]
     if not hosts:
         return []
@@ -262,24 +272,38 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
             bufs[s].copy_(hosts[i], non_blocking=hosts[i].is_pinned())
             copied[s].record(copy)
 
-    issue_copy(0)
-    out = []
-    for i, h in enumerate(hosts):
+    for h in hosts:
         if tuple(h.shape) != shape or h.dtype != dtype:
             raise ValueError("em_stochastic_steps needs batches of one shape and dtype")
+    # No host sync between steps: the status words stay sticky over the
+    # sequence (a failed step makes every later M-step a no-op, so the
+    # parameters end where the reference's exception would leave them); each
+    # step's LL sum and error words go to a device log read once at the end.
+    eng, ws, stats, status, root = model.step_buffers(min(chunk, shape[0]))
+    ll_off = int(eng.sizes.stats_ll_offset)
+    log_ll = torch.empty((len(hosts), 2), dtype=torch.float64, device=dev)
+    log_st = torch.empty((len(hosts), _native.STATUS_WORDS), dtype=torch.int32, device=dev)
+    eng.status_reset(status)
+    issue_copy(0)
+    for i in range(len(hosts)):
         s = i & 1
         cur.wait_event(copied[s])
         if u8:
             engine.decode_u8(bufs[s], normalize, out=xf)  # frees bufs[s] for batch i + 2
             used[s].record(cur)
-            eng, stats, status = _graph_step(model, xf, lam, eps_w, chunk)
+            eng, stats, status = _graph_step(model, xf, lam, eps_w, chunk, sticky=True)
         else:
-            eng, stats, status = _graph_step(model, bufs[s], lam, eps_w, chunk)
+            eng, stats, status = _graph_step(model, bufs[s], lam, eps_w, chunk, sticky=True)
             used[s].record(cur)
         if i + 1 < len(hosts):
             issue_copy(i + 1)
-        out.append(_finish_step(model, eng, stats, status, lam))
-    return out
+        log_ll[i].copy_(stats[ll_off:ll_off + 2])
+        log_st[i].copy_(status)
+        model.params.mark_compute_current(eng)
+    lls = log_ll.cpu().tolist()
+    for words in log_st.cpu().tolist():
+        engine._raise_words(words, model.family)
+    return [a / b for a, b in lls]
 
 
 def em_full_step(model: EinetModel, data, eps_w=engine.EPS_W, chunk=4096,

@@ -311,6 +311,27 @@ def test_pipelined_steps_equal_sequential_steps():
     assert torch.equal(ms[0].params.flat, ms[1].params.flat)
 
 
+def test_pipelined_steps_stop_at_the_first_failing_step():
+    """A pipelined sequence whose third batch leaves the support raises the
+    reference exception (lowest bad variable of that batch) and leaves the
+    parameters exactly as after the first two steps."""
+    rg, fam, k, gen = config("C1")
+    good = [gen(64, seed=s).astype(np.float32) for s in range(4)]
+    bad = good[2].copy()
+    bad[7, 9] = 3.0
+    bad[20, 4] = 2.0
+    later = good[3].copy()
+    later[1, 1] = 5.0  # a later failure with a lower index must not win
+    seq = [good[0], good[1], bad, later]
+    ma = E.build_model(rg, fam, k=k, seed=0, data=good[0])
+    mb = E.build_model(rg, fam, k=k, seed=0, data=good[0])
+    with pytest.raises(E.UnsupportedValueError, match="variable 4"):
+        trainer.em_stochastic_steps(ma, [torch.from_numpy(b).pin_memory() for b in seq], 0.5)
+    for b in seq[:2]:
+        trainer.em_stochastic_step(mb, b, 0.5)
+    assert torch.equal(ma.params.flat, mb.params.flat)
+
+
 def test_shape_mismatch_raises():
     m = _gauss_model(11, data=np.zeros((4, 4)))
     with pytest.raises(E.EngineError):
