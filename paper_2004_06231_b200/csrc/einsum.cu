@@ -320,6 +320,27 @@ __device__ __forceinline__ float gather_rho_tile(const WsView &ws, int q0, int q
   return acc;
 }
 
+// gather_rho_tile for up to RE_MAX tile entries of one thread at once: slot by
+// slot (the same summation order per entry), all entries' loads of one slot in
+// flight together. idx(j) = tile entry of item j, or < 0 for none.
+constexpr int RE_MAX = 16;
+template <typename F>
+__device__ __forceinline__ void gather_rho_many(const WsView &ws, int q0, int q1,
+                                                const int *__restrict__ csr_slot, bool one,
+                                                int64_t b0, F idx, float (&acc)[RE_MAX]) {
+#pragma unroll
+  for (int j = 0; j < RE_MAX; ++j) acc[j] = one ? 1.0f : 0.0f;
+  if (one) return;
+  for (int q = q0; q < q1; ++q) {
+    const float *sp = ws.slots + tb_idx(csr_slot[q], b0, 0, ws.bc, ws.ks);
+#pragma unroll
+    for (int j = 0; j < RE_MAX; ++j) {
+      const int x = idx(j);
+      if (x >= 0) acc[j] += sp[x];
+    }
+  }
+}
+
 // Deterministic CTA sum of one double per thread (fixed tree, 4 warps).
 __device__ __forceinline__ double cta_sum128(double v, double *red) {
 #pragma unroll
@@ -348,6 +369,13 @@ __global__ void __launch_bounds__(128) k_mixing_bwd(
   const int q0 = csr_off[os], q1 = csr_off[os + 1];
   const bool one = ones[os] != 0;
   const float *oo = ws.off + tb_idx(os, b0, 0, ws.bc, ws.ks);
+  const int ne = Ko * 32;
+  const bool many = ne <= 128 * RE_MAX;
+  float rho[RE_MAX];  // this thread's entries e = tid + 128 j of the slab's rho
+  if (many)
+    gather_rho_many(ws, q0, q1, csr_slot, one, b0,
+                    [&](int j) { const int e = threadIdx.x + 128 * j; return e < ne ? e : -1; },
+                    rho);
   for (int c = 0; c < dmax; ++c) {
     float run = 0.f;
     if (mask[m * dmax + c]) {
@@ -355,7 +383,21 @@ __global__ void __launch_bounds__(128) k_mixing_bwd(
       const float wc = w[m * dmax + c];
       const float *oc = ws.off + tb_idx(sl, b0, 0, ws.bc, ws.ks);
       float *dst = ws.slots + tb_idx(mix_slot[m * dmax + c], b0, 0, ws.bc, ws.ks);
-      for (int e = threadIdx.x; e < Ko * 32; e += 128) {
+#pragma unroll
+      for (int j = 0; j < RE_MAX; ++j) {
+        const int e = threadIdx.x + 128 * j;
+        if (!many || e >= ne) break;
+        const int64_t b = b0 + (e & 31);
+        if (b >= B) continue;
+        const double so = slab_shift(ws, os)[b], sc = slab_shift(ws, sl)[b];
+        const bool ok = so != -CUDART_INF && sc != -CUDART_INF;
+        const float dk = (ok ? (float)(sc - so) : 0.f) + oc[e] - oo[e];
+        const float ratio = (ok && isfinite(dk)) ? expf(dk) : 0.f;
+        const float contrib = rho[j] * wc * ratio;
+        dst[e] = contrib;
+        run += contrib;
+      }
+      for (int e = threadIdx.x; !many && e < ne; e += 128) {
         const int64_t b = b0 + (e & 31);
         if (b >= B) continue;
         const double so = slab_shift(ws, os)[b], sc = slab_shift(ws, sl)[b];
@@ -391,15 +433,35 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
   const float *oo = ws.off + tb_idx(os, b0, 0, ws.bc, ws.ks);
   float *rt = RT + tb_idx(l, b0, 0, ws.bc, ws.ks);
   if (RTM == nullptr) {
-    for (int e = threadIdx.x; e < Ko * 32; e += 128) {
-      const int64_t b = b0 + (e & 31);
-      float v = 0.f;
-      if (b < B) {
-        const float r = slab_shift(ws, os)[b] == -CUDART_INF ? 0.f : expf(oo[e]);
-        const float rho = gather_rho_tile(ws, q0, q1, csr_slot, one, b0, e);
-        v = r > 0.f ? rho / r : 0.f;
+    const int ne = Ko * 32;
+    if (ne <= 128 * RE_MAX) {
+      float rhos[RE_MAX];
+      gather_rho_many(ws, q0, q1, csr_slot, one, b0,
+                      [&](int j) { const int e = threadIdx.x + 128 * j; return e < ne ? e : -1; },
+                      rhos);
+#pragma unroll
+      for (int j = 0; j < RE_MAX; ++j) {
+        const int e = threadIdx.x + 128 * j;
+        if (e >= ne) break;
+        const int64_t b = b0 + (e & 31);
+        float v = 0.f;
+        if (b < B) {
+          const float r = slab_shift(ws, os)[b] == -CUDART_INF ? 0.f : expf(oo[e]);
+          v = r > 0.f ? rhos[j] / r : 0.f;
+        }
+        rt[e] = v;  // samples past the batch hold 0 (the W statistics sum whole blocks)
       }
-      rt[e] = v;  // samples past the batch hold 0 (the W statistics sum whole blocks)
+    } else {
+      for (int e = threadIdx.x; e < ne; e += 128) {
+        const int64_t b = b0 + (e & 31);
+        float v = 0.f;
+        if (b < B) {
+          const float r = slab_shift(ws, os)[b] == -CUDART_INF ? 0.f : expf(oo[e]);
+          const float rho = gather_rho_tile(ws, q0, q1, csr_slot, one, b0, e);
+          v = r > 0.f ? rho / r : 0.f;
+        }
+        rt[e] = v;
+      }
     }
     if (RTB) {
       __syncthreads();
@@ -409,24 +471,57 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
   }
   // tensor-core path: also the RT bf16 A-operand tile (width kob, zero padded)
   const int64_t ntl = ws.bc / 128;
-  for (int e = threadIdx.x; e < (kob / 4) * 32; e += 128) {
-    const int bl = e & 31, q = e >> 5;
-    const int64_t b = b0 + bl;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-    const bool live = b < B && slab_shift(ws, os)[b] != -CUDART_INF;
+  const int ne = (kob / 4) * 32;
+  if (ne <= 128 * (RE_MAX / 4)) {
+    // all of this thread's entries gathered together: item j = 4 it + u
+    float rhos[RE_MAX];
+    gather_rho_many(ws, q0, q1, csr_slot, one, b0,
+                    [&](int j) {
+                      const int e = threadIdx.x + 128 * (j >> 2), k = 4 * (e >> 5) + (j & 3);
+                      return (e < ne && k < Ko) ? k * 32 + (e & 31) : -1;
+                    },
+                    rhos);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k = 4 * q + u;
-      if (k >= Ko) continue;
-      const int x = k * 32 + bl;
-      if (b < B) {
-        const float r = live ? expf(oo[x]) : 0.f;
-        const float rho = gather_rho_tile(ws, q0, q1, csr_slot, one, b0, x);
-        v[u] = r > 0.f ? rho / r : 0.f;
+    for (int it = 0; it < RE_MAX / 4; ++it) {
+      const int e = threadIdx.x + 128 * it;
+      if (e >= ne) break;
+      const int bl = e & 31, q = e >> 5;
+      const int64_t b = b0 + bl;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      const bool live = b < B && slab_shift(ws, os)[b] != -CUDART_INF;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = 4 * q + u;
+        if (k >= Ko) continue;
+        const int x = k * 32 + bl;
+        if (b < B) {
+          const float r = live ? expf(oo[x]) : 0.f;
+          v[u] = r > 0.f ? rhos[4 * it + u] / r : 0.f;
+        }
+        rt[x] = v[u];
       }
-      rt[x] = v[u];
+      store_bf16_quad(RTM, l, b, q, ntl, kob, make_float4(v[0], v[1], v[2], v[3]));
     }
-    store_bf16_quad(RTM, l, b, q, ntl, kob, make_float4(v[0], v[1], v[2], v[3]));
+  } else {
+    for (int e = threadIdx.x; e < ne; e += 128) {
+      const int bl = e & 31, q = e >> 5;
+      const int64_t b = b0 + bl;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      const bool live = b < B && slab_shift(ws, os)[b] != -CUDART_INF;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = 4 * q + u;
+        if (k >= Ko) continue;
+        const int x = k * 32 + bl;
+        if (b < B) {
+          const float r = live ? expf(oo[x]) : 0.f;
+          const float rho = gather_rho_tile(ws, q0, q1, csr_slot, one, b0, x);
+          v[u] = r > 0.f ? rho / r : 0.f;
+        }
+        rt[x] = v[u];
+      }
+      store_bf16_quad(RTM, l, b, q, ntl, kob, make_float4(v[0], v[1], v[2], v[3]));
+    }
   }
   if (RTB) {
     __syncthreads();

@@ -508,19 +508,47 @@ __global__ void __launch_bounds__(128) k_leaf_rho(WsView ws, const int *csr_off,
   const int q0 = csr_off[slab], q1 = csr_off[slab + 1];
   const bool one = ones[slab] != 0;
   float *rho = ws.rho + tb_idx(leaf, b0, 0, ws.bc, K);
-  for (int e = threadIdx.x; e < K * 32; e += 128) {
-    float v = 0.f;
-    if (b0 + (e & 31) < B) {
-      if (one) {
-        v = 1.f;
-      } else {
-        for (int q = q0; q < q1; ++q) v += ws.slots[tb_idx(csr_slot[q], b0, 0, ws.bc, ws.ks) + e];
+  constexpr int NE = 16;  // entries per thread gathered together (K <= 64)
+  const int ne = K * 32;
+  if (ne <= 128 * NE) {
+    // slot by slot (the per-entry summation order of the loop below), every
+    // entry's load of one slot in flight at once
+    float acc[NE];
+#pragma unroll
+    for (int j = 0; j < NE; ++j) acc[j] = one ? 1.f : 0.f;
+    for (int q = q0; !one && q < q1; ++q) {
+      const float *sp = ws.slots + tb_idx(csr_slot[q], b0, 0, ws.bc, ws.ks);
+#pragma unroll
+      for (int j = 0; j < NE; ++j) {
+        const int e = threadIdx.x + 128 * j;
+        if (e < ne) acc[j] += sp[e];
       }
     }
-    rho[e] = v;  // samples past the batch hold 0 (the statistics sum whole blocks)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if ((e & 31) == 0) ppart[((int64_t)blockIdx.x * n_leaf + leaf) * K + (e >> 5)] = (double)v;
+    for (int j = 0; j < NE; ++j) {
+      const int e = threadIdx.x + 128 * j;
+      if (e >= ne) break;
+      float v = b0 + (e & 31) < B ? acc[j] : 0.f;
+      rho[e] = v;  // samples past the batch hold 0 (the statistics sum whole blocks)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if ((e & 31) == 0) ppart[((int64_t)blockIdx.x * n_leaf + leaf) * K + (e >> 5)] = (double)v;
+    }
+  } else {
+    for (int e = threadIdx.x; e < ne; e += 128) {
+      float v = 0.f;
+      if (b0 + (e & 31) < B) {
+        if (one) {
+          v = 1.f;
+        } else {
+          for (int q = q0; q < q1; ++q) v += ws.slots[tb_idx(csr_slot[q], b0, 0, ws.bc, ws.ks) + e];
+        }
+      }
+      rho[e] = v;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if ((e & 31) == 0) ppart[((int64_t)blockIdx.x * n_leaf + leaf) * K + (e >> 5)] = (double)v;
+    }
   }
   if (nn > 0) {  // tensor-core leaf statistics: the block's rho^T B operand
     __syncthreads();
