@@ -369,18 +369,16 @@ def run_ours(args):
     e2e_steps = max(3, args.steps)  # the pipelined API fills once per call
 
     def e2e_leg(xh):
-        if group is None:
-            # the public multi-step API: batch i+1's host->device copy overlaps step i
-            return timed(lambda: trainer.em_stochastic_steps(model, [xh] * e2e_steps, 0.5,
-                                                              chunk=args.chunk), 1)
-        return timed(lambda: step(xh), e2e_steps)  # the API stages the pinned batch
+        # the public multi-step API: batch i+1's host->device copy overlaps step i,
+        # no host wait between steps (N > 1: the NCCL all-reduces between graphs)
+        return timed(lambda: trainer.em_stochastic_steps(model, [xh] * e2e_steps, 0.5,
+                                                          chunk=args.chunk,
+                                                          process_group=group), 1)
 
     # the u8 and fp32 host batches decode to the same device values
     assert torch.equal(engine.as_device_batch(x_u8.to(dev)), x_dev)
     for xh in (x_u8, x_host):  # staging buffers and their graphs exist before timing
-        trainer.em_stochastic_steps(model, [xh] * 2, 0.5, chunk=args.chunk)
-        if group is not None:
-            step(xh)
+        trainer.em_stochastic_steps(model, [xh] * 2, 0.5, chunk=args.chunk, process_group=group)
     ms_e2e = e2e_leg(x_u8)
     ms_e2e_f32 = e2e_leg(x_host)
 

@@ -145,7 +145,7 @@ def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_
         else:
             ge, gm = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             with torch.cuda.graph(ge):
-                accumulate(model, xd, chunk)
+                accumulate(model, xd, chunk, reset_status=not sticky)
             with torch.cuda.graph(gm):
                 eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
             gs = (ge, gm)
@@ -222,7 +222,7 @@ def _host_batch(batch) -> torch.Tensor:
 
 
 def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
-                        chunk=4096, normalize=None) -> list:
+                        chunk=4096, normalize=None, process_group=None) -> list:
     """Consecutive gliding-average EM steps over a sequence of host batches of
     one shape (equivalent to calling ``em_stochastic_step`` on each): the
     host->device copy of batch i+1 runs on a copy stream into the other half
@@ -234,13 +234,16 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     parameters left as after the steps before it, as a loop of
     ``em_stochastic_step`` would. Returns the list of mean LLs. uint8 batches
     are copied as bytes and decoded on the device (see
-    ``em_stochastic_step``)."""
+    ``em_stochastic_step``). With an NCCL ``process_group`` each step is the
+    E-step graph, the all-reduces of the statistics and error words, and the
+    M-step graph, still without a host wait."""
     hosts = [_host_batch(b) for b in batches]
     if not hosts:
         return []
-    if lam == 0.0 or not _graphs_enabled() or hosts[0].is_cuda:
-        return [em_stochastic_step(model, b, lam, eps_w, chunk, normalize=normalize)
-                for b in hosts]
+    if (lam == 0.0 or not _graphs_enabled() or hosts[0].is_cuda or
+            (process_group is not None and not _nccl_group(process_group))):
+        return [em_stochastic_step(model, b, lam, eps_w, chunk, process_group=process_group,
+                                   normalize=normalize) for b in hosts]
     shape = tuple(hosts[0].shape)
     dtype = hosts[0].dtype
     if shape[0] == 0:
@@ -291,9 +294,11 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
         if u8:
             engine.decode_u8(bufs[s], normalize, out=xf)  # frees bufs[s] for batch i + 2
             used[s].record(cur)
-            eng, stats, status = _graph_step(model, xf, lam, eps_w, chunk, sticky=True)
+            eng, stats, status = _graph_step(model, xf, lam, eps_w, chunk, process_group,
+                                             sticky=True)
         else:
-            eng, stats, status = _graph_step(model, bufs[s], lam, eps_w, chunk, sticky=True)
+            eng, stats, status = _graph_step(model, bufs[s], lam, eps_w, chunk, process_group,
+                                             sticky=True)
             used[s].record(cur)
         if i + 1 < len(hosts):
             issue_copy(i + 1)
