@@ -201,6 +201,83 @@ __global__ void k_einsum_fwd_generic(WsView ws, const float *__restrict__ EA,
   }
 }
 
+// Forward for 64 < K <= 128 on CUDA cores (the register-tile kernel above
+// keeps a sample's EA, EB rows in registers, which stops scaling past 64).
+// out[b,k] = log sum_i EA[b,i] sum_j W[k,i,j] EB[b,j] (engine.py:91-109) as a
+// tiled GEMM per (row, k): the CTA stages W[k] transposed ([j][i]) and the
+// tile's EB, EA rows in shared memory; a thread accumulates s[b][i] =
+// sum_j W[k,i,j] EB[b,j] for 4 samples x 8 i (per j: one 16-byte EB load, two
+// 16-byte W loads, 32 FMAs), folds in EA[b,i] and the 16 i-groups are summed
+// in fixed order. grid (ceil(B/64), rows, K_out), block 256.
+constexpr int FB_TB = 64, FB_KP = 128, FB_WS = FB_KP + 4;
+size_t fwd_big_smem() {
+  return sizeof(float) * ((size_t)FB_KP * FB_WS + 2 * FB_KP * FB_TB + 16 * FB_TB);
+}
+__global__ void __launch_bounds__(256) k_einsum_fwd_big(WsView ws, const float *__restrict__ EA,
+                                                        const float *__restrict__ EB,
+                                                        const int *out_slab,
+                                                        const float *__restrict__ W, int64_t B,
+                                                        int K, int Ko) {
+  extern __shared__ __align__(16) float fsm[];
+  float *wt = fsm;                       // [j][FB_WS]: W[k][i][j] at wt[j][i]
+  float *ebs = wt + FB_KP * FB_WS;       // [j][64]
+  float *eas = ebs + FB_KP * FB_TB;      // [i][64]
+  float *red = eas + FB_KP * FB_TB;      // [16][64]
+  const int tid = threadIdx.x, l = blockIdx.y, k = blockIdx.z;
+  const int64_t b0 = (int64_t)blockIdx.x * FB_TB;
+  const float *Wk = W + ((int64_t)l * Ko + k) * K * K;
+  for (int e = tid; e < FB_KP * FB_KP; e += 256) {
+    const int i = e / FB_KP, j = e - i * FB_KP;
+    wt[j * FB_WS + i] = (i < K && j < K) ? Wk[i * K + j] : 0.f;
+  }
+  for (int e = tid; e < FB_KP * FB_TB; e += 256) {
+    const int r = e >> 6, s = e & 63;
+    const int64_t b = b0 + s;
+    float vb = 0.f, va = 0.f;
+    if (r < K && b < ws.bc) {
+      const int64_t x = ev_idx(l, b, r, ws.bc, K);
+      vb = EB[x];
+      va = EA[x];
+    }
+    ebs[e] = vb;
+    eas[e] = va;
+  }
+  __syncthreads();
+  const int sg = tid & 15, ig = tid >> 4;
+  float s[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s[a][c] = 0.f;
+  for (int j = 0; j < K; ++j) {
+    const float4 eb = *(const float4 *)(ebs + j * FB_TB + sg * 4);
+    const float4 w0 = *(const float4 *)(wt + j * FB_WS + ig * 8);
+    const float4 w1 = *(const float4 *)(wt + j * FB_WS + ig * 8 + 4);
+    const float ebv[4] = {eb.x, eb.y, eb.z, eb.w};
+    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) s[a][c] = fmaf(wv[c], ebv[a], s[a][c]);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    float part = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) part = fmaf(eas[(ig * 8 + c) * FB_TB + sg * 4 + a], s[a][c], part);
+    red[ig * FB_TB + sg * 4 + a] = part;
+  }
+  __syncthreads();
+  if (tid < FB_TB) {
+    const int64_t b = b0 + tid;
+    if (b < B) {
+      float acc = 0.f;
+      for (int g = 0; g < 16; ++g) acc += red[g * FB_TB + tid];
+      slab_off(ws, out_slab[l], b)[k] = acc > 0.f ? logf(acc) : -CUDART_INF_F;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // mixing layers (engine.py:112-122, 268-293)
 // ---------------------------------------------------------------------------
@@ -535,7 +612,7 @@ constexpr int WS_BT = 32;  // samples per fp32 run of the W statistics
 // Register tile 4x4 of (i, j) per thread; block K4*K4 threads.
 __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__restrict__ EB,
                                 const float *__restrict__ RT, int64_t Bc, int ks, int64_t B,
-                                int K, int Ko, int L, int bsplit, double *wpart) {
+                                int K, int Ko, int L, int bsplit, double *wpart, int ti_per) {
   extern __shared__ __align__(16) float sm[];
   const int K4 = (K + 3) / 4;
   const int KP = K4 * 4;
@@ -545,7 +622,9 @@ __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__res
   const int g = blockIdx.x;
   const int l = g / Ko, k = g % Ko;
   const int split = blockIdx.y;
-  const int ti = threadIdx.x / K4, tj = threadIdx.x % K4;
+  // K > 64: the slice's i-rows of 4 are split over blockIdx.z (<= 256 threads)
+  const int ti = blockIdx.z * ti_per + threadIdx.x / K4, tj = threadIdx.x % K4;
+  const bool act = ti < K4;
   const int64_t per = (B + bsplit - 1) / bsplit;
   const int64_t bb = split * per, be = min(B, bb + per);
   float acc[4][4];
@@ -569,7 +648,7 @@ __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__res
     for (int e = threadIdx.x; e < WS_BT; e += blockDim.x)
       rt_s[e] = e < nb ? RT[tb_idx(l, t + e, k, Bc, ks)] : 0.f;
     __syncthreads();
-    for (int bl = 0; bl < nb; ++bl) {
+    for (int bl = 0; act && bl < nb; ++bl) {
       const float r = rt_s[bl];
       const float4 a4 = *(const float4 *)(ea_s + bl * KP + 4 * ti);
       const float4 e4 = *(const float4 *)(eb_s + bl * KP + 4 * tj);
@@ -594,7 +673,7 @@ __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__res
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int i = 4 * ti + u, j = 4 * tj + v;
-      if (i < K && j < K) dst[i * K + j] = tot[u][v];
+      if (act && i < K && j < K) dst[i * K + j] = tot[u][v];
     }
 }
 
@@ -770,7 +849,17 @@ static void einsum_forward_simt(const LayerPlan &L, const float *w32, const floa
   else if (K <= 40) fwd_simt<40>(L, w32, EA, EB, w, B, K, st);
   else if (K <= 48) fwd_simt<48>(L, w32, EA, EB, w, B, K, st);
   else if (K <= 64) fwd_simt<64>(L, w32, EA, EB, w, B, K, st);
-  else {
+  else if (K <= FB_KP) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_einsum_fwd_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)fwd_big_smem());
+      attr = true;
+    }
+    dim3 grid(ceil_div(B, FB_TB), L.rows, L.k_out);
+    k_einsum_fwd_big<<<grid, 256, fwd_big_smem(), st>>>(w, EA, EB, L.d_out_slab, w32 + L.w_off,
+                                                       B, K, L.k_out);
+  } else {
     dim3 grid(ceil_div(B, 128), L.rows);
     k_einsum_fwd_generic<<<grid, 128, 0, st>>>(w, EA, EB, L.d_out_slab, w32 + L.w_off, B, K,
                                                L.k_out);
@@ -899,9 +988,11 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
         const int bs = wstats_bsplit(p, L, B);
         const int K4 = (K + 3) / 4;
         const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT);
-        dim3 g2(L.rows * L.k_out, bs);
-        k_einsum_wstats<<<g2, K4 * K4, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K, L.k_out,
-                                                   L.rows, bs, w.wpart);
+        int ti_per = K4;
+        while (ti_per * K4 > 256) ti_per = (ti_per + 1) / 2;
+        dim3 g2(L.rows * L.k_out, bs, ceil_div(K4, ti_per));
+        k_einsum_wstats<<<g2, ti_per * K4, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K, L.k_out,
+                                                       L.rows, bs, w.wpart, ti_per);
         launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);
       }
     }

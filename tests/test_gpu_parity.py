@@ -162,6 +162,61 @@ def test_c3_full_batch_vs_oracle():
         close(phi2, op.phi, P_RTOL, PHI_ATOL)
 
 
+def test_c4_celeba_shape_vs_oracle():
+    """BASELINE.json configs[3]: the CelebA-shaped 128x128x3 PD EiNet (delta 32
+    vertical, K=40, 49152 variables in 4 leaf regions of 12288) through
+    forward, back-pass statistics and two EM steps at B=8."""
+    rg, fam, k, gen = config("C4")
+    circuit = E.compile_graph(rg, k)
+    x = gen(8, seed=6).astype(np.float32).astype(np.float64)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=gen(64, seed=7))
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    op = O.OracleParams({i: f32(w) for i, w in ein.items()}, {i: f32(w) for i, w in mix.items()},
+                        f32(phi))
+    p = engine.Parameters.from_numpy(circuit, fam, op.einsum, op.mixing, op.phi)
+    tr = O.forward(circuit, op, fam.to_dict(), x)
+    got = E.forward(circuit, p, fam, x)
+    ll_close(got.log_likelihood, tr.root[:, 0])
+    st = O.backward(circuit, op, fam.to_dict(), tr)
+    gs = E.backward(circuit, p, fam, got)
+    for i in st.einsum:
+        close(gs.einsum[i], st.einsum[i], P_RTOL, 1e-6 * 8)
+    close(gs.acc_pt, st.acc_pt, P_RTOL, 1e-6 * 8)
+    model = E.EinetModel(circuit, p, fam)
+    for step in range(2):
+        want_ll, op = O.em_step(circuit, op, fam.to_dict(), x, 0.5)
+        ll = trainer.em_stochastic_step(model, x, 0.5)
+        assert abs(ll - want_ll) <= LL_RTOL * abs(want_ll)
+        e2, m2, phi2 = p.to_numpy()
+        for i in e2:
+            close(e2[i], op.einsum[i], P_RTOL, 1e-9)
+        close(phi2, op.phi, P_RTOL, PHI_ATOL)
+
+
+@pytest.mark.parametrize("k", [72, 96, 128])
+def test_large_k_cuda_core_path_vs_oracle(k):
+    """K > 64 (BASELINE.json configs[4] sweeps K up to 128) runs the CUDA-core
+    kernels (tiled forward for K <= 128): forward and one EM step vs oracle."""
+    rg = E.random_binary_tree(12, StructureConfig(depth=2, replicas=2, seed=4))
+    x = np.random.default_rng(k).normal(0.4, 0.3, (48, 12)).astype(np.float32).astype(np.float64)
+    fam = E.GaussianFamily()
+    circuit = E.compile_graph(rg, k)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=1, data=x)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    op = O.OracleParams({i: f32(w) for i, w in ein.items()}, {i: f32(w) for i, w in mix.items()},
+                        f32(phi))
+    p = engine.Parameters.from_numpy(circuit, fam, op.einsum, op.mixing, op.phi)
+    ll_close(E.forward(circuit, p, fam, x).log_likelihood,
+             O.forward(circuit, op, fam.to_dict(), x).root[:, 0])
+    want_ll, op = O.em_step(circuit, op, fam.to_dict(), x, 0.5)
+    ll = trainer.em_stochastic_step(E.EinetModel(circuit, p, fam), x, 0.5)
+    assert abs(ll - want_ll) <= LL_RTOL * abs(want_ll)
+    e2, m2, phi2 = p.to_numpy()
+    for i in e2:
+        close(e2[i], op.einsum[i], P_RTOL, 1e-9)
+    close(phi2, op.phi, P_RTOL, PHI_ATOL)
+
+
 # ---------------------------------------------------------------------------
 # reference properties (test_trainer.py, test_engine.py, test_acceptance.py)
 # ---------------------------------------------------------------------------
