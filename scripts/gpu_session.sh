@@ -23,7 +23,7 @@ launches)
   echo "launches rc=$?" >> $OUT/status.txt ;;
 full)
   timeout 900 ncu --set full --clock-control none --import-source on -s 10 -c ${NCU_COUNT:-8} \
-    -k "regex:${NCU_KERNELS:-k_leaf_fwd|k_einsum_wstats_tc|k_einsum_childrho_tc|k_leaf_stats|k_einsum_fwd_tc}" \
+    -k "regex:${NCU_KERNELS:-k_leaf_fwd_dmma|k_contract_tc|k_wstats_tc|k_leaf_stats_tc}" \
     -o $OUT/full python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/full.log 2>&1
   echo "full rc=$?" >> $OUT/status.txt ;;
 esac
