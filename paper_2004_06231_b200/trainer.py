@@ -259,20 +259,23 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
         bufs = [torch.empty(shape, dtype=dtype, device=dev) for _ in range(2)]
         model.__dict__[key] = bufs
     u8 = dtype == torch.uint8
-    if u8:
-        xf = model.__dict__.get("_staging")
-        if xf is None or tuple(xf.shape) != shape:
-            xf = torch.empty(shape, dtype=torch.float32, device=dev)
-            model.__dict__["_staging"] = xf
+    if u8:  # u8 batches are decoded on the copy stream into their own fp32 halves
+        xfs = model.__dict__.get("_stage2_dec")
+        if xfs is None or tuple(xfs[0].shape) != shape:
+            xfs = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
+            model.__dict__["_stage2_dec"] = xfs
     cur = torch.cuda.current_stream(dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     used = [torch.cuda.Event(), torch.cuda.Event()]
 
     def issue_copy(i):
+        # batch i's copy (and decode) into half i % 2 once step i - 2 is done with it
         s = i & 1
         copy.wait_stream(cur) if i < 2 else copy.wait_event(used[s])
         with torch.cuda.stream(copy):
             bufs[s].copy_(hosts[i], non_blocking=hosts[i].is_pinned())
+            if u8:
+                engine.decode_u8(bufs[s], normalize, out=xfs[s])
             copied[s].record(copy)
 
     for h in hosts:
@@ -291,15 +294,9 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     for i in range(len(hosts)):
         s = i & 1
         cur.wait_event(copied[s])
-        if u8:
-            engine.decode_u8(bufs[s], normalize, out=xf)  # frees bufs[s] for batch i + 2
-            used[s].record(cur)
-            eng, stats, status = _graph_step(model, xf, lam, eps_w, chunk, process_group,
-                                             sticky=True)
-        else:
-            eng, stats, status = _graph_step(model, bufs[s], lam, eps_w, chunk, process_group,
-                                             sticky=True)
-            used[s].record(cur)
+        eng, stats, status = _graph_step(model, xfs[s] if u8 else bufs[s], lam, eps_w, chunk,
+                                         process_group, sticky=True)
+        used[s].record(cur)
         if i + 1 < len(hosts):
             issue_copy(i + 1)
         log_ll[i].copy_(stats[ll_off:ll_off + 2])
