@@ -386,13 +386,38 @@ __global__ void __launch_bounds__(256) k_leaf_finalize(
   const int nb = (int)min((int64_t)32, B - b0);
   const int slab = leaf_slab[leaf];
   bool bad = false;
-  for (int e = threadIdx.x; e < nb * K; e += 256) {
-    const int bl = e / K, k = e - bl * K;
-    const double *src = part + ((int64_t)leaf * ws.bc + b0) * K + e;
-    double s = 0.0;
-    for (int q = 0; q < dsplit; ++q) s += src[(int64_t)q * n_leaf * ws.bc * K];
-    vals[bl * (K + 1) + k] = cnst[leaf * K + k] + sign * s;
-    bad |= !isfinite(s);
+  const int64_t qs = (int64_t)n_leaf * ws.bc * K;  // split stride
+  const double *base = part + ((int64_t)leaf * ws.bc + b0) * K;
+  if ((K & 1) == 0) {
+    // two adjacent entries per thread: 16-byte loads, every split's load in
+    // flight before the (split-ordered) sums
+    for (int e2 = threadIdx.x; e2 < nb * K / 2; e2 += 256) {
+      const int e = 2 * e2, bl = e / K, k = e - bl * K;
+      double s0 = 0.0, s1 = 0.0;
+      for (int q0 = 0; q0 < dsplit; q0 += 8) {
+        double2 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q0 + q < dsplit) v[q] = __ldcs((const double2 *)(base + (q0 + q) * qs + e));
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q0 + q < dsplit) {
+            s0 += v[q].x;
+            s1 += v[q].y;
+          }
+      }
+      vals[bl * (K + 1) + k] = cnst[leaf * K + k] + sign * s0;
+      vals[bl * (K + 1) + k + 1] = cnst[leaf * K + k + 1] + sign * s1;
+      bad |= !isfinite(s0) || !isfinite(s1);
+    }
+  } else {
+    for (int e = threadIdx.x; e < nb * K; e += 256) {
+      const int bl = e / K, k = e - bl * K;
+      double s = 0.0;
+      for (int q = 0; q < dsplit; ++q) s += base[q * qs + e];
+      vals[bl * (K + 1) + k] = cnst[leaf * K + k] + sign * s;
+      bad |= !isfinite(s);
+    }
   }
   if (bad && status) atomicMin(&status[2], 0);  // non-finite x reached a leaf row
   __syncthreads();
