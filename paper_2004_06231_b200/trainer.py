@@ -398,7 +398,9 @@ class _EpochPlan:
         self.eps_w, self.chunk = cfg.eps_w, cfg.chunk
         self.bs = self.n if self.full else cfg.batch_size
         self.nb = -(-self.n // self.bs)
-        self.ll_chunk = min(cfg.chunk, self.bs, self.n)
+        # epoch log-likelihoods in chunks of up to cfg.chunk (the reference's
+        # log_likelihood chunking), on their own engine bucket
+        self.ll_chunk = min(cfg.chunk, self.n)
         self.order = None if self.full else torch.empty(self.n, dtype=torch.int64, device=dev)
         self.logs = torch.empty((self.nb, _native.STATUS_WORDS), dtype=torch.int32, device=dev)
         self.sums = torch.empty(self.nb, dtype=torch.float64, device=dev)
