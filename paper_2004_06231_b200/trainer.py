@@ -240,10 +240,12 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     hosts = [_host_batch(b) for b in batches]
     if not hosts:
         return []
-    if (lam == 0.0 or not _graphs_enabled() or hosts[0].is_cuda or
+    if (lam == 0.0 or not _graphs_enabled() or
             (process_group is not None and not _nccl_group(process_group))):
         return [em_stochastic_step(model, b, lam, eps_w, chunk, process_group=process_group,
                                    normalize=normalize) for b in hosts]
+    if hosts[0].is_cuda:
+        return _device_steps(model, hosts, lam, eps_w, chunk, normalize, process_group)
     shape = tuple(hosts[0].shape)
     dtype = hosts[0].dtype
     if shape[0] == 0:
@@ -299,6 +301,46 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
         used[s].record(cur)
         if i + 1 < len(hosts):
             issue_copy(i + 1)
+        log_ll[i].copy_(stats[ll_off:ll_off + 2])
+        log_st[i].copy_(status)
+        model.params.mark_compute_current(eng)
+    lls = log_ll.cpu().tolist()
+    for words in log_st.cpu().tolist():
+        engine._raise_words(words, model.family)
+    return [a / b for a, b in lls]
+
+
+def _device_steps(model, batches, lam, eps_w, chunk, normalize, process_group):
+    """em_stochastic_steps over device-resident batches: fp32 batches are used
+    in place (one CUDA graph per distinct buffer), u8 batches are decoded into
+    the two fp32 staging halves; sticky error words and device logs as in the
+    host pipeline, one host sync at the end."""
+    dev = model.params.flat.device
+    if not all(b.is_cuda for b in batches):
+        raise ValueError("em_stochastic_steps needs all batches on the host or all on the device")
+    shape = tuple(batches[0].shape)
+    if shape[0] == 0:
+        raise ValueError("empty batch")
+    if any(tuple(b.shape) != shape or b.dtype != batches[0].dtype for b in batches):
+        raise ValueError("em_stochastic_steps needs batches of one shape and dtype")
+    u8 = batches[0].dtype == torch.uint8
+    if u8:
+        xfs = model.__dict__.get("_stage2_dec")
+        if xfs is None or tuple(xfs[0].shape) != shape:
+            xfs = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
+            model.__dict__["_stage2_dec"] = xfs
+    eng, ws, stats, status, root = model.step_buffers(min(chunk, shape[0]))
+    ll_off = int(eng.sizes.stats_ll_offset)
+    log_ll = torch.empty((len(batches), 2), dtype=torch.float64, device=dev)
+    log_st = torch.empty((len(batches), _native.STATUS_WORDS), dtype=torch.int32, device=dev)
+    eng.status_reset(status)
+    for i, b in enumerate(batches):
+        if u8:
+            xd = engine.decode_u8(b, normalize, out=xfs[i & 1])
+        else:
+            xd = engine.as_device_batch(b)
+        eng, stats, status = _graph_step(model, xd, lam, eps_w, chunk, process_group,
+                                         sticky=True)
         log_ll[i].copy_(stats[ll_off:ll_off + 2])
         log_st[i].copy_(status)
         model.params.mark_compute_current(eng)

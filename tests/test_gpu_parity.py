@@ -366,6 +366,24 @@ def test_pipelined_steps_equal_sequential_steps():
     assert torch.equal(ms[0].params.flat, ms[1].params.flat)
 
 
+def test_device_resident_pipelined_steps_equal_sequential_steps():
+    """em_stochastic_steps on device-resident fp32 and u8 batches (no copies,
+    no host wait) equals em_stochastic_step per batch bitwise."""
+    rg, fam, k, gen = config("C2")
+    xs = [gen(256, seed=s) for s in range(3)]
+    for kind in ("f32", "u8"):
+        if kind == "f32":
+            dev = [torch.from_numpy(x.astype(np.float32)).cuda() for x in xs]
+        else:
+            dev = [torch.from_numpy(np.rint(x * 255).astype(np.uint8)).cuda() for x in xs]
+        ma = E.build_model(rg, fam, k=k, seed=0, data=xs[0])
+        mb = E.build_model(rg, fam, k=k, seed=0, data=xs[0])
+        la = trainer.em_stochastic_steps(ma, dev, 0.5, chunk=128)
+        lb = [trainer.em_stochastic_step(mb, b, 0.5, chunk=128) for b in dev]
+        assert la == lb
+        assert torch.equal(ma.params.flat, mb.params.flat)
+
+
 def test_pipelined_steps_stop_at_the_first_failing_step():
     """A pipelined sequence whose third batch leaves the support raises the
     reference exception (lowest bad variable of that batch) and leaves the
