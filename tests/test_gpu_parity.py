@@ -141,6 +141,65 @@ def test_random_fixtures_vs_oracle(seed):
     close(st.acc_pt, ost.acc_pt, P_RTOL, 1e-6 * len(data))
 
 
+def _random_tc_model(seed):
+    """Random structures on the tensor-core / DMMA paths: K a multiple of 8,
+    RAT or PD graphs, all three families, ragged batch sizes."""
+    rng = np.random.default_rng(1000 + seed)
+    k = int(rng.choice([8, 16, 24, 32, 40, 48, 56, 64]))
+    if seed % 3 == 2:
+        h, w = int(rng.integers(2, 5)), int(rng.integers(2, 5))
+        rg = E.poon_domingos(h, w, StructureConfig(deltas=(1,), axes="both"))
+    else:
+        d = int(rng.integers(4, 33))
+        depth = min(int(rng.integers(1, 4)), int(np.floor(np.log2(d))))
+        rg = random_binary_tree(d, StructureConfig(depth=depth,
+                                                   replicas=int(rng.integers(1, 4)),
+                                                   seed=int(rng.integers(1 << 30))))
+    d = rg.d_vars
+    b = int(rng.integers(33, 300))
+    kind = ["gaussian", "categorical", "binomial"][seed % 3 if seed % 3 != 2 else 0]
+    if kind == "gaussian":
+        fam = E.GaussianFamily()
+        data = rng.normal(0.3, 0.5, size=(b, d))
+    elif kind == "categorical":
+        fam = E.CategoricalFamily(int(rng.integers(2, 5)))
+        data = rng.integers(0, fam.num_states, size=(b, d)).astype(float)
+    else:
+        fam = E.BinomialFamily(int(rng.integers(1, 9)))
+        data = rng.integers(0, fam.n_trials + 1, size=(b, d)).astype(float)
+    data = data.astype(np.float32).astype(np.float64)
+    circuit = E.compile_graph(rg, k)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=seed, data=data)
+    mask = rng.random(d) < 0.25 if seed % 4 == 1 else None
+    return circuit, fam, data, (ein, mix, phi), mask
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_tensor_core_paths_vs_oracle(seed):
+    circuit, fam, data, (ein, mix, phi), mask = _random_tc_model(seed)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)
+    op = O.OracleParams({i: f32(w) for i, w in ein.items()}, {i: f32(w) for i, w in mix.items()},
+                        f32(phi))
+    p = engine.Parameters.from_numpy(circuit, fam, op.einsum, op.mixing, op.phi)
+    tr = engine.forward(circuit, p, fam, data, marg_mask=mask)
+    otr = O.forward(circuit, op, fam.to_dict(), data, mask)
+    ll_close(tr.log_likelihood, otr.log_likelihood)
+    st = engine.backward(circuit, p, fam, tr)
+    ost = O.backward(circuit, op, fam.to_dict(), otr)
+    for i in ost.einsum:
+        close(st.einsum[i], ost.einsum[i], P_RTOL, 1e-6 * len(data))
+    close(st.acc_p, ost.acc_p, P_RTOL, 1e-6 * len(data))
+    close(st.acc_pt, ost.acc_pt, P_RTOL, 1e-6 * len(data))
+    if mask is None:
+        want_ll, op = O.em_step(circuit, op, fam.to_dict(), data, 0.5)
+        ll = trainer.em_stochastic_step(E.EinetModel(circuit, p, fam), data, 0.5)
+        assert abs(ll - want_ll) <= LL_RTOL * max(abs(want_ll), 1.0)
+        e2, m2, phi2 = p.to_numpy()
+        for i in e2:
+            close(e2[i], op.einsum[i], P_RTOL, 1e-9)
+        close(phi2, op.phi, P_RTOL, PHI_ATOL)
+
+
 def test_c3_full_batch_vs_oracle():
     """The headline configuration at B=64 through the whole EM step."""
     rg, fam, k, gen = config("C3")
