@@ -322,8 +322,8 @@ __global__ void __launch_bounds__(128) k_mixing_fwd(
         if (sc[c] > sh || sc[c] != sc[c]) sh = sc[c];
       }
     }
-    if (wid == 0) slab_shift(ws, os)[b] = sh;
-    for (int k = wid; k < Ko; k += 4) {
+    if (wid == 0 && blockIdx.z == 0) slab_shift(ws, os)[b] = sh;
+    for (int k = wid + 4 * blockIdx.z; k < Ko; k += 4 * gridDim.z) {
       const int e = k * 32 + lane;
       if (sh == -CUDART_INF) {
         o[e] = 0.f;
@@ -356,8 +356,8 @@ __global__ void __launch_bounds__(128) k_mixing_fwd(
     const double scc = slab_shift(ws, src[c])[b];
     if (scc > sh || scc != scc) sh = scc;
   }
-  if (wid == 0) slab_shift(ws, os)[b] = sh;
-  for (int k = wid; k < Ko; k += 4) {
+  if (wid == 0 && blockIdx.z == 0) slab_shift(ws, os)[b] = sh;
+  for (int k = wid + 4 * blockIdx.z; k < Ko; k += 4 * gridDim.z) {
     const int e = k * 32 + lane;
     if (sh == -CUDART_INF) {
       o[e] = 0.f;
@@ -919,7 +919,11 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
       count_launch(2);
     } else {
       ProfScope prof("mixing_fwd", st);
-      dim3 grid(ceil_div(B, 32), L.rows);
+      // small batches: the k-range is split over blockIdx.z to fill the SMs
+      const int64_t ctas = (int64_t)ceil_div(B, 32) * L.rows;
+      const int kz = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.k_out, 4),
+                                                                 ceil_div(2 * p.num_sms, ctas)));
+      dim3 grid(ceil_div(B, 32), L.rows, kz);
       k_mixing_fwd<<<grid, 128, 8 * L.dmax, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
                                          c.mix32 + L.mix_off, B, L.k_out, L.dmax, L.index,
                                          status);
