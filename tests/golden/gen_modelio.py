@@ -20,7 +20,7 @@ import numpy as np
 
 REF = "/root/reference/pkg/src"
 HERE = os.path.dirname(os.path.abspath(__file__))
-CASES = ["rat_gaussian", "rat_categorical4", "pd_lift_gaussian_image"]
+CASES = ["rat_gaussian", "rat_categorical4", "pd_lift_gaussian_image", "rat_binomial"]
 
 
 def provenance(name):

@@ -34,6 +34,8 @@ CASES = [
     ("rat_categorical4", None),
     ("rat_categorical4", [1, 2]),
     ("pd_lift_gaussian_image", None),
+    ("rat_binomial", [0, 4]),
+    ("pd_lift_gaussian_image", list(range(0, 48, 2))),
 ]
 
 

@@ -25,7 +25,7 @@ from paper_2004_06231_b200.structures import RegionGraph
 
 from tests.helpers import GOLDEN, Case
 
-FILES = ["rat_gaussian", "rat_categorical4", "pd_lift_gaussian_image"]
+FILES = ["rat_gaussian", "rat_categorical4", "pd_lift_gaussian_image", "rat_binomial"]
 
 
 def read(name):
