@@ -122,3 +122,60 @@ def test_acceptance_persistence(seed, tmp_path):
     modelio.save_model(path, model)
     again = modelio.load_model(path)
     assert np.array_equal(model.log_likelihood(x), again.log_likelihood(x))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_acceptance_gradient_identity(seed):
+    """Criterion 03 (test_acceptance.py:56-89): the device EM statistics are
+    the reference's gradient identity -- acc / (w * B) = d mean LL / d w for
+    einsum and mixing weights, acc_p / B = d mean LL / d (leaf log offset) --
+    checked against fp64 central differences of the oracle's forward pass."""
+    from oracle import einet_oracle as O
+    rng = np.random.default_rng(300 + seed)
+    d = int(rng.integers(2, 8))
+    depth = min(int(rng.integers(1, 3)), int(np.floor(np.log2(d))))
+    rg = E.random_binary_tree(d, StructureConfig(depth=depth, replicas=int(rng.integers(1, 4)),
+                                                 seed=seed))
+    if seed % 2:
+        fam = E.CategoricalFamily(3)
+        x = rng.integers(0, 3, (24, d)).astype(float)
+    else:
+        fam = E.GaussianFamily()
+        x = rng.normal(size=(24, d)).astype(np.float32).astype(np.float64)
+    circuit = E.compile_graph(rg, int(rng.choice([2, 3, 8])))
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=seed, data=x)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    op = O.OracleParams({i: f32(w) for i, w in ein.items()}, {i: f32(w) for i, w in mix.items()},
+                        f32(phi))
+    p = engine.Parameters.from_numpy(circuit, fam, op.einsum, op.mixing, op.phi)
+    st = E.backward(circuit, p, fam, E.forward(circuit, p, fam, x))
+    doc, B, h = fam.to_dict(), len(x), 1e-6
+
+    def mean_ll(params, offset=None):
+        return float(np.mean(O.forward(circuit, params, doc, x,
+                                       leaf_log_offset=offset).root[:, 0]))
+
+    def check(want, plus, minus):
+        got = (plus - minus) / (2 * h)
+        assert abs(got - want) <= 1e-3 * max(abs(want), 1e-3), (got, want)
+
+    for _ in range(2):
+        li = list(st.einsum)[int(rng.integers(len(st.einsum)))]
+        idx = tuple(int(rng.integers(s)) for s in st.einsum[li].shape)
+        want = st.einsum[li][idx] / (op.einsum[li][idx] * B)
+        a, b = op.copy(), op.copy()
+        a.einsum[li][idx] += h
+        b.einsum[li][idx] -= h
+        check(want, mean_ll(a), mean_ll(b))
+    for li, acc in st.mixing.items():
+        m, c = (int(v) for v in np.argwhere(circuit.layers[li].mask)[0])
+        want = acc[m, c] / (op.mixing[li][m, c] * B)
+        a, b = op.copy(), op.copy()
+        a.mixing[li][m, c] += h
+        b.mixing[li][m, c] -= h
+        check(want, mean_ll(a), mean_ll(b))
+        break
+    dd, kk, rr = (int(rng.integers(s)) for s in st.acc_p.shape)
+    off = np.zeros(op.phi.shape[:3])
+    off[dd, kk, rr] = h
+    check(st.acc_p[dd, kk, rr] / B, mean_ll(op, off), mean_ll(op, -off))
