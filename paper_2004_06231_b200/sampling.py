@@ -54,7 +54,7 @@ def _run(circuit, params, family, n, seed, trace=None, x_e=None, evidence_mask=N
                                    p(ev), n, int(seed) & 0xFFFFFFFFFFFFFFFF, p(scratch), p(out),
                                    p(status), engine._stream()), "einet_sample")
     _raise_sampling([int(v) for v in status.cpu().tolist()], family)
-    return out.cpu().numpy()
+    return engine.to_host(out)
 
 
 def sample(circuit, params, family, n, seed=0):
