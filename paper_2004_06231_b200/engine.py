@@ -554,6 +554,12 @@ def as_device_batch(x, device=None, normalize=None) -> torch.Tensor:
     a = np.asarray(x, dtype=np.float64)
     if a.ndim == 1:
         a = a[None, :]
+    if a.nbytes >= _PINNED_MIN_BYTES:
+        # large batches: ATen converts fp64 -> fp32 (round to nearest, like
+        # numpy's astype) on all host threads straight into a pinned block
+        h = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+        h.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        return h.to(device or "cuda", non_blocking=True)
     return _upload(torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)),
                    device or "cuda")
 

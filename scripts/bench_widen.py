@@ -5,7 +5,8 @@ right half given the left half over a batch, and EINM1 save / load through
 the device paths. Each GPU leg is timed end to end through the public API
 (numpy results on the host), best of 3 after a warm-up; the sampling legs
 also time the oracle's restatement of the reference's per-sample descent
-(oracle.sample_philox, one host core) on a bounded sample.
+(oracle.sample_philox, one host core) on a bounded sample. Also the plain
+log-likelihood (forward) throughput from a device-resident and a numpy batch.
 
     python scripts/bench_widen.py [--out profiles/r01_widen_bench.json]
 """
@@ -55,6 +56,13 @@ def main():
     out = {"model": "C3 SVHN-shape 32x32x3 PD EiNet K=40", "data": "synthetic"}
 
     n = 16384
+    xd = engine.as_device_batch(x[:n])
+    t = best_of(lambda: m.log_likelihood(xd, chunk=n))
+    out["log_likelihood"] = {"batch": n, "input": "device-resident fp32", "s": t,
+                             "samples_per_s": n / t}
+    t = best_of(lambda: m.log_likelihood(x[:n], chunk=n))
+    out["log_likelihood_numpy"] = {"batch": n, "input": "numpy float64", "s": t,
+                                   "samples_per_s": n / t}
     t = best_of(lambda: m.sample(n, seed=1))
     out["sample"] = {"n": n, "s": t, "samples_per_s": n / t}
     n = 4096
