@@ -551,7 +551,9 @@ def as_device_batch(x, device=None, normalize=None) -> torch.Tensor:
         if not t.is_cuda:
             return _upload(t.to(torch.float32).contiguous(), device or "cuda")
         return t.to(device=device or "cuda", dtype=torch.float32).contiguous()
-    a = np.asarray(x, dtype=np.float64)
+    a = np.asarray(x)
+    if a.dtype != np.float32:
+        a = np.asarray(a, dtype=np.float64)
     if a.ndim == 1:
         a = a[None, :]
     if a.nbytes >= _PINNED_MIN_BYTES:

@@ -212,8 +212,11 @@ def _host_batch(batch) -> torch.Tensor:
     elif engine._is_u8(batch):
         t = torch.from_numpy(np.ascontiguousarray(batch))
     else:
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(batch, dtype=np.float64),
-                                                  dtype=np.float32))
+        a = np.asarray(batch)
+        if a.dtype == np.float32:
+            t = torch.from_numpy(np.ascontiguousarray(a))
+        else:  # ATen converts on all host threads (round to nearest, as numpy)
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(torch.float32)
     if t.dim() == 1:
         t = t[None, :]
     if t.dtype not in (torch.float32, torch.uint8):
