@@ -516,8 +516,7 @@ class _EpochPlan:
                 model.params.compute_for(model.step_buffers(s)[0])
             torch.cuda.current_stream().synchronize()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, capture_error_mode=os.environ.get("EINET_CAPTURE_MODE",
-                                                                        "global")):
+            with torch.cuda.graph(g):
                 eng = self._body(model)
             self.graph = (g, self._buffer_key(model), eng)
         if use_graph:
