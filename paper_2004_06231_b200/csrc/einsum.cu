@@ -782,30 +782,30 @@ __global__ void k_root_out(WsView ws, int slab, int64_t B, int kr, double *out) 
   out[e] = s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[k];
 }
 
-__global__ void k_ll_partial(WsView ws, int slab, int64_t B, double *part) {
-  __shared__ double red[8];
-  const int64_t b = (int64_t)blockIdx.x * 256 + threadIdx.x;
+// Sum of the batch's root log-likelihoods into stats (ll, count): one CTA,
+// fixed summation order (strided fp64 runs, then warp and CTA trees).
+__global__ void __launch_bounds__(1024) k_ll_sum(WsView ws, int slab, int64_t B, double *ll,
+                                                 double count) {
+  __shared__ double red[32];
   double v = 0.0;
-  if (b < B) {
-    const double s = slab_shift(ws, slab)[b];
-    v = s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[0];
+  const double *sh = slab_shift(ws, slab);
+  for (int64_t b = threadIdx.x; b < B; b += 1024) {
+    const double s = sh[b];
+    v += s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[0];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += red[w];
-    part[blockIdx.x] = s;
+  if (threadIdx.x < 32) {
+    v = red[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) {
+      ll[0] += v;
+      ll[1] += count;
+    }
   }
-}
-
-__global__ void k_ll_finish(const double *part, int n, double *ll, double count) {
-  double s = 0.0;
-  for (int i = 0; i < n; ++i) s += part[i];
-  ll[0] += s;
-  ll[1] += count;
 }
 
 // ---------------------------------------------------------------------------
@@ -952,10 +952,9 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   // log-likelihood sum of the batch (root entry 0) and the sample count
   {
     ProfScope prof("ll_sum", st);
-    const int nb = ceil_div(B, 256);
-    k_ll_partial<<<nb, 256, 0, st>>>(w, p.root_out_slab, B, w.llpart);
-    k_ll_finish<<<1, 1, 0, st>>>(w.llpart, nb, stats + p.sizes.stats_ll_offset, (double)B);
-    count_launch(2);
+    k_ll_sum<<<1, 1024, 0, st>>>(w, p.root_out_slab, B, stats + p.sizes.stats_ll_offset,
+                                  (double)B);
+    count_launch();
   }
   for (int li = (int)p.layers.size() - 1; li >= 0; --li) {
     const LayerPlan &L = p.layers[li];
