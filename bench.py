@@ -110,6 +110,14 @@ class ClockSampler:
             self._stop.wait(0.005)
 
     def __enter__(self):
+        # the timed loop holds the GIL between launches: a short switch
+        # interval lets the sampling thread in every millisecond
+        self._switch = sys.getswitchinterval()
+        sys.setswitchinterval(0.001)
+        try:
+            self.rows.append(self._sample())
+        except Exception:
+            pass
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -117,6 +125,11 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        sys.setswitchinterval(self._switch)
+        try:
+            self.rows.append(self._sample())
+        except Exception:
+            pass
 
     def summary(self):
         if not self.rows:
