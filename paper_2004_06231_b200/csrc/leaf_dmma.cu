@@ -270,7 +270,7 @@ static double fwd_dmma_shape(const Plan &p, int64_t B, int *ds_out) {
       device_slots((const void *)k_leaf_fwd_dmma<NT, MT, WARPS>, 32 * WARPS, smem, p.num_sms);
   // at least 4 chunks of 32 variables per split keep the double buffer busy
   const int cap = std::max(1, std::min(kMaxDSplit, ceil_div(p.max_scope, LD_VC) / 4));
-  const int ds = pick_split(tiles, slots, 1, cap, 0.95);
+  const int ds = pick_split(tiles, slots, 1, cap, 0.90);
   *ds_out = ds;
   const int64_t n = tiles * ds;
   return (double)n / (double)(ceil_div(n, slots) * slots);
