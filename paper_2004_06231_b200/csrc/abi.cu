@@ -428,7 +428,8 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   for (auto &L : p->layers) {
     if (L.kind != EINET_LAYER_EINSUM) continue;
     int64_t lw = (int64_t)L.rows * L.k_out * K * K;
-    int64_t blocks = (int64_t)L.rows * L.k_out;
+    int64_t blocks = (int64_t)L.rows * ((L.k_out + wstats_simt_kc(K, L.k_out) - 1) /
+                                        wstats_simt_kc(K, L.k_out));
     int64_t bs = std::min<int64_t>(std::max<int64_t>(1, (2 * p->num_sms + blocks - 1) / blocks),
                                    std::min<int64_t>(kMaxBSplit, (Bc + 63) / 64));
     // tensor-core W statistics: fp32 partials per (segment, slot) (wstats_tc.cu)

@@ -10,6 +10,7 @@
 //             deterministic replacement for np.add.at (engine.py:315-316).
 #pragma once
 
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -225,6 +226,11 @@ int pick_split(int64_t ctas_per_split, int64_t slots, int lo, int hi, double goo
 int64_t device_slots(const void *kernel, int block, size_t smem, int num_sms);
 
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+// CUDA-core W statistics: output components per CTA (einsum.cu k_einsum_wstats)
+inline int wstats_simt_kc(int K, int Ko) {
+  const int K4 = (K + 3) / 4;
+  return K4 * K4 <= 256 ? std::max(1, std::min(Ko, 256 / (K4 * K4))) : 1;
+}
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 }  // namespace einet

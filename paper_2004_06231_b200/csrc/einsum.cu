@@ -612,19 +612,24 @@ constexpr int WS_BT = 32;  // samples per fp32 run of the W statistics
 // Register tile 4x4 of (i, j) per thread; block K4*K4 threads.
 __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__restrict__ EB,
                                 const float *__restrict__ RT, int64_t Bc, int ks, int64_t B,
-                                int K, int Ko, int L, int bsplit, double *wpart, int ti_per) {
+                                int K, int Ko, int L, int bsplit, double *wpart, int ti_per,
+                                int kc) {
   extern __shared__ __align__(16) float sm[];
   const int K4 = (K + 3) / 4;
   const int KP = K4 * 4;
   float *ea_s = sm;                     // [WS_BT][KP]
   float *eb_s = ea_s + WS_BT * KP;      // [WS_BT][KP]
-  float *rt_s = eb_s + WS_BT * KP;      // [WS_BT]
-  const int g = blockIdx.x;
-  const int l = g / Ko, k = g % Ko;
+  float *rt_s = eb_s + WS_BT * KP;      // [WS_BT][kc]
+  // blockIdx.x = (row l, chunk of kc output components): the chunk's slices
+  // share the EA / EB staging (small K: kc K4^2 threads instead of K4^2)
+  const int nkc = (Ko + kc - 1) / kc;
+  const int l = blockIdx.x / nkc, k0 = (blockIdx.x % nkc) * kc;
+  const int tpk = ti_per * K4, kk = threadIdx.x / tpk, rr = threadIdx.x - kk * tpk;
+  const int k = k0 + kk;
   const int split = blockIdx.y;
   // K > 64: the slice's i-rows of 4 are split over blockIdx.z (<= 256 threads)
-  const int ti = blockIdx.z * ti_per + threadIdx.x / K4, tj = threadIdx.x % K4;
-  const bool act = ti < K4;
+  const int ti = blockIdx.z * ti_per + rr / K4, tj = rr % K4;
+  const bool act = ti < K4 && k < Ko;
   const int64_t per = (B + bsplit - 1) / bsplit;
   const int64_t bb = split * per, be = min(B, bb + per);
   float acc[4][4];
@@ -645,11 +650,13 @@ __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__res
       ea_s[e] = ok ? EA[ev_idx(l, t + bl, i, Bc, K)] : 0.f;
       eb_s[e] = ok ? EB[ev_idx(l, t + bl, i, Bc, K)] : 0.f;
     }
-    for (int e = threadIdx.x; e < WS_BT; e += blockDim.x)
-      rt_s[e] = e < nb ? RT[tb_idx(l, t + e, k, Bc, ks)] : 0.f;
+    for (int e = threadIdx.x; e < WS_BT * kc; e += blockDim.x) {
+      const int bl = e / kc, kq = e - bl * kc;
+      rt_s[e] = (bl < nb && k0 + kq < Ko) ? RT[tb_idx(l, t + bl, k0 + kq, Bc, ks)] : 0.f;
+    }
     __syncthreads();
     for (int bl = 0; act && bl < nb; ++bl) {
-      const float r = rt_s[bl];
+      const float r = rt_s[bl * kc + kk];
       const float4 a4 = *(const float4 *)(ea_s + bl * KP + 4 * ti);
       const float4 e4 = *(const float4 *)(eb_s + bl * KP + 4 * tj);
       const float au[4] = {r * a4.x, r * a4.y, r * a4.z, r * a4.w};
@@ -936,8 +943,8 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
   return check_cuda(cudaGetLastError(), "forward kernels");
 }
 
-static int wstats_bsplit(const Plan &p, const LayerPlan &L, int64_t B) {
-  int64_t blocks = (int64_t)L.rows * L.k_out;
+static int wstats_bsplit(const Plan &p, const LayerPlan &L, int64_t B, int64_t blocks = -1) {
+  if (blocks < 0) blocks = (int64_t)L.rows * L.k_out;
   int64_t bs = std::max<int64_t>(1, (2 * p.num_sms + blocks - 1) / blocks);
   return (int)std::min<int64_t>(bs, std::min<int64_t>(kMaxBSplit, (B + 63) / 64));
 }
@@ -988,14 +995,18 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
         int rc = launch_wstats_tc(p, L, EA, EB, w, B, params + L.w_off, stats + L.w_off, st);
         if (rc) return rc;
       } else {
-        const int bs = wstats_bsplit(p, L, B);
         const int K4 = (K + 3) / 4;
-        const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT);
         int ti_per = K4;
         while (ti_per * K4 > 256) ti_per = (ti_per + 1) / 2;
-        dim3 g2(L.rows * L.k_out, bs, ceil_div(K4, ti_per));
-        k_einsum_wstats<<<g2, ti_per * K4, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K, L.k_out,
-                                                       L.rows, bs, w.wpart, ti_per);
+        // small K: several output components per CTA (shared EA / EB staging)
+        const int kc = wstats_simt_kc(K, L.k_out);
+        const int nkc = ceil_div(L.k_out, kc);
+        const int bs = wstats_bsplit(p, L, B, (int64_t)L.rows * nkc);
+        const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT * kc);
+        dim3 g2(L.rows * nkc, bs, ceil_div(K4, ti_per));
+        k_einsum_wstats<<<g2, kc * ti_per * K4, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K,
+                                                            L.k_out, L.rows, bs, w.wpart, ti_per,
+                                                            kc);
         launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);
       }
     }

@@ -1,6 +1,7 @@
 """EinsumLayer contraction sweep (BASELINE.json configs[4]): K in
 {10, 20, 40, 64, 128} x batch in {64, 256, 1024, 4096} on the SVHN-shaped PD
-graph (lifted 32x32x3, delta 8 vertical), forward pass only.
+graph (lifted 32x32x3, delta 8 vertical): the forward contraction and the two
+back-pass GEMMs (W statistics, child responsibilities) of an EM step.
 
     python scripts/sweep_einsum.py [--out profiles/r01_einsum_sweep.json]
 
@@ -25,7 +26,8 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from paper_2004_06231_b200 import _native, engine  # noqa: E402
+from paper_2004_06231_b200 import _native, engine, trainer  # noqa: E402
+from paper_2004_06231_b200.model import EinetModel  # noqa: E402
 from paper_2004_06231_b200.compiler import compile_graph  # noqa: E402
 from paper_2004_06231_b200.data import config  # noqa: E402
 
@@ -73,12 +75,30 @@ def main():
             ms = prof["einsum_fwd"][0] / args.reps
             tfs = flops * b / (ms / 1e3) / 1e12
             gbs = nbytes * b / (ms / 1e3) / 1e9
+            # the back-pass GEMMs of one uncaptured EM step (W statistics: the
+            # forward's flops; child responsibilities: twice them)
+            model = EinetModel(circuit, params, fam)
+            trainer.em_stochastic_step(model, xd, 0.0)
+            torch.cuda.synchronize()
+            _native.profile_enable(True)
+            for _ in range(max(1, args.reps // 4)):
+                trainer.em_stochastic_step(model, xd, 0.0)
+            torch.cuda.synchronize()
+            bprof = _native.profile_read()
+            _native.profile_enable(False)
+            nb = max(1, args.reps // 4)
+            ws_ms = bprof["einsum_wstats"][0] / nb
+            cr_ms = bprof["einsum_childrho"][0] / nb
             line = {"k": k, "batch": b, "path": "tcgen05 3xBF16" if tc else "CUDA cores fp32",
                     "einsum_fwd_us": ms * 1e3, "tflops": tfs, "gbs": gbs,
                     "frac_bf16_peak": tfs / bf16,
                     "frac_bf16_peak_3x": 3 * tfs / bf16 if tc else None,
                     "frac_hbm": gbs / hbm, "flops_per_sample": flops,
-                    "bytes_per_sample": nbytes, "rows": rows}
+                    "bytes_per_sample": nbytes, "rows": rows,
+                    "wstats_us": ws_ms * 1e3,
+                    "wstats_tflops": flops * b / (ws_ms / 1e3) / 1e12,
+                    "childrho_us": cr_ms * 1e3,
+                    "childrho_tflops": 2 * flops * b / (cr_ms / 1e3) / 1e12}
             print(json.dumps(line), flush=True)
             lines.append(line)
         del params
