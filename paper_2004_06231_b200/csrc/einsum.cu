@@ -776,6 +776,99 @@ __global__ void k_einsum_childrho_generic(const float *__restrict__ EA,
   }
 }
 
+// Child responsibilities for 48 < K <= 128 on CUDA cores (engine.py:294-316):
+//   left[b,i]  = EA[b,i] sum_k RT[b,k] sum_j W[k,i,j] EB[b,j]
+//   right[b,j] = EB[b,j] sum_k RT[b,k] sum_i W[k,i,j] EA[b,i]
+// per (row, 64-sample tile): W[k] staged in shared memory one output component
+// at a time, RT folded into the EB / EA operand, a 4-sample x 8-entry register
+// tile per thread for each side. grid (ceil(B/64), rows), block 256.
+constexpr int CB_WS = FB_KP + 1;  // odd row stride: the 8-row column reads hit 8 banks
+size_t childrho_big_smem() {
+  return sizeof(float) * ((size_t)FB_KP * CB_WS + 3 * FB_KP * FB_TB);
+}
+__global__ void __launch_bounds__(256) k_einsum_childrho_big(
+    const float *__restrict__ EA, const float *__restrict__ EB, const float *__restrict__ RT,
+    const float *__restrict__ W, WsView ws, const int *slot_left, const int *slot_right,
+    int64_t B, int K, int Ko) {
+  extern __shared__ __align__(16) float csm[];
+  float *wk = csm;                      // [i][CB_WS] = W[k][i][j]
+  float *ebs = wk + FB_KP * CB_WS;      // [j][64]
+  float *eas = ebs + FB_KP * FB_TB;     // [i][64]
+  float *rts = eas + FB_KP * FB_TB;     // [k][64]
+  const int tid = threadIdx.x, l = blockIdx.y;
+  const int64_t b0 = (int64_t)blockIdx.x * FB_TB;
+  for (int e = tid; e < FB_KP * FB_TB; e += 256) {
+    const int r = e >> 6, s = e & 63;
+    const int64_t b = b0 + s;
+    float vb = 0.f, va = 0.f, vr = 0.f;
+    if (b < ws.bc) {
+      if (r < K) {
+        const int64_t x = ev_idx(l, b, r, ws.bc, K);
+        vb = EB[x];
+        va = EA[x];
+      }
+      if (r < Ko) vr = RT[tb_idx(l, b, r, ws.bc, ws.ks)];
+    }
+    ebs[e] = vb;
+    eas[e] = va;
+    rts[e] = vr;
+  }
+  const int sg = tid & 15, ig = tid >> 4;  // samples 4 sg .. +3, entries 8 ig .. +7
+  float al[4][8], ar[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) al[a][c] = ar[a][c] = 0.f;
+  const float *Wl = W + (int64_t)l * Ko * K * K;
+  for (int k = 0; k < Ko; ++k) {
+    __syncthreads();
+    const float *src = Wl + (int64_t)k * K * K;
+    for (int e = tid; e < FB_KP * FB_KP; e += 256) {
+      const int i = e / FB_KP, j = e - i * FB_KP;
+      wk[i * CB_WS + j] = (i < K && j < K) ? src[i * K + j] : 0.f;
+    }
+    __syncthreads();
+    const float4 r4 = *(const float4 *)(rts + k * FB_TB + sg * 4);
+    const float rv[4] = {r4.x, r4.y, r4.z, r4.w};
+    for (int j = 0; j < K; ++j) {  // left side: entries i = 8 ig + c
+      const float4 e4 = *(const float4 *)(ebs + j * FB_TB + sg * 4);
+      const float eb[4] = {rv[0] * e4.x, rv[1] * e4.y, rv[2] * e4.z, rv[3] * e4.w};
+      float wv[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) wv[c] = wk[(ig * 8 + c) * CB_WS + j];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) al[a][c] = fmaf(wv[c], eb[a], al[a][c]);
+    }
+    for (int i = 0; i < K; ++i) {  // right side: entries j = 8 ig + c
+      const float4 a4 = *(const float4 *)(eas + i * FB_TB + sg * 4);
+      const float ea[4] = {rv[0] * a4.x, rv[1] * a4.y, rv[2] * a4.z, rv[3] * a4.w};
+      float wv[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) wv[c] = wk[i * CB_WS + ig * 8 + c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) ar[a][c] = fmaf(wv[c], ea[a], ar[a][c]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int s = sg * 4 + a;
+    const int64_t b = b0 + s;
+    if (b >= B) continue;
+    const Col32 dl = slot_ptr(ws, slot_left[l], b), dr = slot_ptr(ws, slot_right[l], b);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int x = ig * 8 + c;
+      if (x >= K) continue;
+      dl[x] = eas[x * FB_TB + s] * al[a][c];
+      dr[x] = ebs[x * FB_TB + s] * ar[a][c];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // root outputs and the log-likelihood sum
 // ---------------------------------------------------------------------------
@@ -884,7 +977,17 @@ static void einsum_childrho_simt(const LayerPlan &L, const float *w32, const flo
   else if (K <= 32) childrho_simt<32>(L, w32, EA, EB, w, B, K, st);
   else if (K <= 40) childrho_simt<40>(L, w32, EA, EB, w, B, K, st);
   else if (K <= 48) childrho_simt<48>(L, w32, EA, EB, w, B, K, st);
-  else {
+  else if (K <= FB_KP) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_einsum_childrho_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)childrho_big_smem());
+      attr = true;
+    }
+    dim3 grid(ceil_div(B, FB_TB), L.rows);
+    k_einsum_childrho_big<<<grid, 256, childrho_big_smem(), st>>>(
+        EA, EB, w.rt, w32 + L.w_off, w, L.d_slot_left, L.d_slot_right, B, K, L.k_out);
+  } else {
     dim3 grid(ceil_div(B, 128), L.rows);
     k_einsum_childrho_generic<<<grid, 128, 0, st>>>(EA, EB, w.rt, w32 + L.w_off, w,
                                                     L.d_slot_left, L.d_slot_right, B, K,
