@@ -75,3 +75,23 @@ def test_estimator_params_round_trip():
 def test_weight_projection_simplex():
     w = E.project_einsum_weights(np.random.default_rng(0).random((3, 2, 4, 4)))
     assert np.allclose(w.sum(axis=(2, 3)), 1.0, atol=1e-12) and w.min() >= 1e-12
+
+
+def test_host_batch_conversions():
+    """trainer._host_batch: float32 and uint8 pass through unchanged, float64
+    converts (multi-threaded ATen) exactly like numpy's astype(float32)."""
+    import numpy as np
+    import torch
+
+    from paper_2004_06231_b200 import trainer
+    rng = np.random.default_rng(0)
+    x64 = rng.normal(size=(300, 70)) * 123.456
+    t = trainer._host_batch(x64)
+    assert t.dtype == torch.float32 and t.is_contiguous()
+    assert np.array_equal(t.numpy(), x64.astype(np.float32))
+    x32 = x64.astype(np.float32)
+    assert np.array_equal(trainer._host_batch(x32).numpy(), x32)
+    u8 = rng.integers(0, 256, (5, 9)).astype(np.uint8)
+    tu = trainer._host_batch(u8)
+    assert tu.dtype == torch.uint8 and np.array_equal(tu.numpy(), u8)
+    assert tuple(trainer._host_batch(x64[0]).shape) == (1, 70)
