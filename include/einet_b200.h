@@ -41,7 +41,9 @@ extern "C" {
 /* Device status words written by forward/backward (int32[4]).
  * [0] lowest variable index with an unsupported value (INT32_MAX = none)
  * [1] lowest layer index with NaN entering an einsum layer (INT32_MAX = none)
- * [2] family-specific detail code, [3] reserved. */
+ * [2] family-specific detail code (internal)
+ * [3] 0 = another rank of the process group failed this EM step
+ *     (einet_status_from_stats); sampling: a slab with all-zero weights. */
 #define EINET_STATUS_WORDS 4
 
 /* One einsum or mixing layer of a compiled LayeredCircuit (compiler.py:28-45). */
@@ -85,10 +87,10 @@ typedef struct {
   int64_t params_f64;       /* master params: [W layers | mixing | phi(D,K,R,T)]   */
   int64_t phi_offset;       /* element offset of phi inside params               */
   int64_t mixing_offset;    /* element offset of the first mixing layer          */
-  int64_t stats_f64;        /* EM statistics: [n_W | n_mix | acc_pt | P | ll,n]   */
+  int64_t stats_f64;        /* EM statistics: [n_W | n_mix | acc_pt | P | ll,n,f] */
   int64_t stats_acc_pt_offset;
   int64_t stats_p_offset;   /* compressed acc_p: (n_leaf, K)                     */
-  int64_t stats_ll_offset;  /* [ll_sum, n_samples]                               */
+  int64_t stats_ll_offset;  /* [ll_sum, n_samples, failed ranks]                 */
   int64_t compute_bytes;    /* derived device tensors (prepare / mstep output)   */
   int64_t workspace_bytes;  /* per-chunk activations, responsibilities, scratch  */
   int64_t max_chunk;        /* largest batch one forward/backward call accepts  */
@@ -134,13 +136,26 @@ int einet_plan_set_tensor_cores(einet_plan *plan, int enable);
  * Call once per step; forward/backward only lower them (atomicMin). */
 int einet_status_reset(int32_t *status, void *stream);
 
+/* One collective per data-parallel EM update (the reference's
+ * merge, engine.py:228-236, is the all-reduce(sum) of the stats buffer).
+ * einet_status_to_stats: stats[ll+2] = 1 if this rank's status words report
+ *   an error, else 0 -- enqueue after the last einet_backward of the step, so
+ *   the sum over ranks counts the failing ranks.
+ * einet_status_from_stats: after the all-reduce, set status word 3 to 0 when
+ *   that count is non-zero; einet_mstep then skips the update on every rank.
+ *   Only then does the host need the exact words (a MIN all-reduce). */
+int einet_status_to_stats(einet_plan *plan, const int32_t *status, double *stats,
+                          void *stream);
+int einet_status_from_stats(einet_plan *plan, const double *stats, int32_t *status,
+                            void *stream);
+
 /* Zero a stats buffer (engine._zero_stats, engine.py:239-244). */
 int einet_stats_zero(einet_plan *plan, double *stats, void *stream);
 
 /* Fused M-step: targets (trainer.py:69-86), gliding average with step lam
  * (trainer.py:110-115), projections (trainer.py:89-96, engine.py:46-54,
  * family.project) and re-derivation of the compute tensors. Skips the
- * update when the status word reports an error. lam == 0 must not be passed
+ * update when a status word reports an error (words 0, 1, 3). lam == 0 must not be passed
  * (the host returns early, trainer.py:107-108). */
 int einet_mstep(einet_plan *plan, double *params, void *compute, const double *stats,
                 double lam, double eps_w, const int32_t *status, void *stream);
@@ -165,8 +180,6 @@ int einet_ef_log_prob(einet_plan *plan, const double *params, const float *x,
                       int64_t batch, const uint8_t *marg_mask, double *out,
                       int32_t *status, void *stream);
 
-/* Standalone EinsumLayer contraction (engine.log_einsum_exp, engine.py:91-109):
- * left/right (B, L, K) fp64, w (L, K_out, K, K) fp64 -> out (B, L, K_out). */
 /* Batched ancestral sampling (engine.py:331-423, sample / conditional_sample).
  * Writes n complete assignments to out (n, d_vars) fp64, deterministic in
  * seed: every decision of sample b uses a Philox4x32-10 uniform keyed by
@@ -210,6 +223,8 @@ int einet_params_from_blob(const uint8_t *blob, int64_t blob_len, const int64_t 
 int einet_params_to_blob(const double *params, const int64_t *table, int32_t n_tensors,
                          int64_t max_count, uint8_t *blob, void *stream);
 
+/* Standalone EinsumLayer contraction (engine.log_einsum_exp, engine.py:91-109):
+ * left/right (B, L, K) fp64, w (L, K_out, K, K) fp64 -> out (B, L, K_out). */
 int einet_log_einsum_exp(const double *left, const double *right, const double *w,
                          int64_t batch, int32_t rows, int32_t k, int32_t k_out,
                          double *out, void *stream);

@@ -64,6 +64,8 @@ EXPORTS = {
     "einet_backward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                                  c_void_p, c_void_p, c_void_p]),
     "einet_status_reset": (c_int32, [c_void_p, c_void_p]),
+    "einet_status_to_stats": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "einet_status_from_stats": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "einet_plan_set_tensor_cores": (c_int32, [c_void_p, c_int32]),
     "einet_stats_zero": (c_int32, [c_void_p, c_void_p, c_void_p]),
     "einet_mstep": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double,

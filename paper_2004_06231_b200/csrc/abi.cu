@@ -368,7 +368,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   z.stats_acc_pt_offset = p->n_w + p->n_mix;
   z.stats_p_offset = z.stats_acc_pt_offset + p->n_phi;
   z.stats_ll_offset = z.stats_p_offset + (int64_t)p->n_leaf * K;
-  z.stats_f64 = z.stats_ll_offset + 2;
+  z.stats_f64 = z.stats_ll_offset + 3;  // [ll_sum, n, failed ranks]
   z.max_chunk = max_chunk;
   z.suff_dim = p->suff;
 
@@ -592,6 +592,20 @@ int einet_backward(einet_plan *plan, const double *params, const void *compute,
 int einet_status_reset(int32_t *status, void *stream) {
   if (!status) return fail(EINET_ERR_USAGE, "null argument");
   return launch_status_reset(status, (cudaStream_t)stream);
+}
+
+int einet_status_to_stats(einet_plan *plan, const int32_t *status, double *stats,
+                          void *stream) {
+  if (!plan || !status || !stats) return fail(EINET_ERR_USAGE, "null argument");
+  return launch_status_to_stats(status, stats + plan->impl.sizes.stats_ll_offset + 2,
+                                (cudaStream_t)stream);
+}
+
+int einet_status_from_stats(einet_plan *plan, const double *stats, int32_t *status,
+                            void *stream) {
+  if (!plan || !status || !stats) return fail(EINET_ERR_USAGE, "null argument");
+  return launch_status_from_stats(stats + plan->impl.sizes.stats_ll_offset + 2, status,
+                                  (cudaStream_t)stream);
 }
 
 int einet_plan_set_tensor_cores(einet_plan *plan, int enable) {

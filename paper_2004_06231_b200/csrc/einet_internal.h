@@ -176,6 +176,8 @@ int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
                        const uint8_t *mask, double *out, int32_t *status,
                        cudaStream_t st);
 int launch_status_reset(int32_t *status, cudaStream_t st);
+int launch_status_to_stats(const int32_t *status, double *flag, cudaStream_t st);
+int launch_status_from_stats(const double *flag, int32_t *status, cudaStream_t st);
 void plan_tc_tiling(Plan &p);
 int64_t wstats_tc_slots(const Plan &p, const LayerPlan &L, int64_t B);
 int launch_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB, WsView &w,

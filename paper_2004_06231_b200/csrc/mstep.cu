@@ -67,7 +67,8 @@ void launch_reduce_partials(double *dst, const double *part, int nparts, int64_t
 }
 
 __device__ __forceinline__ bool step_failed(const int32_t *status) {
-  return status && (status[0] != INT_MAX || status[1] != INT_MAX);
+  // word 3 = 0: another rank of the process group failed this step
+  return status && (status[0] != INT_MAX || status[1] != INT_MAX || status[3] != INT_MAX);
 }
 
 // Deterministic block sum (fixed shuffle tree, fixed warp order). blockDim 256.
@@ -255,8 +256,8 @@ __global__ void __launch_bounds__(256) k_mstep_leaf_gauss(
     const int64_t e = ((int64_t)d * K + k) * R + r;
     double *ph = phi + e * 2;
     double m = ph[0], s2 = ph[1];
-    if (l >= 0) {
-      const double p = P[(int64_t)l * K + k];
+    {  // every entry, covered or not (uncovered: acc_p = 0 -> keep), like k_mstep_leaf
+      const double p = l >= 0 ? P[(int64_t)l * K + k] : 0.0;
       const bool keep = p <= kEpsCount;
       const double t0 = keep ? m : acc_pt[e * 2] / p;
       const double t1 = keep ? s2 : acc_pt[e * 2 + 1] / p;
@@ -429,6 +430,32 @@ int launch_log_einsum_exp(const double *left, const double *right, const double 
 
 __global__ void k_status_reset(int32_t *status) {
   if (threadIdx.x < EINET_STATUS_WORDS) status[threadIdx.x] = INT_MAX;
+}
+
+// Cross-rank error protocol (one collective per EM update): the E-step ends by
+// writing its own failure flag into the statistics buffer, which the stats
+// all-reduce(sum) turns into the number of failing ranks; the M-step starts
+// by turning a non-zero count into status word 3, so every rank skips the
+// same update (the exact error words travel in a MIN all-reduce only then).
+__global__ void k_status_to_stats(const int32_t *status, double *flag) {
+  if (threadIdx.x == 0)
+    *flag = (status[0] != INT_MAX || status[1] != INT_MAX || status[3] != INT_MAX) ? 1.0 : 0.0;
+}
+
+__global__ void k_status_from_stats(const double *flag, int32_t *status) {
+  if (threadIdx.x == 0 && *flag > 0.0) status[3] = 0;
+}
+
+int launch_status_to_stats(const int32_t *status, double *flag, cudaStream_t st) {
+  k_status_to_stats<<<1, 32, 0, st>>>(status, flag);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "status to stats");
+}
+
+int launch_status_from_stats(const double *flag, int32_t *status, cudaStream_t st) {
+  k_status_from_stats<<<1, 32, 0, st>>>(flag, status);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "status from stats");
 }
 
 int launch_status_reset(int32_t *status, cudaStream_t st) {

@@ -214,6 +214,16 @@ class _Engine:
         _native.check(self._lib.einet_status_reset(_ptr(status), _stream()),
                       "einet_status_reset")
 
+    def status_to_stats(self, status, stats):
+        """stats[ll+2] = this rank's failure flag (enqueue after the last backward)."""
+        _native.check(self._lib.einet_status_to_stats(self.handle, _ptr(status), _ptr(stats),
+                                                      _stream()), "einet_status_to_stats")
+
+    def status_from_stats(self, stats, status):
+        """After the all-reduce: status word 3 = 0 when any rank failed."""
+        _native.check(self._lib.einet_status_from_stats(self.handle, _ptr(stats), _ptr(status),
+                                                        _stream()), "einet_status_from_stats")
+
     def prepare(self, flat, compute, mask=None, offset=None):
         _native.check(self._lib.einet_prepare(self.handle, _ptr(flat), _ptr(compute),
                                               _ptr(mask), _ptr(offset), _stream()),

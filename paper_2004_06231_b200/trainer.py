@@ -67,7 +67,7 @@ def accumulate(model: EinetModel, batch: torch.Tensor, chunk: int, reset_status=
     n = batch.shape[0]
     eng, ws, stats, status, root = model.step_buffers(min(chunk, max(n, 1)))
     compute = model.params.compute_for(eng)
-    stats.zero_()
+    stats.zero_()  # an empty local shard contributes zero statistics
     if reset_status:
         eng.status_reset(status)
     step = eng.max_chunk if chunk >= eng.max_chunk else chunk
@@ -84,14 +84,6 @@ _GRAPH_CACHE_SIZE = 8
 
 def _graphs_enabled() -> bool:
     return os.environ.get("EINET_CUDA_GRAPHS", "1") != "0" and not _native.PROFILING
-
-
-def _nccl_group(group) -> bool:
-    try:
-        import torch.distributed as dist
-        return dist.get_backend(group) == "nccl"
-    except Exception:
-        return False
 
 
 def _stage_batch(model: EinetModel, batch, normalize=None) -> torch.Tensor:
@@ -117,19 +109,37 @@ def _stage_batch(model: EinetModel, batch, normalize=None) -> torch.Tensor:
     return st
 
 
+def _e_step_tail(eng, stats, status, process_group):
+    """End of a data-parallel E-step: this rank's failure flag into the
+    statistics buffer, so the single all-reduce also counts failing ranks."""
+    if process_group is not None:
+        eng.status_to_stats(status, stats)
+
+
+def _reduce(eng, stats, status, process_group):
+    """The one collective of a data-parallel EM update: all-reduce(sum) of the
+    packed statistics buffer (reference ``BackwardStats.merge``,
+    engine.py:228-236), then status word 3 from the failing-rank count."""
+    if process_group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=process_group)
+        eng.status_from_stats(stats, status)
+
+
 def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_group=None,
                 sticky=False):
     """Replay (capturing on first use) the CUDA graph of one EM step on the
     device batch ``xd``; returns (engine, stats, status). With a process group
-    the step is two graphs (E-step, M-step) around the all-reduce of the
-    statistics and of the status words (NCCL, outside the graphs).
+    the step is two graphs (E-step, M-step) around the one all-reduce of the
+    statistics buffer (outside the graphs; NCCL or gloo).
     ``sticky``: the graph does not reset the status words."""
     n = xd.shape[0]
     eng, ws, stats, status, root = model.step_buffers(min(chunk, max(n, 1)))
     compute = model.params.compute_for(eng)  # prepares outside the graph if stale
+    # every buffer the graph reads or writes is part of the key
     key = (xd.data_ptr(), tuple(xd.shape), float(lam), float(eps_w), int(chunk),
-           model.params.flat.data_ptr(), ws.data_ptr(), compute.data_ptr(),
-           process_group is not None, bool(sticky))
+           model.params.flat.data_ptr(), ws.data_ptr(), compute.data_ptr(), stats.data_ptr(),
+           status.data_ptr(), root.data_ptr(), process_group is not None, bool(sticky))
     cache = model.__dict__.setdefault("_graphs", {})
     gs = cache.get(key)
     if gs is None:
@@ -146,7 +156,9 @@ def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_
             ge, gm = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             with torch.cuda.graph(ge):
                 accumulate(model, xd, chunk, reset_status=not sticky)
+                _e_step_tail(eng, stats, status, process_group)
             with torch.cuda.graph(gm):
+                eng.status_from_stats(stats, status)
                 eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
             gs = (ge, gm)
         cache[key] = gs
@@ -156,7 +168,6 @@ def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_
         import torch.distributed as dist
         gs[0].replay()
         dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=process_group)
-        dist.all_reduce(status, op=dist.ReduceOp.MIN, group=process_group)
         gs[1].replay()
     return eng, stats, status
 
@@ -167,39 +178,59 @@ def em_stochastic_step(model: EinetModel, batch, lam, eps_w=engine.EPS_W, chunk=
     batch (reference ``trainer.py:99-117``). ``lam == 0`` leaves every
     parameter bitwise unchanged.
 
-    With ``process_group`` the statistics are summed across ranks (one NCCL
-    all-reduce of the packed buffer) and every rank applies the identical
-    M-step; the returned mean LL is then the global one.
+    With ``process_group`` this rank's ``batch`` is its shard of the global
+    batch (it may be empty): the statistics are summed across ranks by ONE
+    all-reduce of the packed buffer (which also counts failing ranks), every
+    rank applies the identical M-step, and the returned mean LL is the global
+    one. The error words cross ranks (a MIN all-reduce) only when some rank
+    failed.
 
     A uint8 batch (an EIND1 payload, reference ``modelio.py:145-166``) is
     copied as bytes and decoded on the device: divided by 255 unless
     ``normalize`` is False, like the reference's ``load_dataset``.
     """
-    use_graph = (lam != 0.0 and _graphs_enabled() and
-                 (process_group is None or _nccl_group(process_group)))
+    use_graph = lam != 0.0 and _graphs_enabled()
     xd = (_stage_batch(model, batch, normalize) if use_graph
           else engine.as_device_batch(batch, normalize=normalize))
-    if xd.shape[0] == 0:
+    if xd.shape[0] == 0 and process_group is None:
         raise ValueError("empty batch")
     if use_graph:
         eng, stats, status = _graph_step(model, xd, lam, eps_w, chunk, process_group)
     else:
         eng, stats, status, compute = accumulate(model, xd, chunk)
-        if process_group is not None:
-            import torch.distributed as dist
-            dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=process_group)
-            dist.all_reduce(status, op=dist.ReduceOp.MIN, group=process_group)
+        _e_step_tail(eng, stats, status, process_group)
+        _reduce(eng, stats, status, process_group)
         if lam != 0.0:
             eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
-    return _finish_step(model, eng, stats, status, lam)
+    return _finish_step(model, eng, stats, status, lam, process_group)
 
 
-def _finish_step(model, eng, stats, status, lam) -> float:
+def _cross_rank_words(words, process_group, status):
+    """Exact error words of a step some rank failed (word 3 set): one MIN
+    all-reduce of the status words, issued by every rank of the group (they
+    all see the same failing-rank count)."""
+    if process_group is None or words[3] == _native.STATUS_NONE:
+        return words
+    import torch.distributed as dist
+    dist.all_reduce(status, op=dist.ReduceOp.MIN, group=process_group)
+    return status.cpu().tolist()
+
+
+def _raise_step_words(words, family):
+    engine._raise_words(words, family)
+    if words[3] != _native.STATUS_NONE:
+        raise engine.EngineError("EM step failed on another rank")
+
+
+def _finish_step(model, eng, stats, status, lam, process_group=None) -> float:
     """Read the LL sum and the error words (one device->host copy, syncs),
     raise the reference exceptions, return the mean LL."""
     ll_off = int(eng.sizes.stats_ll_offset)
     info = torch.cat([stats[ll_off:ll_off + 2], status.to(torch.float64)]).cpu().tolist()
-    engine._raise_words([int(v) for v in info[2:]], model.family)
+    words = _cross_rank_words([int(v) for v in info[2:]], process_group, status)
+    _raise_step_words(words, model.family)
+    if info[1] == 0:
+        raise ValueError("empty batch")
     if lam != 0.0:
         model.params.mark_compute_current(eng)
     return info[0] / info[1]
@@ -239,19 +270,19 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     are copied as bytes and decoded on the device (see
     ``em_stochastic_step``). With an NCCL ``process_group`` each step is the
     E-step graph, the all-reduces of the statistics and error words, and the
-    M-step graph, still without a host wait."""
+    M-step graph, still without a host wait; the error words cross ranks
+    (a MIN all-reduce of the logs) only when some rank failed."""
     hosts = [_host_batch(b) for b in batches]
     if not hosts:
         return []
-    if (lam == 0.0 or not _graphs_enabled() or
-            (process_group is not None and not _nccl_group(process_group))):
+    if lam == 0.0 or not _graphs_enabled():
         return [em_stochastic_step(model, b, lam, eps_w, chunk, process_group=process_group,
                                    normalize=normalize) for b in hosts]
     if hosts[0].is_cuda:
         return _device_steps(model, hosts, lam, eps_w, chunk, normalize, process_group)
     shape = tuple(hosts[0].shape)
     dtype = hosts[0].dtype
-    if shape[0] == 0:
+    if shape[0] == 0 and process_group is None:
         raise ValueError("empty batch")
     dev = model.params.flat.device
     copy = model.__dict__.get("_copy_stream")
@@ -307,9 +338,23 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
         log_ll[i].copy_(stats[ll_off:ll_off + 2])
         log_st[i].copy_(status)
         model.params.mark_compute_current(eng)
+    return _finish_steps(model, log_ll, log_st, process_group)
+
+
+def _finish_steps(model, log_ll, log_st, process_group):
+    """Raise the first failing step's reference exception (after the steps'
+    logs are read once), else return the mean LLs."""
     lls = log_ll.cpu().tolist()
-    for words in log_st.cpu().tolist():
-        engine._raise_words(words, model.family)
+    rows = log_st.cpu().tolist()
+    if process_group is not None and any(r[3] != _native.STATUS_NONE for r in rows):
+        import torch.distributed as dist
+        dist.all_reduce(log_st, op=dist.ReduceOp.MIN, group=process_group)
+        rows = log_st.cpu().tolist()
+    for words in rows:
+        _raise_step_words(words, model.family)
+    for a, b in lls:
+        if b == 0:
+            raise ValueError("empty batch")
     return [a / b for a, b in lls]
 
 
@@ -322,7 +367,7 @@ def _device_steps(model, batches, lam, eps_w, chunk, normalize, process_group):
     if not all(b.is_cuda for b in batches):
         raise ValueError("em_stochastic_steps needs all batches on the host or all on the device")
     shape = tuple(batches[0].shape)
-    if shape[0] == 0:
+    if shape[0] == 0 and process_group is None:
         raise ValueError("empty batch")
     if any(tuple(b.shape) != shape or b.dtype != batches[0].dtype for b in batches):
         raise ValueError("em_stochastic_steps needs batches of one shape and dtype")
@@ -347,10 +392,7 @@ def _device_steps(model, batches, lam, eps_w, chunk, normalize, process_group):
         log_ll[i].copy_(stats[ll_off:ll_off + 2])
         log_st[i].copy_(status)
         model.params.mark_compute_current(eng)
-    lls = log_ll.cpu().tolist()
-    for words in log_st.cpu().tolist():
-        engine._raise_words(words, model.family)
-    return [a / b for a, b in lls]
+    return _finish_steps(model, log_ll, log_st, process_group)
 
 
 def em_full_step(model: EinetModel, data, eps_w=engine.EPS_W, chunk=4096,
@@ -485,7 +527,12 @@ class _EpochPlan:
                 idx = self.order[lo:lo + self.bs]
                 xb = self.stage[idx.shape[0]]
                 torch.index_select(self.xd, 0, idx, out=xb)
-            eng, stats, status, compute = accumulate(model, xb, self.chunk)
+            # error words are reset once per epoch (the model's one status
+            # buffer): after a failing batch every later M-step is a no-op, so
+            # the parameters stay as after the last good batch, where the
+            # reference's exception leaves them
+            eng, stats, status, compute = accumulate(model, xb, self.chunk,
+                                                     reset_status=bi == 0)
             if self.lam != 0.0:
                 eng.mstep(model.params.flat, compute, stats, self.lam, self.eps_w, status)
             self.logs[bi].copy_(status)
@@ -505,21 +552,20 @@ class _EpochPlan:
             self.h_perm.copy_(torch.from_numpy(perm))
             self.order.copy_(self.h_perm, non_blocking=True)
         use_graph = self.lam != 0.0 and _graphs_enabled()
-        if use_graph and self.graph is not None and self.graph[1] != self._buffer_key(model):
-            self.graph = None  # buffers moved (e.g. evicted workspace): capture again
-        if use_graph and self.graph is None:
-            # buffers and compute copies exist before capture (nothing is
-            # allocated for the engine inside the graph)
-            sizes = {min(self.chunk, b) for b in
-                     ([self.n] if self.full else list(self.stage))} | {self.ll_chunk}
-            for s in sizes:
-                model.params.compute_for(model.step_buffers(s)[0])
-            torch.cuda.current_stream().synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                eng = self._body(model)
-            self.graph = (g, self._buffer_key(model), eng)
         if use_graph:
+            # parameters may have changed since the capture (setters, another
+            # trainer): stale compute copies are re-derived in place first, and
+            # buffers must exist before a capture (nothing is allocated inside)
+            for s in self._sizes():
+                model.params.compute_for(model.step_buffers(s)[0])
+            if self.graph is not None and self.graph[1] != self._buffer_key(model):
+                self.graph = None  # buffers moved (e.g. evicted workspace): capture again
+            if self.graph is None:
+                torch.cuda.current_stream().synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    eng = self._body(model)
+                self.graph = (g, self._buffer_key(model), eng)
             self.graph[0].replay()
             eng = self.graph[2]
         else:
@@ -531,9 +577,13 @@ class _EpochPlan:
         self.h_lstat.copy_(self.lstat, non_blocking=True)
         self.h_ll.copy_(self.ll, non_blocking=True)
 
+    def _sizes(self):
+        return {min(self.chunk, b) for b in
+                ([self.n] if self.full else list(self.stage))} | {self.ll_chunk}
+
     def _buffer_key(self, model):
-        return tuple(sorted((k, b[1].data_ptr(), b[2].data_ptr())
-                            for k, b in model._buffers.items())) + (
+        return tuple(sorted((k, b[1].data_ptr(), b[2].data_ptr(), b[3].data_ptr(),
+                             b[4].data_ptr()) for k, b in model._buffers.items())) + (
             model.params._compute.data_ptr() if model.params._compute is not None else 0,)
 
 

@@ -106,3 +106,46 @@ def moment_z(s, g, key):
         mine = np.stack([(s == v).mean(axis=0) for v in range(f.shape[1])], axis=1)
         zs.append(z(mine, f, np.maximum(mine * (1 - mine), 1.0 / n)))
     return max(float(np.max(v)) for v in zs)
+
+
+# ---------------------------------------------------------------------------
+# host-side packing in the device statistics layout (distributed tests)
+# ---------------------------------------------------------------------------
+
+def pack_stats(circuit, family, einsum, mixing, acc_pt, acc_p, ll_sum, n_samples, failed=0.0):
+    """Reference-layout statistics -> flat fp64 vector in the device layout
+    (acc_p compressed to one value per (leaf region, k))."""
+    from paper_2004_06231_b200.distributed import stats_layout
+    L = stats_layout(circuit, family)
+    lay = L["layout"]
+    out = np.zeros(L["total"])
+    for i, (off, shape) in lay.einsum.items():
+        out[off:off + int(np.prod(shape))] = np.asarray(einsum[i]).ravel()
+    for i, (off, shape, _) in lay.mixing.items():
+        out[off:off + int(np.prod(shape))] = np.asarray(mixing[i]).ravel()
+    n_phi = int(np.prod(lay.phi_shape))
+    out[L["acc_pt"]:L["acc_pt"] + n_phi] = np.asarray(acc_pt).ravel()
+    leaf = circuit.layers[0]
+    acc_p = np.asarray(acc_p)
+    for li, (scope, rep) in enumerate(zip(leaf.scopes, leaf.replica)):
+        out[L["p"] + li * circuit.k:L["p"] + (li + 1) * circuit.k] = acc_p[scope[0], :, int(rep)]
+    out[L["ll"]:L["ll"] + 3] = (ll_sum, n_samples, failed)
+    return out
+
+
+def unpack_stats(circuit, family, flat):
+    """Flat fp64 vector -> (einsum, mixing, acc_pt, acc_p, ll_sum, n_samples)."""
+    from paper_2004_06231_b200.distributed import stats_layout
+    L = stats_layout(circuit, family)
+    lay = L["layout"]
+    flat = np.asarray(flat, dtype=np.float64)
+    einsum = {i: flat[o:o + int(np.prod(s))].reshape(s) for i, (o, s) in lay.einsum.items()}
+    mixing = {i: flat[o:o + int(np.prod(s))].reshape(s) for i, (o, s, _) in lay.mixing.items()}
+    n_phi = int(np.prod(lay.phi_shape))
+    acc_pt = flat[L["acc_pt"]:L["acc_pt"] + n_phi].reshape(lay.phi_shape)
+    acc_p = np.zeros(lay.phi_shape[:3])
+    leaf = circuit.layers[0]
+    for li, (scope, rep) in enumerate(zip(leaf.scopes, leaf.replica)):
+        acc_p[np.asarray(scope), :, int(rep)] = flat[L["p"] + li * circuit.k:
+                                                     L["p"] + (li + 1) * circuit.k]
+    return einsum, mixing, acc_pt, acc_p, float(flat[L["ll"]]), float(flat[L["ll"] + 1])

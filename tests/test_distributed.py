@@ -1,6 +1,10 @@
-"""Multi-process (gloo, world size 2) check of the data-parallel EM logic:
-contiguous shards, the packed statistics layout, one all-reduce(sum) and the
-replicated M-step reproduce the single-process EM step."""
+"""Multi-process (gloo, world size 2, CPU) checks of the data-parallel EM
+host logic: contiguous shards (including empty ones), the
+packed statistics layout, the merge semantics of one all-reduce(sum) with the
+replicated M-step (oracle statistics), and the cross-rank error protocol of
+``trainer`` (error words cross ranks in a MIN all-reduce only when the summed
+failure flag says some rank failed). The product step on two ranks runs in
+``tests/test_gpu_multirank.py``."""
 
 import os
 import socket
@@ -11,6 +15,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import paper_2004_06231_b200 as E
+from paper_2004_06231_b200 import _native, trainer
 from paper_2004_06231_b200 import distributed as D
 from paper_2004_06231_b200.compiler import compile_graph
 from paper_2004_06231_b200.engine import init_parameters_host
@@ -18,6 +24,8 @@ from paper_2004_06231_b200.expfam import GaussianFamily
 from paper_2004_06231_b200.structures import StructureConfig, lift_channels, poon_domingos
 
 from oracle import einet_oracle as O
+
+from .helpers import pack_stats, unpack_stats
 
 
 def _setup():
@@ -46,29 +54,36 @@ def _worker(rank, world, port, q):
     lo, hi = D.shard_range(len(x), rank, world)
     tr = O.forward(circuit, p, fam.to_dict(), x[lo:hi])
     st = O.backward(circuit, p, fam.to_dict(), tr)
-    flat = torch.from_numpy(D.pack_stats(circuit, fam, st.einsum, st.mixing, st.acc_pt, st.acc_p,
+    flat = torch.from_numpy(pack_stats(circuit, fam, st.einsum, st.mixing, st.acc_pt, st.acc_p,
                                          st.ll_sum, st.n_samples))
-    D.allreduce_stats(flat)
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM)
     q.put((rank, flat.numpy().copy()))
     dist.barrier()
     dist.destroy_process_group()
 
 
 def test_shard_range_covers_batch():
-    for n in (1, 7, 37, 4096):
+    for n in (0, 1, 7, 37, 4096):
         for world in (1, 2, 3, 8):
             spans = [D.shard_range(n, r, world) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+    assert D.shard_range(1, 1, 2) == (1, 1)  # n < world: an empty shard
+    with pytest.raises(ValueError):
+        D.shard_range(4, 2, 2)
+    x = np.arange(10)[:, None]
+    assert np.array_equal(np.concatenate([D.local_shard(x, r, 3) for r in range(3)]), x)
 
 
 def test_pack_unpack_round_trip():
     circuit, fam, x, p = _setup()
     tr = O.forward(circuit, p, fam.to_dict(), x)
     st = O.backward(circuit, p, fam.to_dict(), tr)
-    flat = D.pack_stats(circuit, fam, st.einsum, st.mixing, st.acc_pt, st.acc_p, st.ll_sum,
+    flat = pack_stats(circuit, fam, st.einsum, st.mixing, st.acc_pt, st.acc_p, st.ll_sum,
                         st.n_samples)
-    ein, mix, acc_pt, acc_p, ll, n = D.unpack_stats(circuit, fam, flat)
+    ein, mix, acc_pt, acc_p, ll, n = unpack_stats(circuit, fam, flat)
     for i in st.einsum:
         assert np.array_equal(ein[i], st.einsum[i])
     for i in st.mixing:
@@ -95,7 +110,7 @@ def test_two_rank_allreduce_equals_full_batch_em():
     circuit, fam, x, p = _setup()
     tr = O.forward(circuit, p, fam.to_dict(), x)
     full = O.backward(circuit, p, fam.to_dict(), tr)
-    ein, mix, acc_pt, acc_p, ll, n = D.unpack_stats(circuit, fam, results[0])
+    ein, mix, acc_pt, acc_p, ll, n = unpack_stats(circuit, fam, results[0])
     merged = O.OracleStats(ein, mix, acc_p, acc_pt, int(n), ll)
     for i in full.einsum:
         np.testing.assert_allclose(ein[i], full.einsum[i], rtol=1e-12, atol=1e-15)
@@ -109,3 +124,69 @@ def test_two_rank_allreduce_equals_full_batch_em():
     for i in want.einsum:
         np.testing.assert_allclose(got.einsum[i], want.einsum[i], rtol=1e-10, atol=1e-15)
     np.testing.assert_allclose(got.phi, want.phi, rtol=1e-10, atol=1e-15)
+
+
+NONE = _native.STATUS_NONE
+
+
+def _protocol_worker(rank, world, port, q):
+    """Each rank holds its own device-style logs of 3 pipelined steps; rank 1
+    failed in step 1 (variable 5), rank 0 in step 2 (variable 2). The summed
+    failure flag set word 3 on both ranks from step 1 on (sticky). Both ranks
+    must raise step 1's error (variable 5) after ONE extra collective; with no
+    failure no collective is issued at all."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calls = []
+    real = dist.all_reduce
+
+    def counting(t, *a, **k):
+        calls.append(tuple(t.shape))
+        return real(t, *a, **k)
+
+    dist.all_reduce = counting
+    try:
+        model = type("M", (), {"family": E.GaussianFamily()})()
+        ll = torch.tensor([[-10.0, 4.0], [-12.0, 4.0], [-9.0, 4.0]], dtype=torch.float64)
+        ok = torch.full((3, 4), NONE, dtype=torch.int32)
+        out = {"ok": trainer._finish_steps(model, ll, ok, dist.group.WORLD),
+               "ok_calls": list(calls)}
+        bad = torch.full((3, 4), NONE, dtype=torch.int32)
+        bad[1:, 3] = 0
+        if rank == 1:
+            bad[1:, 0] = 5
+        else:
+            bad[2:, 0] = 2
+        try:
+            trainer._finish_steps(model, ll, bad, dist.group.WORLD)
+            out["err"] = None
+        except E.UnsupportedValueError as e:
+            out["err"] = str(e)
+        out["bad_calls"] = calls[len(out["ok_calls"]):]
+        q.put((rank, out))
+        dist.barrier()
+    finally:
+        dist.all_reduce = real
+        dist.destroy_process_group()
+
+
+def test_two_rank_error_protocol():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_protocol_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = dict(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for r in range(world):
+        got = results[r]
+        assert got["ok"] == [-2.5, -3.0, -2.25]
+        assert got["ok_calls"] == []          # no failure: no collective beyond the stats
+        assert got["bad_calls"] == [(3, 4)]   # one MIN all-reduce of the step logs
+        assert got["err"] == "variable 5: non-finite value"

@@ -13,6 +13,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 import paper_2004_06231_b200 as E
 from paper_2004_06231_b200 import trainer
@@ -96,3 +97,49 @@ def test_train_many_raises_reference_errors():
     models = [E.build_model(rg, fam, k=k, seed=i, data=good) for i in range(2)]
     with pytest.raises(E.UnsupportedValueError):
         trainer.train_many(models, [good, bad], cfg)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [900, 610])  # 610: the ragged last batch uses another bucket
+def test_train_stops_at_failing_batch(n):
+    """after a failing batch the epoch's later M-steps are no-ops, so
+    the parameters are those after the last good batch, as the reference's
+    exception leaves them (trainer.py:146-155)."""
+    from paper_2004_06231_b200.data import config
+    rg, fam, k, gen = config("C1")
+    x = gen(n, seed=3)
+    bs = 300
+    cfg = trainer.TrainerConfig(epochs=1, batch_size=bs, step_size=0.5, seed=5)
+    perm = np.random.default_rng(cfg.seed).permutation(n)
+    bad_batch = 1
+    x[perm[bad_batch * bs + 2], 4] = 3.0  # outside {0, 1}
+    m = E.build_model(rg, fam, k=k, seed=0, data=x)
+    ref = E.build_model(rg, fam, k=k, seed=0, data=x)
+    with pytest.raises(E.UnsupportedValueError, match="variable 4"):
+        trainer.train(m, x, cfg)
+    for bi in range(bad_batch):
+        trainer.em_stochastic_step(ref, x[perm[bi * bs:(bi + 1) * bs]], 0.5)
+    assert np.array_equal(m.params.flat.cpu().numpy(), ref.params.flat.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_train_after_parameter_change_uses_new_parameters():
+    """a cached epoch graph replayed after the parameters were set
+    from the host must see the new parameters (compute copies re-derived)."""
+    from paper_2004_06231_b200.data import config
+    rg, fam, k, gen = config("C2")
+    x = gen(300, seed=1)
+    cfg = trainer.TrainerConfig(epochs=1, batch_size=100, step_size=0.5, seed=2)
+    a = E.build_model(rg, fam, k=k, seed=0, data=x)
+    b = E.build_model(rg, fam, k=k, seed=7, data=x)
+    trainer.train(a, x, cfg)                       # captures a's epoch graph
+    a.params.phi = b.params.phi                    # host setters -> touch()
+    for i in b.params.einsum.keys():
+        a.params.einsum[i] = b.params.einsum[i]
+    for i in b.params.mixing.keys():
+        a.params.mixing[i] = b.params.mixing[i]
+    assert torch.equal(a.params.flat, b.params.flat)
+    ma = trainer.train(a, x, cfg)                  # replays the cached graph
+    mb = trainer.train(b, x, cfg)
+    assert torch.equal(a.params.flat, b.params.flat)
+    assert [e.train_ll for e in ma] == [e.train_ll for e in mb]
