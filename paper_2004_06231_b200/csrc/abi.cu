@@ -143,6 +143,8 @@ static void free_plan_memory(Plan *p) {
   f(p->d_lseg_vec);
   f(p->d_phi_seg);
   f(p->d_leaf_pvo);
+  f(p->d_i8_tab);
+  f(p->d_i8_col);
   f(p->d_scope_pos);
   f(p->d_tiledesc);
   f(p->d_csr_off);
@@ -391,17 +393,26 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   p->c_active = seg(D + 1);
   p->c_logh = seg(8 * (int64_t)(std::max(p->n_trials, 0) + 1));
   p->leaf_dmma = p->family == EINET_FAMILY_GAUSSIAN && K % 8 == 0 && K <= 64;
-  if (p->leaf_dmma) {
+  if (p->family == EINET_FAMILY_GAUSSIAN) {
     p->h_leaf_pvo.assign(p->n_leaf + 1, 0);
     for (int l = 0; l < p->n_leaf; ++l)
       p->h_leaf_pvo[l + 1] =
           p->h_leaf_pvo[l] + (int)align_up(p->h_scope_off[l + 1] - p->h_scope_off[l], 32);
+  }
+  if (p->leaf_dmma) {
     p->c_leafimg = seg(16 * (int64_t)K * p->h_leaf_pvo.back());
     p->c_cm2 = seg(8 * (int64_t)p->n_leaf * K);
   }
   {
     const char *env = getenv("EINET_DISABLE_TC");
     p->use_tc = !(env && env[0] == '1');
+  }
+  std::vector<int> i8_tab, i8_col;
+  if (p->family == EINET_FAMILY_GAUSSIAN) plan_leaf_i8(*p, i8_tab, i8_col);
+  if (p->leaf_i8) {
+    p->c_i8img = seg((int64_t)p->i8_ng * 96 * (p->h_leaf_pvo.back() / 32));
+    p->c_i8c = seg(16 * (int64_t)p->n_leaf * p->i8_k8);
+    p->c_i8mask = seg(4 * (int64_t)(p->h_leaf_pvo.back() / 32));
   }
   plan_tc_tiling(*p);
   for (auto &L : p->layers) {
@@ -464,6 +475,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     p->w_rtb = seg(any_tc ? 8 * p->max_rows * Bc * nnmax : 0);
     p->w_rhob = seg(8 * (int64_t)p->n_leaf * Bc * ((K + 15) / 16 * 16));
   }
+  p->w_i8flag = seg(16);
   p->w_scratch_end = off;
   z.workspace_bytes = off;
 
@@ -478,7 +490,9 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   if ((rc = upload(&p->d_lseg_v0, lseg_v0))) return rc;
   if ((rc = upload(&p->d_lseg_vec, lseg_vec))) return rc;
   if ((rc = upload(&p->d_phi_seg, phi_seg))) return rc;
-  if (p->leaf_dmma && (rc = upload(&p->d_leaf_pvo, p->h_leaf_pvo))) return rc;
+  if (!p->h_leaf_pvo.empty() && (rc = upload(&p->d_leaf_pvo, p->h_leaf_pvo))) return rc;
+  if (p->leaf_i8 && (rc = upload(&p->d_i8_tab, i8_tab))) return rc;
+  if (p->leaf_i8 && (rc = upload(&p->d_i8_col, i8_col))) return rc;
   {
     std::vector<int> pos((size_t)R * D, -1);
     for (int l = 0; l < d->n_leaf; ++l)

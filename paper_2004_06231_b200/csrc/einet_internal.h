@@ -103,6 +103,14 @@ struct Plan {
   std::vector<int> h_leaf_pvo;     // padded variable offset per leaf (n_leaf + 1)
   int *d_leaf_pvo = nullptr;
   int *d_scope_pos = nullptr;      // (R, D): position of d in its leaf's scope, or -1
+  // INT8 tensor-core Gaussian leaf forward (leaf_i8.cu): scopes padded to 32
+  // like the DMMA image, K padded to 8 (<= 40), 6 digits per column
+  int leaf_i8 = 0, i8_k8 = 0, i8_ng = 0;
+  int64_t c_i8img = 0, c_i8c = 0;  // compute: digit tiles, per-(leaf, k) scale and C
+  int64_t c_i8mask = 0;            // compute: active-variable mask per padded chunk
+  int *d_i8_tab = nullptr;         // per padded chunk: leaf, variables, flags, 0
+  int *d_i8_col = nullptr;         // per padded chunk: 32 variable indices
+  int64_t w_i8flag = 0;            // workspace: off-grid flag of the last i8 forward
   // fused M-step (mstep.cu): per-einsum-layer tile geometry, temp leaf terms
   int64_t *d_tiledesc = nullptr;   // einsum layers x TD_WORDS (mstep.cu)
   int n_tiledesc = 0;
@@ -184,10 +192,15 @@ int launch_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *
                      int64_t B, const double *Wl, double *stats, cudaStream_t st);
 int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_prepare_leaf_dmma(Plan &p, uint8_t *compute, cudaStream_t st);
+int launch_prepare_leaf_i8(Plan &p, uint8_t *compute, cudaStream_t st);
+void plan_leaf_i8(Plan &p, std::vector<int> &tab, std::vector<int> &col);
+bool leaf_i8_supported(const Plan &p);
+int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t B, uint8_t *wsb,
+                       int *flag, cudaStream_t st);
 struct CompView;
 struct WsView;
 int launch_leaf_fwd_dmma(Plan &p, const CompView &c, const float *x, int64_t B, const WsView &w,
-                         int32_t *status, cudaStream_t st, int *ds_out);
+                         int32_t *status, cudaStream_t st, int *ds_out, const int *gate);
 int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *compute,
                        const float *EA, const float *EB, const WsView &w, int64_t B,
                        cudaStream_t st);

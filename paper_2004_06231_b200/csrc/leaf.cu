@@ -13,6 +13,7 @@
 // leaf row is accurate to ~1e-5 absolute even at |log p| ~ 1e4.
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include "kern_common.cuh"
 
@@ -184,6 +185,7 @@ int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_
   int rc = launch_prepare_tc_tiles(p, compute, st);
   if (rc) return rc;
   if ((rc = launch_prepare_leaf_dmma(p, compute, st))) return rc;
+  if ((rc = launch_prepare_leaf_i8(p, compute, st))) return rc;
   return check_cuda(cudaGetLastError(), "prepare kernels");
 }
 
@@ -202,7 +204,8 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
     const int *__restrict__ scope_off, const int *__restrict__ scope_vars,
     const int *__restrict__ leaf_rep, const double2 *__restrict__ lp,
     const uint8_t *__restrict__ active, double *__restrict__ part, int64_t Bc, int n_leaf,
-    int dsplit, int32_t *status) {
+    int dsplit, int32_t *status, const int *gate) {
+  if (gate && *(volatile const int *)gate == 0) return;  // the INT8 pass covered the batch
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int KG = blockDim.x / 32;
   const int KP = KG * LF_KPT;
@@ -378,7 +381,9 @@ __global__ void __launch_bounds__(1024) k_leaf_fwd_discrete(
 // written coalesced.
 __global__ void __launch_bounds__(256) k_leaf_finalize(
     const double *__restrict__ part, int dsplit, const double *__restrict__ cnst, int64_t B,
-    int K, int n_leaf, const int *leaf_slab, WsView ws, double sign, int32_t *status) {
+    int K, int n_leaf, const int *leaf_slab, WsView ws, double sign, int32_t *status,
+    const int *gate) {
+  if (gate && *(volatile const int *)gate == 0) return;  // the INT8 pass covered the batch
   extern __shared__ double vals[];  // [32][K+1]
   __shared__ double mxs[32];
   const int leaf = blockIdx.y;
@@ -470,8 +475,20 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
   WsView w = ws_view(p, wsb);
   const int KG = ceil_div(p.k, LF_KPT);
   int ds;
+  // Image data: the INT8 tensor-core pass (leaf_i8.cu) writes the slabs; the
+  // kernels below run only when it flagged an off-grid value (gate != 0).
+  const int *gate = nullptr;
+  if (leaf_i8_supported(p)) {
+    int *flag = (int *)(wsb + p.w_i8flag);
+    int rc = check_cuda(cudaMemsetAsync(flag, 0, sizeof(int), st), "leaf i8 flag");
+    if (!rc) rc = launch_leaf_fwd_i8(p, compute, x, B, wsb, flag, st);
+    if (rc) return rc;
+    gate = flag;
+    const char *dbg = getenv("EINET_I8_DEBUG");
+    if (dbg && (atoi(dbg) & 32)) return 0;  // diagnostics: no fallback launches
+  }
   if (p.leaf_dmma && p.use_tc) {
-    int rc = launch_leaf_fwd_dmma(p, c, x, B, w, status, st, &ds);
+    int rc = launch_leaf_fwd_dmma(p, c, x, B, w, status, st, &ds, gate);
     if (rc) return rc;
   } else if (p.family == EINET_FAMILY_GAUSSIAN) {
     const int kg = std::min(KG, 8);          // <= 64 k entries per CTA
@@ -487,7 +504,7 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
     dim3 grid(ceil_div(B, LF_TB), p.n_leaf, ds * nkc);
     k_leaf_fwd_gauss<<<grid, threads, smem, st>>>(
         x, B, p.d_vars, p.k, p.num_replicas, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
-        (const double2 *)c.leafp, c.active, w.leafpart, w.bc, p.n_leaf, ds, status);
+        (const double2 *)c.leafp, c.active, w.leafpart, w.bc, p.n_leaf, ds, status, gate);
   } else {
     const int threads = 32 * KG;
     if (threads > 1024) return fail(EINET_ERR_USAGE, "k too large for the leaf kernel (k <= 256)");
@@ -505,7 +522,7 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
                          (int)fsmem);
   k_leaf_finalize<<<g2, 256, fsmem, st>>>(w.leafpart, ds, c.cnst, B, p.k, p.n_leaf, p.d_leaf_slab,
                                       w, p.family == EINET_FAMILY_GAUSSIAN ? -1.0 : 1.0,
-                                      status);
+                                      status, gate);
   count_launch(2);
   if (p.leaf_dmma && p.use_tc) {
     k_leaf_check<<<2 * p.num_sms, 256, 0, st>>>(x, B, p.d_vars, c.active, status);

@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(32 * WARPS, 8 / WARPS + 1) k_leaf_fwd_dmma(
     const int *__restrict__ scope_vars, const int *__restrict__ leaf_rep,
     const int *__restrict__ pvo, const double *__restrict__ img, const float *__restrict__ center,
     const double *__restrict__ cm2, const uint8_t *__restrict__ active, double *__restrict__ part,
-    int64_t Bc, int n_leaf, int dsplit, int32_t *status) {
+    int64_t Bc, int n_leaf, int dsplit, int32_t *status, const int *gate) {
+  if (gate && *(volatile const int *)gate == 0) return;  // the INT8 pass covered the batch
   constexpr int K = NT * 8;
   constexpr int TBS = WARPS * 8 * MT;
   constexpr int IS = (LD_VC / 2) * NT * 32;  // doubles per image chunk
@@ -278,12 +279,13 @@ static double fwd_dmma_shape(const Plan &p, int64_t B, int *ds_out) {
 
 template <int NT, int MT, int WARPS>
 static void launch_fwd_dmma_t(Plan &p, const CompView &c, const float *x, int64_t B,
-                              const WsView &w, int32_t *status, cudaStream_t st, int ds) {
+                              const WsView &w, int32_t *status, cudaStream_t st, int ds,
+                              const int *gate) {
   constexpr int TBS = WARPS * 8 * MT;
   dim3 grid(ceil_div(B, TBS), p.n_leaf, ds);
   k_leaf_fwd_dmma<NT, MT, WARPS><<<grid, 32 * WARPS, fwd_dmma_smem<NT, MT, WARPS>(), st>>>(
       x, B, p.d_vars, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep, p.d_leaf_pvo, c.leafimg,
-      c.center, c.cm2, c.active, w.leafpart, w.bc, p.n_leaf, ds, status);
+      c.center, c.cm2, c.active, w.leafpart, w.bc, p.n_leaf, ds, status, gate);
 }
 
 // 8-warp CTAs reuse each coefficient fragment over more samples; 4-warp CTAs
@@ -291,31 +293,32 @@ static void launch_fwd_dmma_t(Plan &p, const CompView &c, const float *x, int64_
 // fills the waves clearly better.
 template <int NT, int MT>
 static int launch_fwd_dmma_nt(Plan &p, const CompView &c, const float *x, int64_t B,
-                              const WsView &w, int32_t *status, cudaStream_t st, int *ds_out) {
+                              const WsView &w, int32_t *status, cudaStream_t st, int *ds_out,
+                              const int *gate) {
   int ds8, ds4;
   const double e8 = fwd_dmma_shape<NT, MT, 8>(p, B, &ds8);
   const double e4 = fwd_dmma_shape<NT, MT, 4>(p, B, &ds4);
   if (e4 > e8 + 0.03) {
-    launch_fwd_dmma_t<NT, MT, 4>(p, c, x, B, w, status, st, ds4);
+    launch_fwd_dmma_t<NT, MT, 4>(p, c, x, B, w, status, st, ds4, gate);
     *ds_out = ds4;
   } else {
-    launch_fwd_dmma_t<NT, MT, 8>(p, c, x, B, w, status, st, ds8);
+    launch_fwd_dmma_t<NT, MT, 8>(p, c, x, B, w, status, st, ds8, gate);
     *ds_out = ds8;
   }
   return 0;
 }
 
 int launch_leaf_fwd_dmma(Plan &p, const CompView &c, const float *x, int64_t B, const WsView &w,
-                         int32_t *status, cudaStream_t st, int *ds_out) {
+                         int32_t *status, cudaStream_t st, int *ds_out, const int *gate) {
   switch (p.k / 8) {
-    case 1: return launch_fwd_dmma_nt<1, 4>(p, c, x, B, w, status, st, ds_out);
-    case 2: return launch_fwd_dmma_nt<2, 4>(p, c, x, B, w, status, st, ds_out);
-    case 3: return launch_fwd_dmma_nt<3, 4>(p, c, x, B, w, status, st, ds_out);
-    case 4: return launch_fwd_dmma_nt<4, 4>(p, c, x, B, w, status, st, ds_out);
-    case 5: return launch_fwd_dmma_nt<5, 4>(p, c, x, B, w, status, st, ds_out);
-    case 6: return launch_fwd_dmma_nt<6, 2>(p, c, x, B, w, status, st, ds_out);
-    case 7: return launch_fwd_dmma_nt<7, 2>(p, c, x, B, w, status, st, ds_out);
-    case 8: return launch_fwd_dmma_nt<8, 2>(p, c, x, B, w, status, st, ds_out);
+    case 1: return launch_fwd_dmma_nt<1, 4>(p, c, x, B, w, status, st, ds_out, gate);
+    case 2: return launch_fwd_dmma_nt<2, 4>(p, c, x, B, w, status, st, ds_out, gate);
+    case 3: return launch_fwd_dmma_nt<3, 4>(p, c, x, B, w, status, st, ds_out, gate);
+    case 4: return launch_fwd_dmma_nt<4, 4>(p, c, x, B, w, status, st, ds_out, gate);
+    case 5: return launch_fwd_dmma_nt<5, 4>(p, c, x, B, w, status, st, ds_out, gate);
+    case 6: return launch_fwd_dmma_nt<6, 2>(p, c, x, B, w, status, st, ds_out, gate);
+    case 7: return launch_fwd_dmma_nt<7, 2>(p, c, x, B, w, status, st, ds_out, gate);
+    case 8: return launch_fwd_dmma_nt<8, 2>(p, c, x, B, w, status, st, ds_out, gate);
     default: return fail(EINET_ERR_UNSUPPORTED, "DMMA leaf forward needs K % 8 == 0, K <= 64");
   }
 }

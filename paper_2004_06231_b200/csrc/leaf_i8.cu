@@ -1,0 +1,624 @@
+// Gaussian leaf forward on the INT8 tensor cores (tcgen05 kind::i8), exact
+// integer accumulation, for image data on the 1/255 grid.
+//
+// Reference semantics: expfam.py:92-115 (Gaussian log density) summed over a
+// leaf region's scope (expfam.py:297-309). Image datasets reach the
+// reference as u8 pixels divided by 255 in float64 (modelio.py:137-168), so
+// x = u / 255 with an integer u in [0, 255]. For such x
+//
+//   Q[b, k] = sum_d a_dk (u_bd / 255 - mu_dk)^2,   a = 1 / (2 var) = sa^2
+//           = sum_d  G_h[d,k] h_bd + G_l[d,k] l_bd + G_u[d,k] u_bd  +  C_k
+//
+// with the integer features u, h = u^2 >> 8, l = u^2 & 255 (all u8) and
+// G_h = 256 a / 255^2, G_l = a / 255^2, G_u = -2 a mu / 255, C_k = sum a mu^2.
+// Each coefficient column k of a leaf is scaled by a power of two 2^E_k so
+// its largest |G| is <= 127 and written as S signed 8-bit digits
+// (G = 2^(E-8) sum_s g_s 2^(-7 s), first digit in [-127, 127], the others
+// in [-64, 64]); the digits are the MMA's N dimension (column k*S + s). The
+// int32 accumulation of u8 x s8 products is exact (one chunk of 32 variables
+// adds at most 96 * 255 * 127 in magnitude, so scopes up to 690 chunks =
+// 22080 variables are safe; the plan checks), and the only error is the
+// coefficient truncation after S digits: 2^-43 relative to the column's
+// largest coefficient -- no cancellation between the expanded terms, unlike
+// any floating-point accumulation of the expanded form.
+//
+// Data on the grid is evaluated at u / 255 exactly, the reference's own value
+// for its u8 datasets. A batch holding any active value off the grid (or a
+// non-finite one) sets `flag`; the launcher then runs the FP64 path
+// (leaf_dmma.cu) for the whole batch, which evaluates the fp32 values as
+// given and raises the support errors.
+//
+// One CTA per 128-sample tile walks every leaf's scope in chunks of 32
+// variables (scopes padded to 32, the DMMA image's padding), through two
+// rings: raw x chunks (6 stages) and MMA operands A | B (3 stages).
+//   * warps 0..3 gather a chunk's x with cp.async (16 bytes per four
+//     consecutive aligned variables when the chunk allows it) into a padded
+//     [sample][36] fp32 tile;
+//   * warps 4..11 turn x into the u8 features (validating the grid) and
+//     write the A tile (128 samples x 96 bytes, K-major core matrices);
+//   * warp 17 bulk-copies the chunk's digit tile (B, NG x 96 bytes);
+//   * warp 16 issues 3 MMAs (u | h | l K-steps) per chunk into one of two
+//     TMEM accumulators (one per leaf, alternating);
+//   * warps 12..15 drain a finished leaf: Q in fp64, the leaf row
+//     cnst - Q, and the slab (shift = max over k, fp32 offsets).
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+
+#include "kern_common.cuh"
+#include "tc_common.cuh"
+
+namespace einet {
+
+constexpr int LI_VC = 32;              // scope variables per chunk
+constexpr int LI_S = 6;                // coefficient digits per column
+constexpr int LI_KB = 3 * LI_VC;       // K bytes per chunk: u | h | l
+constexpr int LI_XP = 36;              // padded x row (floats)
+constexpr int LI_XST = 6;              // x ring stages (raw fp32 chunks)
+constexpr int LI_AST = 3;              // A | B ring stages (MMA operands)
+constexpr int LI_GW = 4, LI_CW = 8, LI_EW = 4;
+constexpr int LI_MMA_WARP = LI_GW + LI_CW + LI_EW;  // 16
+constexpr int LI_BW = LI_MMA_WARP + 1;              // 17: digit-tile loader
+constexpr int LI_THREADS = 32 * (LI_BW + 1);        // 576
+constexpr int LI_XBYTES = 128 * LI_XP * 4;          // 18432
+constexpr int LI_ABYTES = 128 * LI_KB;              // 12288
+constexpr int LI_ACC_STRIDE = 256;                  // TMEM columns between accumulators
+constexpr int LI_F_VEC = 1, LI_F_FIRST = 2, LI_F_LAST = 4;  // chunk table flags
+constexpr int LI_WIN = 16;             // chunks per metadata window
+
+// Coefficients of variable d, component k (lp = (sa, -mu sa) fp64).
+__device__ __forceinline__ void i8_coefs(double2 q, double &gu, double &gh, double &gl) {
+  const double a = q.x * q.x;
+  gu = 2.0 * q.x * q.y / 255.0;
+  gh = a * (256.0 / 65025.0);
+  gl = a / 65025.0;
+}
+
+// Per (leaf, k): scale 2^(E-8) with max |G| * 2^(8-E) <= 127 and the scope
+// sum C = sum (mu sa)^2 (fixed-order tree). grid (n_leaf, K8), block 256.
+__global__ void __launch_bounds__(256) k_i8_colscale(const double2 *__restrict__ lp,
+                                                     const uint8_t *__restrict__ active,
+                                                     const int *scope_off, const int *scope_vars,
+                                                     const int *leaf_rep, int D, int K, int K8,
+                                                     double *i8c) {
+  __shared__ double red[2][8];
+  const int leaf = blockIdx.x, k = blockIdx.y, r = leaf_rep[leaf];
+  double mx = 0.0, cs = 0.0;
+  if (k < K) {
+    for (int q = scope_off[leaf] + threadIdx.x; q < scope_off[leaf + 1]; q += 256) {
+      const int d = scope_vars[q];
+      if (!active[d]) continue;
+      const double2 v = lp[((int64_t)r * D + d) * K + k];
+      double gu, gh, gl;
+      i8_coefs(v, gu, gh, gl);
+      mx = fmax(mx, fmax(fabs(gu), fmax(fabs(gh), fabs(gl))));
+      cs += v.y * v.y;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    cs += __shfl_down_sync(0xffffffffu, cs, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = mx;
+    red[1][threadIdx.x >> 5] = cs;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0, s = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      m = fmax(m, red[0][w]);
+      s += red[1][w];
+    }
+    double scale = 1.0;
+    if (m > 0.0 && isfinite(m)) {
+      int e;
+      frexp(m * (256.0 / 127.0), &e);
+      while (m * ldexp(1.0, 8 - e) > 127.0) ++e;
+      scale = ldexp(1.0, e - 8);
+    }
+    i8c[((int64_t)leaf * K8 + k) * 2] = scale;
+    i8c[((int64_t)leaf * K8 + k) * 2 + 1] = s;
+  }
+}
+
+// Digit tiles: one thread per (padded chunk pc, component k, chunk variable
+// v) writes the S digits (columns n = k * S + s) of the three coefficients.
+// Tile pc is NG rows x 96 K-bytes in K-major core matrices (byte (n, j) at
+// (j / 16) * NG * 16 + (n / 8) * 128 + (n % 8) * 16 + j % 16).
+__global__ void k_i8_img(const double2 *__restrict__ lp, const int4 *__restrict__ tab,
+                         const int *__restrict__ col, const uint32_t *__restrict__ amask,
+                         const int *__restrict__ leaf_rep, const double *__restrict__ i8c,
+                         int D, int K, int K8, int NG, int64_t npc, uint8_t *__restrict__ img) {
+  const int64_t n_all = npc * K8 * LI_VC;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_all;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(e & (LI_VC - 1));
+    const int k = (int)((e >> 5) % K8);
+    const int64_t pc = (e >> 5) / K8;
+    const int leaf = tab[pc].x;
+    double gu = 0.0, gh = 0.0, gl = 0.0;
+    if (k < K && ((amask[pc] >> v) & 1u)) {
+      const int d = col[pc * LI_VC + v];
+      const double2 q = lp[((int64_t)leaf_rep[leaf] * D + d) * K + k];
+      i8_coefs(q, gu, gh, gl);
+      const double inv = 1.0 / i8c[((int64_t)leaf * K8 + k) * 2];  // power of two
+      gu *= inv;
+      gh *= inv;
+      gl *= inv;
+    }
+    uint8_t *tile = img + pc * (int64_t)NG * LI_KB;
+    double g3[3] = {gu, gh, gl};
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      const int j = f * LI_VC + v;
+      uint8_t *base = tile + (j >> 4) * (NG * 16) + (j & 15);
+      double r = g3[f];
+#pragma unroll
+      for (int sdig = 0; sdig < LI_S; ++sdig) {
+        const double dv = rint(r);
+        r = (r - dv) * 128.0;
+        const int n = k * LI_S + sdig;
+        base[(n >> 3) * 128 + (n & 7) * 16] = (uint8_t)(int8_t)(int)dv;
+      }
+    }
+  }
+}
+
+// Active-variable mask per padded chunk (bit v: variable v of the chunk is
+// real and not marginalised). One warp per chunk.
+__global__ void k_i8_mask(const int4 *__restrict__ tab, const int *__restrict__ col,
+                          const uint8_t *__restrict__ active, int npc, uint32_t *amask) {
+  const int pc = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (pc >= npc) return;
+  const bool on = lane < tab[pc].y && active[col[pc * LI_VC + lane]] != 0;
+  const uint32_t m = __ballot_sync(0xffffffffu, on);
+  if (lane == 0) amask[pc] = m;
+}
+
+struct LeafI8Args {
+  const float *x;
+  const int *leaf_slab;
+  const int4 *tab;           // per padded chunk: {leaf, variables, flags, 0} (LI_F_*)
+  const int *col;            // per padded chunk: 32 variable indices (0 = padding)
+  const uint32_t *amask;     // per padded chunk: active-variable bit mask (compute)
+  const uint8_t *img;        // [pc][NG x 96]
+  const double *i8c;         // [leaf][K8][scale, C]
+  const double *cnst;        // [leaf][K]
+  int *flag;                 // 1 when an active value is off the grid
+  WsView ws;
+  int64_t B;
+  int D, K, K8, NG, n_leaf, npc;
+  int debug;                 // EINET_I8_DEBUG ablations (diagnostics only)
+};
+
+// instruction descriptor: kind::i8, A u8, B s8, D s32, K-major
+__host__ __device__ constexpr uint32_t idesc_u8s8(int M, int N) {
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void li_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+// x (fp32) -> u in [0, 255] with x == fl32(u / 255) exactly. e = 255 x - u is
+// exact in fp32 (fma; |e| < 2^-16 needs <= 16 significant bits), and x is the
+// correctly rounded u / 255 iff |e| <= 255 ulp(x) / 2 (u / 255 is never a
+// rounding midpoint). NaN / inf / off-grid values fail.
+__device__ __forceinline__ bool grid_u8(float x, uint32_t &u) {
+  // rint(255 x) through the 1.5 * 2^23 magic constant (FFMA, no conversions)
+  const float t = fmaf(x, 255.f, 12582912.f);
+  const int ui = __float_as_int(t) - 0x4B400000;
+  u = (uint32_t)ui & 255u;
+  const float e = fmaf(x, 255.f, -(t - 12582912.f));
+  const float lim = __uint_as_float(__float_as_uint(x) & 0x7f800000u) * (127.5f * 1.1920928955078125e-7f);
+  return (uint32_t)ui <= 255u && (fabsf(e) <= lim || x == 0.f);
+}
+
+__global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t xfull[LI_XST], xempty[LI_XST], abfull[LI_AST], abempty[LI_AST],
+      accfull[2], accempty[2];
+  __shared__ uint32_t xmask[LI_XST];               // active-variable mask of the staged chunk
+  __shared__ int xinfo[LI_XST], abinfo[LI_AST];     // leaf | flags << 24
+  __shared__ int win_col[2][LI_WIN][LI_VC];         // chunk metadata windows (gather warps)
+  __shared__ int4 win_tab[2][LI_WIN];
+  __shared__ uint32_t win_am[2][LI_WIN];
+  __shared__ double ks_c[2][3][40];                 // per-leaf epilogue constants
+  __shared__ uint32_t tbase;
+  __shared__ int bad_any;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int NG = a.NG;
+  const uint32_t bbytes = (uint32_t)(NG * LI_KB);
+  const uint32_t ab_bytes = LI_ABYTES + bbytes;
+  uint8_t *xring = sm;                                // [LI_XST][128][LI_XP] fp32
+  uint8_t *abring = sm + (size_t)LI_XST * LI_XBYTES;  // [LI_AST][A | B]
+  const int64_t b0 = (int64_t)blockIdx.x * 128;
+  if (w == LI_MMA_WARP) tc::tmem_alloc(&tbase, 512);
+  if (t == 0) {
+    for (int s = 0; s < LI_XST; ++s) {
+      tc::mbar_init(&xfull[s], 32 * LI_GW + 1);
+      tc::mbar_init(&xempty[s], LI_CW);
+    }
+    for (int s = 0; s < LI_AST; ++s) {
+      tc::mbar_init(&abfull[s], LI_CW + 1);
+      tc::mbar_init(&abempty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&accfull[i], 1);
+      tc::mbar_init(&accempty[i], LI_EW);
+    }
+    bad_any = 0;
+    tc::mbar_fence_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+
+  if (w < LI_GW) {
+    // ---- gather x into the x ring ----
+    // Chunk metadata (table entry, variable indices, active mask) moves in
+    // windows of LI_WIN chunks: window W+1 is loaded into registers while W
+    // is processed and published to shared memory between windows, so no
+    // global-load latency sits between a freed stage and its refill.
+    const int nwin = (a.npc + LI_WIN - 1) / LI_WIN;
+    int rc[4];
+    int4 rt = make_int4(0, 0, 0, 0);
+    uint32_t ra = 0;
+    auto load_win = [&](int W) {
+      const int base = W * LI_WIN;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = t + 128 * i, c = base + (e >> 5);
+        rc[i] = c < a.npc ? a.col[(int64_t)c * LI_VC + (e & 31)] : 0;
+      }
+      if (t < LI_WIN && base + t < a.npc) {
+        rt = a.tab[base + t];
+        ra = a.amask[base + t];
+      }
+    };
+    auto store_win = [&](int W) {
+      const int wb = W & 1;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = t + 128 * i;
+        win_col[wb][e >> 5][e & 31] = rc[i];
+      }
+      if (t < LI_WIN) {
+        win_tab[wb][t] = rt;
+        win_am[wb][t] = ra;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * LI_GW) : "memory");
+    };
+    load_win(0);
+    store_win(0);
+    for (int W = 0; W < nwin; ++W) {
+      if (W + 1 < nwin) load_win(W + 1);
+      const int wb = W & 1;
+      const int pc_end = min(a.npc, (W + 1) * LI_WIN);
+      for (int pc = W * LI_WIN; pc < pc_end; ++pc) {
+        const int ci = pc - W * LI_WIN;
+        const int4 tb = win_tab[wb][ci];
+        const int nv = tb.y;
+        const int s = pc % LI_XST, ph = (pc / LI_XST) & 1;
+        tc::mbar_wait(&xempty[s], ph ^ 1);
+        float *xr = (float *)(xring + (size_t)s * LI_XBYTES);
+        if (t == 0) {
+          xmask[s] = win_am[wb][ci];
+          xinfo[s] = tb.x | (tb.z << 24);
+          li_arrive(&xfull[s]);
+        }
+        if (a.debug & 8) {
+          // diagnostics: no x loads
+        } else if (tb.z & LI_F_VEC) {
+          const int qd = t & 7;
+          const bool real = 4 * qd < nv;
+          const int d = win_col[wb][ci][4 * qd];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = (t >> 3) + 16 * i;
+            const int64_t b = b0 + r;
+            const bool ok = real && b < a.B;
+            const float *src = a.x + (ok ? b * a.D + d : 0);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                             tc::smem_u32(xr + r * LI_XP + 4 * qd)),
+                         "l"(src), "r"(ok ? 16 : 0));
+          }
+        } else {
+          const bool real = lane < nv;
+          const int d = win_col[wb][ci][lane];
+          for (int r = w; r < 128; r += LI_GW) {
+            const int64_t b = b0 + r;
+            const bool ok = real && b < a.B;
+            const float *src = a.x + (ok ? b * a.D + d : 0);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                             tc::smem_u32(xr + r * LI_XP + lane)),
+                         "l"(src), "r"(ok ? 4 : 0));
+          }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                         tc::smem_u32(&xfull[s]))
+                     : "memory");
+      }
+      if (W + 1 < nwin) store_win(W + 1);
+    }
+  } else if (w < LI_GW + LI_CW) {
+    // ---- x -> u8 features (A tile) ----
+    const int ct = t - 32 * LI_GW;  // 0..255
+    const int g = ct >> 7, row = ct & 127;
+    const uint32_t aoff = (uint32_t)((row >> 3) * 128 + (row & 7) * 16);
+    bool bad = false;
+    for (int pc = 0; pc < a.npc; ++pc) {
+      const int xs = pc % LI_XST, xph = (pc / LI_XST) & 1;
+      const int as = pc % LI_AST, aph = (pc / LI_AST) & 1;
+      tc::mbar_wait(&xfull[xs], xph);
+      const float *xr = (const float *)(xring + (size_t)xs * LI_XBYTES) + row * LI_XP + 16 * g;
+      float4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = *(const float4 *)(xr + 4 * q);
+      const uint32_t m = xmask[xs] >> (16 * g);
+      const int info = xinfo[xs];
+      __syncwarp();
+      if (lane == 0) li_arrive(&xempty[xs]);  // the x stage is free again
+      uint32_t uw[4], hw[4], lw[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (a.debug & 128) {  // diagnostics: no conversion work
+          uw[q] = hw[q] = lw[q] = __float_as_uint(v[q].x);
+          continue;
+        }
+        const float xv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+        uint32_t pu = 0, ph2 = 0, pl = 0;
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          uint32_t u;
+          const bool ok = grid_u8(xv[z], u);
+          const bool act = (m >> (4 * q + z)) & 1u;
+          bad |= act && !ok;
+          u = act ? u : 0u;
+          const uint32_t sq = u * u;
+          pu |= u << (8 * z);
+          ph2 |= (sq >> 8) << (8 * z);
+          pl |= (sq & 255u) << (8 * z);
+        }
+        uw[q] = pu;
+        hw[q] = ph2;
+        lw[q] = pl;
+      }
+      tc::mbar_wait(&abempty[as], aph ^ 1);
+      uint8_t *at = abring + (size_t)as * ab_bytes;
+      *(uint4 *)(at + g * 2048 + aoff) = make_uint4(uw[0], uw[1], uw[2], uw[3]);
+      *(uint4 *)(at + (g + 2) * 2048 + aoff) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *(uint4 *)(at + (g + 4) * 2048 + aoff) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      if (ct == 0) abinfo[as] = info;
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) li_arrive(&abfull[as]);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&bad_any, 1);
+  } else if (w == LI_BW) {
+    // ---- digit tiles (B operand) into the A|B ring ----
+    for (int pc = 0; pc < a.npc; ++pc) {
+      const int as = pc % LI_AST, aph = (pc / LI_AST) & 1;
+      tc::mbar_wait(&abempty[as], aph ^ 1);
+      const bool leader = tc::elect_one();
+      if (leader && (a.debug & 16)) {
+        li_arrive(&abfull[as]);
+      } else if (leader) {
+        tc::mbar_arrive_expect_tx(&abfull[as], bbytes);
+        tc::bulk_g2s(abring + (size_t)as * ab_bytes + LI_ABYTES, a.img + (int64_t)pc * bbytes,
+                     bbytes, &abfull[as]);
+      }
+      __syncwarp();
+    }
+  } else if (w == LI_MMA_WARP) {
+    // ---- MMA issuer ----
+    const uint32_t id = idesc_u8s8(128, NG);
+    for (int pc = 0; pc < a.npc; ++pc) {
+      const int as = pc % LI_AST, aph = (pc / LI_AST) & 1;
+      tc::mbar_wait(&abfull[as], aph);
+      const int info = abinfo[as];
+      const int leaf = info & 0xffffff;
+      const bool first = ((info >> 24) & LI_F_FIRST) != 0;
+      const bool last = ((info >> 24) & LI_F_LAST) != 0;
+      const int buf = leaf & 1;
+      if (first) tc::mbar_wait(&accempty[buf], ((leaf >> 1) & 1) ^ 1);
+      tc::fence_after();
+      if (tc::elect_one()) {
+        const uint32_t sa = tc::smem_u32(abring + (size_t)as * ab_bytes);
+        const uint32_t sb = sa + LI_ABYTES;
+        const uint32_t d = tm + (uint32_t)(buf * LI_ACC_STRIDE);
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks)
+          if (!(a.debug & 4))
+            mma_i8(d, tc::kstep_desc(sa, 128, ks), tc::kstep_desc(sb, NG, ks), id,
+                   (first && ks == 0) ? 0u : 1u);
+        tc::mma_commit(&abempty[as]);
+        if (last) tc::mma_commit(&accfull[buf]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---- epilogue: leaf rows and slabs ----
+    // Per leaf: (cnst, scale, C) per k staged in shared memory, then two
+    // passes over the accumulator (max over k, then the fp32 offsets). int32
+    // -> double through the 1.5 * 2^52 magic constant (one DADD).
+    const int q = w & 3;
+    const int et = t - 32 * (LI_GW + LI_CW);  // 0..127
+    const int64_t b = b0 + 32 * q + lane;
+    const bool live = b < a.B;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    const int K = a.K, K8 = a.K8;
+    auto i2d = [](float raw) {
+      return __hiloint2double(0x43380000, (int)(__float_as_uint(raw) ^ 0x80000000u)) -
+             6755401588539392.0;
+    };
+    for (int leaf = 0; leaf < a.n_leaf; ++leaf) {
+      const int buf = leaf & 1;
+      if (et < K) {
+        ks_c[buf][0][et] = a.cnst[(int64_t)leaf * K + et];
+        ks_c[buf][1][et] = a.i8c[((int64_t)leaf * K8 + et) * 2];
+        ks_c[buf][2][et] = a.i8c[((int64_t)leaf * K8 + et) * 2 + 1];
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * LI_EW) : "memory");
+      tc::mbar_wait(&accfull[buf], (leaf >> 1) & 1);
+      tc::fence_after();
+      const uint32_t acc = tm + lane_off + (uint32_t)(buf * LI_ACC_STRIDE);
+      const int slab = a.leaf_slab[leaf];
+      double mx = -CUDART_INF;
+      for (int pass = 0; pass < ((a.debug & 2) ? 0 : 2); ++pass) {
+        for (int k0 = 0; k0 < K8; k0 += 8) {
+          float raw[48];
+          tc::tmem_ld16(acc + k0 * LI_S, *(float(*)[16])(raw));
+          tc::tmem_ld16(acc + k0 * LI_S + 16, *(float(*)[16])(raw + 16));
+          tc::tmem_ld16(acc + k0 * LI_S + 32, *(float(*)[16])(raw + 32));
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int k = k0 + j;
+            if (k >= K) break;
+            double h = i2d(raw[j * LI_S + LI_S - 1]);
+#pragma unroll
+            for (int sd = LI_S - 2; sd >= 0; --sd) h = fma(h, 0.0078125, i2d(raw[j * LI_S + sd]));
+            const double val = ks_c[buf][0][k] - fma(ks_c[buf][1][k], h, ks_c[buf][2][k]);
+            if (pass == 0) {
+              mx = fmax(mx, val);
+            } else if (live) {
+              a.ws.off[tb_idx(slab, b, k, a.ws.bc, a.ws.ks)] =
+                  mx == -CUDART_INF ? 0.f : (float)(val - mx);
+            }
+          }
+        }
+        if (pass == 0 && live) slab_shift(a.ws, slab)[b] = mx;
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) li_arrive(&accempty[buf]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (t == 0 && bad_any) atomicOr(a.flag, 1);
+  if (w == LI_MMA_WARP) tc::tmem_dealloc(tm, 512);
+}
+
+static size_t leaf_i8_smem(int NG) {
+  return (size_t)LI_XST * LI_XBYTES + (size_t)LI_AST * (LI_ABYTES + NG * LI_KB);
+}
+
+bool leaf_i8_supported(const Plan &p) { return p.leaf_i8 != 0 && p.use_tc; }
+
+int launch_prepare_leaf_i8(Plan &p, uint8_t *compute, cudaStream_t st) {
+  if (!p.leaf_i8) return 0;
+  CompView c = comp_view(p, compute);
+  double *i8c = (double *)(compute + p.c_i8c);
+  uint8_t *img = compute + p.c_i8img;
+  k_i8_colscale<<<dim3(p.n_leaf, p.i8_k8), 256, 0, st>>>(
+      (const double2 *)c.leafp, c.active, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
+      p.d_vars, p.k, p.i8_k8, i8c);
+  const int64_t npc = p.h_leaf_pvo.back() / LI_VC;
+  k_i8_mask<<<ceil_div(npc * 32, 256), 256, 0, st>>>((const int4 *)p.d_i8_tab, p.d_i8_col,
+                                                     c.active, (int)npc,
+                                                     (uint32_t *)(compute + p.c_i8mask));
+  count_launch();
+  const int64_t n_all = npc * p.i8_k8 * LI_VC;
+  k_i8_img<<<(int)std::min<int64_t>((n_all + 255) / 256, 8192), 256, 0, st>>>(
+      (const double2 *)c.leafp, (const int4 *)p.d_i8_tab, p.d_i8_col,
+      (const uint32_t *)(compute + p.c_i8mask), p.d_leaf_rep, i8c, p.d_vars, p.k, p.i8_k8,
+      p.i8_ng, npc, img);
+  count_launch(2);
+  return check_cuda(cudaGetLastError(), "leaf i8 image");
+}
+
+int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t B, uint8_t *wsb,
+                       int *flag, cudaStream_t st) {
+  CompView c = comp_view(p, compute);
+  LeafI8Args a;
+  a.x = x;
+  a.leaf_slab = p.d_leaf_slab;
+  a.tab = (const int4 *)p.d_i8_tab;
+  a.col = p.d_i8_col;
+  a.amask = (const uint32_t *)(compute + p.c_i8mask);
+  a.img = compute + p.c_i8img;
+  a.i8c = (const double *)(compute + p.c_i8c);
+  a.cnst = c.cnst;
+  a.flag = flag;
+  a.ws = ws_view(p, wsb);
+  a.B = B;
+  a.D = p.d_vars;
+  a.K = p.k;
+  a.K8 = p.i8_k8;
+  a.NG = p.i8_ng;
+  a.n_leaf = p.n_leaf;
+  a.npc = (int)(p.h_leaf_pvo.back() / LI_VC);
+  {
+    const char *env = getenv("EINET_I8_DEBUG");
+    a.debug = env ? atoi(env) : 0;
+  }
+  const size_t smem = leaf_i8_smem(a.NG);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_leaf_fwd_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  k_leaf_fwd_i8<<<ceil_div(B, 128), LI_THREADS, smem, st>>>(a);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "leaf forward i8");
+}
+
+// Host side of the plan: digit-tile geometry, the per-chunk table (leaf,
+// variables, gather mode, first / last chunk of the leaf) and the chunk's
+// variable indices.
+void plan_leaf_i8(Plan &p, std::vector<int> &tab, std::vector<int> &col) {
+  const char *env = getenv("EINET_LEAF_I8");
+  const int k8 = (p.k + 7) / 8 * 8;
+  p.leaf_i8 = p.family == EINET_FAMILY_GAUSSIAN && k8 <= 40 && !(env && env[0] == '0');
+  if (!p.leaf_i8) return;
+  p.i8_k8 = k8;
+  p.i8_ng = k8 * LI_S;
+  // int32 accumulators: one chunk adds at most 96 * 255 * 127 in magnitude
+  if (leaf_i8_smem(p.i8_ng) > 227 * 1024 || p.max_scope > 690 * LI_VC) {
+    p.leaf_i8 = 0;
+    return;
+  }
+  const int npc = p.h_leaf_pvo.back() / LI_VC;
+  tab.assign((size_t)npc * 4, 0);
+  col.assign((size_t)npc * LI_VC, 0);
+  const bool d_ok = p.d_vars % 4 == 0;
+  for (int l = 0; l < p.n_leaf; ++l) {
+    const int sbeg = p.h_scope_off[l], slen = p.h_scope_off[l + 1] - sbeg;
+    for (int c0 = 0; c0 < slen; c0 += LI_VC) {
+      const int pc = (p.h_leaf_pvo[l] + c0) / LI_VC;
+      const int nv = std::min(LI_VC, slen - c0);
+      bool vec = d_ok;
+      for (int q = 0; q < LI_VC && vec; q += 4) {
+        const int pos = c0 + q;
+        if (pos >= slen) break;                        // all-padding quad
+        if (pos + 4 > slen) { vec = false; break; }    // partial quad
+        const int v = p.h_scope_vars[sbeg + pos];
+        if (v % 4) vec = false;
+        for (int z = 1; z < 4 && vec; ++z)
+          if (p.h_scope_vars[sbeg + pos + z] != v + z) vec = false;
+      }
+      for (int v = 0; v < nv; ++v) col[(size_t)pc * LI_VC + v] = p.h_scope_vars[sbeg + c0 + v];
+      tab[(size_t)pc * 4] = l;
+      tab[(size_t)pc * 4 + 1] = nv;
+      tab[(size_t)pc * 4 + 2] = (vec ? LI_F_VEC : 0) | (c0 == 0 ? LI_F_FIRST : 0) |
+                                (c0 + LI_VC >= slen ? LI_F_LAST : 0);
+    }
+  }
+}
+
+}  // namespace einet

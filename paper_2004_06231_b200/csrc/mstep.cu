@@ -373,6 +373,8 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
                                                      p.d_leaf_rep, p.d_vars, K, c.cnst,
                                                      p.leaf_dmma ? c.cm2 : nullptr, status);
     count_launch(2);
+    int rc = launch_prepare_leaf_i8(p, compute, st);
+    if (rc) return rc;
     return check_cuda(cudaGetLastError(), "fused mstep kernels");
   }
   const int64_t n = (int64_t)p.d_vars * K * p.num_replicas;

@@ -149,3 +149,28 @@ def unpack_stats(circuit, family, flat):
         acc_p[np.asarray(scope), :, int(rep)] = flat[L["p"] + li * circuit.k:
                                                      L["p"] + (li + 1) * circuit.k]
     return einsum, mixing, acc_pt, acc_p, float(flat[L["ll"]]), float(flat[L["ll"] + 1])
+
+
+def device_values(x32, active=None):
+    """The float64 values the device evaluates for an fp32 batch.
+
+    Gaussian leaves read image data on the 1/255 grid (every active value
+    equal to float32(u / 255) for an integer u in [0, 255]) at u / 255
+    exactly -- the value the reference's own u8 dataset loader produces
+    (modelio.py:137-168) -- and any other batch at its fp32 values
+    (csrc/leaf_i8.cu). Feeding the oracle these values makes both sides see
+    the same inputs.
+    """
+    x32 = np.asarray(x32, dtype=np.float32)
+    u = np.rint(x32.astype(np.float64) * 255.0)
+    on = (u >= 0) & (u <= 255) & (np.float32(u / 255.0) == x32)
+    if active is not None:
+        on = on | ~np.asarray(active, bool)[None, :]
+    if on.all():
+        out = x32.astype(np.float64)
+        fix = np.isfinite(x32)
+        if active is not None:
+            fix = fix & np.asarray(active, bool)[None, :]
+        out[fix] = u[fix] / 255.0
+        return out
+    return x32.astype(np.float64)
