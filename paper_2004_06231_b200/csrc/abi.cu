@@ -144,6 +144,8 @@ static void free_plan_memory(Plan *p) {
   f(p->d_phi_seg);
   f(p->d_leaf_pvo);
   f(p->d_i8_tab);
+  if (p->side_stream) cudaStreamDestroy(p->side_stream);
+  p->side_stream = nullptr;
   f(p->d_i8_col);
   f(p->d_scope_pos);
   f(p->d_tiledesc);
@@ -493,6 +495,10 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   if (!p->h_leaf_pvo.empty() && (rc = upload(&p->d_leaf_pvo, p->h_leaf_pvo))) return rc;
   if (p->leaf_i8 && (rc = upload(&p->d_i8_tab, i8_tab))) return rc;
   if (p->leaf_i8 && (rc = upload(&p->d_i8_col, i8_col))) return rc;
+  if (p->leaf_i8 &&
+      (rc = check_cuda(cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking),
+                       "side stream")))
+    return rc;
   {
     std::vector<int> pos((size_t)R * D, -1);
     for (int l = 0; l < d->n_leaf; ++l)

@@ -111,6 +111,7 @@ struct Plan {
   int *d_i8_tab = nullptr;         // per padded chunk: leaf, variables, flags, 0
   int *d_i8_col = nullptr;         // per padded chunk: 32 variable indices
   int64_t w_i8flag = 0;            // workspace: off-grid flag of the last i8 forward
+  cudaStream_t side_stream = nullptr;  // captures the fallback body of a conditional node
   // fused M-step (mstep.cu): per-einsum-layer tile geometry, temp leaf terms
   int64_t *d_tiledesc = nullptr;   // einsum layers x TD_WORDS (mstep.cu)
   int n_tiledesc = 0;
@@ -196,7 +197,7 @@ int launch_prepare_leaf_i8(Plan &p, uint8_t *compute, cudaStream_t st);
 void plan_leaf_i8(Plan &p, std::vector<int> &tab, std::vector<int> &col);
 bool leaf_i8_supported(const Plan &p);
 int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t B, uint8_t *wsb,
-                       int *flag, cudaStream_t st);
+                       int *flag, cudaGraphConditionalHandle cond, cudaStream_t st);
 struct CompView;
 struct WsView;
 int launch_leaf_fwd_dmma(Plan &p, const CompView &c, const float *x, int64_t B, const WsView &w,

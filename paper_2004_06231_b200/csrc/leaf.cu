@@ -468,25 +468,16 @@ static int leaf_dsplit(const Plan &p, int64_t B, int tb, int64_t slots, int nkc)
   return pick_split(blocks, slots, 1, cap);
 }
 
-int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
-                        uint8_t *wsb, int32_t *status, cudaStream_t st) {
-  ProfScope prof("leaf_fwd", st);
+// The CUDA-core / FP64 leaf forward + finalize + support check on stream st.
+// gate != nullptr: every kernel returns at once unless *gate != 0 (the INT8
+// pass flagged the batch).
+static int launch_leaf_fallback(Plan &p, const uint8_t *compute, const float *x, int64_t B,
+                                uint8_t *wsb, int32_t *status, cudaStream_t st,
+                                const int *gate) {
   CompView c = comp_view(p, compute);
   WsView w = ws_view(p, wsb);
   const int KG = ceil_div(p.k, LF_KPT);
   int ds;
-  // Image data: the INT8 tensor-core pass (leaf_i8.cu) writes the slabs; the
-  // kernels below run only when it flagged an off-grid value (gate != 0).
-  const int *gate = nullptr;
-  if (leaf_i8_supported(p)) {
-    int *flag = (int *)(wsb + p.w_i8flag);
-    int rc = check_cuda(cudaMemsetAsync(flag, 0, sizeof(int), st), "leaf i8 flag");
-    if (!rc) rc = launch_leaf_fwd_i8(p, compute, x, B, wsb, flag, st);
-    if (rc) return rc;
-    gate = flag;
-    const char *dbg = getenv("EINET_I8_DEBUG");
-    if (dbg && (atoi(dbg) & 32)) return 0;  // diagnostics: no fallback launches
-  }
   if (p.leaf_dmma && p.use_tc) {
     int rc = launch_leaf_fwd_dmma(p, c, x, B, w, status, st, &ds, gate);
     if (rc) return rc;
@@ -529,6 +520,64 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
     count_launch();
   }
   return check_cuda(cudaGetLastError(), "leaf forward kernels");
+}
+
+// Image data: the INT8 tensor-core pass (leaf_i8.cu) writes the slabs and
+// flags an off-grid batch; only then does the fallback sequence run. Under
+// CUDA-graph capture the fallback is the body of a conditional (IF) node whose
+// condition the INT8 kernel sets, so a clean batch costs no launches; eagerly
+// the fallback kernels are launched gated on the flag (they return at once).
+int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
+                        uint8_t *wsb, int32_t *status, cudaStream_t st) {
+  ProfScope prof("leaf_fwd", st);
+  if (!leaf_i8_supported(p)) return launch_leaf_fallback(p, compute, x, B, wsb, status, st, nullptr);
+  int *flag = (int *)(wsb + p.w_i8flag);
+  int rc = check_cuda(cudaMemsetAsync(flag, 0, sizeof(int), st), "leaf i8 flag");
+  if (rc) return rc;
+  const char *dbg = getenv("EINET_I8_DEBUG");
+  const bool no_fallback = dbg && (atoi(dbg) & 32);  // diagnostics
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t *deps = nullptr;
+  size_t ndeps = 0;
+  if ((rc = check_cuda(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &ndeps),
+                       "capture info")))
+    return rc;
+  if (cs != cudaStreamCaptureStatusActive || no_fallback) {
+    if ((rc = launch_leaf_fwd_i8(p, compute, x, B, wsb, flag, 0ULL, st))) return rc;
+    if (no_fallback) return 0;
+    return launch_leaf_fallback(p, compute, x, B, wsb, status, st, flag);
+  }
+  cudaGraphConditionalHandle cond;
+  if ((rc = check_cuda(cudaGraphConditionalHandleCreate(&cond, graph, 0,
+                                                        cudaGraphCondAssignDefault),
+                       "conditional handle")))
+    return rc;
+  if ((rc = launch_leaf_fwd_i8(p, compute, x, B, wsb, flag, cond, st))) return rc;
+  if ((rc = check_cuda(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &ndeps),
+                       "capture info")))
+    return rc;
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = cond;
+  np.conditional.type = cudaGraphCondTypeIf;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  if ((rc = check_cuda(cudaGraphAddNode(&node, graph, deps, ndeps, &np), "conditional node")))
+    return rc;
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  if ((rc = check_cuda(cudaStreamBeginCaptureToGraph(p.side_stream, body, nullptr, nullptr, 0,
+                                                     cudaStreamCaptureModeRelaxed),
+                       "capture fallback")))
+    return rc;
+  rc = launch_leaf_fallback(p, compute, x, B, wsb, status, p.side_stream, nullptr);
+  cudaGraph_t got = nullptr;
+  const int rc2 = check_cuda(cudaStreamEndCapture(p.side_stream, &got), "end fallback capture");
+  if (rc) return rc;
+  if (rc2) return rc2;
+  return check_cuda(cudaStreamUpdateCaptureDependencies(st, &node, 1,
+                                                        cudaStreamSetCaptureDependencies),
+                    "capture dependencies");
 }
 
 // ---------------------------------------------------------------------------

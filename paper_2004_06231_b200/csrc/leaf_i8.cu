@@ -187,6 +187,7 @@ struct LeafI8Args {
   const double *i8c;         // [leaf][K8][scale, C]
   const double *cnst;        // [leaf][K]
   int *flag;                 // 1 when an active value is off the grid
+  cudaGraphConditionalHandle cond;  // != 0 under capture: set to 1 with the flag
   WsView ws;
   int64_t B;
   int D, K, K8, NG, n_leaf, npc;
@@ -510,7 +511,10 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
   }
   tc::fence_before();
   __syncthreads();
-  if (t == 0 && bad_any) atomicOr(a.flag, 1);
+  if (t == 0 && bad_any) {
+    atomicOr(a.flag, 1);
+    if (a.cond) cudaGraphSetConditional(a.cond, 1);
+  }
   if (w == LI_MMA_WARP) tc::tmem_dealloc(tm, 512);
 }
 
@@ -543,7 +547,7 @@ int launch_prepare_leaf_i8(Plan &p, uint8_t *compute, cudaStream_t st) {
 }
 
 int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t B, uint8_t *wsb,
-                       int *flag, cudaStream_t st) {
+                       int *flag, cudaGraphConditionalHandle cond, cudaStream_t st) {
   CompView c = comp_view(p, compute);
   LeafI8Args a;
   a.x = x;
@@ -555,6 +559,7 @@ int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t 
   a.i8c = (const double *)(compute + p.c_i8c);
   a.cnst = c.cnst;
   a.flag = flag;
+  a.cond = cond;
   a.ws = ws_view(p, wsb);
   a.B = B;
   a.D = p.d_vars;
