@@ -147,7 +147,8 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 def work_per_sample(circuit):
-    """Algorithmic flops and HBM bytes per sample for each kernel class."""
+    """Algorithmic flops and HBM bytes per sample for each kernel class
+    (SURVEY.md 8d)."""
     k = circuit.k
     d, r = circuit.d_vars, circuit.num_replicas
     ein = 0
@@ -156,24 +157,33 @@ def work_per_sample(circuit):
             ein += len(layer.left_src) * layer.k_out * k * k
     leaf_elems = d * k * r
     return {
-        # 2 FMA per (var, k): (x*sa + nmsa)^2 accumulated; x read once
-        "leaf_fwd": {"flops": 4 * leaf_elems, "bytes": 4 * d},
-        "einsum_fwd": {"flops": 2 * ein, "bytes": 0},
-        "einsum_wstats": {"flops": 2 * ein, "bytes": 0},
-        "einsum_childrho": {"flops": 4 * ein, "bytes": 0},
+        # (x - mu)^2 / (2 var): 2 FMA per (var, k); x read once
+        "leaf_fwd": {"flops": 4 * leaf_elems, "bytes": 4 * d, "tc": False},
+        "einsum_fwd": {"flops": 2 * ein, "bytes": 0, "tc": True},
+        "einsum_wstats": {"flops": 2 * ein, "bytes": 0, "tc": True},
+        "einsum_childrho": {"flops": 4 * ein, "bytes": 0, "tc": True},
         # rho*y and rho*y^2 per (var, k); x read once
-        "leaf_stats": {"flops": 4 * leaf_elems, "bytes": 4 * d},
+        "leaf_stats": {"flops": 4 * leaf_elems, "bytes": 4 * d, "tc": False},
     }
 
 
-# FP64 tensor-core (DMMA) peak of this pool's B200, measured by
-# scripts/peak_dmma.cu (m16n8k16, 8-16 warps per CTA): MEASURED_PEAKS.json has
-# no FP64 figure, and the Gaussian leaf forward runs on the FP64 tensor pipe.
-FP64_TENSOR_PEAK_TFLOPS = 37.1
+def load_peaks():
+    """(peaks dict, source): MEASURED_PEAKS.json (driver-written), else the
+    profiling recipe's stated fallback."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            doc = json.load(f)
+        return {"hbm_gbs": doc.get("hbm_gbs", 6650.0), "bf16_tflops": doc.get("bf16_tflops", 1590.0),
+                "bf16_tflops_sustained": doc.get("bf16_tflops_sustained", 1400.0),
+                "sm_max_mhz": doc.get("sm_max_mhz", 1965.0)}, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
 
 # ncu DRAM traffic (read + write bytes per launch) of the dominant kernels,
 # from the committed --set full capture
-KERNEL_TRAFFIC = {"leaf_fwd": "k_leaf_fwd_dmma<5, 4, 4>", "leaf_stats": "k_leaf_stats_tc",
+KERNEL_TRAFFIC = {"leaf_fwd": "k_leaf_fwd_i8", "leaf_stats": "k_leaf_stats_tc",
                   "einsum_wstats": "k_wstats_tc<40>", "einsum_childrho": "k_contract_tc<40>",
                   "einsum_fwd": "k_contract_tc<40>"}
 
@@ -189,13 +199,52 @@ def kernel_traffic(name):
         return None
 
 
-def load_peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(path):
-        with open(path) as f:
-            doc = json.load(f)
-        return doc.get("hbm_gbs", 6650.0), doc.get("bf16_tflops", 1590.0), "measured"
-    return 6650.0, 1590.0, "fallback"
+def class_fractions(name, w, B, per_step_ms, groups, peaks):
+    """Roofline fractions of one kernel class from its device time: HBM
+    (algorithmic bytes) and tensor (algorithmic flops, and the 3 MMAs a
+    3xBF16 product issues) against the measured peaks."""
+    out = {}
+    t = per_step_ms / 1e3
+    if w["bytes"]:
+        gbs = w["bytes"] * B / t / 1e9
+        out["hbm_gbs"] = gbs
+        out["hbm_frac"] = gbs / peaks["hbm_gbs"]
+    if w.get("tc"):
+        tf = w["flops"] * B / t / 1e12
+        out["tflops"] = tf
+        out["tc_frac"] = tf / peaks["bf16_tflops"]
+        out["tc_frac_issued_3xbf16"] = 3 * tf / peaks["bf16_tflops"]
+    return out
+
+
+def step_roofline(circuit, B, ms_step, peaks):
+    """Whole-step roofline of SURVEY.md 8d: t_roof = max(F_TC / P_TC,
+    F_CC / P_FP32, bytes / BW) per sample, fraction = t_roof / t_measured.
+    `survey` counts the leaf work on CUDA cores (the survey's formula, FP32
+    SIMT peak provisional: 148 SM x 128 lanes x 2 x max clock); `as_built`
+    counts it on tensor cores, as this build runs it (INT8 leaf forward,
+    3xTF32 leaf statistics), against the bf16 peak (conservative)."""
+    k, d, r = circuit.k, circuit.d_vars, circuit.num_replicas
+    ein = sum(len(l.left_src) * l.k_out * k * k for l in circuit.layers[1:]
+              if type(l).__name__ == "EinsumLayer")
+    f_tc = 3 * 2 * ein                     # forward + W statistics + child responsibilities
+    f_leaf = 4 * d * k * r + 4 * d * k * r  # leaf forward + leaf statistics
+    f_rest = 4 * ein // max(k, 1)          # exp / log / outer-product glue (small)
+    bytes_ = 4 * d                         # x read once
+    p_tc = peaks["bf16_tflops"] * 1e12
+    p_cc = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6
+    bw = peaks["hbm_gbs"] * 1e9
+    t_meas = ms_step / 1e3 / B
+    res = {}
+    for name, tc, cc in (("survey", f_tc, f_leaf + f_rest), ("as_built", f_tc + f_leaf, f_rest)):
+        comps = {"tensor_s": tc / p_tc, "cuda_core_s": cc / p_cc, "hbm_s": bytes_ / bw}
+        t_roof = max(comps.values())
+        res[name] = {"t_roof_ns_per_sample": t_roof * 1e9,
+                     "bound": max(comps, key=comps.get).replace("_s", ""),
+                     "ceiling_samples_per_s": 1.0 / t_roof, "frac": t_roof / t_meas}
+    res["t_measured_ns_per_sample"] = t_meas * 1e9
+    res["fp32_simt_peak"] = "provisional (not in MEASURED_PEAKS.json)"
+    return res
 
 
 # ---------------------------------------------------------------------------
@@ -334,7 +383,10 @@ def run_ours(args):
     # the same batch as the image bytes it was quantised from (k / 255, an
     # EIND1 u8 payload): the e2e leg ships these and decodes on the device
     x_u8 = torch.from_numpy(np.rint(x64 * 255.0).astype(np.uint8)).pin_memory()
-    del x64
+    # the reference caller's type: a float64 NumPy batch (load_dataset returns
+    # float64, modelio.py:137-168); converted to fp32 by all host threads and
+    # copied inside the public call
+    x_np64 = x64
     x_dev = x_host.to(dev)
     init_x = gen(4096, seed=7).astype(np.float32).astype(np.float64)
     ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=init_x)
@@ -404,18 +456,28 @@ def run_ours(args):
         trainer.em_stochastic_steps(model, [xh] * 2, 0.5, chunk=args.chunk, process_group=group)
     ms_e2e = e2e_leg(x_u8)
     ms_e2e_f32 = e2e_leg(x_host)
+    f64_steps = 3
+    trainer.em_stochastic_steps(model, [x_np64] * 2, 0.5, chunk=args.chunk, process_group=group)
+    ms_e2e_f64 = timed(lambda: trainer.em_stochastic_steps(model, [x_np64] * f64_steps, 0.5,
+                                                            chunk=args.chunk,
+                                                            process_group=group), 1)
 
-    # secondary: the SURVEY.md 8d weak-scaling batch (4096 per GPU), same model
-    small = None
-    if args.batch > 4096 and args.small_batch:
-        xs = x_dev[:4096]
-        sstep = lambda n: trainer.em_stochastic_steps(model, [xs] * n, 0.5, chunk=4096,
-                                                      process_group=group)
-        sstep(3)
-        ms_small = timed(lambda: sstep(args.steps), 1)
-        small = {"batch_per_gpu": 4096, "chunk": 4096,
-                 "value": world * 4096 * args.steps / (ms_small / 1e3),
-                 "ms_per_step": ms_small / args.steps}
+    # secondary: the SURVEY.md 8d weak-scaling batch (4096 per GPU) and the
+    # paper's batch (500), same model, device-resident
+    small = []
+    if args.small_batch:
+        for sb in (4096, 500):
+            if sb >= args.batch:
+                continue
+            xs = x_dev[:sb]
+            sstep = lambda n, xs=xs, sb=sb: trainer.em_stochastic_steps(
+                model, [xs] * n, 0.5, chunk=sb, process_group=group)
+            sstep(3)
+            n_sb = max(args.steps, 20)
+            ms_small = timed(lambda: sstep(n_sb), 1)
+            small.append({"batch_per_gpu": sb, "chunk": sb, "steps": n_sb,
+                          "value": world * sb * n_sb / (ms_small / 1e3),
+                          "ms_per_step": ms_small / n_sb})
 
     # per-kernel-class device time of the same step (CUDA events, separate pass)
     _native.profile_enable(True)
@@ -434,16 +496,17 @@ def run_ours(args):
     value = world * B * args.steps / (ms / 1e3)
     e2e = world * B * e2e_steps / (ms_e2e / 1e3)
     e2e_f32 = world * B * e2e_steps / (ms_e2e_f32 / 1e3)
-    hbm, bf16, peak_kind = load_peaks()
+    e2e_f64 = world * B * f64_steps / (ms_e2e_f64 / 1e3)
+    peaks, peak_kind = load_peaks()
     work = work_per_sample(circuit)
     classes = {}
     for name, (tot_ms, cnt) in prof.items():
         per_step = tot_ms / prof_steps
-        w = work.get(name, {"flops": 0, "bytes": 0})
-        classes[name] = {"ms_per_step": per_step, "launch_groups_per_step": cnt / prof_steps,
-                         "share": None,
-                         "tflops": w["flops"] * B / (per_step / 1e3) / 1e12 if w["flops"] else None,
-                         "gbs": w["bytes"] * B / (per_step / 1e3) / 1e9 if w["bytes"] else None}
+        w = work.get(name)
+        c = {"ms_per_step": per_step, "launch_groups_per_step": cnt / prof_steps, "share": None}
+        if w is not None:
+            c.update(class_fractions(name, w, B, per_step, cnt / prof_steps, peaks))
+        classes[name] = c
     total_prof = sum(c["ms_per_step"] for n, c in classes.items() if n not in ("prepare",))
     for c in classes.values():
         c["share"] = c["ms_per_step"] / total_prof if total_prof else None
@@ -451,31 +514,23 @@ def run_ours(args):
     tw = work[top]
     per_launch_ms = prof[top][0] / prof[top][1]
     groups = prof[top][1] / prof_steps
-    if top.startswith("einsum"):
+    if tw.get("tc"):
         achieved = tw["flops"] * B / groups / (per_launch_ms / 1e3) / 1e12
-        roof = {"kernel": top, "bound": "tensor", "achieved": achieved, "peak": bf16,
-                "unit": "TFLOP/s", "frac": achieved / bf16,
-                "peak_source": f"{peak_kind} bf16 dense (MEASURED_PEAKS.json)"}
-    elif top == "leaf_fwd" and circuit.k % 8 == 0 and type(fam).__name__ == "GaussianFamily":
-        # FP64 DMMA leaf forward: 4 D K R algorithmic flops per sample (two
-        # features per variable and component)
-        achieved = tw["flops"] * B / groups / (per_launch_ms / 1e3) / 1e12
-        roof = {"kernel": top, "bound": "tensor", "achieved": achieved,
-                "peak": FP64_TENSOR_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_TENSOR_PEAK_TFLOPS,
-                "peak_source": "measured FP64 tensor-core (DMMA) peak, scripts/peak_dmma.cu "
-                               "(MEASURED_PEAKS.json has no FP64 figure)",
-                "hbm_gbs": tw["bytes"] * B / groups / (per_launch_ms / 1e3) / 1e9}
+        roof = {"kernel": top, "bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"],
+                "frac_issued_3xbf16": 3 * achieved / peaks["bf16_tflops"],
+                "peak_source": f"bf16 dense, {peak_kind}"}
     else:
         achieved = tw["bytes"] * B / groups / (per_launch_ms / 1e3) / 1e9
-        roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm,
-                "peak_source": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
+        roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                "peak_source": f"HBM copy, {peak_kind}"}
     roof["traffic"] = kernel_traffic(top)
     if roof["traffic"] is not None:
         roof["traffic_source"] = "profiles/kernel_traffic.json (ncu dram read+write bytes/launch)"
-        roof["algorithmic_bytes"] = tw["bytes"] * B / groups
+    roof["algorithmic_bytes"] = tw["bytes"] * B / groups
     roof["per_launch_ms"] = per_launch_ms
+    roof["step"] = step_roofline(circuit, B, ms / args.steps, peaks)
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -487,7 +542,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 stats/M-step)",
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "mixed: exact u8 x s8 leaf forward, 3xBF16 contractions (fp32-equivalent), fp64 statistics and M-step",
         "data": "synthetic",
         "config": {"workload": f"{args.config} SVHN-shape 32x32x3 PD EiNet K=40, delta 8 "
                                f"vertical, Gaussian image-mode leaves, EM lambda 0.5",
@@ -499,13 +555,18 @@ def run_ours(args):
                 "input": "pinned host u8 pixels (EIND1 payload, x = k/255), copied and "
                          "decoded on the device inside trainer.em_stochastic_steps",
                 "fp32_host_input": {"value": e2e_f32,
-                                    "h2d_bytes_per_step": int(B * rg.d_vars * 4)}},
+                                    "h2d_bytes_per_step": int(B * rg.d_vars * 4)},
+                "f64_numpy_input": {"value": e2e_f64, "steps": f64_steps,
+                                    "h2d_bytes_per_step": int(B * rg.d_vars * 4),
+                                    "input": "float64 NumPy batch (the reference caller's "
+                                             "type), fp32 conversion on the host inside the "
+                                             "timed call"}},
         "gpu_launches": int(launches),
         "roofline": roof,
         "kernels": classes,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
-        "secondary_b4096": small,
+        "secondary_batches": small,
     }
     print(json.dumps(line), flush=True)
     if group is not None:

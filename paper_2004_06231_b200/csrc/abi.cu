@@ -146,6 +146,11 @@ static void free_plan_memory(Plan *p) {
   f(p->d_i8_tab);
   if (p->side_stream) cudaStreamDestroy(p->side_stream);
   p->side_stream = nullptr;
+  if (p->fork_stream) cudaStreamDestroy(p->fork_stream);
+  p->fork_stream = nullptr;
+  if (p->fork_ev) cudaEventDestroy(p->fork_ev);
+  if (p->join_ev) cudaEventDestroy(p->join_ev);
+  p->fork_ev = p->join_ev = nullptr;
   f(p->d_i8_col);
   f(p->d_scope_pos);
   f(p->d_tiledesc);
@@ -498,6 +503,11 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   if (p->leaf_i8 &&
       (rc = check_cuda(cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking),
                        "side stream")))
+    return rc;
+  if ((rc = check_cuda(cudaStreamCreateWithFlags(&p->fork_stream, cudaStreamNonBlocking),
+                       "fork stream")) ||
+      (rc = check_cuda(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming), "event")) ||
+      (rc = check_cuda(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming), "event")))
     return rc;
   {
     std::vector<int> pos((size_t)R * D, -1);

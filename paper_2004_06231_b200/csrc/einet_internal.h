@@ -112,6 +112,8 @@ struct Plan {
   int *d_i8_col = nullptr;         // per padded chunk: 32 variable indices
   int64_t w_i8flag = 0;            // workspace: off-grid flag of the last i8 forward
   cudaStream_t side_stream = nullptr;  // captures the fallback body of a conditional node
+  cudaStream_t fork_stream = nullptr;  // M-step: leaf branch beside the einsum weights
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   // fused M-step (mstep.cu): per-einsum-layer tile geometry, temp leaf terms
   int64_t *d_tiledesc = nullptr;   // einsum layers x TD_WORDS (mstep.cu)
   int n_tiledesc = 0;
@@ -194,6 +196,7 @@ int launch_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *
 int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_prepare_leaf_dmma(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_prepare_leaf_i8(Plan &p, uint8_t *compute, cudaStream_t st);
+int launch_i8_img(Plan &p, uint8_t *compute, cudaStream_t st);
 void plan_leaf_i8(Plan &p, std::vector<int> &tab, std::vector<int> &col);
 bool leaf_i8_supported(const Plan &p);
 int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t B, uint8_t *wsb,

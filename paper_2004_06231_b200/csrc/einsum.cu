@@ -684,6 +684,91 @@ __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__res
     }
 }
 
+// W statistics of K_out = 1 rows (the root einsum layer):
+//   S[l][i,j] = sum_b RT[b,l] EA[b,l,i] EB[b,l,j]
+// a K x K x B product per row, on CUDA cores (the tensor-core kernel pads
+// K_out to 16). grid (rows, nsplit), block K4*K4 (<= 256): thread (ti, tj)
+// owns rows ti + K4*u and columns tj + K4*v (u, v < 4), so a warp reads
+// consecutive padded rows (conflict-free 16-byte loads). Each CTA sums its
+// contiguous run of 32-sample blocks in fp32 and writes an fp64 partial per
+// split; the partials are reduced in split order (deterministic).
+constexpr int WK1_ROW = 36;
+__global__ void __launch_bounds__(256) k_wstats_k1(const float *__restrict__ EA,
+                                                   const float *__restrict__ EB,
+                                                   const float *__restrict__ RT, int64_t Bc,
+                                                   int ks, int64_t B, int K, int L, int nsplit,
+                                                   double *wpart) {
+  extern __shared__ __align__(16) float smk1[];
+  const int K4 = (K + 3) / 4;
+  float *ea_s = smk1;                  // [K4*4][WK1_ROW], scaled by RT
+  float *eb_s = ea_s + K4 * 4 * WK1_ROW;
+  const int l = blockIdx.x, split = blockIdx.y;
+  const int nblk = (int)((B + 31) / 32);
+  const int c0 = (int)((int64_t)split * nblk / nsplit), c1 = (int)((int64_t)(split + 1) * nblk / nsplit);
+  const int tid = threadIdx.x, ti = tid / K4, tj = tid - ti * K4;
+  const bool act = ti < K4;
+  float acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
+  for (int c = c0; c < c1; ++c) {
+    const int64_t b0 = (int64_t)c * 32;
+    __syncthreads();
+    const float *ea = EA + ev_idx(l, b0, 0, Bc, K), *eb = EB + ev_idx(l, b0, 0, Bc, K);
+    const float *rt = RT + tb_idx(l, b0, 0, Bc, ks);
+    for (int e = tid; e < K4 * 4 * 8; e += blockDim.x) {
+      const int i = e >> 3, q = e & 7;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bv = a;
+      if (i < K) {
+        a = *(const float4 *)(ea + i * EV_ROW + 4 * q);
+        bv = *(const float4 *)(eb + i * EV_ROW + 4 * q);
+        const float4 r = *(const float4 *)(rt + 4 * q);
+        const int nb = (int)min((int64_t)32, B - b0) - 4 * q;  // samples past B count 0
+        a.x = nb > 0 ? a.x * r.x : 0.f;
+        a.y = nb > 1 ? a.y * r.y : 0.f;
+        a.z = nb > 2 ? a.z * r.z : 0.f;
+        a.w = nb > 3 ? a.w * r.w : 0.f;
+        bv.x = nb > 0 ? bv.x : 0.f;
+        bv.y = nb > 1 ? bv.y : 0.f;
+        bv.z = nb > 2 ? bv.z : 0.f;
+        bv.w = nb > 3 ? bv.w : 0.f;
+      }
+      *(float4 *)(ea_s + i * WK1_ROW + 4 * q) = a;
+      *(float4 *)(eb_s + i * WK1_ROW + 4 * q) = bv;
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 a[4], e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = *(const float4 *)(ea_s + (ti + K4 * u) * WK1_ROW + 4 * q);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) e[v] = *(const float4 *)(eb_s + (tj + K4 * v) * WK1_ROW + 4 * q);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            acc[u][v] = fmaf(a[u].x, e[v].x, acc[u][v]);
+            acc[u][v] = fmaf(a[u].y, e[v].y, acc[u][v]);
+            acc[u][v] = fmaf(a[u].z, e[v].z, acc[u][v]);
+            acc[u][v] = fmaf(a[u].w, e[v].w, acc[u][v]);
+          }
+      }
+    }
+  }
+  if (!act) return;
+  double *dst = wpart + ((int64_t)split * L + l) * K * K;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = ti + K4 * u, j = tj + K4 * v;
+      if (i < K && j < K) dst[i * K + j] = (double)acc[u][v];
+    }
+}
+
 // Child responsibilities, one sample per thread; W staged per k-chunk.
 template <int KT>
 __global__ void __launch_bounds__(EF_TB) k_einsum_childrho(
@@ -1094,7 +1179,14 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
     const int64_t lw = (int64_t)L.rows * L.k_out * K * K;
     {
       ProfScope prof("einsum_wstats", st);
-      if (p.use_tc && L.tc) {
+      const int K4 = (K + 3) / 4;
+      if (L.k_out == 1 && K4 * K4 <= 256 && !getenv("EINET_WK1_OFF")) {
+        const int ns = wstats_bsplit(p, L, B, L.rows);
+        const size_t smem = sizeof(float) * 2 * K4 * 4 * WK1_ROW;
+        k_wstats_k1<<<dim3(L.rows, ns), K4 * K4, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K,
+                                                             L.rows, ns, w.wpart);
+        launch_reduce_partials(stats + L.w_off, w.wpart, ns, lw, lw, params + L.w_off, st);
+      } else if (p.use_tc && L.tc) {
         int rc = launch_wstats_tc(p, L, EA, EB, w, B, params + L.w_off, stats + L.w_off, st);
         if (rc) return rc;
       } else {

@@ -248,4 +248,24 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// INT8 leaf forward (leaf_i8.cu): the three coefficients of (variable d,
+// component k) from lp = (sa, -mu sa), and the column scale 2^(E-8) with
+// max |G| * 2^(8-E) <= 127 (1 when the column is empty).
+__device__ __forceinline__ void i8_coefs(double2 q, double &gu, double &gh, double &gl) {
+  const double a = q.x * q.x;
+  gu = 2.0 * q.x * q.y / 255.0;
+  gh = a * (256.0 / 65025.0);
+  gl = a / 65025.0;
+}
+__device__ __forceinline__ double i8_scale(double m) {
+  double scale = 1.0;
+  if (m > 0.0 && isfinite(m)) {
+    int e;
+    frexp(m * (256.0 / 127.0), &e);
+    while (m * ldexp(1.0, 8 - e) > 127.0) ++e;
+    scale = ldexp(1.0, e - 8);
+  }
+  return scale;
+}
+
 }  // namespace einet

@@ -536,6 +536,10 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
   if (rc) return rc;
   const char *dbg = getenv("EINET_I8_DEBUG");
   const bool no_fallback = dbg && (atoi(dbg) & 32);  // diagnostics
+  // EINET_LEAF_COND=0: gated launches inside captured graphs too (ncu cannot
+  // profile kernel nodes of graphs that hold conditional nodes)
+  const char *cenv = getenv("EINET_LEAF_COND");
+  const bool use_cond = !(cenv && cenv[0] == '0');
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaGraph_t graph = nullptr;
   const cudaGraphNode_t *deps = nullptr;
@@ -543,7 +547,7 @@ int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t
   if ((rc = check_cuda(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &ndeps),
                        "capture info")))
     return rc;
-  if (cs != cudaStreamCaptureStatusActive || no_fallback) {
+  if (cs != cudaStreamCaptureStatusActive || no_fallback || !use_cond) {
     if ((rc = launch_leaf_fwd_i8(p, compute, x, B, wsb, flag, 0ULL, st))) return rc;
     if (no_fallback) return 0;
     return launch_leaf_fallback(p, compute, x, B, wsb, status, st, flag);

@@ -304,38 +304,61 @@ __global__ void __launch_bounds__(256) k_mstep_leaf_gauss(
 
 // per (leaf, k): scope sums of the per-variable terms (fixed-order tree):
 // cnst = sum -0.5 (log 2 pi + log var), cm2 = sum m^2. grid (n_leaf, K).
+// With i8c (INT8 leaf forward): also the column scale and C = sum (mu sa)^2
+// of leaf_i8.cu k_i8_colscale, from the freshly written lp (every covered
+// variable is active in the cached training compute).
 __global__ void __launch_bounds__(256) k_leaf_consts(const double *__restrict__ mtmp,
                                                      const int *scope_off, const int *scope_vars,
                                                      const int *leaf_rep, int D, int K,
                                                      double *cnst, double *cm2,
-                                                     const int32_t *status) {
-  __shared__ double red[2][8];
+                                                     const int32_t *status,
+                                                     const double2 *__restrict__ lp, int K8,
+                                                     double *i8c) {
+  __shared__ double red[4][8];
   if (step_failed(status)) return;
   const int leaf = blockIdx.x, k = blockIdx.y, r = leaf_rep[leaf];
-  double a = 0.0, b = 0.0;
+  double a = 0.0, b = 0.0, mx = 0.0, cs = 0.0;
   for (int q = scope_off[leaf] + threadIdx.x; q < scope_off[leaf + 1]; q += 256) {
-    const double *t = mtmp + (((int64_t)r * D + scope_vars[q]) * K + k) * 2;
+    const int d = scope_vars[q];
+    const double *t = mtmp + (((int64_t)r * D + d) * K + k) * 2;
     a += t[0];
     b += t[1];
+    if (i8c) {
+      const double2 v = lp[((int64_t)r * D + d) * K + k];
+      double gu, gh, gl;
+      i8_coefs(v, gu, gh, gl);
+      mx = fmax(mx, fmax(fabs(gu), fmax(fabs(gh), fabs(gl))));
+      cs += v.y * v.y;
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_down_sync(0xffffffffu, a, o);
     b += __shfl_down_sync(0xffffffffu, b, o);
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    cs += __shfl_down_sync(0xffffffffu, cs, o);
   }
   if ((threadIdx.x & 31) == 0) {
     red[0][threadIdx.x >> 5] = a;
     red[1][threadIdx.x >> 5] = b;
+    red[2][threadIdx.x >> 5] = mx;
+    red[3][threadIdx.x >> 5] = cs;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double sa = 0.0, sb = 0.0;
+    double sa = 0.0, sb = 0.0, m = 0.0, sc = 0.0;
     for (int w = 0; w < 8; ++w) {
       sa += red[0][w];
       sb += red[1][w];
+      m = fmax(m, red[2][w]);
+      sc += red[3][w];
     }
     cnst[leaf * K + k] = sa;
     if (cm2) cm2[leaf * K + k] = sb;
+    if (i8c) {
+      i8c[((int64_t)leaf * K8 + k) * 2] = i8_scale(m);
+      i8c[((int64_t)leaf * K8 + k) * 2 + 1] = sc;
+    }
   }
 }
 
@@ -349,6 +372,30 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
   // tensor of the cached, unmasked training compute (tensor-core weight images
   // for tc-capable layers, DMMA leaf image), replacing launch_prepare
   const bool fused = p.family == EINET_FAMILY_GAUSSIAN && p.k <= 64;
+  // The fused leaf branch (Gaussian) is independent of the weight updates:
+  // it runs on the fork stream beside them (two branches of the CUDA graph).
+  cudaStream_t ls = st;
+  if (fused && p.fork_stream) {
+    int rc = check_cuda(cudaEventRecord(p.fork_ev, st), "fork");
+    if (!rc) rc = check_cuda(cudaStreamWaitEvent(p.fork_stream, p.fork_ev, 0), "fork");
+    if (rc) return rc;
+    ls = p.fork_stream;
+  }
+  if (fused) {
+    const int64_t warps = (int64_t)p.num_replicas * p.d_vars;
+    double *mtmp = (double *)(compute + p.c_mtmp);
+    k_mstep_leaf_gauss<<<(int)((warps + 7) / 8), 256, 0, ls>>>(
+        params + p.sizes.phi_offset, stats + p.sizes.stats_acc_pt_offset,
+        stats + p.sizes.stats_p_offset, p.d_leaf_of, p.d_scope_pos, p.d_leaf_pvo, p.d_vars, K,
+        p.num_replicas, lam, p.var_min, p.var_max, status, c, p.leaf_dmma, mtmp);
+    k_leaf_consts<<<dim3(p.n_leaf, K), 256, 0, ls>>>(
+        mtmp, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep, p.d_vars, K, c.cnst,
+        p.leaf_dmma ? c.cm2 : nullptr, status, (const double2 *)c.leafp, p.i8_k8,
+        p.leaf_i8 ? (double *)(compute + p.c_i8c) : nullptr);
+    count_launch(2);
+    int rc = launch_i8_img(p, compute, ls);
+    if (rc) return rc;
+  }
   if (p.n_w) {
     const int nslices = (int)(p.n_w / KK);
     k_mstep_einsum<<<nslices, 256, 0, st>>>(params, c.w32, stats, K, lam, eps_w, status,
@@ -363,18 +410,11 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
     count_launch();
   }
   if (fused) {
-    const int64_t warps = (int64_t)p.num_replicas * p.d_vars;
-    double *mtmp = (double *)(compute + p.c_mtmp);
-    k_mstep_leaf_gauss<<<(int)((warps + 7) / 8), 256, 0, st>>>(
-        params + p.sizes.phi_offset, stats + p.sizes.stats_acc_pt_offset,
-        stats + p.sizes.stats_p_offset, p.d_leaf_of, p.d_scope_pos, p.d_leaf_pvo, p.d_vars, K,
-        p.num_replicas, lam, p.var_min, p.var_max, status, c, p.leaf_dmma, mtmp);
-    k_leaf_consts<<<dim3(p.n_leaf, K), 256, 0, st>>>(mtmp, p.d_scope_off, p.d_scope_vars,
-                                                     p.d_leaf_rep, p.d_vars, K, c.cnst,
-                                                     p.leaf_dmma ? c.cm2 : nullptr, status);
-    count_launch(2);
-    int rc = launch_prepare_leaf_i8(p, compute, st);
-    if (rc) return rc;
+    if (ls != st) {
+      int rc = check_cuda(cudaEventRecord(p.join_ev, ls), "join");
+      if (!rc) rc = check_cuda(cudaStreamWaitEvent(st, p.join_ev, 0), "join");
+      if (rc) return rc;
+    }
     return check_cuda(cudaGetLastError(), "fused mstep kernels");
   }
   const int64_t n = (int64_t)p.d_vars * K * p.num_replicas;
