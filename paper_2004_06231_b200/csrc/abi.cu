@@ -152,6 +152,7 @@ static void free_plan_memory(Plan *p) {
   if (p->join_ev) cudaEventDestroy(p->join_ev);
   p->fork_ev = p->join_ev = nullptr;
   f(p->d_i8_col);
+  f(p->d_i8_grp);
   f(p->d_scope_pos);
   f(p->d_tiledesc);
   f(p->d_csr_off);
@@ -414,8 +415,8 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     const char *env = getenv("EINET_DISABLE_TC");
     p->use_tc = !(env && env[0] == '1');
   }
-  std::vector<int> i8_tab, i8_col;
-  if (p->family == EINET_FAMILY_GAUSSIAN) plan_leaf_i8(*p, i8_tab, i8_col);
+  std::vector<int> i8_tab, i8_col, i8_grp;
+  if (p->family == EINET_FAMILY_GAUSSIAN) plan_leaf_i8(*p, i8_tab, i8_col, i8_grp);
   if (p->leaf_i8) {
     p->c_i8img = seg((int64_t)p->i8_ng * 96 * (p->h_leaf_pvo.back() / 32));
     p->c_i8c = seg(16 * (int64_t)p->n_leaf * p->i8_k8);
@@ -500,6 +501,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   if (!p->h_leaf_pvo.empty() && (rc = upload(&p->d_leaf_pvo, p->h_leaf_pvo))) return rc;
   if (p->leaf_i8 && (rc = upload(&p->d_i8_tab, i8_tab))) return rc;
   if (p->leaf_i8 && (rc = upload(&p->d_i8_col, i8_col))) return rc;
+  if (p->leaf_i8 && (rc = upload(&p->d_i8_grp, i8_grp))) return rc;
   if (p->leaf_i8 &&
       (rc = check_cuda(cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking),
                        "side stream")))

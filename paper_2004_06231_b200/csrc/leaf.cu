@@ -530,7 +530,13 @@ static int launch_leaf_fallback(Plan &p, const uint8_t *compute, const float *x,
 int launch_leaf_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
                         uint8_t *wsb, int32_t *status, cudaStream_t st) {
   ProfScope prof("leaf_fwd", st);
-  if (!leaf_i8_supported(p)) return launch_leaf_fallback(p, compute, x, B, wsb, status, st, nullptr);
+  // below ~1024 samples the FP64 path's short per-CTA chains win (the INT8
+  // kernel walks a leaf pair's whole scope per CTA); EINET_LEAF_I8_MIN_BATCH
+  // overrides (tests force the INT8 path at small sizes)
+  const char *mb = getenv("EINET_LEAF_I8_MIN_BATCH");
+  const int64_t min_batch = mb ? atoll(mb) : 1024;
+  if (!leaf_i8_supported(p) || B < min_batch)
+    return launch_leaf_fallback(p, compute, x, B, wsb, status, st, nullptr);
   int *flag = (int *)(wsb + p.w_i8flag);
   int rc = check_cuda(cudaMemsetAsync(flag, 0, sizeof(int), st), "leaf i8 flag");
   if (rc) return rc;

@@ -43,7 +43,10 @@
 //     cnst - Q, and the slab (shift = max over k, fp32 offsets).
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
+#include <utility>
+#include <vector>
 
 #include "kern_common.cuh"
 #include "tc_common.cuh"
@@ -53,14 +56,15 @@ namespace einet {
 constexpr int LI_VC = 32;              // scope variables per chunk
 constexpr int LI_S = 6;                // coefficient digits per column
 constexpr int LI_KB = 3 * LI_VC;       // K bytes per chunk: u | h | l
-constexpr int LI_XP = 36;              // padded x row (floats)
-constexpr int LI_XST = 6;              // x ring stages (raw fp32 chunks)
-constexpr int LI_AST = 3;              // A | B ring stages (MMA operands)
-constexpr int LI_GW = 4, LI_CW = 8, LI_EW = 4;
-constexpr int LI_MMA_WARP = LI_GW + LI_CW + LI_EW;  // 16
-constexpr int LI_BW = LI_MMA_WARP + 1;              // 17: digit-tile loader
-constexpr int LI_THREADS = 32 * (LI_BW + 1);        // 576
-constexpr int LI_XBYTES = 128 * LI_XP * 4;          // 18432
+constexpr int LI_XP = 32;              // x row (floats; 16-byte granules XOR-swizzled by row)
+constexpr int LI_XST = 7;              // x ring stages (raw fp32 chunks)
+constexpr int LI_AST = 2;              // A ring stages (u8 features)
+constexpr int LI_BST = 3;              // B ring stages (digit tiles)
+constexpr int LI_GW = 2, LI_CW = 16, LI_EW = 4;
+constexpr int LI_MMA_WARP = LI_GW + LI_CW + LI_EW;  // 22
+constexpr int LI_BW = LI_MMA_WARP + 1;              // 23: digit-tile loader
+constexpr int LI_THREADS = 32 * (LI_BW + 1);        // 768
+constexpr int LI_XBYTES = 128 * LI_XP * 4;          // 16384
 constexpr int LI_ABYTES = 128 * LI_KB;              // 12288
 constexpr int LI_ACC_STRIDE = 256;                  // TMEM columns between accumulators
 constexpr int LI_F_VEC = 1, LI_F_FIRST = 2, LI_F_LAST = 4;  // chunk table flags
@@ -176,8 +180,22 @@ struct LeafI8Args {
   WsView ws;
   int64_t B;
   int D, K, K8, NG, n_leaf, npc;
+  const int *grp_pc;         // first chunk of each leaf pair (n_pairs + 1)
+  int grouped;               // 1: blockIdx.y = leaf pair (small batches), 0: all leaves
   int debug;                 // EINET_I8_DEBUG ablations (diagnostics only)
+  long long *trace;          // EINET_I8_TRACE (diagnostics): per-chunk timestamps of CTA 0
 };
+
+__device__ __forceinline__ long long li_now() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define LI_TRACE(slot, pc)                                                  \
+  do {                                                                      \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && (pc) < 128 && lane == 0)               \
+      a.trace[(pc) * 8 + (slot)] = li_now();                                \
+  } while (0)
 
 // instruction descriptor: kind::i8, A u8, B s8, D s32, K-major
 __host__ __device__ constexpr uint32_t idesc_u8s8(int M, int N) {
@@ -202,6 +220,35 @@ __device__ __forceinline__ void li_arrive(uint64_t *bar) {
 // exact in fp32 (fma; |e| < 2^-16 needs <= 16 significant bits), and x is the
 // correctly rounded u / 255 iff |e| <= 255 ulp(x) / 2 (u / 255 is never a
 // rounding midpoint). NaN / inf / off-grid values fail.
+// Paired fp32 arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a).
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x f2x_make(float lo, float hi) {
+  return (f2x)__float_as_uint(lo) | ((f2x)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ f2x f2x_splat(float v) { return f2x_make(v, v); }
+__device__ __forceinline__ uint32_t f2x_lo(f2x v) { return (uint32_t)v; }
+__device__ __forceinline__ uint32_t f2x_hi(f2x v) { return (uint32_t)(v >> 32); }
+__device__ __forceinline__ f2x f2x_fma(f2x a, f2x b, f2x c) {
+  f2x r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2x f2x_mul(f2x a, f2x b) {
+  f2x r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2x f2x_add(f2x a, f2x b) {
+  f2x r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2x f2x_sub(f2x a, f2x b) {
+  f2x r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 __device__ __forceinline__ bool grid_u8(float x, uint32_t &u) {
   // rint(255 x) through the 1.5 * 2^23 magic constant (FFMA, no conversions)
   const float t = fmaf(x, 255.f, 12582912.f);
@@ -217,7 +264,8 @@ __device__ __forceinline__ bool grid_u8(float x, uint32_t &u) {
 template <bool COND>
 __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint64_t xfull[LI_XST], xempty[LI_XST], abfull[LI_AST], abempty[LI_AST],
+  __shared__ uint64_t xfull[LI_XST], xempty[LI_XST], afull[LI_AST], aempty[LI_AST],
+      bfull[LI_BST], bempty[LI_BST],
       accfull[2], accempty[2];
   __shared__ uint32_t xmask[LI_XST];               // active-variable mask of the staged chunk
   __shared__ int xinfo[LI_XST], abinfo[LI_AST];     // leaf | flags << 24
@@ -230,10 +278,15 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   const int NG = a.NG;
   const uint32_t bbytes = (uint32_t)(NG * LI_KB);
-  const uint32_t ab_bytes = LI_ABYTES + bbytes;
-  uint8_t *xring = sm;                                // [LI_XST][128][LI_XP] fp32
-  uint8_t *abring = sm + (size_t)LI_XST * LI_XBYTES;  // [LI_AST][A | B]
+  uint8_t *xring = sm;                                 // [LI_XST][128][LI_XP] fp32
+  uint8_t *aring = sm + (size_t)LI_XST * LI_XBYTES;    // [LI_AST][128 x 96] u8
+  uint8_t *bring = aring + (size_t)LI_AST * LI_ABYTES; // [LI_BST][NG x 96] s8
   const int64_t b0 = (int64_t)blockIdx.x * 128;
+  // this CTA's chunks [pcb, pce) and leaves [lb, le)
+  const int pcb = a.grouped ? a.grp_pc[blockIdx.y] : 0;
+  const int pce = a.grouped ? a.grp_pc[blockIdx.y + 1] : a.npc;
+  const int lb = a.grouped ? 2 * blockIdx.y : 0;
+  const int le = a.grouped ? min(lb + 2, a.n_leaf) : a.n_leaf;
   if (w == LI_MMA_WARP) tc::tmem_alloc(&tbase, 512);
   if (t == 0) {
     for (int s = 0; s < LI_XST; ++s) {
@@ -241,8 +294,12 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
       tc::mbar_init(&xempty[s], LI_CW);
     }
     for (int s = 0; s < LI_AST; ++s) {
-      tc::mbar_init(&abfull[s], LI_CW + 1);
-      tc::mbar_init(&abempty[s], 1);
+      tc::mbar_init(&afull[s], LI_CW);
+      tc::mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < LI_BST; ++s) {
+      tc::mbar_init(&bfull[s], 1);
+      tc::mbar_init(&bempty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&accfull[i], 1);
@@ -262,18 +319,20 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
     // windows of LI_WIN chunks: window W+1 is loaded into registers while W
     // is processed and published to shared memory between windows, so no
     // global-load latency sits between a freed stage and its refill.
-    const int nwin = (a.npc + LI_WIN - 1) / LI_WIN;
-    int rc[4];
+    const int nwin = (pce - pcb + LI_WIN - 1) / LI_WIN;
+    constexpr int GT = 32 * LI_GW;                  // gather threads
+    constexpr int NRC = LI_WIN * LI_VC / GT;        // window column entries per thread
+    int rc[NRC];
     int4 rt = make_int4(0, 0, 0, 0);
     uint32_t ra = 0;
     auto load_win = [&](int W) {
-      const int base = W * LI_WIN;
+      const int base = pcb + W * LI_WIN;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int e = t + 128 * i, c = base + (e >> 5);
-        rc[i] = c < a.npc ? a.col[(int64_t)c * LI_VC + (e & 31)] : 0;
+      for (int i = 0; i < NRC; ++i) {
+        const int e = t + GT * i, c = base + (e >> 5);
+        rc[i] = c < pce ? a.col[(int64_t)c * LI_VC + (e & 31)] : 0;
       }
-      if (t < LI_WIN && base + t < a.npc) {
+      if (t < LI_WIN && base + t < pce) {
         rt = a.tab[base + t];
         ra = a.amask[base + t];
       }
@@ -281,8 +340,8 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
     auto store_win = [&](int W) {
       const int wb = W & 1;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int e = t + 128 * i;
+      for (int i = 0; i < NRC; ++i) {
+        const int e = t + GT * i;
         win_col[wb][e >> 5][e & 31] = rc[i];
       }
       if (t < LI_WIN) {
@@ -296,13 +355,14 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
     for (int W = 0; W < nwin; ++W) {
       if (W + 1 < nwin) load_win(W + 1);
       const int wb = W & 1;
-      const int pc_end = min(a.npc, (W + 1) * LI_WIN);
-      for (int pc = W * LI_WIN; pc < pc_end; ++pc) {
-        const int ci = pc - W * LI_WIN;
+      const int pc_end = min(pce, pcb + (W + 1) * LI_WIN);
+      for (int pc = pcb + W * LI_WIN; pc < pc_end; ++pc) {
+        const int ci = pc - pcb - W * LI_WIN;
         const int4 tb = win_tab[wb][ci];
         const int nv = tb.y;
-        const int s = pc % LI_XST, ph = (pc / LI_XST) & 1;
+        const int s = (pc - pcb) % LI_XST, ph = ((pc - pcb) / LI_XST) & 1;
         tc::mbar_wait(&xempty[s], ph ^ 1);
+        if (w == 0) LI_TRACE(0, pc);
         float *xr = (float *)(xring + (size_t)s * LI_XBYTES);
         if (t == 0) {
           xmask[s] = win_am[wb][ci];
@@ -316,13 +376,13 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
           const bool real = 4 * qd < nv;
           const int d = win_col[wb][ci][4 * qd];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = (t >> 3) + 16 * i;
+          for (int i = 0; i < 1024 / GT; ++i) {
+            const int r = (t >> 3) + (GT / 8) * i;
             const int64_t b = b0 + r;
             const bool ok = real && b < a.B;
             const float *src = a.x + (ok ? b * a.D + d : 0);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
-                             tc::smem_u32(xr + r * LI_XP + 4 * qd)),
+                             tc::smem_u32(xr + r * LI_XP + 4 * (qd ^ (r & 7)))),
                          "l"(src), "r"(ok ? 16 : 0));
           }
         } else {
@@ -333,7 +393,7 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
             const bool ok = real && b < a.B;
             const float *src = a.x + (ok ? b * a.D + d : 0);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
-                             tc::smem_u32(xr + r * LI_XP + lane)),
+                             tc::smem_u32(xr + r * LI_XP + 4 * ((lane >> 2) ^ (r & 7)) + (lane & 3))),
                          "l"(src), "r"(ok ? 4 : 0));
           }
         }
@@ -345,99 +405,127 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
     }
   } else if (w < LI_GW + LI_CW) {
     // ---- x -> u8 features (A tile) ----
-    const int ct = t - 32 * LI_GW;  // 0..255
+    // Thread (row, g): 8 variables 8g..8g+7 of one sample. Paired fp32 math
+    // (FFMA2 / FMUL2 / FADD2) and byte permutes:
+    //   t = 255 x + 1.5*2^23  (its low byte is u = rint(255 x)),  uf = t - 1.5*2^23,
+    //   q = fl32(uf / 255) by one FMA-refined reciprocal product (exact for
+    //   every u in [0, 255]), valid <=> x == q and 0 <= u <= 255;
+    //   s = uf^2 + 2^23 holds u^2 in its low 16 bits (h = byte 1, l = byte 0).
+    const int ct = t - 32 * LI_GW;  // 0 .. 32*LI_CW-1
     const int g = ct >> 7, row = ct & 127;
-    const uint32_t aoff = (uint32_t)((row >> 3) * 128 + (row & 7) * 16);
-    bool bad = false;
-    for (int pc = 0; pc < a.npc; ++pc) {
-      const int xs = pc % LI_XST, xph = (pc / LI_XST) & 1;
-      const int as = pc % LI_AST, aph = (pc / LI_AST) & 1;
+    const uint32_t aoff = (uint32_t)((g >> 1) * 2048 + (row >> 3) * 128 + (row & 7) * 16 + 8 * (g & 1));
+    uint32_t bad = 0;
+    const f2x kM = f2x_splat(12582912.f), k255 = f2x_splat(255.f), kn255 = f2x_splat(-255.f);
+    const f2x kC = f2x_splat(1.f / 255.f), kS = f2x_splat(8388608.f), knM = f2x_splat(-12582912.f);
+    for (int pc = pcb; pc < pce; ++pc) {
+      const int i = pc - pcb;
+      const int xs = i % LI_XST, xph = (i / LI_XST) & 1;
+      const int as = i % LI_AST, aph = (i / LI_AST) & 1;
       tc::mbar_wait(&xfull[xs], xph);
-      const float *xr = (const float *)(xring + (size_t)xs * LI_XBYTES) + row * LI_XP + 16 * g;
-      float4 v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = *(const float4 *)(xr + 4 * q);
-      const uint32_t m = xmask[xs] >> (16 * g);
+      if (w == LI_GW) LI_TRACE(1, pc);
+      const float *xr = (const float *)(xring + (size_t)xs * LI_XBYTES) + row * LI_XP;
+      const float4 v0 = *(const float4 *)(xr + 4 * ((2 * g) ^ (row & 7)));
+      const float4 v1 = *(const float4 *)(xr + 4 * ((2 * g + 1) ^ (row & 7)));
+      const uint32_t m = (xmask[xs] >> (8 * g)) & 0xffu;
       const int info = xinfo[xs];
       __syncwarp();
       if (lane == 0) li_arrive(&xempty[xs]);  // the x stage is free again
-      uint32_t uw[4], hw[4], lw[4];
+      f2x xv[4] = {f2x_make(v0.x, v0.y), f2x_make(v0.z, v0.w), f2x_make(v1.x, v1.y),
+                   f2x_make(v1.z, v1.w)};
+      uint32_t tb[8], sb[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (a.debug & 128) {  // diagnostics: no conversion work
-          uw[q] = hw[q] = lw[q] = __float_as_uint(v[q].x);
-          continue;
-        }
-        const float xv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-        uint32_t pu = 0, ph2 = 0, pl = 0;
-#pragma unroll
-        for (int z = 0; z < 4; ++z) {
-          uint32_t u;
-          const bool ok = grid_u8(xv[z], u);
-          const bool act = (m >> (4 * q + z)) & 1u;
-          bad |= act && !ok;
-          u = act ? u : 0u;
-          const uint32_t sq = u * u;
-          pu |= u << (8 * z);
-          ph2 |= (sq >> 8) << (8 * z);
-          pl |= (sq & 255u) << (8 * z);
-        }
-        uw[q] = pu;
-        hw[q] = ph2;
-        lw[q] = pl;
+      for (int h = 0; h < 4; ++h) {
+        const f2x tt = f2x_fma(xv[h], k255, kM);
+        const f2x uf = f2x_add(tt, knM);
+        const f2x q0 = f2x_mul(uf, kC);
+        const f2x r = f2x_fma(q0, kn255, uf);
+        const f2x q = f2x_fma(r, kC, q0);
+        const f2x d = f2x_sub(xv[h], q);
+        const f2x sq = f2x_fma(uf, uf, kS);
+        tb[2 * h] = f2x_lo(tt);
+        tb[2 * h + 1] = f2x_hi(tt);
+        sb[2 * h] = f2x_lo(sq);
+        sb[2 * h + 1] = f2x_hi(sq);
+        const uint32_t dl = f2x_lo(d), dh = f2x_hi(d);
+        const uint32_t e0 = dl | ((tb[2 * h] ^ 0x4B400000u) & 0xffffff00u);
+        const uint32_t e1 = dh | ((tb[2 * h + 1] ^ 0x4B400000u) & 0xffffff00u);
+        bad |= (((m >> (2 * h)) & 1u) ? e0 : 0u) | (((m >> (2 * h + 1)) & 1u) ? e1 : 0u);
       }
-      tc::mbar_wait(&abempty[as], aph ^ 1);
-      uint8_t *at = abring + (size_t)as * ab_bytes;
-      *(uint4 *)(at + g * 2048 + aoff) = make_uint4(uw[0], uw[1], uw[2], uw[3]);
-      *(uint4 *)(at + (g + 2) * 2048 + aoff) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-      *(uint4 *)(at + (g + 4) * 2048 + aoff) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      // pack bytes: u = byte 0 of t, l = byte 0 of s, h = byte 1 of s
+      uint32_t uw0 = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
+      uint32_t uw1 = __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410);
+      uint32_t lw0 = __byte_perm(__byte_perm(sb[0], sb[1], 0x0040), __byte_perm(sb[2], sb[3], 0x0040), 0x5410);
+      uint32_t lw1 = __byte_perm(__byte_perm(sb[4], sb[5], 0x0040), __byte_perm(sb[6], sb[7], 0x0040), 0x5410);
+      uint32_t hw0 = __byte_perm(__byte_perm(sb[0], sb[1], 0x0051), __byte_perm(sb[2], sb[3], 0x0051), 0x5410);
+      uint32_t hw1 = __byte_perm(__byte_perm(sb[4], sb[5], 0x0051), __byte_perm(sb[6], sb[7], 0x0051), 0x5410);
+      if (m != 0xffu) {  // marginalised / padding variables: features 0
+        const uint32_t bm0 = ((m & 15u) * 0x00204081u & 0x01010101u) * 0xffu;
+        const uint32_t bm1 = ((m >> 4) * 0x00204081u & 0x01010101u) * 0xffu;
+        uw0 &= bm0; lw0 &= bm0; hw0 &= bm0;
+        uw1 &= bm1; lw1 &= bm1; hw1 &= bm1;
+      }
+      if (a.debug & 128) bad = 0;
+      if (w == LI_GW) LI_TRACE(2, pc);
+      tc::mbar_wait(&aempty[as], aph ^ 1);
+      if (w == LI_GW) LI_TRACE(3, pc);
+      uint8_t *at = aring + (size_t)as * LI_ABYTES + aoff;
+      *(uint2 *)at = make_uint2(uw0, uw1);
+      *(uint2 *)(at + 2 * 2048) = make_uint2(hw0, hw1);
+      *(uint2 *)(at + 4 * 2048) = make_uint2(lw0, lw1);
       if (ct == 0) abinfo[as] = info;
       tc::fence_async_smem();
       __syncwarp();
-      if (lane == 0) li_arrive(&abfull[as]);
+      if (lane == 0) li_arrive(&afull[as]);
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&bad_any, 1);
+    if (__any_sync(0xffffffffu, bad != 0) && lane == 0) atomicOr(&bad_any, 1);
   } else if (w == LI_BW) {
     // ---- digit tiles (B operand) into the A|B ring ----
-    for (int pc = 0; pc < a.npc; ++pc) {
-      const int as = pc % LI_AST, aph = (pc / LI_AST) & 1;
-      tc::mbar_wait(&abempty[as], aph ^ 1);
+    for (int pc = pcb; pc < pce; ++pc) {
+      const int bs = (pc - pcb) % LI_BST, bph = ((pc - pcb) / LI_BST) & 1;
+      tc::mbar_wait(&bempty[bs], bph ^ 1);
+      LI_TRACE(4, pc);
       const bool leader = tc::elect_one();
       if (leader && (a.debug & 16)) {
-        li_arrive(&abfull[as]);
+        li_arrive(&bfull[bs]);
       } else if (leader) {
-        tc::mbar_arrive_expect_tx(&abfull[as], bbytes);
-        tc::bulk_g2s(abring + (size_t)as * ab_bytes + LI_ABYTES, a.img + (int64_t)pc * bbytes,
-                     bbytes, &abfull[as]);
+        tc::mbar_arrive_expect_tx(&bfull[bs], bbytes);
+        tc::bulk_g2s(bring + (size_t)bs * bbytes, a.img + (int64_t)pc * bbytes, bbytes,
+                     &bfull[bs]);
       }
       __syncwarp();
     }
   } else if (w == LI_MMA_WARP) {
     // ---- MMA issuer ----
     const uint32_t id = idesc_u8s8(128, NG);
-    for (int pc = 0; pc < a.npc; ++pc) {
-      const int as = pc % LI_AST, aph = (pc / LI_AST) & 1;
-      tc::mbar_wait(&abfull[as], aph);
+    for (int pc = pcb; pc < pce; ++pc) {
+      const int i = pc - pcb;
+      const int as = i % LI_AST, aph = (i / LI_AST) & 1;
+      const int bs = i % LI_BST, bph = (i / LI_BST) & 1;
+      tc::mbar_wait(&afull[as], aph);
+      tc::mbar_wait(&bfull[bs], bph);
+      LI_TRACE(5, pc);
       const int info = abinfo[as];
       const int leaf = info & 0xffffff;
       const bool first = ((info >> 24) & LI_F_FIRST) != 0;
       const bool last = ((info >> 24) & LI_F_LAST) != 0;
       const int buf = leaf & 1;
-      if (first) tc::mbar_wait(&accempty[buf], ((leaf >> 1) & 1) ^ 1);
+      if (first) tc::mbar_wait(&accempty[buf], (((leaf - lb) >> 1) & 1) ^ 1);
       tc::fence_after();
       if (tc::elect_one()) {
-        const uint32_t sa = tc::smem_u32(abring + (size_t)as * ab_bytes);
-        const uint32_t sb = sa + LI_ABYTES;
+        const uint32_t sa = tc::smem_u32(aring + (size_t)as * LI_ABYTES);
+        const uint32_t sb = tc::smem_u32(bring + (size_t)bs * bbytes);
         const uint32_t d = tm + (uint32_t)(buf * LI_ACC_STRIDE);
 #pragma unroll
         for (int ks = 0; ks < 3; ++ks)
           if (!(a.debug & 4))
             mma_i8(d, tc::kstep_desc(sa, 128, ks), tc::kstep_desc(sb, NG, ks), id,
                    (first && ks == 0) ? 0u : 1u);
-        tc::mma_commit(&abempty[as]);
+        tc::mma_commit(&aempty[as]);
+        tc::mma_commit(&bempty[bs]);
         if (last) tc::mma_commit(&accfull[buf]);
       }
       __syncwarp();
+      LI_TRACE(6, pc);
     }
   } else {
     // ---- epilogue: leaf rows and slabs ----
@@ -454,7 +542,7 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
       return __hiloint2double(0x43380000, (int)(__float_as_uint(raw) ^ 0x80000000u)) -
              6755401588539392.0;
     };
-    for (int leaf = 0; leaf < a.n_leaf; ++leaf) {
+    for (int leaf = lb; leaf < le; ++leaf) {
       const int buf = leaf & 1;
       if (et < K) {
         ks_c[buf][0][et] = a.cnst[(int64_t)leaf * K + et];
@@ -462,7 +550,7 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
         ks_c[buf][2][et] = a.i8c[((int64_t)leaf * K8 + et) * 2 + 1];
       }
       asm volatile("bar.sync 2, %0;" ::"n"(32 * LI_EW) : "memory");
-      tc::mbar_wait(&accfull[buf], (leaf >> 1) & 1);
+      tc::mbar_wait(&accfull[buf], ((leaf - lb) >> 1) & 1);
       tc::fence_after();
       const uint32_t acc = tm + lane_off + (uint32_t)(buf * LI_ACC_STRIDE);
       const int slab = a.leaf_slab[leaf];
@@ -507,7 +595,7 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
 }
 
 static size_t leaf_i8_smem(int NG) {
-  return (size_t)LI_XST * LI_XBYTES + (size_t)LI_AST * (LI_ABYTES + NG * LI_KB);
+  return (size_t)LI_XST * LI_XBYTES + (size_t)LI_AST * LI_ABYTES + (size_t)LI_BST * NG * LI_KB;
 }
 
 bool leaf_i8_supported(const Plan &p) { return p.leaf_i8 != 0 && p.use_tc; }
@@ -582,10 +670,36 @@ int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t 
                          (int)smem);
     attr = smem;
   }
+  a.trace = nullptr;
+  static long long *trace_buf = nullptr;
+  const bool tracing = getenv("EINET_I8_TRACE") != nullptr;
+  if (tracing) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 128 * 8 * sizeof(long long));
+    cudaMemsetAsync(trace_buf, 0, 128 * 8 * sizeof(long long), st);
+    a.trace = trace_buf;
+  }
+  // few sample tiles: one CTA per (tile, leaf pair) shortens each CTA's chunk
+  // chain; enough tiles to fill the GPU: one CTA walks every leaf
+  const int tiles = ceil_div(B, 128), npairs = (p.n_leaf + 1) / 2;
+  a.grp_pc = p.d_i8_grp;
+  a.grouped = (tiles < p.num_sms && npairs > 1) ? 1 : 0;
+  const dim3 grid(tiles, a.grouped ? npairs : 1);
   if (cond)
-    k_leaf_fwd_i8<true><<<ceil_div(B, 128), LI_THREADS, smem, st>>>(a);
+    k_leaf_fwd_i8<true><<<grid, LI_THREADS, smem, st>>>(a);
   else
-    k_leaf_fwd_i8<false><<<ceil_div(B, 128), LI_THREADS, smem, st>>>(a);
+    k_leaf_fwd_i8<false><<<grid, LI_THREADS, smem, st>>>(a);
+  if (tracing) {
+    long long h[128 * 8];
+    cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const long long t0 = h[0];
+    fprintf(stderr, "i8 trace (ns from the first gather): gather_go conv_xfull conv_abwait "
+                    "conv_abgo bload_go mma_full mma_done\n");
+    for (int i = 0; i < 128; i += 4)
+      fprintf(stderr, "  pc %2d %7lld %7lld %7lld %7lld %7lld %7lld %7lld\n", i, h[i * 8] - t0,
+              h[i * 8 + 1] - t0, h[i * 8 + 2] - t0, h[i * 8 + 3] - t0, h[i * 8 + 4] - t0,
+              h[i * 8 + 5] - t0, h[i * 8 + 6] - t0);
+  }
   count_launch();
   return check_cuda(cudaGetLastError(), "leaf forward i8");
 }
@@ -593,7 +707,7 @@ int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t 
 // Host side of the plan: digit-tile geometry, the per-chunk table (leaf,
 // variables, gather mode, first / last chunk of the leaf) and the chunk's
 // variable indices.
-void plan_leaf_i8(Plan &p, std::vector<int> &tab, std::vector<int> &col) {
+void plan_leaf_i8(Plan &p, std::vector<int> &tab, std::vector<int> &col, std::vector<int> &grp) {
   const char *env = getenv("EINET_LEAF_I8");
   const int k8 = (p.k + 7) / 8 * 8;
   p.leaf_i8 = p.family == EINET_FAMILY_GAUSSIAN && k8 <= 40 && !(env && env[0] == '0');
@@ -609,27 +723,51 @@ void plan_leaf_i8(Plan &p, std::vector<int> &tab, std::vector<int> &col) {
   tab.assign((size_t)npc * 4, 0);
   col.assign((size_t)npc * LI_VC, 0);
   const bool d_ok = p.d_vars % 4 == 0;
-  for (int l = 0; l < p.n_leaf; ++l) {
-    const int sbeg = p.h_scope_off[l], slen = p.h_scope_off[l + 1] - sbeg;
-    for (int c0 = 0; c0 < slen; c0 += LI_VC) {
-      const int pc = (p.h_leaf_pvo[l] + c0) / LI_VC;
-      const int nv = std::min(LI_VC, slen - c0);
-      bool vec = d_ok;
-      for (int q = 0; q < LI_VC && vec; q += 4) {
-        const int pos = c0 + q;
-        if (pos >= slen) break;                        // all-padding quad
-        if (pos + 4 > slen) { vec = false; break; }    // partial quad
-        const int v = p.h_scope_vars[sbeg + pos];
-        if (v % 4) vec = false;
-        for (int z = 1; z < 4 && vec; ++z)
-          if (p.h_scope_vars[sbeg + pos + z] != v + z) vec = false;
-      }
-      for (int v = 0; v < nv; ++v) col[(size_t)pc * LI_VC + v] = p.h_scope_vars[sbeg + c0 + v];
-      tab[(size_t)pc * 4] = l;
-      tab[(size_t)pc * 4 + 1] = nv;
-      tab[(size_t)pc * 4 + 2] = (vec ? LI_F_VEC : 0) | (c0 == 0 ? LI_F_FIRST : 0) |
-                                (c0 + LI_VC >= slen ? LI_F_LAST : 0);
+  // Chunk order: the two leaves of each pair (l, l+1) interleaved chunk by
+  // chunk (their accumulators are the two TMEM buffers), so neighbouring
+  // scopes -- adjacent strips of an image row in Poon-Domingos graphs -- are
+  // read close together and share DRAM bursts.
+  // The first leaf of a pair runs T chunks alone (while the previous pair's
+  // second leaf drains) and finishes T chunks early (its epilogue then
+  // overlaps the second leaf's tail), so the accumulators never stall the
+  // MMAs at pair boundaries.
+  std::vector<std::pair<int, int>> order;  // (leaf, first scope position)
+  grp.clear();
+  for (int l0 = 0; l0 < p.n_leaf; l0 += 2) {
+    grp.push_back((int)order.size());
+    const int l1 = l0 + 1 < p.n_leaf ? l0 + 1 : -1;
+    const int c0n = (p.h_scope_off[l0 + 1] - p.h_scope_off[l0] + LI_VC - 1) / LI_VC;
+    const int c1n = l1 >= 0 ? (p.h_scope_off[l1 + 1] - p.h_scope_off[l1] + LI_VC - 1) / LI_VC : 0;
+    const int T = std::min(4, std::min(c0n, c1n) / 4);
+    int i0 = 0, i1 = 0;
+    for (; i0 < T; ++i0) order.emplace_back(l0, i0 * LI_VC);
+    while (i0 < c0n - T || (i0 < c0n && i1 >= c1n)) {
+      order.emplace_back(l0, (i0++) * LI_VC);
+      if (i1 < c1n) order.emplace_back(l1, (i1++) * LI_VC);
     }
+    for (; i0 < c0n; ++i0) order.emplace_back(l0, i0 * LI_VC);
+    for (; i1 < c1n; ++i1) order.emplace_back(l1, i1 * LI_VC);
+  }
+  grp.push_back((int)order.size());
+  for (int pc = 0; pc < (int)order.size(); ++pc) {
+    const int l = order[pc].first, c0 = order[pc].second;
+    const int sbeg = p.h_scope_off[l], slen = p.h_scope_off[l + 1] - sbeg;
+    const int nv = std::min(LI_VC, slen - c0);
+    bool vec = d_ok;
+    for (int q = 0; q < LI_VC && vec; q += 4) {
+      const int pos = c0 + q;
+      if (pos >= slen) break;                        // all-padding quad
+      if (pos + 4 > slen) { vec = false; break; }    // partial quad
+      const int v = p.h_scope_vars[sbeg + pos];
+      if (v % 4) vec = false;
+      for (int z = 1; z < 4 && vec; ++z)
+        if (p.h_scope_vars[sbeg + pos + z] != v + z) vec = false;
+    }
+    for (int v = 0; v < nv; ++v) col[(size_t)pc * LI_VC + v] = p.h_scope_vars[sbeg + c0 + v];
+    tab[(size_t)pc * 4] = l;
+    tab[(size_t)pc * 4 + 1] = nv;
+    tab[(size_t)pc * 4 + 2] = (vec ? LI_F_VEC : 0) | (c0 == 0 ? LI_F_FIRST : 0) |
+                              (c0 + LI_VC >= slen ? LI_F_LAST : 0);
   }
 }
 

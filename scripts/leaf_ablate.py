@@ -39,12 +39,10 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         one()
         sys.exit(0)
-    settings = [("i8 nofb", {"EINET_I8_DEBUG": "32"}),
+    settings = [("i8", {}), ("i8 nofb", {"EINET_I8_DEBUG": "32"}),
                 ("nofb noepi", {"EINET_I8_DEBUG": "34"}), ("nofb nomma", {"EINET_I8_DEBUG": "36"}),
-                ("nofb nox", {"EINET_I8_DEBUG": "40"}), ("nofb noB", {"EINET_I8_DEBUG": "48"}),
-                ("nofb noconv", {"EINET_I8_DEBUG": "160"}), ("nofb nox noconv", {"EINET_I8_DEBUG": "168"}),
-                ("nofb nox noconv noB", {"EINET_I8_DEBUG": "184"}),
-                ("nofb all", {"EINET_I8_DEBUG": "190"})]
+                ("i8 B=500", {"ABL_B": "500"}), ("fp64 B=500", {"ABL_B": "500", "EINET_LEAF_I8": "0"}),
+                ("fp64 dmma", {"EINET_LEAF_I8": "0"})]
     for name, env in settings:
         e = dict(os.environ, **env)
         out = subprocess.run([sys.executable, __file__, "one"], env=e, capture_output=True,
