@@ -687,12 +687,12 @@ __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__res
 // W statistics of K_out = 1 rows (the root einsum layer):
 //   S[l][i,j] = sum_b RT[b,l] EA[b,l,i] EB[b,l,j]
 // a K x K x B product per row, on CUDA cores (the tensor-core kernel pads
-// K_out to 16). grid (rows, nsplit), block K4*K4 (<= 256): thread (ti, tj)
-// owns rows ti + K4*u and columns tj + K4*v (u, v < 4), so a warp reads
-// consecutive padded rows (conflict-free 16-byte loads). Each CTA sums its
-// contiguous run of 32-sample blocks in fp32 and writes an fp64 partial per
-// split; the partials are reduced in split order (deterministic).
-constexpr int WK1_ROW = 36;
+// K_out to 16). grid (rows, nsplit), block >= K4*K4: thread (ti, tj) owns rows
+// ti + K4*u and columns tj + K4*v (u, v < 4), so a warp reads consecutive
+// padded rows (conflict-free 16-byte loads). The 32-sample EA / EB / RT blocks
+// (contiguous, ev_idx / tb_idx; zero past the batch) are double-buffered with
+// cp.async. Each CTA sums its contiguous run of blocks in fp32 and writes an
+// fp64 partial per split; the partials are reduced in split order.
 __global__ void __launch_bounds__(256) k_wstats_k1(const float *__restrict__ EA,
                                                    const float *__restrict__ EB,
                                                    const float *__restrict__ RT, int64_t Bc,
@@ -700,52 +700,60 @@ __global__ void __launch_bounds__(256) k_wstats_k1(const float *__restrict__ EA,
                                                    double *wpart) {
   extern __shared__ __align__(16) float smk1[];
   const int K4 = (K + 3) / 4;
-  float *ea_s = smk1;                  // [K4*4][WK1_ROW], scaled by RT
-  float *eb_s = ea_s + K4 * 4 * WK1_ROW;
+  const int evf = K * EV_ROW;                       // floats per EA (or EB) block
+  const int stage = 2 * evf + 32;                   // EA | EB | RT
   const int l = blockIdx.x, split = blockIdx.y;
   const int nblk = (int)((B + 31) / 32);
   const int c0 = (int)((int64_t)split * nblk / nsplit), c1 = (int)((int64_t)(split + 1) * nblk / nsplit);
   const int tid = threadIdx.x, ti = tid / K4, tj = tid - ti * K4;
   const bool act = ti < K4;
+  auto load = [&](int c, int buf) {
+    const int64_t b0 = (int64_t)c * 32;
+    const float *ea = EA + ev_idx(l, b0, 0, Bc, K), *eb = EB + ev_idx(l, b0, 0, Bc, K);
+    const float *rt = RT + tb_idx(l, b0, 0, Bc, ks);
+    float *dst = smk1 + buf * stage;
+    for (int e = tid; e < evf / 4; e += blockDim.x) {
+      cp_async16(dst + 4 * e, ea + 4 * e);
+      cp_async16(dst + evf + 4 * e, eb + 4 * e);
+    }
+    if (tid < 8) cp_async16(dst + 2 * evf + 4 * tid, rt + 4 * tid);
+    cp_async_commit();
+  };
   float acc[4][4];
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
+  if (c0 < c1) load(c0, 0);
   for (int c = c0; c < c1; ++c) {
-    const int64_t b0 = (int64_t)c * 32;
-    __syncthreads();
-    const float *ea = EA + ev_idx(l, b0, 0, Bc, K), *eb = EB + ev_idx(l, b0, 0, Bc, K);
-    const float *rt = RT + tb_idx(l, b0, 0, Bc, ks);
-    for (int e = tid; e < K4 * 4 * 8; e += blockDim.x) {
-      const int i = e >> 3, q = e & 7;
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bv = a;
-      if (i < K) {
-        a = *(const float4 *)(ea + i * EV_ROW + 4 * q);
-        bv = *(const float4 *)(eb + i * EV_ROW + 4 * q);
-        const float4 r = *(const float4 *)(rt + 4 * q);
-        const int nb = (int)min((int64_t)32, B - b0) - 4 * q;  // samples past B count 0
-        a.x = nb > 0 ? a.x * r.x : 0.f;
-        a.y = nb > 1 ? a.y * r.y : 0.f;
-        a.z = nb > 2 ? a.z * r.z : 0.f;
-        a.w = nb > 3 ? a.w * r.w : 0.f;
-        bv.x = nb > 0 ? bv.x : 0.f;
-        bv.y = nb > 1 ? bv.y : 0.f;
-        bv.z = nb > 2 ? bv.z : 0.f;
-        bv.w = nb > 3 ? bv.w : 0.f;
-      }
-      *(float4 *)(ea_s + i * WK1_ROW + 4 * q) = a;
-      *(float4 *)(eb_s + i * WK1_ROW + 4 * q) = bv;
+    const int buf = (c - c0) & 1;
+    if (c + 1 < c1) {
+      load(c + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const float *ea_s = smk1 + buf * stage, *eb_s = ea_s + evf, *rt_s = eb_s + evf;
     if (act) {
-#pragma unroll
+#pragma unroll 2
       for (int q = 0; q < 8; ++q) {
+        const float4 r = *(const float4 *)(rt_s + 4 * q);
         float4 a[4], e[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) a[u] = *(const float4 *)(ea_s + (ti + K4 * u) * WK1_ROW + 4 * q);
+        for (int u = 0; u < 4; ++u) {
+          const int i = ti + K4 * u;
+          a[u] = i < K ? *(const float4 *)(ea_s + i * EV_ROW + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+          a[u].x *= r.x;
+          a[u].y *= r.y;
+          a[u].z *= r.z;
+          a[u].w *= r.w;
+        }
 #pragma unroll
-        for (int v = 0; v < 4; ++v) e[v] = *(const float4 *)(eb_s + (tj + K4 * v) * WK1_ROW + 4 * q);
+        for (int v = 0; v < 4; ++v) {
+          const int j = tj + K4 * v;
+          e[v] = j < K ? *(const float4 *)(eb_s + j * EV_ROW + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -757,6 +765,7 @@ __global__ void __launch_bounds__(256) k_wstats_k1(const float *__restrict__ EA,
           }
       }
     }
+    __syncthreads();
   }
   if (!act) return;
   double *dst = wpart + ((int64_t)split * L + l) * K * K;
@@ -1182,8 +1191,9 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
       const int K4 = (K + 3) / 4;
       if (L.k_out == 1 && K4 * K4 <= 256 && !getenv("EINET_WK1_OFF")) {
         const int ns = wstats_bsplit(p, L, B, L.rows);
-        const size_t smem = sizeof(float) * 2 * K4 * 4 * WK1_ROW;
-        k_wstats_k1<<<dim3(L.rows, ns), K4 * K4, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K,
+        const size_t smem = sizeof(float) * 2 * (2 * K * EV_ROW + 32);
+        const int threads = std::max(128, (K4 * K4 + 31) / 32 * 32);
+        k_wstats_k1<<<dim3(L.rows, ns), threads, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K,
                                                              L.rows, ns, w.wpart);
         launch_reduce_partials(stats + L.w_off, w.wpart, ns, lw, lw, params + L.w_off, st);
       } else if (p.use_tc && L.tc) {
