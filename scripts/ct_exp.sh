@@ -1,1 +1,6 @@
-for d in 0 1 2 3; do EINET_CT_DEBUG=$d timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/ctexp/b$d.json 2>/dev/null; done
+#!/bin/bash
+# contraction experiments: class times under EINET_CT_DEBUG / EINET_CT_G variants
+OUT=gpurun_out/${1:-ctexp}; mkdir -p $OUT
+for g in ${GS:-1 2}; do for d in ${DS:-0 1 2 4 5}; do
+  echo "G=$g debug=$d $(EINET_CT_G=$g EINET_CT_DEBUG=$d python scripts/class_times.py 2>&1 | tail -1)" >> $OUT/exp.txt
+done; done
