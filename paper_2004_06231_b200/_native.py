@@ -11,7 +11,8 @@ import os
 from ctypes import POINTER, c_double, c_int32, c_int64, c_uint8, c_void_p
 
 LIB_NAME = "libeinet_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get(  # EINET_LIB_PATH: A/B timing of another build (diagnostics)
+    "EINET_LIB_PATH", os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME))
 
 OK = 0
 ERR_USAGE = 1
