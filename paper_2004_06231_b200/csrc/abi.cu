@@ -32,6 +32,13 @@ int check_cuda(cudaError_t err, const char *what) {
   return EINET_ERR_CUDA;
 }
 void count_launch(int n) { g_launches += n; }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("EINET_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int pick_split(int64_t per, int64_t slots, int lo, int hi, double good) {
   lo = std::max(lo, 1);

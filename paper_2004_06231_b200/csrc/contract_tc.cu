@@ -130,6 +130,7 @@ __device__ __forceinline__ float dot_f32x2(const float (&v)[K], const float (&e)
 
 template <int K, bool FWD>
 __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, WsView ws) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar_wf, bar_we, bar_af[CT_STAGES], bar_ae[CT_STAGES], bar_cf[2], bar_ce[2],
       bar_ef[CT_STAGES], bar_ee[CT_STAGES];
@@ -473,7 +474,7 @@ static int contract_t(Plan &p, ContractArgs &a, const WsView &w, cudaStream_t st
     cudaMemsetAsync(trace_buf, 0, 64 * 8 * sizeof(long long), st);
     a.trace = trace_buf;
   }
-  k_contract_tc<K, FWD><<<grid, CT_THREADS, smem, st>>>(a, w);
+  launch_k(k_contract_tc<K, FWD>, grid, CT_THREADS, smem, st, a, w);
   if (tracing) {
     long long h[64 * 8];
     cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);

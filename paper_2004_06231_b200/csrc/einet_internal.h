@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/einet_b200.h"
@@ -135,6 +136,37 @@ struct Plan {
   int *d_mixrow_off = nullptr, *d_mixrow_len = nullptr;
   uint8_t *d_mix_mask_all = nullptr;
 };
+
+// ---- launches: programmatic dependent launch (PDL) ---------------------------
+// Every kernel is launched with programmatic stream serialization and starts
+// with EINET_KERNEL_PROLOGUE(): griddepcontrol.wait (the predecessor grid has
+// completed and its writes are visible) before anything else, so the launch
+// of the next kernel of the stream (or CUDA graph) overlaps this one's drain.
+// The dependents are released at grid completion (an early
+// griddepcontrol.launch_dependents let waiting CTAs take SM slots and cost
+// 2-4% at 16384 samples). Every CTA executes the wait, so dependencies stay
+// transitive. EINET_PDL=0 launches without the attribute (A/B timing:
+// -2.6% step time at 500 samples, neutral at 16384).
+#define EINET_KERNEL_PROLOGUE()                                   \
+  do {                                                            \
+    asm volatile("griddepcontrol.wait;" ::: "memory");            \
+  } while (0)
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args &&...args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  (void)cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---- error handling ---------------------------------------------------------
 void set_error(const std::string &msg);

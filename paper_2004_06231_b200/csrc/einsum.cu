@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(128) k_einsum_prep_fwd(
     const int *__restrict__ out_slab, int64_t B, int K, float *__restrict__ EA,
     float *__restrict__ EB, float *__restrict__ EBM, float *__restrict__ EAM, int kp,
     int layer_index, int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ float mx[2][32];
   __shared__ unsigned char dead[32];
   const int l = blockIdx.y, t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const float *__
                                                       const int *__restrict__ out_slab,
                                                       const float *__restrict__ W, int64_t B,
                                                       int K, int Ko) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(16) float wsm[];
   const int l = blockIdx.y;
   const int k0 = blockIdx.z * EF_KC;
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_fwd(WsView ws, const float *__
 __global__ void k_einsum_fwd_generic(WsView ws, const float *__restrict__ EA,
                                      const float *__restrict__ EB, const int *out_slab,
                                      const float *__restrict__ W, int64_t B, int K, int Ko) {
+  EINET_KERNEL_PROLOGUE();
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
@@ -218,6 +221,7 @@ __global__ void __launch_bounds__(256) k_einsum_fwd_big(WsView ws, const float *
                                                         const int *out_slab,
                                                         const float *__restrict__ W, int64_t B,
                                                         int K, int Ko) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(16) float fsm[];
   float *wt = fsm;                       // [j][FB_WS]: W[k][i][j] at wt[j][i]
   float *ebs = wt + FB_KP * FB_WS;       // [j][64]
@@ -293,6 +297,7 @@ __global__ void __launch_bounds__(128) k_mixing_fwd(
     WsView ws, const int *__restrict__ src_slab, const uint8_t *__restrict__ mask,
     const int *__restrict__ out_slab, const float *__restrict__ w, int64_t B, int Ko, int dmax,
     int layer_index, int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ int msm[];
   int *src = msm;                        // [dmax], -1 = masked
   float *wc = (float *)(msm + dmax);     // [dmax]
@@ -439,6 +444,7 @@ __global__ void __launch_bounds__(128) k_mixing_bwd(
     const float *__restrict__ w, const int *csr_off, const int *__restrict__ csr_slot,
     const uint8_t *ones, int64_t B, int Ko, int dmax, double *mixpart, int64_t mix_off,
     int64_t n_mix) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ double red[4];
   const int m = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
@@ -502,6 +508,7 @@ __global__ void __launch_bounds__(128) k_mixing_bwd(
 __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
     WsView ws, const int *out_slab, const int *csr_off, const int *__restrict__ csr_slot,
     const uint8_t *ones, int64_t B, int Ko, float *RT, float *RTM, int kob, float *RTB, int nn) {
+  EINET_KERNEL_PROLOGUE();
   const int l = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int os = out_slab[l];
@@ -614,6 +621,7 @@ __global__ void k_einsum_wstats(const float *__restrict__ EA, const float *__res
                                 const float *__restrict__ RT, int64_t Bc, int ks, int64_t B,
                                 int K, int Ko, int L, int bsplit, double *wpart, int ti_per,
                                 int kc) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(16) float sm[];
   const int K4 = (K + 3) / 4;
   const int KP = K4 * 4;
@@ -698,6 +706,7 @@ __global__ void __launch_bounds__(256) k_wstats_k1(const float *__restrict__ EA,
                                                    const float *__restrict__ RT, int64_t Bc,
                                                    int ks, int64_t B, int K, int L, int nsplit,
                                                    double *wpart) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(16) float smk1[];
   const int K4 = (K + 3) / 4;
   const int evf = K * EV_ROW;                       // floats per EA (or EB) block
@@ -784,6 +793,7 @@ __global__ void __launch_bounds__(EF_TB) k_einsum_childrho(
     const float *__restrict__ EA, const float *__restrict__ EB, const float *__restrict__ RT,
     const float *__restrict__ W, WsView ws, const int *slot_left, const int *slot_right,
     int64_t B, int K, int Ko) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(16) float wsm[];
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * EF_TB + threadIdx.x;
@@ -842,6 +852,7 @@ __global__ void k_einsum_childrho_generic(const float *__restrict__ EA,
                                           const float *__restrict__ W, WsView ws,
                                           const int *slot_left, const int *slot_right,
                                           int64_t B, int K, int Ko) {
+  EINET_KERNEL_PROLOGUE();
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
@@ -884,6 +895,7 @@ __global__ void __launch_bounds__(256) k_einsum_childrho_big(
     const float *__restrict__ EA, const float *__restrict__ EB, const float *__restrict__ RT,
     const float *__restrict__ W, WsView ws, const int *slot_left, const int *slot_right,
     int64_t B, int K, int Ko) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(16) float csm[];
   float *wk = csm;                      // [i][CB_WS] = W[k][i][j]
   float *ebs = wk + FB_KP * CB_WS;      // [j][64]
@@ -968,6 +980,7 @@ __global__ void __launch_bounds__(256) k_einsum_childrho_big(
 // ---------------------------------------------------------------------------
 
 __global__ void k_root_out(WsView ws, int slab, int64_t B, int kr, double *out) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= B * kr) return;
   const int64_t b = e / kr;
@@ -980,6 +993,7 @@ __global__ void k_root_out(WsView ws, int slab, int64_t B, int kr, double *out) 
 // fixed summation order (strided fp64 runs, then warp and CTA trees).
 __global__ void __launch_bounds__(1024) k_ll_sum(WsView ws, int slab, int64_t B, double *ll,
                                                  double count) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ double red[32];
   double v = 0.0;
   const double *sh = slab_shift(ws, slab);
@@ -1014,7 +1028,7 @@ static void fwd_simt(const LayerPlan &L, const float *w32, const float *EA, cons
     cudaFuncSetAttribute(k_einsum_fwd<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   dim3 grid(ceil_div(B, EF_TB), L.rows, ceil_div(L.k_out, EF_KC));
-  k_einsum_fwd<KT><<<grid, EF_TB, smem, st>>>(w, EA, EB, L.d_out_slab, w32 + L.w_off, B, K,
+  launch_k(k_einsum_fwd<KT>, grid, EF_TB, smem, st, w, EA, EB, L.d_out_slab, w32 + L.w_off, B, K,
                                               L.k_out);
 }
 
@@ -1026,7 +1040,7 @@ static void childrho_simt(const LayerPlan &L, const float *w32, const float *EA,
     cudaFuncSetAttribute(k_einsum_childrho<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   dim3 grid(ceil_div(B, EF_TB), L.rows);
-  k_einsum_childrho<KT><<<grid, EF_TB, smem, st>>>(EA, EB, w.rt, w32 + L.w_off, w,
+  launch_k(k_einsum_childrho<KT>, grid, EF_TB, smem, st, EA, EB, w.rt, w32 + L.w_off, w,
                                                    L.d_slot_left, L.d_slot_right, B, K,
                                                    L.k_out);
 }
@@ -1051,11 +1065,11 @@ static void einsum_forward_simt(const LayerPlan &L, const float *w32, const floa
       attr = true;
     }
     dim3 grid(ceil_div(B, FB_TB), L.rows, L.k_out);
-    k_einsum_fwd_big<<<grid, 256, fwd_big_smem(), st>>>(w, EA, EB, L.d_out_slab, w32 + L.w_off,
+    launch_k(k_einsum_fwd_big, grid, 256, fwd_big_smem(), st, w, EA, EB, L.d_out_slab, w32 + L.w_off,
                                                        B, K, L.k_out);
   } else {
     dim3 grid(ceil_div(B, 128), L.rows);
-    k_einsum_fwd_generic<<<grid, 128, 0, st>>>(w, EA, EB, L.d_out_slab, w32 + L.w_off, B, K,
+    launch_k(k_einsum_fwd_generic, grid, 128, 0, st, w, EA, EB, L.d_out_slab, w32 + L.w_off, B, K,
                                                L.k_out);
   }
 }
@@ -1079,11 +1093,11 @@ static void einsum_childrho_simt(const LayerPlan &L, const float *w32, const flo
       attr = true;
     }
     dim3 grid(ceil_div(B, FB_TB), L.rows);
-    k_einsum_childrho_big<<<grid, 256, childrho_big_smem(), st>>>(
+    launch_k(k_einsum_childrho_big, grid, 256, childrho_big_smem(), st, 
         EA, EB, w.rt, w32 + L.w_off, w, L.d_slot_left, L.d_slot_right, B, K, L.k_out);
   } else {
     dim3 grid(ceil_div(B, 128), L.rows);
-    k_einsum_childrho_generic<<<grid, 128, 0, st>>>(EA, EB, w.rt, w32 + L.w_off, w,
+    launch_k(k_einsum_childrho_generic, grid, 128, 0, st, EA, EB, w.rt, w32 + L.w_off, w,
                                                     L.d_slot_left, L.d_slot_right, B, K,
                                                     L.k_out);
   }
@@ -1111,7 +1125,7 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
         const bool tcl = p.use_tc && L.tc;
         float *EBM = tcl ? w.ebm + (int64_t)L.erow_base * w.bc * p.kp : nullptr;
         float *EAM = tcl && L.direct ? w.eam + (int64_t)L.erow_base * w.bc * p.kp : nullptr;
-        k_einsum_prep_fwd<<<grid, 128, 0, st>>>(w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
+        launch_k(k_einsum_prep_fwd, grid, 128, 0, st, w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
                                                 B, p.k, EA, EB, EBM, EAM, p.kp, L.index, status);
       }
       ProfScope prof("einsum_fwd", st);
@@ -1128,14 +1142,14 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
       const int kz = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.k_out, 4),
                                                                  ceil_div(2 * p.num_sms, ctas)));
       dim3 grid(ceil_div(B, 32), L.rows, kz);
-      k_mixing_fwd<<<grid, 128, 8 * L.dmax, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
+      launch_k(k_mixing_fwd, grid, 128, 8 * L.dmax, st, w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
                                          c.mix32 + L.mix_off, B, L.k_out, L.dmax, L.index,
                                          status);
       count_launch();
     }
   }
   const int64_t n = B * p.k_root;
-  k_root_out<<<ceil_div(n, 256), 256, 0, st>>>(w, p.root_out_slab, B, p.k_root, root_out);
+  launch_k(k_root_out, ceil_div(n, 256), 256, 0, st, w, p.root_out_slab, B, p.k_root, root_out);
   count_launch();
   return check_cuda(cudaGetLastError(), "forward kernels");
 }
@@ -1156,7 +1170,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   // log-likelihood sum of the batch (root entry 0) and the sample count
   {
     ProfScope prof("ll_sum", st);
-    k_ll_sum<<<1, 1024, 0, st>>>(w, p.root_out_slab, B, stats + p.sizes.stats_ll_offset,
+    launch_k(k_ll_sum, 1, 1024, 0, st, w, p.root_out_slab, B, stats + p.sizes.stats_ll_offset,
                                   (double)B);
     count_launch();
   }
@@ -1166,7 +1180,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
       ProfScope prof("mixing_bwd", st);
       const int nb = ceil_div(B, 32);
       dim3 grid(nb, L.rows);
-      k_mixing_bwd<<<grid, 128, 0, st>>>(w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
+      launch_k(k_mixing_bwd, grid, 128, 0, st, w, L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
                                         L.d_mix_slot, c.mix32 + L.mix_off, p.d_csr_off,
                                         p.d_csr_slot, p.d_slab_ones, B, L.k_out, L.dmax,
                                         w.mixpart, L.mix_off, p.n_mix);
@@ -1180,7 +1194,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
       ProfScope prof("einsum_bwd_rt", st);
       dim3 g1(ceil_div(B, 32), L.rows);
       const bool tcl = p.use_tc && L.tc;
-      k_einsum_bwd_rt<<<g1, 128, 0, st>>>(w, L.d_out_slab, p.d_csr_off, p.d_csr_slot,
+      launch_k(k_einsum_bwd_rt, g1, 128, 0, st, w, L.d_out_slab, p.d_csr_off, p.d_csr_slot,
                                           p.d_slab_ones, B, L.k_out, w.rt,
                                           tcl && !L.direct ? w.rtm : nullptr, L.kob,
                                           tcl ? w.rtb : nullptr, L.nn);
@@ -1193,7 +1207,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
         const int ns = wstats_bsplit(p, L, B, L.rows);
         const size_t smem = sizeof(float) * 2 * (2 * K * EV_ROW + 32);
         const int threads = std::max(128, (K4 * K4 + 31) / 32 * 32);
-        k_wstats_k1<<<dim3(L.rows, ns), threads, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K,
+        launch_k(k_wstats_k1, dim3(L.rows, ns), threads, smem, st, EA, EB, w.rt, w.bc, w.ks, B, K,
                                                              L.rows, ns, w.wpart);
         launch_reduce_partials(stats + L.w_off, w.wpart, ns, lw, lw, params + L.w_off, st);
       } else if (p.use_tc && L.tc) {
@@ -1209,7 +1223,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
         const int bs = wstats_bsplit(p, L, B, (int64_t)L.rows * nkc);
         const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT * kc);
         dim3 g2(L.rows * nkc, bs, ceil_div(K4, ti_per));
-        k_einsum_wstats<<<g2, kc * ti_per * K4, smem, st>>>(EA, EB, w.rt, w.bc, w.ks, B, K,
+        launch_k(k_einsum_wstats, g2, kc * ti_per * K4, smem, st, EA, EB, w.rt, w.bc, w.ks, B, K,
                                                             L.k_out, L.rows, bs, w.wpart, ti_per,
                                                             kc);
         launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);

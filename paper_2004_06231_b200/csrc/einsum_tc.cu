@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(128) k_selftest_gemm(const float *__restrict__
                                                        const float *__restrict__ B,
                                                        float *__restrict__ D, int N, int K,
                                                        uint32_t tcols, int a_in_tmem) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
@@ -115,7 +116,7 @@ int launch_selftest_gemm(const float *A, const float *B, float *D, int N, int K,
   while (cols < (uint32_t)N) cols *= 2;
   const size_t smem = sizeof(float) * 2 * (128 + N) * K;
   cudaFuncSetAttribute(k_selftest_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_selftest_gemm<<<1, 128, smem, st>>>(A, B, D, N, K, cols, a_tmem);
+  launch_k(k_selftest_gemm, 1, 128, smem, st, A, B, D, N, K, cols, a_tmem);
   count_launch();
   return check_cuda(cudaGetLastError(), "selftest gemm");
 }
@@ -190,6 +191,7 @@ __device__ __forceinline__ void put_bf16_hilo(uint8_t *tile, int64_t lo_bytes, u
 __global__ void k_build_tiles(const float *__restrict__ W, uint8_t *fw, uint8_t *uw,
                               uint8_t *vw, int L, int Ko, int K, int kp, int kg, int ng,
                               int fw_rows, int ig, int ni, int uw_rows, int kob) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t n_fw = (int64_t)L * ng * fw_rows * kp;
   const int64_t n_uw = (int64_t)L * ni * uw_rows * kob;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_fw + 2 * n_uw;
@@ -223,6 +225,7 @@ __global__ void k_build_tiles(const float *__restrict__ W, uint8_t *fw, uint8_t 
 // direct right tile of a K_out == 1 row: rows n = j, K dim = i (kp), value W[l,0,i,j]
 __global__ void k_build_rw(const float *__restrict__ W, uint8_t *rw, int L, int K, int kp,
                            int rows) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t n_rw = (int64_t)L * rows * kp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_rw;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -240,13 +243,13 @@ int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st) {
     if (!L.tc) continue;
     if (L.direct) {
       const int64_t n = (int64_t)L.rows * L.rw_rows * p.kp;
-      k_build_rw<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+      launch_k(k_build_rw, (int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
           c.w32 + L.w_off, compute + L.vw_off, L.rows, p.k, p.kp, L.rw_rows);
       count_launch();
     }
     const int64_t n = (int64_t)L.rows * (L.ng * L.fw_rows * p.kp +
                                          (L.direct ? 0 : 2 * L.ni * L.uw_rows * L.kob));
-    k_build_tiles<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+    launch_k(k_build_tiles, (int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
         c.w32 + L.w_off, compute + L.fw_off, compute + L.uw_off, compute + L.vw_off, L.rows,
         L.k_out, p.k, p.kp, L.kg, L.ng, L.fw_rows, L.ig, L.direct ? 0 : L.ni, L.uw_rows, L.kob);
     count_launch();

@@ -17,6 +17,7 @@ namespace einet {
 __global__ void __launch_bounds__(256) k_decode_u8(const uint8_t *__restrict__ src, int64_t count,
                                                    double divisor, float *__restrict__ dst,
                                                    int vec) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ float lut[256];
   lut[threadIdx.x] = (float)((double)threadIdx.x / divisor);
   __syncthreads();
@@ -53,7 +54,7 @@ int launch_decode_u8(const uint8_t *src, int64_t count, double divisor, float *d
   // while step i runs; a narrow grid leaves the step its SMs (measured: 1.139
   // vs 1.157 ms per pipelined step with eight per SM)
   const int blocks = (int)std::min<int64_t>((int64_t)sms * 2, (work + 255) / 256);
-  k_decode_u8<<<blocks, 256, 0, st>>>(src, count, divisor, dst, vec);
+  launch_k(k_decode_u8, blocks, 256, 0, st, src, count, divisor, dst, vec);
   count_launch();
   return check_cuda(cudaGetLastError(), "decode_u8");
 }
@@ -127,6 +128,7 @@ static const CrcTables &crc_tables() {
 __global__ void __launch_bounds__(256) k_crc32_segments(const uint8_t *__restrict__ data,
                                                         int64_t len, CrcTables tabs,
                                                         uint32_t *acc) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ uint32_t tab[256];
   __shared__ uint32_t x2n[64];
   tab[threadIdx.x] = tabs.byte[threadIdx.x];
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(256) k_crc32_segments(const uint8_t *__restric
 }
 
 __global__ void k_crc32_final(int64_t len, CrcTables tabs, uint32_t *acc) {
+  EINET_KERNEL_PROLOGUE();
   *acc = ~(crc_multmodp(crc_x2nmodp(tabs.x2n, (uint64_t)len, 3), 0xFFFFFFFFu) ^ *acc);
 }
 
@@ -167,10 +170,10 @@ int launch_crc32(const uint8_t *data, int64_t len, uint32_t *crc, cudaStream_t s
   if (rc) return rc;
   if (len > 0) {
     const int64_t segs = (len + CRC_SEG - 1) / CRC_SEG;
-    k_crc32_segments<<<(int)((segs + 255) / 256), 256, 0, st>>>(data, len, t, crc);
+    launch_k(k_crc32_segments, (int)((segs + 255) / 256), 256, 0, st, data, len, t, crc);
     count_launch();
   }
-  k_crc32_final<<<1, 1, 0, st>>>(len, t, crc);
+  launch_k(k_crc32_final, 1, 1, 0, st, len, t, crc);
   count_launch();
   return check_cuda(cudaGetLastError(), "crc32");
 }
@@ -189,6 +192,7 @@ __device__ inline uint32_t load_u32(const uint8_t *p) {
 __global__ void k_blob_to_params(const uint8_t *__restrict__ blob, int64_t blob_len,
                                  const int64_t *__restrict__ table, double *__restrict__ params,
                                  int32_t *bad) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t *e = table + (int64_t)blockIdx.x * BLOB_COLS;
   const int64_t off = e[0], ndim = e[1], dst = e[6], count = e[7];
   const int64_t pay = off + 4 + 4 * ndim;
@@ -213,6 +217,7 @@ __global__ void k_blob_to_params(const uint8_t *__restrict__ blob, int64_t blob_
 
 __global__ void k_params_to_blob(const double *__restrict__ params,
                                  const int64_t *__restrict__ table, uint8_t *__restrict__ blob) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t *e = table + (int64_t)blockIdx.x * BLOB_COLS;
   const int64_t off = e[0], ndim = e[1], src = e[6], count = e[7];
   uint32_t *hdr = reinterpret_cast<uint32_t *>(blob + off);
@@ -235,7 +240,7 @@ int launch_blob_to_params(const uint8_t *blob, int64_t blob_len, const int64_t *
                           int n_tensors, int64_t max_count, double *params, int32_t *bad,
                           cudaStream_t st) {
   if (n_tensors < 1) return EINET_OK;
-  k_blob_to_params<<<dim3(n_tensors, blob_grid_y(max_count)), 256, 0, st>>>(blob, blob_len, table,
+  launch_k(k_blob_to_params, dim3(n_tensors, blob_grid_y(max_count)), 256, 0, st, blob, blob_len, table,
                                                                           params, bad);
   count_launch();
   return check_cuda(cudaGetLastError(), "blob_to_params");
@@ -244,7 +249,7 @@ int launch_blob_to_params(const uint8_t *blob, int64_t blob_len, const int64_t *
 int launch_params_to_blob(const double *params, const int64_t *table, int n_tensors,
                           int64_t max_count, uint8_t *blob, cudaStream_t st) {
   if (n_tensors < 1) return EINET_OK;
-  k_params_to_blob<<<dim3(n_tensors, blob_grid_y(max_count)), 256, 0, st>>>(params, table, blob);
+  launch_k(k_params_to_blob, dim3(n_tensors, blob_grid_y(max_count)), 256, 0, st, params, table, blob);
   count_launch();
   return check_cuda(cudaGetLastError(), "params_to_blob");
 }

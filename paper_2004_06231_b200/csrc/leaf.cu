@@ -29,6 +29,7 @@ constexpr int LF_TB = 32 * LF_NS;  // samples per CTA
 // ---------------------------------------------------------------------------
 
 __global__ void k_to_f32(const double *__restrict__ src, float *__restrict__ dst, int64_t n) {
+  EINET_KERNEL_PROLOGUE();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = (float)src[i];
@@ -37,6 +38,7 @@ __global__ void k_to_f32(const double *__restrict__ src, float *__restrict__ dst
 // active[d] = not marginalised; active[D] = 1 when a mask was given (the DMMA
 // leaf forward then zeroes masked / non-finite x before the contraction).
 __global__ void k_prepare_active(const uint8_t *mask, uint8_t *active, int D) {
+  EINET_KERNEL_PROLOGUE();
   int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d < D) active[d] = mask ? (mask[d] ? 0 : 1) : 1;
   if (d == 0) active[D] = mask ? 1 : 0;
@@ -45,6 +47,7 @@ __global__ void k_prepare_active(const uint8_t *mask, uint8_t *active, int D) {
 // phi (D,K,R,2) = (mean, second moment) -> fp64 (sa, -mu*sa), [r][d][k]
 __global__ void k_prepare_gauss(const double *__restrict__ phi, const uint8_t *active,
                                 double2 *lp, float *center, int D, int K, int R) {
+  EINET_KERNEL_PROLOGUE();
   int64_t n = (int64_t)R * D * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -64,6 +67,7 @@ __global__ void k_prepare_gauss(const double *__restrict__ phi, const uint8_t *a
 // categorical: log phi per state, [r][d][k][s]; masked variables -> 0
 __global__ void k_prepare_cat(const double *__restrict__ phi, const uint8_t *active, double *lp,
                               int D, int K, int R, int S) {
+  EINET_KERNEL_PROLOGUE();
   int64_t n = (int64_t)R * D * K * S;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -80,6 +84,7 @@ __global__ void k_prepare_cat(const double *__restrict__ phi, const uint8_t *act
 // binomial: (theta, A) with log p(x) = log h(x) + x*theta + A
 __global__ void k_prepare_binom(const double *__restrict__ phi, const uint8_t *active,
                                 double2 *lp, int D, int K, int R, int n_trials) {
+  EINET_KERNEL_PROLOGUE();
   int64_t n = (int64_t)R * D * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -95,6 +100,7 @@ __global__ void k_prepare_binom(const double *__restrict__ phi, const uint8_t *a
 }
 
 __global__ void k_prepare_logh(double *logh, int n) {
+  EINET_KERNEL_PROLOGUE();
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x <= n) logh[x] = lgamma((double)n + 1.0) - lgamma((double)x + 1.0) -
                         lgamma((double)(n - x) + 1.0);
@@ -106,6 +112,7 @@ __global__ void __launch_bounds__(256) k_prepare_const(
     const double *__restrict__ phi, const uint8_t *active, const double *leaf_offset,
     const int *scope_off, const int *scope_vars, const int *leaf_rep, double *cnst, int D,
     int K, int R, int family) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ double red[8];
   const int leaf = blockIdx.x, k = blockIdx.y;
   const int r = leaf_rep[leaf];
@@ -140,6 +147,7 @@ __global__ void __launch_bounds__(256) k_prepare_const(
 // equals the one the M-step left behind bit for bit.
 __global__ void __launch_bounds__(256) k_prepare_center(const double *__restrict__ phi,
                                                         float *center, int D, int K, int R) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= (int64_t)R * D) return;
@@ -158,27 +166,27 @@ int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_
   const int D = p.d_vars, K = p.k, R = p.num_replicas;
   const double *phi = params + p.sizes.phi_offset;
   auto grid_for = [](int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 4096); };
-  if (p.n_w) k_to_f32<<<grid_for(p.n_w), 256, 0, st>>>(params, c.w32, p.n_w);
-  if (p.n_mix) k_to_f32<<<grid_for(p.n_mix), 256, 0, st>>>(params + p.n_w, c.mix32, p.n_mix);
-  k_prepare_active<<<ceil_div(D, 256), 256, 0, st>>>(mask, c.active, D);
+  if (p.n_w) launch_k(k_to_f32, grid_for(p.n_w), 256, 0, st, params, c.w32, p.n_w);
+  if (p.n_mix) launch_k(k_to_f32, grid_for(p.n_mix), 256, 0, st, params + p.n_w, c.mix32, p.n_mix);
+  launch_k(k_prepare_active, ceil_div(D, 256), 256, 0, st, mask, c.active, D);
   const int64_t rdk = (int64_t)R * D * K;
   if (p.family == EINET_FAMILY_GAUSSIAN) {
-    k_prepare_gauss<<<grid_for(rdk), 256, 0, st>>>(phi, c.active, (double2 *)c.leafp,
+    launch_k(k_prepare_gauss, grid_for(rdk), 256, 0, st, phi, c.active, (double2 *)c.leafp,
                                                    c.center, D, K, R);
   } else if (p.family == EINET_FAMILY_CATEGORICAL) {
-    k_prepare_cat<<<grid_for(rdk * p.num_states), 256, 0, st>>>(phi, c.active, (double *)c.leafp,
+    launch_k(k_prepare_cat, grid_for(rdk * p.num_states), 256, 0, st, phi, c.active, (double *)c.leafp,
                                                                D, K, R, p.num_states);
   } else {
-    k_prepare_binom<<<grid_for(rdk), 256, 0, st>>>(phi, c.active, (double2 *)c.leafp, D, K, R,
+    launch_k(k_prepare_binom, grid_for(rdk), 256, 0, st, phi, c.active, (double2 *)c.leafp, D, K, R,
                                                    p.n_trials);
-    k_prepare_logh<<<ceil_div(p.n_trials + 1, 256), 256, 0, st>>>(c.logh, p.n_trials);
+    launch_k(k_prepare_logh, ceil_div(p.n_trials + 1, 256), 256, 0, st, c.logh, p.n_trials);
     count_launch();
   }
-  k_prepare_const<<<dim3(p.n_leaf, K), 256, 0, st>>>(phi, c.active, leaf_offset,
+  launch_k(k_prepare_const, dim3(p.n_leaf, K), 256, 0, st, phi, c.active, leaf_offset,
                                                      p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
                                                      c.cnst, D, K, R, p.family);
   if (p.family == EINET_FAMILY_GAUSSIAN) {
-    k_prepare_center<<<ceil_div((int64_t)R * D * 32, 256), 256, 0, st>>>(phi, c.center, D, K, R);
+    launch_k(k_prepare_center, ceil_div((int64_t)R * D * 32, 256), 256, 0, st, phi, c.center, D, K, R);
     count_launch();
   }
   count_launch((p.n_w ? 1 : 0) + (p.n_mix ? 1 : 0) + 3);
@@ -205,6 +213,7 @@ __global__ void __launch_bounds__(256) k_leaf_fwd_gauss(
     const int *__restrict__ leaf_rep, const double2 *__restrict__ lp,
     const uint8_t *__restrict__ active, double *__restrict__ part, int64_t Bc, int n_leaf,
     int dsplit, int32_t *status, const int *gate) {
+  EINET_KERNEL_PROLOGUE();
   if (gate && *(volatile const int *)gate == 0) return;  // the INT8 pass covered the batch
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int KG = blockDim.x / 32;
@@ -323,6 +332,7 @@ __global__ void __launch_bounds__(1024) k_leaf_fwd_discrete(
     const int *scope_vars, const int *leaf_rep, const void *lpv, const uint8_t *active,
     const double *logh, int family, int S, int n_trials, double *part, int64_t Bc,
     int n_leaf, int dsplit, int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   const int leaf = blockIdx.y, split = blockIdx.z;
   const int lane = threadIdx.x & 31, kq = threadIdx.x >> 5;
   const int sbeg = scope_off[leaf], slen = scope_off[leaf + 1] - sbeg;
@@ -383,6 +393,7 @@ __global__ void __launch_bounds__(256) k_leaf_finalize(
     const double *__restrict__ part, int dsplit, const double *__restrict__ cnst, int64_t B,
     int K, int n_leaf, const int *leaf_slab, WsView ws, double sign, int32_t *status,
     const int *gate) {
+  EINET_KERNEL_PROLOGUE();
   if (gate && *(volatile const int *)gate == 0) return;  // the INT8 pass covered the batch
   extern __shared__ double vals[];  // [32][K+1]
   __shared__ double mxs[32];
@@ -453,6 +464,7 @@ __global__ void __launch_bounds__(256) k_leaf_finalize(
 // holding a non-finite value (atomicMin, like the gathering kernels).
 __global__ void k_leaf_check(const float *__restrict__ x, int64_t B, int D,
                              const uint8_t *__restrict__ active, int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   if (status[2] == INT_MAX) return;
   const int64_t n = B * D;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -493,7 +505,7 @@ static int launch_leaf_fallback(Plan &p, const uint8_t *compute, const float *x,
     ds = leaf_dsplit(p, B, LF_TB,
                      device_slots((const void *)k_leaf_fwd_gauss, threads, smem, p.num_sms), nkc);
     dim3 grid(ceil_div(B, LF_TB), p.n_leaf, ds * nkc);
-    k_leaf_fwd_gauss<<<grid, threads, smem, st>>>(
+    launch_k(k_leaf_fwd_gauss, grid, threads, smem, st, 
         x, B, p.d_vars, p.k, p.num_replicas, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
         (const double2 *)c.leafp, c.active, w.leafpart, w.bc, p.n_leaf, ds, status, gate);
   } else {
@@ -501,7 +513,7 @@ static int launch_leaf_fallback(Plan &p, const uint8_t *compute, const float *x,
     if (threads > 1024) return fail(EINET_ERR_USAGE, "k too large for the leaf kernel (k <= 256)");
     ds = leaf_dsplit(p, B, 32, 2LL * p.num_sms, 1);
     dim3 grid(ceil_div(B, 32), p.n_leaf, ds);
-    k_leaf_fwd_discrete<<<grid, threads, 0, st>>>(
+    launch_k(k_leaf_fwd_discrete, grid, threads, 0, st, 
         x, B, p.d_vars, p.k, p.num_replicas, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
         c.leafp, c.active, c.logh, p.family, p.num_states, p.n_trials, w.leafpart, w.bc,
         p.n_leaf, ds, status);
@@ -511,12 +523,12 @@ static int launch_leaf_fallback(Plan &p, const uint8_t *compute, const float *x,
   if (fsmem > 48 * 1024)
     cudaFuncSetAttribute(k_leaf_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)fsmem);
-  k_leaf_finalize<<<g2, 256, fsmem, st>>>(w.leafpart, ds, c.cnst, B, p.k, p.n_leaf, p.d_leaf_slab,
+  launch_k(k_leaf_finalize, g2, 256, fsmem, st, w.leafpart, ds, c.cnst, B, p.k, p.n_leaf, p.d_leaf_slab,
                                       w, p.family == EINET_FAMILY_GAUSSIAN ? -1.0 : 1.0,
                                       status, gate);
   count_launch(2);
   if (p.leaf_dmma && p.use_tc) {
-    k_leaf_check<<<2 * p.num_sms, 256, 0, st>>>(x, B, p.d_vars, c.active, status);
+    launch_k(k_leaf_check, 2 * p.num_sms, 256, 0, st, x, B, p.d_vars, c.active, status);
     count_launch();
   }
   return check_cuda(cudaGetLastError(), "leaf forward kernels");
@@ -603,6 +615,7 @@ __global__ void __launch_bounds__(128) k_leaf_rho(WsView ws, const int *csr_off,
                                                   const uint8_t *ones, const int *leaf_slab,
                                                   int64_t B, int K, int n_leaf, double *ppart,
                                                   int nn) {
+  EINET_KERNEL_PROLOGUE();
   const int leaf = blockIdx.y;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int slab = leaf_slab[leaf];
@@ -672,6 +685,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats_gauss(
     const int *scope_vars, const int *leaf_rep, const float *__restrict__ rho_all, int64_t Bc,
     const float *__restrict__ center, const uint8_t *__restrict__ active, double *lspart,
     int64_t n_phi, int lsplit, int nkc) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ __align__(16) float ys[LS_BT][LS_VT];
   __shared__ __align__(16) float y2s[LS_BT][LS_VT];
   extern __shared__ __align__(16) float rs[];  // [LS_BT][KPC]
@@ -781,6 +795,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats_discrete(
     const int *scope_off, const int *scope_vars, const int *leaf_rep,
     const float *__restrict__ rho_all, int64_t Bc, const uint8_t *__restrict__ active,
     double *lspart, int64_t n_phi, int lsplit) {
+  EINET_KERNEL_PROLOGUE();
   const int leaf = blockIdx.y, split = blockIdx.z;
   const int sbeg = scope_off[leaf], slen = scope_off[leaf + 1] - sbeg;
   const int v0 = blockIdx.x * LS_VC;
@@ -835,7 +850,7 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
   double *Pcall = (double *)(wsb + p.w_tmp_p);
   {
   ProfScope prof("leaf_rho", st);
-  k_leaf_rho<<<dim3(nb, p.n_leaf), 128, 0, st>>>(w, p.d_csr_off, p.d_csr_slot, p.d_slab_ones,
+  launch_k(k_leaf_rho, dim3(nb, p.n_leaf), 128, 0, st, w, p.d_csr_off, p.d_csr_slot, p.d_slab_ones,
                                                  p.d_leaf_slab, B, K, p.n_leaf, w.ppart,
                                                  leaf_tc_supported(p) ? (K + 15) / 16 * 16 : 0);
   launch_reduce_partials_store(Pcall, w.ppart, nb, (int64_t)p.n_leaf * K,
@@ -858,11 +873,11 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
     const int kq = std::min(K4, 16);
     const int nkc = ceil_div(K4, kq);
     dim3 g(ceil_div(p.max_scope, LS_VT) * nkc, p.n_leaf, ls);
-    k_leaf_stats_gauss<<<g, 16 * kq, sizeof(float) * LS_BT * kq * 4, st>>>(
+    launch_k(k_leaf_stats_gauss, g, 16 * kq, sizeof(float) * LS_BT * kq * 4, st, 
         x, B, D, K, R, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep, w.rho, w.bc, c.center,
         c.active, w.lspart, n_phi, ls, nkc);
   } else {
-    k_leaf_stats_discrete<<<grid, 256, 0, st>>>(x, B, D, K, R, T, p.family, p.d_scope_off,
+    launch_k(k_leaf_stats_discrete, grid, 256, 0, st, x, B, D, K, R, T, p.family, p.d_scope_off,
                                                p.d_scope_vars, p.d_leaf_rep, w.rho, w.bc,
                                                c.active, w.lspart, n_phi, ls);
   }
@@ -878,6 +893,7 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
 
 __global__ void k_expand_acc_p(const double *P, const int *leaf_of, double *acc_p, int D, int K,
                                int R) {
+  EINET_KERNEL_PROLOGUE();
   int64_t n = (int64_t)D * K * R;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -891,7 +907,7 @@ __global__ void k_expand_acc_p(const double *P, const int *leaf_of, double *acc_
 
 int launch_expand_acc_p(Plan &p, const double *stats, double *acc_p, cudaStream_t st) {
   int64_t n = (int64_t)p.d_vars * p.k * p.num_replicas;
-  k_expand_acc_p<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+  launch_k(k_expand_acc_p, (int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st, 
       stats + p.sizes.stats_p_offset, p.d_leaf_of, acc_p, p.d_vars, p.k, p.num_replicas);
   count_launch();
   return check_cuda(cudaGetLastError(), "expand acc_p");
@@ -901,6 +917,7 @@ int launch_expand_acc_p(Plan &p, const double *stats, double *acc_p, cudaStream_
 __global__ void k_ef_log_prob(const double *__restrict__ phi, const float *__restrict__ x,
                               int64_t B, int D, int K, int R, int family, int S, int n_trials,
                               const uint8_t *mask, double *out, int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   int64_t n = B * D * K * R;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -940,7 +957,7 @@ __global__ void k_ef_log_prob(const double *__restrict__ phi, const float *__res
 int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
                        const uint8_t *mask, double *out, int32_t *status, cudaStream_t st) {
   int64_t n = B * p.d_vars * p.k * p.num_replicas;
-  k_ef_log_prob<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+  launch_k(k_ef_log_prob, (int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
       params + p.sizes.phi_offset, x, B, p.d_vars, p.k, p.num_replicas, p.family, p.num_states,
       p.n_trials, mask, out, status);
   count_launch();
@@ -949,6 +966,7 @@ int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
 
 __global__ void k_export_rows(WsView ws, const int *slabs, int nrows, int64_t B, int K,
                               double *out) {
+  EINET_KERNEL_PROLOGUE();
   int64_t n = B * nrows * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -965,7 +983,7 @@ int launch_export_buffer(Plan &p, const uint8_t *wsb, int64_t B, double *out, cu
   WsView w = ws_view(p, wsb);
   int64_t n = B * p.nbr * p.k;
   if (n == 0) return EINET_OK;
-  k_export_rows<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+  launch_k(k_export_rows, (int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
       w, nullptr, p.nbr, B, p.k, out);
   count_launch();
   return check_cuda(cudaGetLastError(), "export buffer");
@@ -975,7 +993,7 @@ int launch_export_leaf_rows(Plan &p, const uint8_t *wsb, int64_t B, double *out,
                             cudaStream_t st) {
   WsView w = ws_view(p, wsb);
   int64_t n = B * p.n_leaf * p.k;
-  k_export_rows<<<(int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+  launch_k(k_export_rows, (int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
       w, p.d_leaf_slab, p.n_leaf, B, p.k, out);
   count_launch();
   return check_cuda(cudaGetLastError(), "export leaf rows");

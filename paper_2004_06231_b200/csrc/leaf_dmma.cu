@@ -42,6 +42,7 @@ __global__ void k_prepare_leaf_img(const double2 *__restrict__ lp, const float *
                                    const int *__restrict__ scope_vars, const int *leaf_rep,
                                    const int *__restrict__ pvo, int n_leaf, int D, int K,
                                    double *__restrict__ img, int64_t n_img) {
+  EINET_KERNEL_PROLOGUE();
   const int NT = K / 8;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_img;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(256) k_prepare_cm2(const double2 *__restrict__
                                                      const int *scope_off, const int *scope_vars,
                                                      const int *leaf_rep, int D, int K,
                                                      double *cm2) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ double red[8];
   const int leaf = blockIdx.x, k = blockIdx.y, r = leaf_rep[leaf];
   double acc = 0.0;
@@ -98,10 +100,10 @@ int launch_prepare_leaf_dmma(Plan &p, uint8_t *compute, cudaStream_t st) {
   if (!p.leaf_dmma) return 0;
   CompView c = comp_view(p, compute);
   const int64_t n_img = (int64_t)p.h_leaf_pvo.back() * 2 * p.k;
-  k_prepare_leaf_img<<<(int)std::min<int64_t>((n_img + 255) / 256, 8192), 256, 0, st>>>(
+  launch_k(k_prepare_leaf_img, (int)std::min<int64_t>((n_img + 255) / 256, 8192), 256, 0, st, 
       (const double2 *)c.leafp, c.center, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
       p.d_leaf_pvo, p.n_leaf, p.d_vars, p.k, c.leafimg, n_img);
-  k_prepare_cm2<<<dim3(p.n_leaf, p.k), 256, 0, st>>>((const double2 *)c.leafp, c.center,
+  launch_k(k_prepare_cm2, dim3(p.n_leaf, p.k), 256, 0, st, (const double2 *)c.leafp, c.center,
                                                       p.d_scope_off, p.d_scope_vars,
                                                       p.d_leaf_rep, p.d_vars, p.k, c.cm2);
   count_launch(2);
@@ -126,6 +128,7 @@ __global__ void __launch_bounds__(32 * WARPS, 8 / WARPS + 1) k_leaf_fwd_dmma(
     const int *__restrict__ pvo, const double *__restrict__ img, const float *__restrict__ center,
     const double *__restrict__ cm2, const uint8_t *__restrict__ active, double *__restrict__ part,
     int64_t Bc, int n_leaf, int dsplit, int32_t *status, const int *gate) {
+  EINET_KERNEL_PROLOGUE();
   if (gate && *(volatile const int *)gate == 0) return;  // the INT8 pass covered the batch
   constexpr int K = NT * 8;
   constexpr int TBS = WARPS * 8 * MT;
@@ -283,7 +286,7 @@ static void launch_fwd_dmma_t(Plan &p, const CompView &c, const float *x, int64_
                               const int *gate) {
   constexpr int TBS = WARPS * 8 * MT;
   dim3 grid(ceil_div(B, TBS), p.n_leaf, ds);
-  k_leaf_fwd_dmma<NT, MT, WARPS><<<grid, 32 * WARPS, fwd_dmma_smem<NT, MT, WARPS>(), st>>>(
+  launch_k(k_leaf_fwd_dmma<NT, MT, WARPS>, grid, 32 * WARPS, fwd_dmma_smem<NT, MT, WARPS>(), st, 
       x, B, p.d_vars, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep, p.d_leaf_pvo, c.leafimg,
       c.center, c.cm2, c.active, w.leafpart, w.bc, p.n_leaf, ds, status, gate);
 }

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(256) k_i8_colscale(const double2 *__restrict__
                                                      const int *scope_off, const int *scope_vars,
                                                      const int *leaf_rep, int D, int K, int K8,
                                                      double *i8c) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ double red[2][8];
   const int leaf = blockIdx.x, k = blockIdx.y, r = leaf_rep[leaf];
   double mx = 0.0, cs = 0.0;
@@ -120,6 +121,7 @@ __global__ void k_i8_img(const double2 *__restrict__ lp, const int4 *__restrict_
                          const int *__restrict__ col, const uint32_t *__restrict__ amask,
                          const int *__restrict__ leaf_rep, const double *__restrict__ i8c,
                          int D, int K, int K8, int NG, int64_t npc, uint8_t *__restrict__ img) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t n_all = npc * K8 * LI_VC;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_all;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -159,6 +161,7 @@ __global__ void k_i8_img(const double2 *__restrict__ lp, const int4 *__restrict_
 // real and not marginalised). One warp per chunk.
 __global__ void k_i8_mask(const int4 *__restrict__ tab, const int *__restrict__ col,
                           const uint8_t *__restrict__ active, int npc, uint32_t *amask) {
+  EINET_KERNEL_PROLOGUE();
   const int pc = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (pc >= npc) return;
   const bool on = lane < tab[pc].y && active[col[pc * LI_VC + lane]] != 0;
@@ -263,6 +266,7 @@ __device__ __forceinline__ bool grid_u8(float x, uint32_t &u) {
 // since ncu does not profile kernels that reference the device graph API).
 template <bool COND>
 __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t xfull[LI_XST], xempty[LI_XST], afull[LI_AST], aempty[LI_AST],
       bfull[LI_BST], bempty[LI_BST],
@@ -605,7 +609,7 @@ int launch_i8_img(Plan &p, uint8_t *compute, cudaStream_t st) {
   CompView c = comp_view(p, compute);
   const int64_t npc = p.h_leaf_pvo.back() / LI_VC;
   const int64_t n_all = npc * p.i8_k8 * LI_VC;
-  k_i8_img<<<(int)std::min<int64_t>((n_all + 255) / 256, 8192), 256, 0, st>>>(
+  launch_k(k_i8_img, (int)std::min<int64_t>((n_all + 255) / 256, 8192), 256, 0, st, 
       (const double2 *)c.leafp, (const int4 *)p.d_i8_tab, p.d_i8_col,
       (const uint32_t *)(compute + p.c_i8mask), p.d_leaf_rep, (const double *)(compute + p.c_i8c),
       p.d_vars, p.k, p.i8_k8, p.i8_ng, npc, compute + p.c_i8img);
@@ -618,16 +622,16 @@ int launch_prepare_leaf_i8(Plan &p, uint8_t *compute, cudaStream_t st) {
   CompView c = comp_view(p, compute);
   double *i8c = (double *)(compute + p.c_i8c);
   uint8_t *img = compute + p.c_i8img;
-  k_i8_colscale<<<dim3(p.n_leaf, p.i8_k8), 256, 0, st>>>(
+  launch_k(k_i8_colscale, dim3(p.n_leaf, p.i8_k8), 256, 0, st, 
       (const double2 *)c.leafp, c.active, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep,
       p.d_vars, p.k, p.i8_k8, i8c);
   const int64_t npc = p.h_leaf_pvo.back() / LI_VC;
-  k_i8_mask<<<ceil_div(npc * 32, 256), 256, 0, st>>>((const int4 *)p.d_i8_tab, p.d_i8_col,
+  launch_k(k_i8_mask, ceil_div(npc * 32, 256), 256, 0, st, (const int4 *)p.d_i8_tab, p.d_i8_col,
                                                      c.active, (int)npc,
                                                      (uint32_t *)(compute + p.c_i8mask));
   count_launch();
   const int64_t n_all = npc * p.i8_k8 * LI_VC;
-  k_i8_img<<<(int)std::min<int64_t>((n_all + 255) / 256, 8192), 256, 0, st>>>(
+  launch_k(k_i8_img, (int)std::min<int64_t>((n_all + 255) / 256, 8192), 256, 0, st, 
       (const double2 *)c.leafp, (const int4 *)p.d_i8_tab, p.d_i8_col,
       (const uint32_t *)(compute + p.c_i8mask), p.d_leaf_rep, i8c, p.d_vars, p.k, p.i8_k8,
       p.i8_ng, npc, img);
@@ -685,9 +689,9 @@ int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t 
   a.grouped = (tiles < p.num_sms && npairs > 1) ? 1 : 0;
   const dim3 grid(tiles, a.grouped ? npairs : 1);
   if (cond)
-    k_leaf_fwd_i8<true><<<grid, LI_THREADS, smem, st>>>(a);
+    launch_k(k_leaf_fwd_i8<true>, grid, LI_THREADS, smem, st, a);
   else
-    k_leaf_fwd_i8<false><<<grid, LI_THREADS, smem, st>>>(a);
+    launch_k(k_leaf_fwd_i8<false>, grid, LI_THREADS, smem, st, a);
   if (tracing) {
     long long h[128 * 8];
     cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);

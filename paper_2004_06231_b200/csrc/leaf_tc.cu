@@ -73,6 +73,7 @@ __host__ __device__ inline int64_t ls_cta_of(int64_t u, int64_t U, int64_t G) {
 }
 
 __global__ void __launch_bounds__(LS_THREADS, 1) k_leaf_stats_tc(LeafStatsArgs a) {
+  EINET_KERNEL_PROLOGUE();
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t s_full[LS_STAGES], s_empty[LS_STAGES], a_full[LS_ASTAGES],
       a_empty[LS_ASTAGES], c_full, c_empty;
@@ -305,6 +306,7 @@ __global__ void k_leaf_stats_finish(const float *__restrict__ part, const double
                                     const uint8_t *__restrict__ active, double *acc_pt, int D,
                                     int K, int R, int64_t n_phi, int64_t nq, int64_t units,
                                     int grid) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t n = (int64_t)D * K * R;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -395,9 +397,9 @@ int launch_leaf_stats_tc(Plan &p, const uint8_t *compute, const float *x, int64_
     cudaFuncSetAttribute(k_leaf_stats_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  k_leaf_stats_tc<<<a.grid, LS_THREADS, smem, st>>>(a);
+  launch_k(k_leaf_stats_tc, a.grid, LS_THREADS, smem, st, a);
   const int64_t n = (int64_t)p.d_vars * p.k * p.num_replicas;
-  k_leaf_stats_finish<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+  launch_k(k_leaf_stats_finish, (int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st, 
       a.part, Pcall, c.center, p.d_leaf_of, p.d_phi_seg, c.active,
       stats + p.sizes.stats_acc_pt_offset, p.d_vars, p.k, p.num_replicas, p.n_phi, a.nq,
       a.units, a.grid);

@@ -15,6 +15,7 @@ namespace einet {
 __global__ void k_reduce_partials(double *__restrict__ dst, const double *__restrict__ part,
                                   int nparts, int64_t n, int64_t stride,
                                   const double *__restrict__ scale, int store) {
+  EINET_KERNEL_PROLOGUE();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -28,6 +29,7 @@ __global__ void k_reduce_partials(double *__restrict__ dst, const double *__rest
 __global__ void __launch_bounds__(256) k_reduce_partials_cta(
     double *__restrict__ dst, const double *__restrict__ part, int nparts, int64_t stride,
     const double *__restrict__ scale, int store) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ double red[8];
   const int64_t i = blockIdx.x;
   double s = 0.0;
@@ -47,10 +49,10 @@ static void reduce_partials(double *dst, const double *part, int nparts, int64_t
                             int64_t stride, const double *scale, int store, cudaStream_t st) {
   if (n <= 0) return;
   if (nparts >= 64 && n <= 65536) {
-    k_reduce_partials_cta<<<(unsigned)n, 256, 0, st>>>(dst, part, nparts, stride, scale, store);
+    launch_k(k_reduce_partials_cta, (unsigned)n, 256, 0, st, dst, part, nparts, stride, scale, store);
   } else {
     const int grid = (int)std::min<int64_t>((n + kReduceThreads - 1) / kReduceThreads, 8192);
-    k_reduce_partials<<<grid, kReduceThreads, 0, st>>>(dst, part, nparts, n, stride, scale,
+    launch_k(k_reduce_partials, grid, kReduceThreads, 0, st, dst, part, nparts, n, stride, scale,
                                                        store);
   }
   count_launch();
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(256) k_mstep_einsum(double *__restrict__ W,
                                                       const int32_t *status,
                                                       const int64_t *__restrict__ tiledesc,
                                                       int ntd, uint8_t *compute, int kp) {
+  EINET_KERNEL_PROLOGUE();
   const int KK = K * K;
   __shared__ double red[8];
   if (step_failed(status)) return;
@@ -165,6 +168,7 @@ __global__ void k_mstep_mixing(double *__restrict__ Wm, float *__restrict__ m32,
                                const double *__restrict__ n, const int *row_off,
                                const int *row_len, const uint8_t *mask, int nrows, double lam,
                                double eps, const int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nrows || step_failed(status)) return;
   const int o = row_off[r], len = row_len[r];
@@ -192,6 +196,7 @@ __global__ void k_mstep_leaf(double *__restrict__ phi, const double *__restrict_
                              int D, int K, int R, int T, int family, double lam,
                              double var_min, double var_max, double p_min, int n_trials,
                              const int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   if (step_failed(status)) return;
   const int64_t n = (int64_t)D * K * R;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -243,6 +248,7 @@ __global__ void __launch_bounds__(256) k_mstep_leaf_gauss(
     const int *__restrict__ leaf_of, const int *__restrict__ scope_pos,
     const int *__restrict__ pvo, int D, int K, int R, double lam, double var_min,
     double var_max, const int32_t *status, CompView c, int dmma, double *__restrict__ mtmp) {
+  EINET_KERNEL_PROLOGUE();
   if (step_failed(status)) return;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= R * D) return;
@@ -314,6 +320,7 @@ __global__ void __launch_bounds__(256) k_leaf_consts(const double *__restrict__ 
                                                      const int32_t *status,
                                                      const double2 *__restrict__ lp, int K8,
                                                      double *i8c) {
+  EINET_KERNEL_PROLOGUE();
   __shared__ double red[4][8];
   if (step_failed(status)) return;
   const int leaf = blockIdx.x, k = blockIdx.y, r = leaf_rep[leaf];
@@ -384,11 +391,11 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
   if (fused) {
     const int64_t warps = (int64_t)p.num_replicas * p.d_vars;
     double *mtmp = (double *)(compute + p.c_mtmp);
-    k_mstep_leaf_gauss<<<(int)((warps + 7) / 8), 256, 0, ls>>>(
+    launch_k(k_mstep_leaf_gauss, (int)((warps + 7) / 8), 256, 0, ls, 
         params + p.sizes.phi_offset, stats + p.sizes.stats_acc_pt_offset,
         stats + p.sizes.stats_p_offset, p.d_leaf_of, p.d_scope_pos, p.d_leaf_pvo, p.d_vars, K,
         p.num_replicas, lam, p.var_min, p.var_max, status, c, p.leaf_dmma, mtmp);
-    k_leaf_consts<<<dim3(p.n_leaf, K), 256, 0, ls>>>(
+    launch_k(k_leaf_consts, dim3(p.n_leaf, K), 256, 0, ls, 
         mtmp, p.d_scope_off, p.d_scope_vars, p.d_leaf_rep, p.d_vars, K, c.cnst,
         p.leaf_dmma ? c.cm2 : nullptr, status, (const double2 *)c.leafp, p.i8_k8,
         p.leaf_i8 ? (double *)(compute + p.c_i8c) : nullptr);
@@ -398,13 +405,13 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
   }
   if (p.n_w) {
     const int nslices = (int)(p.n_w / KK);
-    k_mstep_einsum<<<nslices, 256, 0, st>>>(params, c.w32, stats, K, lam, eps_w, status,
+    launch_k(k_mstep_einsum, nslices, 256, 0, st, params, c.w32, stats, K, lam, eps_w, status,
                                             fused ? p.d_tiledesc : nullptr,
                                             p.n_tiledesc, compute, p.kp);
     count_launch();
   }
   if (p.n_mixrows) {
-    k_mstep_mixing<<<ceil_div(p.n_mixrows, 128), 128, 0, st>>>(
+    launch_k(k_mstep_mixing, ceil_div(p.n_mixrows, 128), 128, 0, st, 
         params + p.n_w, c.mix32, stats + p.n_w, p.d_mixrow_off, p.d_mixrow_len,
         p.d_mix_mask_all, p.n_mixrows, lam, eps_w, status);
     count_launch();
@@ -418,7 +425,7 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
     return check_cuda(cudaGetLastError(), "fused mstep kernels");
   }
   const int64_t n = (int64_t)p.d_vars * K * p.num_replicas;
-  k_mstep_leaf<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+  launch_k(k_mstep_leaf, (int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st, 
       params + p.sizes.phi_offset, stats + p.sizes.stats_acc_pt_offset,
       stats + p.sizes.stats_p_offset, p.d_leaf_of, p.d_vars, K, p.num_replicas, p.suff,
       p.family, lam, p.var_min, p.var_max, p.p_min, p.n_trials, status);
@@ -435,6 +442,7 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
 __global__ void k_log_einsum_exp(const double *__restrict__ left, const double *__restrict__ right,
                                  const double *__restrict__ w, int64_t B, int L, int K, int Ko,
                                  double *out) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= B * L * Ko) return;
   const int k = (int)(e % Ko);
@@ -465,12 +473,13 @@ __global__ void k_log_einsum_exp(const double *__restrict__ left, const double *
 int launch_log_einsum_exp(const double *left, const double *right, const double *w, int64_t B,
                           int L, int K, int Ko, double *out, cudaStream_t st) {
   const int64_t n = B * L * Ko;
-  k_log_einsum_exp<<<ceil_div(n, 128), 128, 0, st>>>(left, right, w, B, L, K, Ko, out);
+  launch_k(k_log_einsum_exp, ceil_div(n, 128), 128, 0, st, left, right, w, B, L, K, Ko, out);
   count_launch();
   return check_cuda(cudaGetLastError(), "log_einsum_exp");
 }
 
 __global__ void k_status_reset(int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   if (threadIdx.x < EINET_STATUS_WORDS) status[threadIdx.x] = INT_MAX;
 }
 
@@ -480,28 +489,30 @@ __global__ void k_status_reset(int32_t *status) {
 // by turning a non-zero count into status word 3, so every rank skips the
 // same update (the exact error words travel in a MIN all-reduce only then).
 __global__ void k_status_to_stats(const int32_t *status, double *flag) {
+  EINET_KERNEL_PROLOGUE();
   if (threadIdx.x == 0)
     *flag = (status[0] != INT_MAX || status[1] != INT_MAX || status[3] != INT_MAX) ? 1.0 : 0.0;
 }
 
 __global__ void k_status_from_stats(const double *flag, int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   if (threadIdx.x == 0 && *flag > 0.0) status[3] = 0;
 }
 
 int launch_status_to_stats(const int32_t *status, double *flag, cudaStream_t st) {
-  k_status_to_stats<<<1, 32, 0, st>>>(status, flag);
+  launch_k(k_status_to_stats, 1, 32, 0, st, status, flag);
   count_launch();
   return check_cuda(cudaGetLastError(), "status to stats");
 }
 
 int launch_status_from_stats(const double *flag, int32_t *status, cudaStream_t st) {
-  k_status_from_stats<<<1, 32, 0, st>>>(flag, status);
+  launch_k(k_status_from_stats, 1, 32, 0, st, flag, status);
   count_launch();
   return check_cuda(cudaGetLastError(), "status from stats");
 }
 
 int launch_status_reset(int32_t *status, cudaStream_t st) {
-  k_status_reset<<<1, 32, 0, st>>>(status);
+  launch_k(k_status_reset, 1, 32, 0, st, status);
   count_launch();
   return check_cuda(cudaGetLastError(), "status reset");
 }

@@ -60,6 +60,7 @@ __device__ __forceinline__ int search_right(const double *cdf, int n, double t) 
 __global__ void k_sample_cdf(const double *__restrict__ W, WsView ws, const int *left_slab,
                              const int *right_slab, const int *out_slab, int rows, int Ko, int K,
                              int conditional, double *cdf) {
+  EINET_KERNEL_PROLOGUE();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * Ko) return;
   const int l = e / Ko, k = e % Ko;
@@ -90,6 +91,7 @@ __global__ void k_sample_cdf(const double *__restrict__ W, WsView ws, const int 
 __global__ void k_sample_einsum(const double *__restrict__ cdf, int16_t *kk, int64_t n, int K,
                                 int Ko, const int *left_slab, const int *right_slab,
                                 const int *out_slab, uint64_t seed, int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   const int l = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= n) return;
@@ -115,6 +117,7 @@ __global__ void k_sample_mixing(const double *__restrict__ wm, WsView ws, int16_
                                 int64_t n, int dmax, const int *src_slab, const uint8_t *mask,
                                 const int *out_slab, int conditional, uint64_t seed,
                                 int32_t *status) {
+  EINET_KERNEL_PROLOGUE();
   const int m = blockIdx.y;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= n) return;
@@ -163,6 +166,7 @@ __global__ void k_sample_leaves(const double *__restrict__ phi, const int16_t *k
                                 const int *leaf_of, const int *leaf_slab, int num_slabs,
                                 const double *x_e, const uint8_t *evidence, uint64_t seed,
                                 double *out) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n * D) return;
   const int d = (int)(e % D);
@@ -230,6 +234,7 @@ int64_t sample_scratch_bytes(const Plan &p, int64_t n) {
 }
 
 __global__ void k_sample_root(int16_t *kk_root, int64_t n) {
+  EINET_KERNEL_PROLOGUE();
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b < n) kk_root[b] = 0;  // the scalar root carries component 0
 }
@@ -246,13 +251,13 @@ int launch_sample(Plan &p, const double *params, const uint8_t *wsb, int conditi
   int rc = check_cuda(cudaMemsetAsync(kk, 0xFF, 2 * (size_t)p.num_slabs * n, st), "sample init");
   if (rc) return rc;
   const int nb = ceil_div(n, 128);
-  k_sample_root<<<nb, 128, 0, st>>>(kk + (int64_t)p.root_out_slab * n, n);
+  launch_k(k_sample_root, nb, 128, 0, st, kk + (int64_t)p.root_out_slab * n, n);
   count_launch();
   const int K = p.k;
   for (auto &L : p.layers) {
     if (L.kind != EINET_LAYER_EINSUM) continue;
     const int nthr = L.rows * L.k_out;
-    k_sample_cdf<<<ceil_div(nthr, 128), 128, 0, st>>>(params + L.w_off, ws, L.d_left_slab,
+    launch_k(k_sample_cdf, ceil_div(nthr, 128), 128, 0, st, params + L.w_off, ws, L.d_left_slab,
                                                        L.d_right_slab, L.d_out_slab, L.rows,
                                                        L.k_out, K, conditional, cdf + L.w_off);
     count_launch();
@@ -261,17 +266,17 @@ int launch_sample(Plan &p, const double *params, const uint8_t *wsb, int conditi
     const LayerPlan &L = p.layers[li];
     dim3 grid(nb, L.rows);
     if (L.kind == EINET_LAYER_EINSUM) {
-      k_sample_einsum<<<grid, 128, 0, st>>>(cdf + L.w_off, kk, n, K, L.k_out, L.d_left_slab,
+      launch_k(k_sample_einsum, grid, 128, 0, st, cdf + L.w_off, kk, n, K, L.k_out, L.d_left_slab,
                                             L.d_right_slab, L.d_out_slab, seed, status);
     } else {
-      k_sample_mixing<<<grid, 128, 0, st>>>(params + p.n_w + L.mix_off, ws, kk, n, L.dmax,
+      launch_k(k_sample_mixing, grid, 128, 0, st, params + p.n_w + L.mix_off, ws, kk, n, L.dmax,
                                             L.d_mix_src_slab, L.d_mix_mask, L.d_out_slab,
                                             conditional, seed, status);
     }
     count_launch();
   }
   const int64_t tot = n * p.d_vars;
-  k_sample_leaves<<<(int)((tot + 255) / 256), 256, 0, st>>>(
+  launch_k(k_sample_leaves, (int)((tot + 255) / 256), 256, 0, st, 
       params + p.sizes.phi_offset, kk, n, p.d_vars, K, p.num_replicas, p.family, p.num_states,
       p.n_trials, p.d_leaf_of, p.d_leaf_slab, p.num_slabs, x_e, evidence, seed, out);
   count_launch();
