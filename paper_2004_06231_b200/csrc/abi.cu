@@ -10,6 +10,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <deque>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -82,6 +83,16 @@ void profile_record(const char *name, cudaEvent_t start, cudaEvent_t stop) {
       return;
     }
   g_prof.push_back(ProfClass{name, {{start, stop}}});
+}
+const char *prof_layer_name(const char *base, int layer) {
+  static const bool per_layer = getenv("EINET_PROFILE_LAYERS") != nullptr;
+  if (!per_layer || !g_profiling) return base;
+  static std::deque<std::string> pool;  // interned: pointers stay valid
+  const std::string name = std::string(base) + "@" + std::to_string(layer);
+  for (const auto &n : pool)
+    if (n == name) return n.c_str();
+  pool.push_back(name);
+  return pool.back().c_str();
 }
 static void profile_clear() {
   for (auto &c : g_prof)

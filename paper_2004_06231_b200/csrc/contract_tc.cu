@@ -125,6 +125,7 @@ __device__ __forceinline__ float dot_f32x2(const float (&v)[K], const float (&e)
   float a0, a1, a2, a3;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc[0]));
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a2), "=f"(a3) : "l"(acc[1]));
+  if (K & 1) a0 = fmaf(v[K - 1], e[K - 1], a0);
   return (a0 + a2) + (a1 + a3);
 }
 
@@ -342,21 +343,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
         const uint32_t ta = tm + lane_off + (uint32_t)(buf * 256);
         if (a.direct) {
           float v[K];
-          int u = 0;
-#pragma unroll
-          for (; u + 16 <= K; u += 16) {
-            float c16[16];
-            tc::tmem_ld16(ta + u, c16);
-#pragma unroll
-            for (int z = 0; z < 16; ++z) v[u + z] = c16[z];
-          }
-#pragma unroll
-          for (; u < K; u += 8) {
-            float c8[8];
-            tc::tmem_ld8(ta + u, c8);
-#pragma unroll
-            for (int z = 0; z < 8; ++z) v[u + z] = c8[z];
-          }
+          tc::tmem_ld_cols<K>(ta, v);
           tc::tmem_wait_ld();
           const float rt = sv[0];
           if (live) {
@@ -372,25 +359,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
 #pragma unroll
             for (int gi = 0; gi < OPW; ++gi) {
               const int ol = half + 2 * (g0 + gi);
-              if (g0 + gi < NPW && ol < nol) {
-                int u = 0;
-#pragma unroll
-                for (; u + 32 <= K; u += 32) tc::tmem_ld32(ta + ol * K + u, &v[gi][u]);
-#pragma unroll
-                for (; u + 16 <= K; u += 16) {
-                  float c16[16];
-                  tc::tmem_ld16(ta + ol * K + u, c16);
-#pragma unroll
-                  for (int z = 0; z < 16; ++z) v[gi][u + z] = c16[z];
-                }
-#pragma unroll
-                for (; u < K; u += 8) {
-                  float c8[8];
-                  tc::tmem_ld8(ta + ol * K + u, c8);
-#pragma unroll
-                  for (int z = 0; z < 8; ++z) v[gi][u + z] = c8[z];
-                }
-              }
+              if (g0 + gi < NPW && ol < nol) tc::tmem_ld_cols<K>(ta + ol * K, v[gi]);
             }
             tc::tmem_wait_ld();
 #pragma unroll
@@ -549,7 +518,9 @@ int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *com
   }
   switch (K) {
     case 8: return mode == 0 ? contract_t<8, true>(p, a, w, st) : contract_t<8, false>(p, a, w, st);
+    case 10: return mode == 0 ? contract_t<10, true>(p, a, w, st) : contract_t<10, false>(p, a, w, st);
     case 16: return mode == 0 ? contract_t<16, true>(p, a, w, st) : contract_t<16, false>(p, a, w, st);
+    case 20: return mode == 0 ? contract_t<20, true>(p, a, w, st) : contract_t<20, false>(p, a, w, st);
     case 24: return mode == 0 ? contract_t<24, true>(p, a, w, st) : contract_t<24, false>(p, a, w, st);
     case 32: return mode == 0 ? contract_t<32, true>(p, a, w, st) : contract_t<32, false>(p, a, w, st);
     case 40: return mode == 0 ? contract_t<40, true>(p, a, w, st) : contract_t<40, false>(p, a, w, st);

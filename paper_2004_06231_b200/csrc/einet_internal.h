@@ -179,6 +179,9 @@ void count_launch(int n = 1);
 // launches; einet_profile_query sums the elapsed times per class.
 bool profiling_enabled();
 void profile_record(const char *name, cudaEvent_t start, cudaEvent_t stop);
+// Per-layer class names ("einsum_fwd@3") when EINET_PROFILE_LAYERS is set
+// (the C5 sweep times one EinsumLayer of a larger graph); else `base`.
+const char *prof_layer_name(const char *base, int layer);
 struct ProfScope {
   const char *name;
   cudaStream_t st;

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(128) k_einsum_prep_fwd(
     }
     return;
   }
-  // tensor-core path (K % 8 == 0): also the EB (and for direct child-rho rows
+  // tensor-core path: also the EB (and for direct child-rho rows
   // EA) bf16 A-operand tiles, width kp (entries K..kp-1 are zero)
   const int64_t ntl = ws.bc / 128;
   for (int e = t; e < (kp / 4) * 32; e += 128) {
@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(128) k_einsum_prep_fwd(
     if (4 * q < K) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
+        if (4 * q + u >= K) break;
         const int x = (4 * q + u) * 32 + bl, xe = (4 * q + u) * EV_ROW + bl;
         va[u] = d ? 0.f : expf(ol[x] - mx[0][bl]);
         vb[u] = d ? 0.f : expf(orr[x] - mx[1][bl]);
@@ -1120,7 +1121,7 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
     if (L.kind == EINET_LAYER_EINSUM) {
       float *EA = (float *)layer_ea(p, w, L), *EB = (float *)layer_eb(p, w, L);
       {
-        ProfScope prof("einsum_prep", st);
+        ProfScope prof(prof_layer_name("einsum_prep", L.index), st);
         dim3 grid(ceil_div(B, 32), L.rows);
         const bool tcl = p.use_tc && L.tc;
         float *EBM = tcl ? w.ebm + (int64_t)L.erow_base * w.bc * p.kp : nullptr;
@@ -1128,7 +1129,7 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
         launch_k(k_einsum_prep_fwd, grid, 128, 0, st, w, L.d_left_slab, L.d_right_slab, L.d_out_slab,
                                                 B, p.k, EA, EB, EBM, EAM, p.kp, L.index, status);
       }
-      ProfScope prof("einsum_fwd", st);
+      ProfScope prof(prof_layer_name("einsum_fwd", L.index), st);
       if (p.use_tc && L.tc)
         rc = launch_contract_tc(p, L, 0, compute, EA, EB, w, B, st);
       else
@@ -1191,7 +1192,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
     }
     const float *EA = layer_ea(p, w, L), *EB = layer_eb(p, w, L);
     {
-      ProfScope prof("einsum_bwd_rt", st);
+      ProfScope prof(prof_layer_name("einsum_bwd_rt", L.index), st);
       dim3 g1(ceil_div(B, 32), L.rows);
       const bool tcl = p.use_tc && L.tc;
       launch_k(k_einsum_bwd_rt, g1, 128, 0, st, w, L.d_out_slab, p.d_csr_off, p.d_csr_slot,
@@ -1201,7 +1202,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
     }
     const int64_t lw = (int64_t)L.rows * L.k_out * K * K;
     {
-      ProfScope prof("einsum_wstats", st);
+      ProfScope prof(prof_layer_name("einsum_wstats", L.index), st);
       const int K4 = (K + 3) / 4;
       if (L.k_out == 1 && K4 * K4 <= 256 && !getenv("EINET_WK1_OFF")) {
         const int ns = wstats_bsplit(p, L, B, L.rows);
@@ -1230,7 +1231,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
       }
     }
     {
-      ProfScope prof("einsum_childrho", st);
+      ProfScope prof(prof_layer_name("einsum_childrho", L.index), st);
       if (p.use_tc && L.tc) {
         int rc = launch_contract_tc(p, L, 1, compute, EA, EB, w, B, st);
         if (!rc) rc = launch_contract_tc(p, L, 2, compute, EA, EB, w, B, st);

@@ -148,7 +148,9 @@ void plan_tc_tiling(Plan &p) {
   for (auto &L : p.layers) {
     L.tc = 0;
     if (L.kind != EINET_LAYER_EINSUM) continue;
-    if (K % 8 != 0 || K < 8 || K > 64 || p.ks % 4 != 0) continue;
+    // K multiple of 8 up to 64, and K = 10, 20 (BASELINE configs C1, C2, C5):
+    // the MMA K dimension is padded to 16 with zero operand entries
+    if (!((K % 8 == 0 && K >= 8 && K <= 64) || K == 10 || K == 20)) continue;
     const int Ko = L.k_out;
     int kg = std::max(1, std::min(Ko, 256 / K));
     while (kg > 1 && fwd_smem(round_up(kg * K, 16), K, kp) > TC_SMEM_MAX) --kg;

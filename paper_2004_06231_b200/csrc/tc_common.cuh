@@ -171,6 +171,58 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float *v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float *v) {
+  uint32_t r[2];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+               : "=r"(r[0]), "=r"(r[1])
+               : "r"(taddr));
+  v[0] = __uint_as_float(r[0]);
+  v[1] = __uint_as_float(r[1]);
+}
+__device__ __forceinline__ void tmem_ld1(uint32_t taddr, float *v) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  v[0] = __uint_as_float(r);
+}
+// N consecutive accumulator columns (any N) of this warp's 32 lanes into v[0..N):
+// x32 / x16 / x8 / x4 / x2 / x1 pieces; completes at tmem_wait_ld()
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float *v) {
+  int u = 0;
+#pragma unroll
+  for (; u + 32 <= N; u += 32) tmem_ld32(taddr + u, v + u);
+#pragma unroll
+  for (; u + 16 <= N; u += 16) {
+    float c[16];
+    tmem_ld16(taddr + u, c);
+#pragma unroll
+    for (int z = 0; z < 16; ++z) v[u + z] = c[z];
+  }
+#pragma unroll
+  for (; u + 8 <= N; u += 8) {
+    float c[8];
+    tmem_ld8(taddr + u, c);
+#pragma unroll
+    for (int z = 0; z < 8; ++z) v[u + z] = c[z];
+  }
+  if (N - u >= 4) {
+    tmem_ld4(taddr + u, v + u);
+    u += 4;
+  }
+  if (N - u >= 2) {
+    tmem_ld2(taddr + u, v + u);
+    u += 2;
+  }
+  if (N - u >= 1) tmem_ld1(taddr + u, v + u);
+}
 // bf16 pair (lo address = first element) packed in one 32-bit word
 __device__ __forceinline__ uint32_t pack_bf16x2(__nv_bfloat16 a, __nv_bfloat16 b) {
   return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
