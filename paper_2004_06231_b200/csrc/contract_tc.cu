@@ -459,12 +459,17 @@ static int contract_t(Plan &p, ContractArgs &a, const WsView &w, cudaStream_t st
   return check_cuda(cudaGetLastError(), "einsum contraction (tcgen05)");
 }
 
+int launch_contract_big(Plan &p, const LayerPlan &L, int mode, const uint8_t *compute,
+                        const float *EA, const float *EB, const WsView &w, int64_t B,
+                        cudaStream_t st);
+
 // mode 0: forward, 1: left child responsibilities, 2: right
 int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *compute,
                        const float *EA, const float *EB, const WsView &w, int64_t B,
                        cudaStream_t st) {
   ContractArgs a;
   const int K = p.k;
+  if (K > 64) return launch_contract_big(p, L, mode, compute, EA, EB, w, B, st);
   a.B = B;
   a.ntl = (B + 127) / 128;
   a.L = L.rows;

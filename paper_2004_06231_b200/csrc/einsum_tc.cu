@@ -141,25 +141,30 @@ static int64_t cr_smem(int rows_tile, int kob, int K) {
 size_t wstats_smem(int K, int nn);  // wstats_tc.cu
 static int64_t ws_smem(int K, int nn) { return (int64_t)wstats_smem(K, nn); }
 
+size_t contract_big_smem(int K, int ka, int64_t tile_bytes);  // contract_big.cu
+
 void plan_tc_tiling(Plan &p) {
   const int K = p.k;
   p.kp = round_up(K, 16);
   const int kp = p.kp;
+  // large K (96, 128): one output per weight chunk, tile-stationary kernel
+  // (contract_big.cu) streaming the chunks
+  const bool big = K == 96 || K == 128;
   for (auto &L : p.layers) {
     L.tc = 0;
     if (L.kind != EINET_LAYER_EINSUM) continue;
     // K multiple of 8 up to 64, and K = 10, 20 (BASELINE configs C1, C2, C5):
     // the MMA K dimension is padded to 16 with zero operand entries
-    if (!((K % 8 == 0 && K >= 8 && K <= 64) || K == 10 || K == 20)) continue;
+    if (!((K % 8 == 0 && K >= 8 && K <= 64) || K == 10 || K == 20 || big)) continue;
     const int Ko = L.k_out;
-    int kg = std::max(1, std::min(Ko, 256 / K));
+    int kg = big ? 1 : std::max(1, std::min(Ko, 256 / K));
     while (kg > 1 && fwd_smem(round_up(kg * K, 16), K, kp) > TC_SMEM_MAX) --kg;
     L.kg = kg;
     L.ng = ceil_div(Ko, kg);
     L.fw_rows = round_up(kg * K, 16);
     L.fw_tile = 4LL * L.fw_rows * kp;
     L.kob = round_up(Ko, 16);
-    int ig = std::max(1, std::min(K, 256 / K));
+    int ig = big ? 1 : std::max(1, std::min(K, 256 / K));
     while (ig > 1 && cr_smem(round_up(ig * K, 16), L.kob, K) > TC_SMEM_MAX) --ig;
     L.ig = ig;
     L.ni = ceil_div(K, ig);
@@ -169,10 +174,17 @@ void plan_tc_tiling(Plan &p) {
     L.direct = Ko == 1;
     L.rw_rows = round_up(K, 16);
     L.rw_tile = 4LL * L.rw_rows * kp;
-    if (L.fw_rows > 256 || L.uw_rows > 256 || L.nn > 64 || L.kob > 256) continue;
-    if (fwd_smem(L.fw_rows, K, kp) > TC_SMEM_MAX || cr_smem(L.uw_rows, L.kob, K) > TC_SMEM_MAX ||
-        ws_smem(K, L.nn) > TC_SMEM_MAX)
+    if (L.fw_rows > 256 || L.uw_rows > 256 || L.nn > 128 || L.kob > 256) continue;
+    if (big) {
+      if (kp % 32 || (!L.direct && L.kob % 32) ||
+          (int64_t)contract_big_smem(K, kp, L.fw_tile) > TC_SMEM_MAX ||
+          (!L.direct && (int64_t)contract_big_smem(K, L.kob, L.uw_tile) > TC_SMEM_MAX) ||
+          ws_smem(K, L.nn) > TC_SMEM_MAX)
+        continue;
+    } else if (L.nn > 64 || fwd_smem(L.fw_rows, K, kp) > TC_SMEM_MAX ||
+               cr_smem(L.uw_rows, L.kob, K) > TC_SMEM_MAX || ws_smem(K, L.nn) > TC_SMEM_MAX) {
       continue;
+    }
     L.tc = 1;
   }
 }

@@ -19,7 +19,7 @@ Work per point: flops = 2 * B * L * K^3 per pass (forward,
 W statistics; the child responsibilities are two such GEMMs, left and right);
 bytes = 4 * (3 * B * L * K + L * K^3) per layer call (the two child
 log-density vectors in, the output out, the weights). Peaks from
-MEASURED_PEAKS.json (bf16 dense, HBM). K % 8 == 0 and K <= 64 and K = 10, 20 run the
+MEASURED_PEAKS.json (bf16 dense, HBM). K % 8 == 0 and K <= 64, K = 10, 20, 96, 128 run the
 tcgen05 kernels (3xBF16: three MMAs per product, so `tc_frac_issued` = 3 x the
 algorithmic fraction), the other K the CUDA-core kernels.
 """
@@ -78,7 +78,7 @@ def main():
         ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=x_all[:256])
         params = engine.Parameters.from_numpy(circuit, fam, ein, mix, phi)
         model = EinetModel(circuit, params, fam)
-        tc = (k % 8 == 0 and 8 <= k <= 64) or k in (10, 20)
+        tc = (k % 8 == 0 and 8 <= k <= 64) or k in (10, 20, 96, 128)
         for b in [int(v) for v in args.batches.split(",")]:
             xd = engine.as_device_batch(x_all[:b])
             for _ in range(3):

@@ -255,9 +255,11 @@ def test_c4_celeba_shape_vs_oracle():
 
 
 @pytest.mark.parametrize("k", [72, 96, 128])
-def test_large_k_cuda_core_path_vs_oracle(k):
-    """K > 64 (BASELINE.json configs[4] sweeps K up to 128) runs the CUDA-core
-    kernels (tiled forward for K <= 128): forward and one EM step vs oracle."""
+def test_large_k_paths_vs_oracle(k):
+    """K > 64 (BASELINE.json configs[4] sweeps K up to 128): K = 96 and 128 run
+    the tile-stationary tcgen05 contraction (contract_big.cu) and the tcgen05
+    W statistics, K = 72 the CUDA-core kernels: forward and one EM step vs
+    oracle."""
     rg = E.random_binary_tree(12, StructureConfig(depth=2, replicas=2, seed=4))
     x = np.random.default_rng(k).normal(0.4, 0.3, (48, 12)).astype(np.float32).astype(np.float64)
     fam = E.GaussianFamily()
