@@ -50,17 +50,20 @@ constexpr int CT_GMAX = 2;        // max weight chunks resident per (row, group)
 constexpr int CT_EPI_WARPS = 8;                 // two per TMEM lane quarter
 constexpr int CT_THREADS = 64 + 32 * CT_EPI_WARPS;
 
+// Per side (forward: one side; child responsibilities: left and right in one
+// launch, the job space being side-major): operand and output pointers.
 struct ContractArgs {
-  const float *a_ops;     // A operand tiles of the layer's first row
+  const float *a_ops[2];  // A operand tiles of the layer's first row
   int64_t a_row_stride;   // bytes per row (ntl * 128 * ka * 4: bf16 hi | lo)
   int ka;                 // MMA K dimension (multiple of 16)
-  const float *e1;        // contraction vector, 32-sample transposed, width K
-  const float *sv;        // per-output scale vector (left/right), width K; null = forward
-  const uint8_t *tiles;   // weight chunk images [row][chunk]
+  const float *e1[2];     // contraction vector, 32-sample transposed, width K
+  const float *sv[2];     // per-output scale vector (left/right), width K; null = forward
+  const uint8_t *tiles[2];  // weight chunk images [row][chunk]
   int64_t tile_bytes;
   int nchunk, og, rows_tile, n_out;
   int G, ngroup;          // weight chunks resident per (row, group) run, groups per row
-  const int *dst;         // per row: output slab (forward) or slot (left/right)
+  const int *dst[2];      // per row: output slab (forward) or slot (left/right)
+  int nside;              // 1 (forward) or 2 (left and right child responsibilities)
   int64_t B, ntl;
   int L;
   int stages;             // A-operand ring depth (2..4, by shared-memory fit)
@@ -76,24 +79,27 @@ __device__ __forceinline__ long long ct_now() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// (pair = row * nchunk + chunk, 128-sample tile) of consecutive jobs, advanced
+// (side, row, chunk group, 128-sample tile) of consecutive jobs, advanced
 // incrementally (64-bit division costs hundreds of cycles in the issue loops)
 struct JobCursor {
-  int pair, jt, l, c;
-  __device__ __forceinline__ void init(int64_t j, int64_t ntl, int nchunk) {
-    pair = (int)(j / ntl);
+  int jt, l, c, side;
+  __device__ __forceinline__ void init(int64_t j, int64_t ntl, int ngroup, int L) {
+    const int pair = (int)(j / ntl);
     jt = (int)(j % ntl);
-    l = pair / nchunk;
-    c = pair % nchunk;
+    c = pair % ngroup;
+    l = (pair / ngroup) % L;
+    side = pair / ngroup / L;
   }
-  // returns true when the next job starts a new (row, chunk) pair
-  __device__ __forceinline__ bool next(int ntl, int nchunk) {
+  // returns true when the next job starts a new (side, row, group)
+  __device__ __forceinline__ bool next(int ntl, int ngroup, int L) {
     if (++jt < ntl) return false;
     jt = 0;
-    ++pair;
-    if (++c == nchunk) {
+    if (++c == ngroup) {
       c = 0;
-      ++l;
+      if (++l == L) {
+        l = 0;
+        ++side;
+      }
     }
     return true;
   }
@@ -137,7 +143,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
       bar_ef[CT_STAGES], bar_ee[CT_STAGES];
   __shared__ uint32_t tbase;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  const int64_t J = (int64_t)a.L * a.ngroup * a.ntl;
+  const int64_t J = (int64_t)a.nside * a.L * a.ngroup * a.ntl;
   const int64_t j0 = (int64_t)blockIdx.x * J / gridDim.x;
   const int64_t j1 = (int64_t)(blockIdx.x + 1) * J / gridDim.x;
   const int64_t wbytes = (a.tile_bytes + 1023) / 1024 * 1024;
@@ -172,11 +178,11 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
     if (lane == 0) {
       const int ntl = (int)a.ntl;
       JobCursor cur;
-      cur.init(j0, a.ntl, a.ngroup);
+      cur.init(j0, a.ntl, a.ngroup, a.L);
       bool fresh = true;
       int q = -1, it = 0, s = 0, ph = 0;
       for (int64_t j = j0; j < j1; ++j, ++it) {
-        const int jt = cur.jt, l = cur.l;
+        const int jt = cur.jt, l = cur.l, sd = cur.side;
         if (fresh) {
           // the group's chunks are consecutive images: one copy
           ++q;
@@ -184,14 +190,14 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
           const int gc = min(a.G, a.nchunk - cur.c * a.G);
           const uint32_t bytes = (uint32_t)(gc * a.tile_bytes);
           tc::mbar_arrive_expect_tx(&bar_wf, bytes);
-          tc::bulk_g2s(wsm, a.tiles + ((int64_t)l * a.nchunk + cur.c * a.G) * a.tile_bytes, bytes,
+          tc::bulk_g2s(wsm, a.tiles[sd] + ((int64_t)l * a.nchunk + cur.c * a.G) * a.tile_bytes, bytes,
                        &bar_wf);
         }
         tc::mbar_wait(&bar_ae[s], ph ^ 1);
         CT_TRACE(0, it);
         tc::mbar_arrive_expect_tx(&bar_af[s], abytes);
         tc::bulk_g2s(abuf + (int64_t)s * abytes,
-                     (const uint8_t *)a.a_ops + l * a.a_row_stride + (int64_t)jt * abytes, abytes,
+                     (const uint8_t *)a.a_ops[sd] + l * a.a_row_stride + (int64_t)jt * abytes, abytes,
                      &bar_af[s]);
         if (++s == a.stages) {
           s = 0;
@@ -201,9 +207,9 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
         const int se = it % a.se, eph = (it / a.se) & 1;
         tc::mbar_wait(&bar_ee[se], eph ^ 1);
         tc::mbar_arrive_expect_tx(&bar_ef[se], ebytes);
-        tc::bulk_g2s(ebuf + se * 4 * K * EV_ROW, a.e1 + ev_idx(l, (int64_t)jt * 128, 0, ws.bc, K),
+        tc::bulk_g2s(ebuf + se * 4 * K * EV_ROW, a.e1[sd] + ev_idx(l, (int64_t)jt * 128, 0, ws.bc, K),
                      ebytes, &bar_ef[se]);
-        fresh = cur.next(ntl, a.ngroup);
+        fresh = cur.next(ntl, a.ngroup, a.L);
       }
     }
   } else if (w == 1) {
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
     const int ntl = (int)a.ntl;
     const uint32_t w_units = (uint32_t)(wbytes >> 4);
     JobCursor cur;
-    cur.init(j0, a.ntl, a.ngroup);
+    cur.init(j0, a.ntl, a.ngroup, a.L);
     int q = 0, it = 0, s = 0, ph = 0, acc_n = 0;
     if (j0 < j1) tc::mbar_wait(&bar_wf, 0);
     for (int64_t j = j0; j < j1; ++j, ++it) {
@@ -262,7 +268,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
         s = 0;
         ph ^= 1;
       }
-      if (cur.next(ntl, a.ngroup) && j + 1 < j1) tc::mbar_wait(&bar_wf, (++q) & 1);
+      if (cur.next(ntl, a.ngroup, a.L) && j + 1 < j1) tc::mbar_wait(&bar_wf, (++q) & 1);
     }
   } else {
     // ---- epilogue: one sample per thread. The two warps of a lane quarter
@@ -281,14 +287,15 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
     float sv_next[NSV];
     const int ntl = (int)a.ntl;
     JobCursor cur, nxt;
-    cur.init(j0, a.ntl, a.ngroup);
+    cur.init(j0, a.ntl, a.ngroup, a.L);
     nxt = cur;
     auto load_next = [&](int64_t j) {
       if (FWD || j >= j1) return;
       const int l = nxt.l, g = nxt.c;
+      const float *svs = a.sv[nxt.side];
       const int64_t b = min((int64_t)nxt.jt * 128 + r, a.B - 1);
       if (a.direct) {
-        sv_next[0] = a.sv[tb_idx(l, b, 0, ws.bc, a.sv_w)];
+        sv_next[0] = svs[tb_idx(l, b, 0, ws.bc, a.sv_w)];
         return;
       }
       const int gc = min(a.G, a.nchunk - g * a.G);
@@ -297,17 +304,17 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
         if (c >= gc) break;
         const int chunk = g * a.G + c;
         const int nol = min(a.og, a.n_out - chunk * a.og);
-        const float *svp = a.sv + ev_idx(l, b, chunk * a.og, ws.bc, K);
+        const float *svp = svs + ev_idx(l, b, chunk * a.og, ws.bc, K);
 #pragma unroll
         for (int u = 0; u < NPW; ++u)
           if (half + 2 * u < nol) sv_next[c * NPW + u] = svp[(half + 2 * u) * EV_ROW];
       }
     };
     load_next(j0);
-    nxt.next(ntl, a.ngroup);
+    nxt.next(ntl, a.ngroup, a.L);
     int it = 0, acc_n = 0;
     for (int64_t j = j0; j < j1; ++j, ++it) {
-      const int l = cur.l, g = cur.c;
+      const int l = cur.l, g = cur.c, sd = cur.side;
       const int gc = min(a.G, a.nchunk - g * a.G);
       const int64_t b = (int64_t)cur.jt * 128 + r;
       const bool live = b < a.B;
@@ -316,8 +323,8 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
 #pragma unroll
       for (int u = 0; u < NSV; ++u) sv[u] = sv_next[u];
       load_next(j + 1);
-      nxt.next(ntl, a.ngroup);
-      cur.next(ntl, a.ngroup);
+      nxt.next(ntl, a.ngroup, a.L);
+      cur.next(ntl, a.ngroup, a.L);
       const int se = it % a.se, eph = (it / a.se) & 1;
       if (w == 2 && lane == 0) CT_TRACE(6, it);
       tc::mbar_wait(&bar_ef[se], eph);
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_ee[se]);
       if (w == 2 && lane == 0) CT_TRACE(3, it);
-      float *out = (FWD ? ws.off : ws.slots) + tb_idx(a.dst[l], bs, 0, ws.bc, ws.ks);
+      float *out = (FWD ? ws.off : ws.slots) + tb_idx(a.dst[sd][l], bs, 0, ws.bc, ws.ks);
 #pragma unroll 1
       for (int c = 0; c < gc; ++c, ++acc_n) {
         const int chunk = g * a.G + c;
@@ -433,7 +440,7 @@ static int contract_t(Plan &p, ContractArgs &a, const WsView &w, cudaStream_t st
                          (int)smem);
     attr = smem;
   }
-  const int64_t J = (int64_t)a.L * a.ngroup * a.ntl;
+  const int64_t J = (int64_t)a.nside * a.L * a.ngroup * a.ntl;
   const int grid = (int)std::min<int64_t>(J, p.num_sms);
   static long long *trace_buf = nullptr;
   a.trace = nullptr;
@@ -463,13 +470,17 @@ int launch_contract_big(Plan &p, const LayerPlan &L, int mode, const uint8_t *co
                         const float *EA, const float *EB, const WsView &w, int64_t B,
                         cudaStream_t st);
 
-// mode 0: forward, 1: left child responsibilities, 2: right
+// mode 0: forward, 1: left child responsibilities, 2: right, 3: both sides in one launch
 int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *compute,
                        const float *EA, const float *EB, const WsView &w, int64_t B,
                        cudaStream_t st) {
   ContractArgs a;
   const int K = p.k;
-  if (K > 64) return launch_contract_big(p, L, mode, compute, EA, EB, w, B, st);
+  if (K > 64) {
+    if (mode != 3) return launch_contract_big(p, L, mode, compute, EA, EB, w, B, st);
+    const int rc = launch_contract_big(p, L, 1, compute, EA, EB, w, B, st);
+    return rc ? rc : launch_contract_big(p, L, 2, compute, EA, EB, w, B, st);
+  }
   a.B = B;
   a.ntl = (B + 127) / 128;
   a.L = L.rows;
@@ -479,47 +490,60 @@ int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *com
     const char *env = getenv("EINET_CT_DEBUG");
     a.debug = env ? atoi(env) : 0;
   }
-  if (mode != 0 && L.direct) {
-    a.direct = 1;
-    a.a_ops = (mode == 1 ? w.ebm : w.eam) + (int64_t)L.erow_base * w.bc * p.kp;
-    a.a_row_stride = w.bc * p.kp * 4;
-    a.ka = p.kp;
-    a.e1 = mode == 1 ? EA : EB;
-    a.sv = w.rt;
-    a.sv_w = w.ks;
-    a.tiles = compute + (mode == 1 ? L.fw_off : L.vw_off);
-    a.tile_bytes = mode == 1 ? L.fw_tile : L.rw_tile;
-    a.nchunk = 1;
-    a.og = K;
-    a.rows_tile = mode == 1 ? L.fw_rows : L.rw_rows;
-    a.n_out = K;
-    a.dst = mode == 1 ? L.d_slot_left : L.d_slot_right;
-  } else if (mode == 0) {
-    a.a_ops = w.ebm + (int64_t)L.erow_base * w.bc * p.kp;
-    a.a_row_stride = w.bc * p.kp * 4;
-    a.ka = p.kp;
-    a.e1 = EA;
-    a.sv = nullptr;
-    a.tiles = compute + L.fw_off;
-    a.tile_bytes = L.fw_tile;
-    a.nchunk = L.ng;
-    a.og = L.kg;
-    a.rows_tile = L.fw_rows;
-    a.n_out = L.k_out;
-    a.dst = L.d_out_slab;
-  } else {
-    a.a_ops = w.rtm;
-    a.a_row_stride = w.bc * L.kob * 4;
-    a.ka = L.kob;
-    a.e1 = mode == 1 ? EB : EA;
-    a.sv = mode == 1 ? EA : EB;
-    a.tiles = compute + (mode == 1 ? L.uw_off : L.vw_off);
-    a.tile_bytes = L.uw_tile;
-    a.nchunk = L.ni;
-    a.og = L.ig;
-    a.rows_tile = L.uw_rows;
-    a.n_out = K;
-    a.dst = mode == 1 ? L.d_slot_left : L.d_slot_right;
+  // mode 3: both child-responsibility sides (left = side 0, right = side 1)
+  a.nside = mode == 3 ? 2 : 1;
+  const int m0 = mode == 3 ? 1 : mode;
+  for (int sd = 0; sd < a.nside; ++sd) {
+    const int md = m0 + sd;  // 0 forward, 1 left, 2 right
+    if (md != 0 && L.direct) {
+      a.direct = 1;
+      a.a_ops[sd] = (md == 1 ? w.ebm : w.eam) + (int64_t)L.erow_base * w.bc * p.kp;
+      a.a_row_stride = w.bc * p.kp * 4;
+      a.ka = p.kp;
+      a.e1[sd] = md == 1 ? EA : EB;
+      a.sv[sd] = w.rt;
+      a.sv_w = w.ks;
+      a.tiles[sd] = compute + (md == 1 ? L.fw_off : L.vw_off);
+      a.tile_bytes = md == 1 ? L.fw_tile : L.rw_tile;  // equal: fw_rows == rw_rows at K_out = 1
+      a.nchunk = 1;
+      a.og = K;
+      a.rows_tile = md == 1 ? L.fw_rows : L.rw_rows;
+      a.n_out = K;
+      a.dst[sd] = md == 1 ? L.d_slot_left : L.d_slot_right;
+    } else if (md == 0) {
+      a.a_ops[sd] = w.ebm + (int64_t)L.erow_base * w.bc * p.kp;
+      a.a_row_stride = w.bc * p.kp * 4;
+      a.ka = p.kp;
+      a.e1[sd] = EA;
+      a.sv[sd] = nullptr;
+      a.tiles[sd] = compute + L.fw_off;
+      a.tile_bytes = L.fw_tile;
+      a.nchunk = L.ng;
+      a.og = L.kg;
+      a.rows_tile = L.fw_rows;
+      a.n_out = L.k_out;
+      a.dst[sd] = L.d_out_slab;
+    } else {
+      a.a_ops[sd] = w.rtm;
+      a.a_row_stride = w.bc * L.kob * 4;
+      a.ka = L.kob;
+      a.e1[sd] = md == 1 ? EB : EA;
+      a.sv[sd] = md == 1 ? EA : EB;
+      a.tiles[sd] = compute + (md == 1 ? L.uw_off : L.vw_off);
+      a.tile_bytes = L.uw_tile;
+      a.nchunk = L.ni;
+      a.og = L.ig;
+      a.rows_tile = L.uw_rows;
+      a.n_out = K;
+      a.dst[sd] = md == 1 ? L.d_slot_left : L.d_slot_right;
+    }
+  }
+  if (a.nside == 1) {
+    a.a_ops[1] = a.a_ops[0];
+    a.e1[1] = a.e1[0];
+    a.sv[1] = a.sv[0];
+    a.tiles[1] = a.tiles[0];
+    a.dst[1] = a.dst[0];
   }
   switch (K) {
     case 8: return mode == 0 ? contract_t<8, true>(p, a, w, st) : contract_t<8, false>(p, a, w, st);

@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(128) k_mixing_fwd(
       }
     }
     if (wid == 0 && blockIdx.z == 0) slab_shift(ws, os)[b] = sh;
+#pragma unroll 4
     for (int k = wid + 4 * blockIdx.z; k < Ko; k += 4 * gridDim.z) {
       const int e = k * 32 + lane;
       if (sh == -CUDART_INF) {
@@ -996,12 +997,20 @@ __global__ void __launch_bounds__(1024) k_ll_sum(WsView ws, int slab, int64_t B,
                                                  double count) {
   EINET_KERNEL_PROLOGUE();
   __shared__ double red[32];
-  double v = 0.0;
   const double *sh = slab_shift(ws, slab);
-  for (int64_t b = threadIdx.x; b < B; b += 1024) {
-    const double s = sh[b];
-    v += s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[0];
+  // four independent strided runs (loads in flight), combined in a fixed order
+  double v4[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t b0 = threadIdx.x; b0 < B; b0 += 4096) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t b = b0 + 1024 * u;
+      if (b < B) {
+        const double s = sh[b];
+        v4[u] += s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[0];
+      }
+    }
   }
+  double v = (v4[0] + v4[1]) + (v4[2] + v4[3]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
@@ -1233,8 +1242,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
     {
       ProfScope prof(prof_layer_name("einsum_childrho", L.index), st);
       if (p.use_tc && L.tc) {
-        int rc = launch_contract_tc(p, L, 1, compute, EA, EB, w, B, st);
-        if (!rc) rc = launch_contract_tc(p, L, 2, compute, EA, EB, w, B, st);
+        int rc = launch_contract_tc(p, L, 3, compute, EA, EB, w, B, st);
         if (rc) return rc;
       } else {
         einsum_childrho_simt(L, c.w32, EA, EB, w, B, K, st);
