@@ -536,9 +536,9 @@ def run_ours(args):
         top = "einsum_contraction (k_contract_tc: einsum_fwd + einsum_childrho)"
         tw = {"flops": sum(work[n]["flops"] for n in ct), "bytes": 0, "tc": True}
         t_step = sum(prof[n][0] for n in ct) / prof_steps
-        launches = sum(prof[n][1] for n in ct) / prof_steps
-        per_launch_ms = t_step / launches
-        groups = launches
+        ct_launches = sum(prof[n][1] for n in ct) / prof_steps
+        per_launch_ms = t_step / ct_launches
+        groups = ct_launches
         traffic_key = "einsum_fwd"
     else:
         top = largest

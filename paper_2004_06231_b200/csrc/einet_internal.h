@@ -206,6 +206,7 @@ struct CompView;
 struct WsView;
 int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_t *mask,
                    const double *leaf_offset, cudaStream_t st);
+int launch_prepare_leaves(Plan &p, const double *params, uint8_t *compute, cudaStream_t st);
 int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B,
                    uint8_t *ws, double *root_out, int32_t *status, cudaStream_t st);
 int launch_backward(Plan &p, const double *params, const uint8_t *compute, const float *x,

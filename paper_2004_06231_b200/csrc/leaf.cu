@@ -197,6 +197,32 @@ int launch_prepare(Plan &p, const double *params, uint8_t *compute, const uint8_
   return check_cuda(cudaGetLastError(), "prepare kernels");
 }
 
+// Leaf compute tensors only (categorical / binomial families after the
+// M-step): the einsum and mixing compute copies are written by the M-step
+// kernels themselves, and the training compute is unmasked (c.active stays
+// all ones), so only the per-(d, k, r) leaf terms and the per-leaf constants
+// are re-derived.
+int launch_prepare_leaves(Plan &p, const double *params, uint8_t *compute, cudaStream_t st) {
+  CompView c = comp_view(p, compute);
+  const int D = p.d_vars, K = p.k, R = p.num_replicas;
+  const double *phi = params + p.sizes.phi_offset;
+  auto grid_for = [](int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 4096); };
+  const int64_t rdk = (int64_t)R * D * K;
+  if (p.family == EINET_FAMILY_CATEGORICAL) {
+    launch_k(k_prepare_cat, grid_for(rdk * p.num_states), 256, 0, st, phi, c.active,
+             (double *)c.leafp, D, K, R, p.num_states);
+  } else if (p.family == EINET_FAMILY_BINOMIAL) {
+    launch_k(k_prepare_binom, grid_for(rdk), 256, 0, st, phi, c.active, (double2 *)c.leafp, D, K,
+             R, p.n_trials);
+  } else {
+    return fail(EINET_ERR_USAGE, "launch_prepare_leaves: categorical / binomial only");
+  }
+  launch_k(k_prepare_const, dim3(p.n_leaf, K), 256, 0, st, phi, c.active, (const double *)nullptr,
+           p.d_scope_off, p.d_scope_vars, p.d_leaf_rep, c.cnst, D, K, R, p.family);
+  count_launch(2);
+  return check_cuda(cudaGetLastError(), "prepare leaves");
+}
+
 // ---------------------------------------------------------------------------
 // leaf forward
 // ---------------------------------------------------------------------------
@@ -805,7 +831,10 @@ __global__ void __launch_bounds__(256) k_leaf_stats_discrete(
   const int64_t per = (B + lsplit - 1) / lsplit;
   const int64_t bb = split * per, be = min(B, bb + per);
   const int64_t n_ent = (int64_t)nv * K * T;
-  for (int64_t e = threadIdx.x; e < n_ent; e += blockDim.x) {
+  // one warp per (variable, k, t) entry; lanes stride over the samples (fp32
+  // runs of <= LS_BT samples folded into fp64), then a fixed shuffle tree
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t e = wid; e < n_ent; e += blockDim.x >> 5) {
     const int t = (int)(e % T);
     const int k = (int)((e / T) % K);
     const int v = (int)(e / ((int64_t)T * K));
@@ -814,7 +843,8 @@ __global__ void __launch_bounds__(256) k_leaf_stats_discrete(
     if (active[d]) {
       float run = 0.f;
       int cnt = 0;
-      for (int64_t b = bb; b < be; ++b) {
+#pragma unroll 4
+      for (int64_t b = bb + lane; b < be; b += 32) {
         const float xv = x[b * D + d];
         const float rr = rho_all[tb_idx(leaf, b, k, Bc, K)];
         if (family == EINET_FAMILY_CATEGORICAL)
@@ -829,7 +859,9 @@ __global__ void __launch_bounds__(256) k_leaf_stats_discrete(
       }
       tot += (double)run;
     }
-    lspart[(int64_t)split * n_phi + ((((int64_t)d * K + k) * R + r) * T + t)] = tot;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_down_sync(0xffffffffu, tot, o);
+    if (lane == 0) lspart[(int64_t)split * n_phi + ((((int64_t)d * K + k) * R + r) * T + t)] = tot;
   }
 }
 

@@ -379,6 +379,10 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
   // tensor of the cached, unmasked training compute (tensor-core weight images
   // for tc-capable layers, DMMA leaf image), replacing launch_prepare
   const bool fused = p.family == EINET_FAMILY_GAUSSIAN && p.k <= 64;
+  // categorical / binomial leaves: the weight and mixing compute copies (and
+  // tensor-core images) come from the M-step kernels as in the fused path;
+  // only the leaf terms are re-derived afterwards (launch_prepare_leaves)
+  const bool fused_w = fused || p.family != EINET_FAMILY_GAUSSIAN;
   // The fused leaf branch (Gaussian) is independent of the weight updates:
   // it runs on the fork stream beside them (two branches of the CUDA graph).
   cudaStream_t ls = st;
@@ -406,7 +410,7 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
   if (p.n_w) {
     const int nslices = (int)(p.n_w / KK);
     launch_k(k_mstep_einsum, nslices, 256, 0, st, params, c.w32, stats, K, lam, eps_w, status,
-                                            fused ? p.d_tiledesc : nullptr,
+                                            fused_w ? p.d_tiledesc : nullptr,
                                             p.n_tiledesc, compute, p.kp);
     count_launch();
   }
@@ -432,6 +436,7 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
   count_launch();
   int rc = check_cuda(cudaGetLastError(), "mstep kernels");
   if (rc) return rc;
+  if (fused_w) return launch_prepare_leaves(p, params, compute, st);
   return launch_prepare(p, params, compute, nullptr, nullptr, st);
 }
 
