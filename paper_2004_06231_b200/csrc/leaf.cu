@@ -502,7 +502,10 @@ __global__ void k_leaf_check(const float *__restrict__ x, int64_t B, int D,
 
 static int leaf_dsplit(const Plan &p, int64_t B, int tb, int64_t slots, int nkc) {
   const int64_t blocks = (int64_t)ceil_div(B, tb) * p.n_leaf * nkc;
-  const int cap = std::max(1, std::min(kMaxDSplit, ceil_div(p.max_scope, 4 * LF_VC)));
+  // at least four 32-variable chunks per split, unless the grid would not
+  // fill a wave (small batches): then down to one chunk per split
+  const int min_chunks = blocks * ceil_div(p.max_scope, 4 * LF_VC) < slots ? 1 : 4;
+  const int cap = std::max(1, std::min(kMaxDSplit, ceil_div(p.max_scope, min_chunks * LF_VC)));
   return pick_split(blocks, slots, 1, cap);
 }
 
