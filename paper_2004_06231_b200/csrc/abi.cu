@@ -480,7 +480,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
                              4 * leaf_stats_slots(*p, Bc) * p->n_phi));
   p->w_ppart = seg(8 * (int64_t)ceil_div(Bc, 32) * p->n_leaf * K);
   p->w_mixpart = seg(8 * (int64_t)ceil_div(Bc, 32) * std::max<int64_t>(p->n_mix, 1));
-  p->w_llpart = seg(8 * (int64_t)ceil_div(Bc, 256));
+  p->w_llpart = seg(8 * ((int64_t)ceil_div(Bc, 256) + 1));  // partials + ticket
   p->w_tmp_s = seg(8 * p->n_phi);
   p->w_tmp_p = seg(8 * (int64_t)p->n_leaf * K);
   {

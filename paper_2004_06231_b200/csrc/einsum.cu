@@ -981,9 +981,11 @@ __global__ void __launch_bounds__(256) k_einsum_childrho_big(
 // root outputs and the log-likelihood sum
 // ---------------------------------------------------------------------------
 
-__global__ void k_root_out(WsView ws, int slab, int64_t B, int kr, double *out) {
+__global__ void k_root_out(WsView ws, int slab, int64_t B, int kr, double *out,
+                           unsigned *ll_ticket) {
   EINET_KERNEL_PROLOGUE();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e == 0) *ll_ticket = 0u;  // k_ll_sum's completion counter
   if (e >= B * kr) return;
   const int64_t b = e / kr;
   const int k = (int)(e % kr);
@@ -991,38 +993,42 @@ __global__ void k_root_out(WsView ws, int slab, int64_t B, int kr, double *out) 
   out[e] = s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[k];
 }
 
-// Sum of the batch's root log-likelihoods into stats (ll, count): one CTA,
-// fixed summation order (strided fp64 runs, then warp and CTA trees).
-__global__ void __launch_bounds__(1024) k_ll_sum(WsView ws, int slab, int64_t B, double *ll,
-                                                 double count) {
+// Sum of the batch's root log-likelihoods into stats (ll, count): one CTA per
+// 256 samples writes a fixed-order partial (strided warp runs, shuffle tree,
+// warp order); the last CTA to finish (ticket counter, zeroed by k_root_out in
+// the forward pass and reset here) adds the partials in index order, so the
+// sum is deterministic whichever CTA finishes last.
+__global__ void __launch_bounds__(256) k_ll_sum(WsView ws, int slab, int64_t B, double *ll,
+                                                double count, double *part, unsigned *ticket) {
   EINET_KERNEL_PROLOGUE();
-  __shared__ double red[32];
+  __shared__ double red[8];
+  __shared__ bool last;
   const double *sh = slab_shift(ws, slab);
-  // four independent strided runs (loads in flight), combined in a fixed order
-  double v4[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t b0 = threadIdx.x; b0 < B; b0 += 4096) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t b = b0 + 1024 * u;
-      if (b < B) {
-        const double s = sh[b];
-        v4[u] += s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[0];
-      }
-    }
+  const int64_t b = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  double v = 0.0;
+  if (b < B) {
+    const double s = sh[b];
+    v = s == -CUDART_INF ? -CUDART_INF : s + (double)slab_off(ws, slab, b)[0];
   }
-  double v = (v4[0] + v4[1]) + (v4[2] + v4[3]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    v = red[threadIdx.x];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) {
-      ll[0] += v;
-      ll[1] += count;
-    }
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double t = 0.0;
+    for (unsigned q = 0; q < gridDim.x; ++q) t += ((volatile double *)part)[q];
+    ll[0] += t;
+    ll[1] += count;
+    *ticket = 0u;
   }
 }
 
@@ -1159,7 +1165,8 @@ int launch_forward(Plan &p, const uint8_t *compute, const float *x, int64_t B, u
     }
   }
   const int64_t n = B * p.k_root;
-  launch_k(k_root_out, ceil_div(n, 256), 256, 0, st, w, p.root_out_slab, B, p.k_root, root_out);
+  launch_k(k_root_out, ceil_div(n, 256), 256, 0, st, w, p.root_out_slab, B, p.k_root, root_out,
+           (unsigned *)(wsb + p.w_llpart) + 2 * ceil_div(w.bc, 256));
   count_launch();
   return check_cuda(cudaGetLastError(), "forward kernels");
 }
@@ -1180,8 +1187,10 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   // log-likelihood sum of the batch (root entry 0) and the sample count
   {
     ProfScope prof("ll_sum", st);
-    launch_k(k_ll_sum, 1, 1024, 0, st, w, p.root_out_slab, B, stats + p.sizes.stats_ll_offset,
-                                  (double)B);
+    double *part = (double *)(wsb + p.w_llpart);
+    launch_k(k_ll_sum, ceil_div(B, 256), 256, 0, st, w, p.root_out_slab, B,
+             stats + p.sizes.stats_ll_offset, (double)B, part,
+             (unsigned *)part + 2 * ceil_div(w.bc, 256));
     count_launch();
   }
   for (int li = (int)p.layers.size() - 1; li >= 0; --li) {
