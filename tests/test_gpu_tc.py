@@ -62,7 +62,7 @@ def _run(circuit, fam, x, op, tc):
     return tr.log_likelihood, st
 
 
-@pytest.mark.parametrize("k", [8, 10, 16, 20, 24, 32, 40, 48, 64])
+@pytest.mark.parametrize("k", [8, 10, 16, 20, 24, 32, 40, 48, 64, 96, 128])
 def test_tensor_core_einsum_matches_simt_and_oracle(k):
     circuit, fam, x, op = _pd_model(k, seed=k)
     assert any(getattr(L, "k_out", 0) for L in circuit.layers[1:])
