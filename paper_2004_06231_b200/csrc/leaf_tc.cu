@@ -184,18 +184,21 @@ __global__ void __launch_bounds__(LS_THREADS, 1) k_leaf_stats_tc(LeafStatsArgs a
           const uint64_t bl = bh + lo_units;
           const uint32_t acc0 = (first && sb == 0) ? 0u : 1u;
           const uint32_t ah0 = tm + 128 + (uint32_t)(as * 128);
+          // 3xTF32 per K-step (hi*hi, hi*lo, lo*hi), the two tiles' MMAs
+          // alternating so consecutive instructions accumulate into different
+          // TMEM accumulators (a chain into one accumulator stalls at N = K:
+          // profiles/r02_probes.md)
 #pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            const uint32_t d = tm + (uint32_t)(g * nn), ah = ah0 + g * 64;
-            tc::mma_tf32_ts(d, ah, bh, id, acc0);
-            tc::mma_tf32_ts(d, ah, bl, id, 1u);
-            tc::mma_tf32_ts(d, ah + 32, bh, id, 1u);
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t kh = bh + ks * kstep_units, kl = bl + ks * kstep_units;
 #pragma unroll
-            for (int ks = 1; ks < 4; ++ks) {
-              const uint64_t kh = bh + ks * kstep_units, kl = bl + ks * kstep_units;
-              tc::mma_tf32_ts(d, ah + 8 * ks, kh, id, 1u);
-              tc::mma_tf32_ts(d, ah + 8 * ks, kl, id, 1u);
-              tc::mma_tf32_ts(d, ah + 32 + 8 * ks, kh, id, 1u);
+            for (int term = 0; term < 3; ++term) {
+#pragma unroll
+              for (int g = 0; g < 2; ++g) {
+                const uint32_t d = tm + (uint32_t)(g * nn), ah = ah0 + g * 64;
+                tc::mma_tf32_ts(d, ah + (term == 2 ? 32 : 0) + 8 * ks, term == 1 ? kl : kh, id,
+                                (ks == 0 && term == 0) ? acc0 : 1u);
+              }
             }
           }
           tc::mma_commit(&a_empty[as]);
