@@ -99,3 +99,24 @@ def test_tensor_core_em_step_matches_oracle():
     for i in m2:
         close(m2[i], op.mixing[i], 1e-4, 1e-9)
     close(phi2, op.phi, 1e-4, 1e-6)
+
+
+@pytest.mark.parametrize("k,chunk", [(20, 96), (40, 128), (128, 100)])
+def test_tensor_core_chunked_em_step_matches_oracle(k, chunk):
+    """Chunked accumulation (trainer.py:57-66) on the tcgen05 paths -- K = 20
+    (padded MMA K dimension), 40, 128 (tile-stationary large-K contraction) --
+    with a ragged last chunk: one EM step against the oracle's unchunked step."""
+    circuit, fam, x, op = _pd_model(k, seed=k + 1)
+    eng = engine.get_engine(circuit, fam, len(x))
+    eng.set_tensor_cores(True)
+    model = E.EinetModel(circuit, engine.Parameters.from_numpy(circuit, fam, op.einsum,
+                                                               op.mixing, op.phi), fam)
+    want_ll, op2 = O.em_step(circuit, op, fam.to_dict(), x, 0.5)
+    ll = trainer.em_stochastic_step(model, x, 0.5, chunk=chunk)
+    assert abs(ll - want_ll) <= 1e-4 * abs(want_ll)
+    e2, m2, phi2 = model.params.to_numpy()
+    for i in e2:
+        close(e2[i], op2.einsum[i], 1e-4, 1e-9)
+    for i in m2:
+        close(m2[i], op2.mixing[i], 1e-4, 1e-9)
+    close(phi2, op2.phi, 1e-4, 1e-6)
