@@ -169,6 +169,13 @@ static void free_plan_memory(Plan *p) {
   if (p->fork_ev) cudaEventDestroy(p->fork_ev);
   if (p->join_ev) cudaEventDestroy(p->join_ev);
   p->fork_ev = p->join_ev = nullptr;
+  if (p->red_stream) cudaStreamDestroy(p->red_stream);
+  p->red_stream = nullptr;
+  for (int i = 0; i < 2; ++i) {
+    if (p->red_fork[i]) cudaEventDestroy(p->red_fork[i]);
+    if (p->red_done[i]) cudaEventDestroy(p->red_done[i]);
+    p->red_fork[i] = p->red_done[i] = nullptr;
+  }
   f(p->d_i8_col);
   f(p->d_i8_grp);
   f(p->d_scope_pos);
@@ -473,7 +480,8 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
     int64_t tc_slots = L.tc ? wstats_tc_slots(*p, L, Bc) : 0;
     wpart = std::max(wpart, std::max(bs * lw, (tc_slots * lw + 1) / 2));
   }
-  p->w_wpart = seg(8 * std::max<int64_t>(wpart, 1));
+  p->wpart_half = align_up(std::max<int64_t>(wpart, 1), 32);
+  p->w_wpart = seg(8 * 2 * p->wpart_half);  // two halves: layer parity
   p->w_rho = seg(4 * (int64_t)p->n_leaf * Bc * K);
   p->max_lsplit = leaf_lsplit(*p, Bc);
   p->w_lspart = seg(std::max(8 * (int64_t)p->max_lsplit * p->n_phi,
@@ -527,8 +535,14 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   if ((rc = check_cuda(cudaStreamCreateWithFlags(&p->fork_stream, cudaStreamNonBlocking),
                        "fork stream")) ||
       (rc = check_cuda(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming), "event")) ||
-      (rc = check_cuda(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming), "event")))
+      (rc = check_cuda(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming), "event")) ||
+      (rc = check_cuda(cudaStreamCreateWithFlags(&p->red_stream, cudaStreamNonBlocking),
+                       "reduction stream")))
     return rc;
+  for (int i = 0; i < 2; ++i)
+    if ((rc = check_cuda(cudaEventCreateWithFlags(&p->red_fork[i], cudaEventDisableTiming), "event")) ||
+        (rc = check_cuda(cudaEventCreateWithFlags(&p->red_done[i], cudaEventDisableTiming), "event")))
+      return rc;
   {
     std::vector<int> pos((size_t)R * D, -1);
     for (int l = 0; l < d->n_leaf; ++l)

@@ -116,6 +116,11 @@ struct Plan {
   cudaStream_t side_stream = nullptr;  // captures the fallback body of a conditional node
   cudaStream_t fork_stream = nullptr;  // M-step: leaf branch beside the einsum weights
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // back-pass: the W-statistics batch reductions run on red_stream beside
+  // the next layer's kernels (double-buffered partials, w_wpart halves)
+  cudaStream_t red_stream = nullptr;
+  cudaEvent_t red_fork[2] = {nullptr, nullptr}, red_done[2] = {nullptr, nullptr};
+  int64_t wpart_half = 0;          // doubles per partial buffer half
   // fused M-step (mstep.cu): per-einsum-layer tile geometry, temp leaf terms
   int64_t *d_tiledesc = nullptr;   // einsum layers x TD_WORDS (mstep.cu)
   int n_tiledesc = 0;
@@ -229,7 +234,8 @@ int launch_status_from_stats(const double *flag, int32_t *status, cudaStream_t s
 void plan_tc_tiling(Plan &p);
 int64_t wstats_tc_slots(const Plan &p, const LayerPlan &L, int64_t B);
 int launch_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *EB, WsView &w,
-                     int64_t B, const double *Wl, double *stats, cudaStream_t st);
+                     int64_t B, const double *Wl, double *stats, cudaStream_t st,
+                     cudaStream_t rst = nullptr, cudaEvent_t fork = nullptr);
 int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_prepare_leaf_dmma(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_prepare_leaf_i8(Plan &p, uint8_t *compute, cudaStream_t st);

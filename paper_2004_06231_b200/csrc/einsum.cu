@@ -1184,6 +1184,8 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   CompView c = comp_view(p, compute);
   WsView w = ws_view(p, wsb);
   const int K = p.k;
+  int eo = 0, rc = 0;
+  bool red_pending[2] = {false, false};
   // log-likelihood sum of the batch (root entry 0) and the sample count
   {
     ProfScope prof("ll_sum", st);
@@ -1219,6 +1221,21 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
                                           tcl ? w.rtb : nullptr, L.nn);
     }
     const int64_t lw = (int64_t)L.rows * L.k_out * K * K;
+    // W-statistics partials alternate between the two halves of w_wpart by
+    // einsum-layer parity; each layer's batch reduction runs on the
+    // reduction stream (rs) beside the next layers' kernels, and the layer two
+    // steps later waits for it before reusing the half
+    const int par = eo++ & 1;
+    double *wpart = w.wpart + par * p.wpart_half;
+    cudaStream_t rs = p.red_stream ? p.red_stream : st;
+    if (red_pending[par] && (rc = check_cuda(cudaStreamWaitEvent(st, p.red_done[par], 0), "wstats join")))
+      return rc;
+    auto red_fork = [&](cudaStream_t r) -> int {
+      if (r == st) return 0;
+      int e = check_cuda(cudaEventRecord(p.red_fork[par], st), "wstats fork");
+      if (!e) e = check_cuda(cudaStreamWaitEvent(r, p.red_fork[par], 0), "wstats fork");
+      return e;
+    };
     {
       ProfScope prof(prof_layer_name("einsum_wstats", L.index), st);
       const int K4 = (K + 3) / 4;
@@ -1227,11 +1244,15 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
         const size_t smem = sizeof(float) * 2 * (2 * K * EV_ROW + 32);
         const int threads = std::max(128, (K4 * K4 + 31) / 32 * 32);
         launch_k(k_wstats_k1, dim3(L.rows, ns), threads, smem, st, EA, EB, w.rt, w.bc, w.ks, B, K,
-                                                             L.rows, ns, w.wpart);
-        launch_reduce_partials(stats + L.w_off, w.wpart, ns, lw, lw, params + L.w_off, st);
+                                                             L.rows, ns, wpart);
+        if ((rc = red_fork(rs))) return rc;
+        launch_reduce_partials(stats + L.w_off, wpart, ns, lw, lw, params + L.w_off, rs);
       } else if (p.use_tc && L.tc) {
-        int rc = launch_wstats_tc(p, L, EA, EB, w, B, params + L.w_off, stats + L.w_off, st);
-        if (rc) return rc;
+        WsView wv = w;
+        wv.wpart = wpart;
+        if ((rc = launch_wstats_tc(p, L, EA, EB, wv, B, params + L.w_off, stats + L.w_off, st, rs,
+                                   p.red_fork[par])))
+          return rc;
       } else {
         const int K4 = (K + 3) / 4;
         int ti_per = K4;
@@ -1243,10 +1264,15 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
         const size_t smem = sizeof(float) * (2 * WS_BT * K4 * 4 + WS_BT * kc);
         dim3 g2(L.rows * nkc, bs, ceil_div(K4, ti_per));
         launch_k(k_einsum_wstats, g2, kc * ti_per * K4, smem, st, EA, EB, w.rt, w.bc, w.ks, B, K,
-                                                            L.k_out, L.rows, bs, w.wpart, ti_per,
+                                                            L.k_out, L.rows, bs, wpart, ti_per,
                                                             kc);
-        launch_reduce_partials(stats + L.w_off, w.wpart, bs, lw, lw, params + L.w_off, st);
+        if ((rc = red_fork(rs))) return rc;
+        launch_reduce_partials(stats + L.w_off, wpart, bs, lw, lw, params + L.w_off, rs);
       }
+    }
+    if (rs != st) {
+      if ((rc = check_cuda(cudaEventRecord(p.red_done[par], rs), "wstats done"))) return rc;
+      red_pending[par] = true;
     }
     {
       ProfScope prof(prof_layer_name("einsum_childrho", L.index), st);
@@ -1259,8 +1285,11 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
     }
     count_launch(3);
   }
-  int rc = launch_leaf_backward(p, compute, x, B, wsb, stats, st);
+  rc = launch_leaf_backward(p, compute, x, B, wsb, stats, st);
   if (rc) return rc;
+  for (int q = 0; q < 2; ++q)  // join the reduction stream
+    if (red_pending[q] && (rc = check_cuda(cudaStreamWaitEvent(st, p.red_done[q], 0), "wstats join")))
+      return rc;
   return check_cuda(cudaGetLastError(), "backward kernels");
 }
 
