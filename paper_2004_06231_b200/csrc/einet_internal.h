@@ -119,7 +119,7 @@ struct Plan {
   // back-pass: the W-statistics batch reductions run on red_stream beside
   // the next layer's kernels (double-buffered partials, w_wpart halves)
   cudaStream_t red_stream = nullptr;
-  cudaEvent_t red_fork[2] = {nullptr, nullptr}, red_done[2] = {nullptr, nullptr};
+  cudaEvent_t red_fork[3] = {nullptr, nullptr, nullptr}, red_done[3] = {nullptr, nullptr, nullptr};
   int64_t wpart_half = 0;          // doubles per partial buffer half
   // fused M-step (mstep.cu): per-einsum-layer tile geometry, temp leaf terms
   int64_t *d_tiledesc = nullptr;   // einsum layers x TD_WORDS (mstep.cu)

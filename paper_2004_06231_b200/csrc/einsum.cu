@@ -1185,7 +1185,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   WsView w = ws_view(p, wsb);
   const int K = p.k;
   int eo = 0, rc = 0;
-  bool red_pending[2] = {false, false};
+  bool red_pending[3] = {false, false, false};
   // log-likelihood sum of the batch (root entry 0) and the sample count
   {
     ProfScope prof("ll_sum", st);
@@ -1205,8 +1205,20 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
                                         L.d_mix_slot, c.mix32 + L.mix_off, p.d_csr_off,
                                         p.d_csr_slot, p.d_slab_ones, B, L.k_out, L.dmax,
                                         w.mixpart, L.mix_off, p.n_mix);
+      // the mixing-weight batch reduction on the reduction stream (its
+      // partials are per layer: no reuse to guard), joined at the end
+      cudaStream_t rs = p.red_stream ? p.red_stream : st;
+      if (rs != st) {
+        if ((rc = check_cuda(cudaEventRecord(p.red_fork[2], st), "mixing fork")) ||
+            (rc = check_cuda(cudaStreamWaitEvent(rs, p.red_fork[2], 0), "mixing fork")))
+          return rc;
+      }
       launch_reduce_partials(stats + p.n_w + L.mix_off, w.mixpart + L.mix_off, nb,
-                             (int64_t)L.rows * L.dmax, p.n_mix, nullptr, st);
+                             (int64_t)L.rows * L.dmax, p.n_mix, nullptr, rs);
+      if (rs != st) {
+        if ((rc = check_cuda(cudaEventRecord(p.red_done[2], rs), "mixing done"))) return rc;
+        red_pending[2] = true;
+      }
       count_launch();
       continue;
     }
@@ -1287,7 +1299,7 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   }
   rc = launch_leaf_backward(p, compute, x, B, wsb, stats, st);
   if (rc) return rc;
-  for (int q = 0; q < 2; ++q)  // join the reduction stream
+  for (int q = 0; q < 3; ++q)  // join the reduction stream
     if (red_pending[q] && (rc = check_cuda(cudaStreamWaitEvent(st, p.red_done[q], 0), "wstats join")))
       return rc;
   return check_cuda(cudaGetLastError(), "backward kernels");
