@@ -528,6 +528,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
   if (p->leaf_i8 && (rc = upload(&p->d_i8_tab, i8_tab))) return rc;
   if (p->leaf_i8 && (rc = upload(&p->d_i8_col, i8_col))) return rc;
   if (p->leaf_i8 && (rc = upload(&p->d_i8_grp, i8_grp))) return rc;
+  p->h_i8_grp = i8_grp;
   if (p->leaf_i8 &&
       (rc = check_cuda(cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking),
                        "side stream")))

@@ -112,6 +112,7 @@ struct Plan {
   int *d_i8_tab = nullptr;         // per padded chunk: leaf, variables, flags, 0
   int *d_i8_col = nullptr;         // per padded chunk: 32 variable indices
   int *d_i8_grp = nullptr;         // first chunk of each leaf pair (pairs + 1)
+  std::vector<int> h_i8_grp;
   int64_t w_i8flag = 0;            // workspace: off-grid flag of the last i8 forward
   cudaStream_t side_stream = nullptr;  // captures the fallback body of a conditional node
   cudaStream_t fork_stream = nullptr;  // M-step: leaf branch beside the einsum weights
@@ -242,6 +243,8 @@ int launch_prepare_leaf_i8(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_i8_img(Plan &p, uint8_t *compute, cudaStream_t st);
 void plan_leaf_i8(Plan &p, std::vector<int> &tab, std::vector<int> &col, std::vector<int> &grp);
 bool leaf_i8_supported(const Plan &p);
+int launch_leaf_finalize_parts(Plan &p, const uint8_t *compute, const double *part, int nsplit,
+                               int64_t B, uint8_t *wsb, cudaStream_t st);
 int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t B, uint8_t *wsb,
                        int *flag, cudaGraphConditionalHandle cond, cudaStream_t st);
 struct CompView;

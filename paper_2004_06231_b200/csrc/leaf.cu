@@ -563,6 +563,23 @@ static int launch_leaf_fallback(Plan &p, const uint8_t *compute, const float *x,
   return check_cuda(cudaGetLastError(), "leaf forward kernels");
 }
 
+// Leaf slabs from split partials of the INT8 pass (leaf_i8.cu scope split):
+// cnst - sum_q part[q] in split order, then the slab shift / offsets.
+int launch_leaf_finalize_parts(Plan &p, const uint8_t *compute, const double *part, int nsplit,
+                               int64_t B, uint8_t *wsb, cudaStream_t st) {
+  CompView c = comp_view(p, compute);
+  WsView w = ws_view(p, wsb);
+  dim3 g2(ceil_div(B, 32), p.n_leaf);
+  const size_t fsmem = sizeof(double) * 32 * (p.k + 1);
+  if (fsmem > 48 * 1024)
+    cudaFuncSetAttribute(k_leaf_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fsmem);
+  launch_k(k_leaf_finalize, g2, 256, fsmem, st, part, nsplit, (const double *)c.cnst, B, p.k,
+           p.n_leaf, (const int *)p.d_leaf_slab, w, -1.0, (int32_t *)nullptr, (const int *)nullptr);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "leaf finalize (INT8 split)");
+}
+
 // Image data: the INT8 tensor-core pass (leaf_i8.cu) writes the slabs and
 // flags an off-grid batch; only then does the fallback sequence run. Under
 // CUDA-graph capture the fallback is the body of a conditional (IF) node whose

@@ -185,6 +185,12 @@ struct LeafI8Args {
   int D, K, K8, NG, n_leaf, npc;
   const int *grp_pc;         // first chunk of each leaf pair (n_pairs + 1)
   int grouped;               // 1: blockIdx.y = leaf pair (small batches), 0: all leaves
+  // scope split (few sample tiles): blockIdx.y = group * nsplit + split; the
+  // group's chunk list is cut into nsplit contiguous ranges whose exact
+  // partial Q (fp64, C added by split 0) go to part[split][leaf][b][k], summed
+  // in split order by k_leaf_finalize; nsplit == 1 writes the slabs directly
+  int nsplit;
+  double *part;
   int debug;                 // EINET_I8_DEBUG ablations (diagnostics only)
   long long *trace;          // EINET_I8_TRACE (diagnostics): per-chunk timestamps of CTA 0
 };
@@ -287,10 +293,16 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
   uint8_t *bring = aring + (size_t)LI_AST * LI_ABYTES; // [LI_BST][NG x 96] s8
   const int64_t b0 = (int64_t)blockIdx.x * 128;
   // this CTA's chunks [pcb, pce) and leaves [lb, le)
-  const int pcb = a.grouped ? a.grp_pc[blockIdx.y] : 0;
-  const int pce = a.grouped ? a.grp_pc[blockIdx.y + 1] : a.npc;
-  const int lb = a.grouped ? 2 * blockIdx.y : 0;
+  const int grp = blockIdx.y / a.nsplit, split = blockIdx.y % a.nsplit;
+  const int g0 = a.grouped ? a.grp_pc[grp] : 0;
+  const int g1 = a.grouped ? a.grp_pc[grp + 1] : a.npc;
+  const int pcb = g0 + (int)((int64_t)(g1 - g0) * split / a.nsplit);
+  const int pce = g0 + (int)((int64_t)(g1 - g0) * (split + 1) / a.nsplit);
+  const int lb = a.grouped ? 2 * grp : 0;
   const int le = a.grouped ? min(lb + 2, a.n_leaf) : a.n_leaf;
+  const bool splitting = a.nsplit > 1;  // (leaves per CTA <= 2, checked by the launcher)
+  // split mode: first / last chunk of each of the (<= 2) leaves in [pcb, pce)
+  __shared__ int s_first[2], s_last[2];
   if (w == LI_MMA_WARP) tc::tmem_alloc(&tbase, 512);
   if (t == 0) {
     for (int s = 0; s < LI_XST; ++s) {
@@ -311,6 +323,15 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
     }
     bad_any = 0;
     tc::mbar_fence_init();
+    if (splitting) {
+      s_first[0] = s_first[1] = -1;
+      s_last[0] = s_last[1] = -1;
+      for (int pc = pcb; pc < pce; ++pc) {
+        const int li = a.tab[pc].x - lb;
+        if (s_first[li] < 0) s_first[li] = pc;
+        s_last[li] = pc;
+      }
+    }
   }
   tc::fence_before();
   __syncthreads();
@@ -510,8 +531,8 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
       LI_TRACE(5, pc);
       const int info = abinfo[as];
       const int leaf = info & 0xffffff;
-      const bool first = ((info >> 24) & LI_F_FIRST) != 0;
-      const bool last = ((info >> 24) & LI_F_LAST) != 0;
+      const bool first = splitting ? pc == s_first[leaf - lb] : ((info >> 24) & LI_F_FIRST) != 0;
+      const bool last = splitting ? pc == s_last[leaf - lb] : ((info >> 24) & LI_F_LAST) != 0;
       const int buf = leaf & 1;
       if (first) tc::mbar_wait(&accempty[buf], (((leaf - lb) >> 1) & 1) ^ 1);
       tc::fence_after();
@@ -554,9 +575,38 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
         ks_c[buf][2][et] = a.i8c[((int64_t)leaf * K8 + et) * 2 + 1];
       }
       asm volatile("bar.sync 2, %0;" ::"n"(32 * LI_EW) : "memory");
+      double *pt = splitting ? a.part + (((int64_t)split * a.n_leaf + leaf) * a.ws.bc + b) * K
+                             : nullptr;
+      if (splitting && s_first[leaf - lb] < 0) {  // no chunk of this leaf here: zero partial
+        if (live)
+          for (int k = 0; k < K; ++k) pt[k] = 0.0;
+        continue;
+      }
       tc::mbar_wait(&accfull[buf], ((leaf - lb) >> 1) & 1);
       tc::fence_after();
       const uint32_t acc = tm + lane_off + (uint32_t)(buf * LI_ACC_STRIDE);
+      if (splitting) {
+        for (int k0 = 0; k0 < K8; k0 += 8) {
+          float raw[48];
+          tc::tmem_ld16(acc + k0 * LI_S, *(float(*)[16])(raw));
+          tc::tmem_ld16(acc + k0 * LI_S + 16, *(float(*)[16])(raw + 16));
+          tc::tmem_ld16(acc + k0 * LI_S + 32, *(float(*)[16])(raw + 32));
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int k = k0 + j;
+            if (k >= K) break;
+            double h = i2d(raw[j * LI_S + LI_S - 1]);
+#pragma unroll
+            for (int sd = LI_S - 2; sd >= 0; --sd) h = fma(h, 0.0078125, i2d(raw[j * LI_S + sd]));
+            if (live) pt[k] = fma(ks_c[buf][1][k], h, split == 0 ? ks_c[buf][2][k] : 0.0);
+          }
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) li_arrive(&accempty[buf]);
+        continue;
+      }
       const int slab = a.leaf_slab[leaf];
       double mx = -CUDART_INF;
       for (int pass = 0; pass < ((a.debug & 2) ? 0 : 2); ++pass) {
@@ -687,11 +737,30 @@ int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t 
   const int tiles = ceil_div(B, 128), npairs = (p.n_leaf + 1) / 2;
   a.grp_pc = p.d_i8_grp;
   a.grouped = (tiles < p.num_sms && npairs > 1) ? 1 : 0;
-  const dim3 grid(tiles, a.grouped ? npairs : 1);
+  const int groups = a.grouped ? npairs : 1;
+  // still fewer CTAs than SMs (few tiles, few large leaves: CelebA-shaped
+  // scopes of 12288 variables): split each group's chunk list, about one wave
+  // of CTAs, at least 8 chunks per split, partials finished by k_leaf_finalize
+  a.nsplit = 1;
+  if ((a.grouped || p.n_leaf <= 2) && (int64_t)tiles * groups < p.num_sms) {
+    const int min_chunks = [&] {
+      int m = INT_MAX;
+      for (int g = 0; g < (int)p.h_i8_grp.size() - 1; ++g)
+        m = std::min(m, p.h_i8_grp[g + 1] - p.h_i8_grp[g]);
+      return a.grouped ? m : a.npc;
+    }();
+    a.nsplit = std::max(1, std::min({kMaxDSplit, p.num_sms / (tiles * groups), min_chunks / 8}));
+  }
+  a.part = (double *)(wsb + p.w_leafpart);
+  const dim3 grid(tiles, groups * a.nsplit);
   if (cond)
     launch_k(k_leaf_fwd_i8<true>, grid, LI_THREADS, smem, st, a);
   else
     launch_k(k_leaf_fwd_i8<false>, grid, LI_THREADS, smem, st, a);
+  if (a.nsplit > 1) {
+    const int rc = launch_leaf_finalize_parts(p, compute, a.part, a.nsplit, B, wsb, st);
+    if (rc) return rc;
+  }
   if (tracing) {
     long long h[128 * 8];
     cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
