@@ -1207,7 +1207,8 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
                                         w.mixpart, L.mix_off, p.n_mix);
       // the mixing-weight batch reduction on the reduction stream (its
       // partials are per layer: no reuse to guard), joined at the end
-      cudaStream_t rs = p.red_stream ? p.red_stream : st;
+      // (the profiler's per-class pass keeps them in line: clean class times)
+    cudaStream_t rs = p.red_stream && !profiling_enabled() ? p.red_stream : st;
       if (rs != st) {
         if ((rc = check_cuda(cudaEventRecord(p.red_fork[2], st), "mixing fork")) ||
             (rc = check_cuda(cudaStreamWaitEvent(rs, p.red_fork[2], 0), "mixing fork")))
@@ -1239,7 +1240,8 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
     // steps later waits for it before reusing the half
     const int par = eo++ & 1;
     double *wpart = w.wpart + par * p.wpart_half;
-    cudaStream_t rs = p.red_stream ? p.red_stream : st;
+    // (the profiler's per-class pass keeps them in line: clean class times)
+    cudaStream_t rs = p.red_stream && !profiling_enabled() ? p.red_stream : st;
     if (red_pending[par] && (rc = check_cuda(cudaStreamWaitEvent(st, p.red_done[par], 0), "wstats join")))
       return rc;
     auto red_fork = [&](cudaStream_t r) -> int {
@@ -1262,8 +1264,8 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
       } else if (p.use_tc && L.tc) {
         WsView wv = w;
         wv.wpart = wpart;
-        if ((rc = launch_wstats_tc(p, L, EA, EB, wv, B, params + L.w_off, stats + L.w_off, st, rs,
-                                   p.red_fork[par])))
+        if ((rc = launch_wstats_tc(p, L, EA, EB, wv, B, params + L.w_off, stats + L.w_off, st,
+                                   rs != st ? rs : nullptr, p.red_fork[par])))
           return rc;
       } else {
         const int K4 = (K + 3) / 4;
