@@ -118,6 +118,7 @@ int upload(T **dst, const std::vector<T> &src) {
 
 int upload_tiledesc(Plan &p) {
   std::vector<int64_t> td;
+  int64_t items = 0;
   const int64_t KK = (int64_t)p.k * p.k;
   for (auto &L : p.layers) {
     if (L.kind != EINET_LAYER_EINSUM) continue;
@@ -141,8 +142,18 @@ int upload_tiledesc(Plan &p) {
     w[TD_UW_TILE] = L.uw_tile;
     w[TD_VW_OFF] = L.vw_off;
     w[TD_RW_TILE] = L.rw_tile;
+    // k_build_tiles_all items (one 8-element K chunk of one tile row each)
+    w[TD_WOFF] = L.w_off;
+    w[TD_IT0] = items;
+    if (L.tc) {
+      w[TD_NFW] = (int64_t)L.rows * L.ng * L.fw_rows * (p.kp / 8);
+      w[TD_NUW] = L.direct ? 0 : (int64_t)L.rows * L.ni * L.uw_rows * (L.kob / 8);
+      w[TD_NRW] = L.direct ? (int64_t)L.rows * L.rw_rows * (p.kp / 8) : 0;
+    }
+    items += w[TD_NFW] + 2 * w[TD_NUW] + w[TD_NRW];
     td.insert(td.end(), w, w + TD_WORDS);
   }
+  p.n_tile_items = items;
   p.n_tiledesc = (int)(td.size() / TD_WORDS);
   return upload(&p.d_tiledesc, td);
 }

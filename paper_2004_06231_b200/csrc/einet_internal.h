@@ -29,7 +29,7 @@ constexpr int kReduceThreads = 256;
 enum TileDescWord {
   TD_SLICE0, TD_ROWS, TD_KO, TD_TC, TD_DIRECT, TD_KG, TD_NG, TD_FW_ROWS, TD_IG, TD_NI,
   TD_UW_ROWS, TD_KOB, TD_RW_ROWS, TD_FW_OFF, TD_FW_TILE, TD_UW_OFF, TD_UW_TILE, TD_VW_OFF,
-  TD_RW_TILE, TD_WORDS
+  TD_RW_TILE, TD_WOFF, TD_IT0, TD_NFW, TD_NUW, TD_NRW, TD_WORDS
 };
 constexpr int EV_ROW = 36;         // padded row of the EA / EB 32-sample blocks (kern_common.cuh)
 
@@ -125,6 +125,7 @@ struct Plan {
   // fused M-step (mstep.cu): per-einsum-layer tile geometry, temp leaf terms
   int64_t *d_tiledesc = nullptr;   // einsum layers x TD_WORDS (mstep.cu)
   int n_tiledesc = 0;
+  int64_t n_tile_items = 0;        // k_build_tiles_all work items (16-byte pieces)
   int64_t c_mtmp = 0;              // compute segment: 2 x R*D*K doubles
   // workspace segments (byte offsets)
   int64_t w_off = 0, w_shift = 0, w_slots = 0, w_leafpart = 0, w_ea = 0, w_eb = 0,
@@ -238,6 +239,7 @@ int launch_wstats_tc(Plan &p, const LayerPlan &L, const float *EA, const float *
                      int64_t B, const double *Wl, double *stats, cudaStream_t st,
                      cudaStream_t rst = nullptr, cudaEvent_t fork = nullptr);
 int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st);
+int launch_build_tiles_all(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_prepare_leaf_dmma(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_prepare_leaf_i8(Plan &p, uint8_t *compute, cudaStream_t st);
 int launch_i8_img(Plan &p, uint8_t *compute, cudaStream_t st);

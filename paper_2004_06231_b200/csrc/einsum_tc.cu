@@ -194,81 +194,101 @@ void plan_tc_tiling(Plan &p) {
 // forward tile g of row l: rows n = kl*K + i (k = g*kg + kl), K dim = j (kp)
 // child-rho tile h of row l: rows n = il*K + j (i = h*ig + il), K dim = k (kob)
 // right child-rho tile h of row l: rows n = jl*K + i (j = h*ig + jl), K dim = k
-__device__ __forceinline__ void put_bf16_hilo(uint8_t *tile, int64_t lo_bytes, uint32_t off,
-                                              float v) {
-  __nv_bfloat16 h, l;
-  tc::split_bf16(v, h, l);
-  *(__nv_bfloat16 *)(tile + off) = h;
-  *(__nv_bfloat16 *)(tile + lo_bytes + off) = l;
-}
-
-__global__ void k_build_tiles(const float *__restrict__ W, uint8_t *fw, uint8_t *uw,
-                              uint8_t *vw, int L, int Ko, int K, int kp, int kg, int ng,
-                              int fw_rows, int ig, int ni, int uw_rows, int kob) {
+// direct right tile of a K_out == 1 row: rows n = j, K dim = i (kp)
+//
+// Every tensor-core weight image of every layer from the fp32 weights, in
+// tile order: one thread per (tile, K chunk of 8, row) writes the chunk's 8
+// bf16 hi and 8 lo values as two 16-byte stores (consecutive threads:
+// consecutive rows = consecutive 16-byte slots of a core-matrix column), zero
+// padding included; one launch for all layers (item ranges in the tile descriptors).
+__global__ void __launch_bounds__(256) k_build_tiles_all(const float *__restrict__ w32,
+                                                         const int64_t *__restrict__ td, int ntd,
+                                                         int64_t n_items, uint8_t *compute,
+                                                         int K, int kp) {
   EINET_KERNEL_PROLOGUE();
-  const int64_t n_fw = (int64_t)L * ng * fw_rows * kp;
-  const int64_t n_uw = (int64_t)L * ni * uw_rows * kob;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_fw + 2 * n_uw;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    float v = 0.f;
-    if (e < n_fw) {
-      const int kk = (int)(e % kp);
-      const int n = (int)((e / kp) % fw_rows);
-      const int64_t tile = e / ((int64_t)kp * fw_rows);  // l * ng + g
-      const int l = (int)(tile / ng), g = (int)(tile % ng);
-      const int kl = n / K, i = n % K, k = g * kg + kl;
-      if (kl < kg && k < Ko && kk < K) v = W[(((int64_t)l * Ko + k) * K + i) * K + kk];
-      put_bf16_hilo(fw + tile * (4LL * fw_rows * kp), 2LL * fw_rows * kp,
-                    tc::kmaj_off16(n, kk, fw_rows), v);
-    } else {
-      const bool right = e >= n_fw + n_uw;
-      const int64_t q = e - n_fw - (right ? n_uw : 0);
-      const int kk = (int)(q % kob);
-      const int n = (int)((q / kob) % uw_rows);
-      const int64_t tile = q / ((int64_t)kob * uw_rows);  // l * ni + h
-      const int l = (int)(tile / ni), h = (int)(tile % ni);
-      const int ol = n / K, in = n % K, o = h * ig + ol;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < n_items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    int q = 0;
+    while (q + 1 < ntd && td[(q + 1) * TD_WORDS + TD_IT0] <= it) ++q;
+    const int64_t *d = td + (int64_t)q * TD_WORDS;
+    const float *W = w32 + d[TD_WOFF];
+    const int Ko = (int)d[TD_KO];
+    int64_t r = it - d[TD_IT0];
+    const int64_t nfw = d[TD_NFW], nuw = d[TD_NUW];
+    float v[8];
+    uint8_t *tile;
+    int rows, kdim, row, kc;
+    if (r < nfw) {  // forward: rows kl*K + i, K dim j
+      rows = (int)d[TD_FW_ROWS];
+      kdim = kp;
+      row = (int)(r % rows);
+      r /= rows;
+      kc = (int)(r % (kdim / 8));
+      const int64_t t = r / (kdim / 8);  // l * ng + g
+      const int ng = (int)d[TD_NG], kg = (int)d[TD_KG];
+      const int l = (int)(t / ng), g = (int)(t % ng);
+      const int kl = row / K, i = row % K, k = g * kg + kl;
+      tile = compute + d[TD_FW_OFF] + t * d[TD_FW_TILE];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {
+        const int j = kc * 8 + z;
+        v[z] = (kl < kg && k < Ko && j < K) ? W[(((int64_t)l * Ko + k) * K + i) * K + j] : 0.f;
+      }
+    } else if (r < nfw + 2 * nuw) {  // child-rho: left rows il*K + j, right jl*K + i; K dim k
+      const bool right = r >= nfw + nuw;
+      r -= right ? nfw + nuw : nfw;
+      rows = (int)d[TD_UW_ROWS];
+      kdim = (int)d[TD_KOB];
+      row = (int)(r % rows);
+      r /= rows;
+      kc = (int)(r % (kdim / 8));
+      const int64_t t = r / (kdim / 8);  // l * ni + h
+      const int ni = (int)d[TD_NI], ig = (int)d[TD_IG];
+      const int l = (int)(t / ni), h = (int)(t % ni);
+      const int ol = row / K, in = row % K, o = h * ig + ol;
       const int i = right ? in : o, j = right ? o : in;
-      if (ol < ig && o < K && kk < Ko) v = W[(((int64_t)l * Ko + kk) * K + i) * K + j];
-      put_bf16_hilo((right ? vw : uw) + tile * (4LL * uw_rows * kob), 2LL * uw_rows * kob,
-                    tc::kmaj_off16(n, kk, uw_rows), v);
+      tile = compute + (right ? d[TD_VW_OFF] : d[TD_UW_OFF]) + t * d[TD_UW_TILE];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {
+        const int kk = kc * 8 + z;
+        v[z] = (ol < ig && o < K && kk < Ko) ? W[(((int64_t)l * Ko + kk) * K + i) * K + j] : 0.f;
+      }
+    } else {  // K_out == 1: right tile rows j, K dim i
+      r -= nfw + 2 * nuw;
+      rows = (int)d[TD_RW_ROWS];
+      kdim = kp;
+      row = (int)(r % rows);
+      r /= rows;
+      kc = (int)(r % (kdim / 8));
+      const int64_t l = r / (kdim / 8);
+      tile = compute + d[TD_VW_OFF] + l * d[TD_RW_TILE];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {
+        const int i = kc * 8 + z;
+        v[z] = (row < K && i < K) ? W[((int64_t)l * K + i) * K + row] : 0.f;
+      }
     }
+    uint32_t hv[4], lv[4];
+#pragma unroll
+    for (int z = 0; z < 4; ++z) tc::split_bf16x2(v[2 * z], v[2 * z + 1], hv[z], lv[z]);
+    const uint32_t off = tc::kmaj_off16(row, kc * 8, rows);
+    *(uint4 *)(tile + off) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    *(uint4 *)(tile + 2LL * rows * kdim + off) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
   }
 }
 
-// direct right tile of a K_out == 1 row: rows n = j, K dim = i (kp), value W[l,0,i,j]
-__global__ void k_build_rw(const float *__restrict__ W, uint8_t *rw, int L, int K, int kp,
-                           int rows) {
-  EINET_KERNEL_PROLOGUE();
-  const int64_t n_rw = (int64_t)L * rows * kp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_rw;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e % kp);
-    const int n = (int)((e / kp) % rows);
-    const int l = (int)(e / ((int64_t)kp * rows));
-    const float v = (n < K && i < K) ? W[((int64_t)l * K + i) * K + n] : 0.f;
-    put_bf16_hilo(rw + l * (4LL * rows * kp), 2LL * rows * kp, tc::kmaj_off16(n, i, rows), v);
-  }
+int launch_build_tiles_all(Plan &p, uint8_t *compute, cudaStream_t st) {
+  if (p.n_tile_items == 0) return 0;
+  CompView c = comp_view(p, compute);
+  launch_k(k_build_tiles_all, (int)std::min<int64_t>((p.n_tile_items + 255) / 256, 4 * p.num_sms),
+           256, 0, st, (const float *)c.w32, (const int64_t *)p.d_tiledesc, p.n_tiledesc,
+           p.n_tile_items, compute, p.k, p.kp);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "build tc tiles");
 }
 
 int launch_prepare_tc_tiles(Plan &p, uint8_t *compute, cudaStream_t st) {
-  CompView c = comp_view(p, compute);
-  for (auto &L : p.layers) {
-    if (!L.tc) continue;
-    if (L.direct) {
-      const int64_t n = (int64_t)L.rows * L.rw_rows * p.kp;
-      launch_k(k_build_rw, (int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
-          c.w32 + L.w_off, compute + L.vw_off, L.rows, p.k, p.kp, L.rw_rows);
-      count_launch();
-    }
-    const int64_t n = (int64_t)L.rows * (L.ng * L.fw_rows * p.kp +
-                                         (L.direct ? 0 : 2 * L.ni * L.uw_rows * L.kob));
-    launch_k(k_build_tiles, (int)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
-        c.w32 + L.w_off, compute + L.fw_off, compute + L.uw_off, compute + L.vw_off, L.rows,
-        L.k_out, p.k, p.kp, L.kg, L.ng, L.fw_rows, L.ig, L.direct ? 0 : L.ni, L.uw_rows, L.kob);
-    count_launch();
-  }
-  return check_cuda(cudaGetLastError(), "build tc tiles");
+  return launch_build_tiles_all(p, compute, st);
 }
 
 __device__ __forceinline__ void store_split4(float *hi, float *lo, float4 v) {

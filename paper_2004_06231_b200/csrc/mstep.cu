@@ -93,9 +93,7 @@ __global__ void __launch_bounds__(256) k_mstep_einsum(double *__restrict__ W,
                                                       float *__restrict__ w32,
                                                       const double *__restrict__ n, int K,
                                                       double lam, double eps,
-                                                      const int32_t *status,
-                                                      const int64_t *__restrict__ tiledesc,
-                                                      int ntd, uint8_t *compute, int kp) {
+                                                      const int32_t *status) {
   EINET_KERNEL_PROLOGUE();
   const int KK = K * K;
   __shared__ double red[8];
@@ -114,52 +112,10 @@ __global__ void __launch_bounds__(256) k_mstep_einsum(double *__restrict__ W,
     s2 += v;
   }
   const double tot = block_sum_256(s2, red);
-  // tensor-core weight images of this (l, k) slice (einsum_tc.cu k_build_tiles
-  // layouts; padding entries were zeroed by the first prepare)
-  const int64_t *td = nullptr;
-  int64_t l = 0, k = 0;
-  if (tiledesc) {
-    for (int q = 0; q < ntd; ++q) {
-      const int64_t *c = tiledesc + (int64_t)q * TD_WORDS;
-      const int64_t rel = (int64_t)blockIdx.x - c[TD_SLICE0];
-      if (rel >= 0 && rel < c[TD_ROWS] * c[TD_KO]) {
-        if (c[TD_TC]) td = c;
-        l = rel / c[TD_KO];
-        k = rel % c[TD_KO];
-        break;
-      }
-    }
-  }
   for (int e = threadIdx.x; e < KK; e += 256) {
     const double v = W[base + e] / tot;
     W[base + e] = v;
     w32[base + e] = (float)v;
-    if (td) {
-      const int i = e / K, j = e - (e / K) * K;
-      __nv_bfloat16 h, lo;
-      tc::split_bf16((float)v, h, lo);
-      auto put = [&](uint8_t *tile, int64_t lo_bytes, uint32_t off) {
-        *(__nv_bfloat16 *)(tile + off) = h;
-        *(__nv_bfloat16 *)(tile + lo_bytes + off) = lo;
-      };
-      {  // forward tile: rows kl*K + i, K dim j (kp)
-        const int64_t kg = td[TD_KG], rows = td[TD_FW_ROWS];
-        const int64_t tile = l * td[TD_NG] + k / kg;
-        put(compute + td[TD_FW_OFF] + tile * td[TD_FW_TILE], 2 * rows * kp,
-            tc::kmaj_off16((int)((k % kg) * K + i), j, (int)rows));
-      }
-      if (td[TD_DIRECT]) {  // K_out == 1: right tile rows j, K dim i (kp)
-        const int64_t rows = td[TD_RW_ROWS];
-        put(compute + td[TD_VW_OFF] + l * td[TD_RW_TILE], 2 * rows * kp,
-            tc::kmaj_off16(j, i, (int)rows));
-      } else {  // left (rows il*K + j) and right (rows jl*K + i) tiles, K dim k (kob)
-        const int64_t ig = td[TD_IG], rows = td[TD_UW_ROWS], kob = td[TD_KOB];
-        put(compute + td[TD_UW_OFF] + (l * td[TD_NI] + i / ig) * td[TD_UW_TILE], 2 * rows * kob,
-            tc::kmaj_off16((int)((i % ig) * K + j), (int)k, (int)rows));
-        put(compute + td[TD_VW_OFF] + (l * td[TD_NI] + j / ig) * td[TD_UW_TILE], 2 * rows * kob,
-            tc::kmaj_off16((int)((j % ig) * K + i), (int)k, (int)rows));
-      }
-    }
   }
 }
 
@@ -409,10 +365,14 @@ int launch_mstep(Plan &p, double *params, uint8_t *compute, const double *stats,
   }
   if (p.n_w) {
     const int nslices = (int)(p.n_w / KK);
-    launch_k(k_mstep_einsum, nslices, 256, 0, st, params, c.w32, stats, K, lam, eps_w, status,
-                                            fused_w ? p.d_tiledesc : nullptr,
-                                            p.n_tiledesc, compute, p.kp);
+    // fp64 update + fp32 copy per (l, k) slice, then the tensor-core images
+    // from the fp32 copy in tile order (coalesced 16-byte stores)
+    launch_k(k_mstep_einsum, nslices, 256, 0, st, params, c.w32, stats, K, lam, eps_w, status);
     count_launch();
+    if (fused_w) {
+      int rc = launch_build_tiles_all(p, compute, st);
+      if (rc) return rc;
+    }
   }
   if (p.n_mixrows) {
     launch_k(k_mstep_mixing, ceil_div(p.n_mixrows, 128), 128, 0, st, 
