@@ -996,8 +996,8 @@ __global__ void k_root_out(WsView ws, int slab, int64_t B, int kr, double *out,
 // Sum of the batch's root log-likelihoods into stats (ll, count): one CTA per
 // 256 samples writes a fixed-order partial (strided warp runs, shuffle tree,
 // warp order); the last CTA to finish (ticket counter, zeroed by k_root_out in
-// the forward pass and reset here) adds the partials in index order, so the
-// sum is deterministic whichever CTA finishes last.
+// the forward pass and reset here) adds the partials in a fixed order (lane
+// runs, shuffle tree), so the sum is deterministic whichever CTA finishes last.
 __global__ void __launch_bounds__(256) k_ll_sum(WsView ws, int slab, int64_t B, double *ll,
                                                 double count, double *part, unsigned *ticket) {
   EINET_KERNEL_PROLOGUE();
@@ -1022,13 +1022,18 @@ __global__ void __launch_bounds__(256) k_ll_sum(WsView ws, int slab, int64_t B, 
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last && threadIdx.x < 32) {
+    // fixed order: lane runs over q = lane + 32 i, then the shuffle tree
     __threadfence();
     double t = 0.0;
-    for (unsigned q = 0; q < gridDim.x; ++q) t += ((volatile double *)part)[q];
-    ll[0] += t;
-    ll[1] += count;
-    *ticket = 0u;
+    for (unsigned q = threadIdx.x; q < gridDim.x; q += 32) t += __ldcg(part + q);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) {
+      ll[0] += t;
+      ll[1] += count;
+      *ticket = 0u;
+    }
   }
 }
 

@@ -45,10 +45,37 @@ __global__ void __launch_bounds__(256) k_reduce_partials_cta(
   }
 }
 
+// 32 consecutive outputs per CTA: warp ty sums parts ty, ty + 8, ... of its
+// 32 columns (coalesced 256-byte rows), then a fixed tree over the 8 warps.
+__global__ void __launch_bounds__(256) k_reduce_partials_tile(
+    double *__restrict__ dst, const double *__restrict__ part, int nparts, int64_t n,
+    int64_t stride, const double *__restrict__ scale, int store) {
+  EINET_KERNEL_PROLOGUE();
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + tx;
+  double s = 0.0;
+  if (i < n) {
+#pragma unroll 4
+    for (int p = ty; p < nparts; p += 8) s += part[(int64_t)p * stride + i];
+  }
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && i < n) {
+    double t = ((red[0][tx] + red[1][tx]) + (red[2][tx] + red[3][tx])) +
+               ((red[4][tx] + red[5][tx]) + (red[6][tx] + red[7][tx]));
+    if (scale) t *= scale[i];
+    dst[i] = store ? t : dst[i] + t;
+  }
+}
+
 static void reduce_partials(double *dst, const double *part, int nparts, int64_t n,
                             int64_t stride, const double *scale, int store, cudaStream_t st) {
   if (n <= 0) return;
-  if (nparts >= 64 && n <= 65536) {
+  if (nparts >= 64 && n >= 2048 && n <= (1 << 22)) {
+    launch_k(k_reduce_partials_tile, (unsigned)((n + 31) / 32), 256, 0, st, dst, part, nparts, n,
+             stride, scale, store);
+  } else if (nparts >= 64 && n <= 65536) {
     launch_k(k_reduce_partials_cta, (unsigned)n, 256, 0, st, dst, part, nparts, stride, scale, store);
   } else {
     const int grid = (int)std::min<int64_t>((n + kReduceThreads - 1) / kReduceThreads, 8192);
