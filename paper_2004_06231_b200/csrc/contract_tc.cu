@@ -71,6 +71,8 @@ struct ContractArgs {
   int direct;             // K_out == 1 child-rho: out[o] = e1[o] * rt * acc[o] (no contraction)
   int sv_w;               // transposed-block width of sv
   int debug;              // EINET_CT_DEBUG (timing experiments only): 1 no epilogue math, 2 no MMA
+  int terms;              // 3: 3xBF16 (default); 1: hi*hi only (EINET_CONTRACT_TERMS=1, forward:
+                          // reduced-precision variant, ~2^-8 relative per layer, own tolerance)
   long long *trace;       // EINET_CT_TRACE (diagnostics): per-job timestamps of CTA 0
 };
 
@@ -195,9 +197,11 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
         }
         tc::mbar_wait(&bar_ae[s], ph ^ 1);
         CT_TRACE(0, it);
-        tc::mbar_arrive_expect_tx(&bar_af[s], abytes);
+        // (single-term variant: the hi half of the tile only)
+        const uint32_t acopy = a.terms == 1 ? abytes / 2 : abytes;
+        tc::mbar_arrive_expect_tx(&bar_af[s], acopy);
         tc::bulk_g2s(abuf + (int64_t)s * abytes,
-                     (const uint8_t *)a.a_ops[sd] + l * a.a_row_stride + (int64_t)jt * abytes, abytes,
+                     (const uint8_t *)a.a_ops[sd] + l * a.a_row_stride + (int64_t)jt * abytes, acopy,
                      &bar_af[s]);
         if (++s == a.stages) {
           s = 0;
@@ -249,8 +253,10 @@ __global__ void __launch_bounds__(CT_THREADS, 1) k_contract_tc(ContractArgs a, W
           uint64_t bh = b_desc0 + (uint64_t)c * w_units, bl = bh + b_lo_units;
           for (int ks = 0; ks < nks; ++ks) {
             tc::mma_bf16(d, ah, bh, id, ks > 0 ? 1u : 0u);
-            tc::mma_bf16(d, ah, bl, id, 1u);
-            tc::mma_bf16(d, al, bh, id, 1u);
+            if (a.terms == 3) {
+              tc::mma_bf16(d, ah, bl, id, 1u);
+              tc::mma_bf16(d, al, bh, id, 1u);
+            }
             ah += a_ks_units;
             al += a_ks_units;
             bh += b_ks_units;
@@ -489,6 +495,8 @@ int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *com
   {
     const char *env = getenv("EINET_CT_DEBUG");
     a.debug = env ? atoi(env) : 0;
+    static const int terms = getenv("EINET_CONTRACT_TERMS") ? atoi(getenv("EINET_CONTRACT_TERMS")) : 3;
+    a.terms = (mode == 0 && terms == 1) ? 1 : 3;
   }
   // mode 3: both child-responsibility sides (left = side 0, right = side 1)
   a.nside = mode == 3 ? 2 : 1;

@@ -120,3 +120,41 @@ def test_tensor_core_chunked_em_step_matches_oracle(k, chunk):
     for i in m2:
         close(m2[i], op2.mixing[i], 1e-4, 1e-9)
     close(phi2, op2.phi, 1e-4, 1e-6)
+
+
+_TERMS1 = r"""
+import sys, json
+import numpy as np
+sys.path.insert(0, '.')
+from tests.test_gpu_tc import _pd_model, _run
+from oracle import einet_oracle as O
+out = {}
+for k in (16, 40, 64):
+    circuit, fam, x, op = _pd_model(k, seed=k)
+    ll, _ = _run(circuit, fam, x, op, True)
+    want = O.forward(circuit, op, fam.to_dict(), x).log_likelihood
+    out[k] = float(np.max(np.abs(ll - want) / np.maximum(np.abs(want), 1)))
+print(json.dumps(out))
+"""
+
+
+def test_single_term_forward_contraction_tolerance():
+    """EINET_CONTRACT_TERMS=1: the reduced-precision forward contraction (one
+    bf16 x bf16 product per term instead of 3xBF16). Its stated tolerance:
+    per-sample log-likelihoods within 2e-3 relative of the oracle (the default
+    3xBF16 path holds 1e-4, test above); checked in a fresh process (the mode
+    is read once per process)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, EINET_CONTRACT_TERMS="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _TERMS1], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    err = json.loads(r.stdout.strip().splitlines()[-1])
+    print("single-term forward: max relative LL error", err)
+    for k, e in err.items():
+        assert e <= 2e-3, (k, e)
