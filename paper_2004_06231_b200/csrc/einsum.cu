@@ -525,6 +525,16 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
       gather_rho_many(ws, q0, q1, csr_slot, one, b0,
                       [&](int j) { const int e = threadIdx.x + 128 * j; return e < ne ? e : -1; },
                       rhos);
+      // every load of the thread before the first store (rt may alias oo for
+      // the compiler: interleaved, each entry would wait a full memory trip)
+      float ov[RE_MAX];
+      const int64_t bt = b0 + (threadIdx.x & 31);  // (128 = 4 x 32: one sample per thread)
+      const bool live = bt < B && slab_shift(ws, os)[bt] != -CUDART_INF;
+#pragma unroll
+      for (int j = 0; j < RE_MAX; ++j) {
+        const int e = threadIdx.x + 128 * j;
+        ov[j] = e < ne && live ? __ldg(oo + e) : 0.f;
+      }
 #pragma unroll
       for (int j = 0; j < RE_MAX; ++j) {
         const int e = threadIdx.x + 128 * j;
@@ -532,7 +542,7 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
         const int64_t b = b0 + (e & 31);
         float v = 0.f;
         if (b < B) {
-          const float r = slab_shift(ws, os)[b] == -CUDART_INF ? 0.f : expf(oo[e]);
+          const float r = live ? expf(ov[j]) : 0.f;
           v = r > 0.f ? rhos[j] / r : 0.f;
         }
         rt[e] = v;  // samples past the batch hold 0 (the W statistics sum whole blocks)
@@ -567,6 +577,16 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
                       return (e < ne && k < Ko) ? k * 32 + (e & 31) : -1;
                     },
                     rhos);
+    // the thread's sample is the same for every item (128 = 4 x 32): its
+    // liveness and all its output log-densities are loaded before any store
+    const int64_t bt = b0 + (threadIdx.x & 31);
+    const bool live = bt < B && slab_shift(ws, os)[bt] != -CUDART_INF;
+    float ov[RE_MAX];
+#pragma unroll
+    for (int j = 0; j < RE_MAX; ++j) {
+      const int e = threadIdx.x + 128 * (j >> 2), k = 4 * (e >> 5) + (j & 3);
+      ov[j] = (e < ne && k < Ko && live) ? __ldg(oo + k * 32 + (e & 31)) : 0.f;
+    }
 #pragma unroll
     for (int it = 0; it < RE_MAX / 4; ++it) {
       const int e = threadIdx.x + 128 * it;
@@ -574,14 +594,13 @@ __global__ void __launch_bounds__(128) k_einsum_bwd_rt(
       const int bl = e & 31, q = e >> 5;
       const int64_t b = b0 + bl;
       float v[4] = {0.f, 0.f, 0.f, 0.f};
-      const bool live = b < B && slab_shift(ws, os)[b] != -CUDART_INF;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int k = 4 * q + u;
         if (k >= Ko) continue;
         const int x = k * 32 + bl;
         if (b < B) {
-          const float r = live ? expf(oo[x]) : 0.f;
+          const float r = live ? expf(ov[4 * it + u]) : 0.f;
           v[u] = r > 0.f ? rhos[4 * it + u] / r : 0.f;
         }
         rt[x] = v[u];
