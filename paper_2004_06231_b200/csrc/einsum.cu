@@ -40,11 +40,87 @@ __global__ void __launch_bounds__(128) k_einsum_prep_fwd(
     int layer_index, int32_t *status) {
   EINET_KERNEL_PROLOGUE();
   __shared__ float mx[2][32];
+  __shared__ float pmx[2][4][32];
   __shared__ unsigned char dead[32];
   const int l = blockIdx.y, t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int nb = (int)min((int64_t)32, B - b0);
   const int ls = left_slab[l], rs = right_slab[l];
+  if (EBM != nullptr && (kp / 4) * 32 <= 4 * 128) {
+    // tensor-core path, one pass: thread = (sample lane, quads q = wid + 4 i);
+    // its child values are loaded once, up front, and give both the per-warp
+    // maxima and the exponentials (stores only after every load)
+    const int nq4 = (kp / 4) * 32;
+    const float *ol = ws.off + tb_idx(ls, b0, 0, ws.bc, ws.ks) + lane;
+    const float *orr = ws.off + tb_idx(rs, b0, 0, ws.bc, ws.ks) + lane;
+    float xl[4][4], xr[4][4];
+    float ml = -CUDART_INF_F, mr = -CUDART_INF_F;
+    bool nan = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int q = (t + 128 * i) >> 5;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = 4 * q + u;
+        const bool ok = t + 128 * i < nq4 && k < K;
+        xl[i][u] = ok ? __ldg(ol + k * 32) : -CUDART_INF_F;
+        xr[i][u] = ok ? __ldg(orr + k * 32) : -CUDART_INF_F;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        nan |= (xl[i][u] != xl[i][u]) | (xr[i][u] != xr[i][u]);
+        ml = fmaxf(ml, xl[i][u]);
+        mr = fmaxf(mr, xr[i][u]);
+      }
+    pmx[0][wid][lane] = ml;
+    pmx[1][wid][lane] = mr;
+    if (nan && lane < nb) atomicMin(&status[1], layer_index);
+    __syncthreads();
+    if (t < 32) {
+      const float m0 = fmaxf(fmaxf(pmx[0][0][t], pmx[0][1][t]), fmaxf(pmx[0][2][t], pmx[0][3][t]));
+      const float m1 = fmaxf(fmaxf(pmx[1][0][t], pmx[1][1][t]), fmaxf(pmx[1][2][t], pmx[1][3][t]));
+      mx[0][t] = m0;
+      mx[1][t] = m1;
+      bool d = true;
+      if (t < nb) {
+        const int64_t b = b0 + t;
+        const double sl = slab_shift(ws, ls)[b], sr = slab_shift(ws, rs)[b];
+        if (sl != sl || sr != sr) atomicMin(&status[1], layer_index);
+        d = sl == -CUDART_INF || sr == -CUDART_INF || m0 == -CUDART_INF_F || m1 == -CUDART_INF_F;
+        slab_shift(ws, out_slab[l])[b] = d ? -CUDART_INF : (sl + (double)m0) + (sr + (double)m1);
+      }
+      dead[t] = d;
+    }
+    __syncthreads();
+    const bool d = dead[lane];
+    const float m0 = mx[0][lane], m1 = mx[1][lane];
+    float *ea = EA + ev_idx(l, b0, 0, ws.bc, K), *eb = EB + ev_idx(l, b0, 0, ws.bc, K);
+    const int64_t ntl = ws.bc / 128;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = t + 128 * i;
+      if (e >= nq4) break;
+      const int q = e >> 5;
+      float va[4] = {0.f, 0.f, 0.f, 0.f}, vb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = 4 * q + u;
+        if (k >= K) break;
+        const int xe = k * EV_ROW + lane;
+        va[u] = d ? 0.f : expf(xl[i][u] - m0);
+        vb[u] = d ? 0.f : expf(xr[i][u] - m1);
+        ea[xe] = va[u];
+        eb[xe] = vb[u];
+      }
+      store_bf16_quad(EBM, l, b0 + lane, q, ntl, kp, make_float4(vb[0], vb[1], vb[2], vb[3]));
+      if (EAM)
+        store_bf16_quad(EAM, l, b0 + lane, q, ntl, kp, make_float4(va[0], va[1], va[2], va[3]));
+    }
+    return;
+  }
   if (wid < 2) {  // warp 0: left maxima, warp 1: right maxima (lane = sample)
     const int slab = wid ? rs : ls;
     const float *o = ws.off + tb_idx(slab, b0, 0, ws.bc, ws.ks) + lane;
@@ -461,6 +537,18 @@ __global__ void __launch_bounds__(128) k_mixing_bwd(
     gather_rho_many(ws, q0, q1, csr_slot, one, b0,
                     [&](int j) { const int e = threadIdx.x + 128 * j; return e < ne ? e : -1; },
                     rho);
+  // one sample per thread (128 = 4 x 32): its shift and output log-densities
+  // are loaded once, each child's before any store (dst may alias them for
+  // the compiler: interleaved, every entry would wait a full memory trip)
+  const int64_t bt = b0 + (threadIdx.x & 31);
+  const bool in = bt < B;
+  const double so_t = in ? slab_shift(ws, os)[bt] : -CUDART_INF;
+  float ov[RE_MAX];
+#pragma unroll
+  for (int j = 0; j < RE_MAX; ++j) {
+    const int e = threadIdx.x + 128 * j;
+    ov[j] = (many && e < ne && in) ? __ldg(oo + e) : 0.f;
+  }
   for (int c = 0; c < dmax; ++c) {
     float run = 0.f;
     if (mask[m * dmax + c]) {
@@ -468,19 +556,26 @@ __global__ void __launch_bounds__(128) k_mixing_bwd(
       const float wc = w[m * dmax + c];
       const float *oc = ws.off + tb_idx(sl, b0, 0, ws.bc, ws.ks);
       float *dst = ws.slots + tb_idx(mix_slot[m * dmax + c], b0, 0, ws.bc, ws.ks);
+      if (many && in) {
+        const double sc = slab_shift(ws, sl)[bt];
+        const bool ok = so_t != -CUDART_INF && sc != -CUDART_INF;
+        const float dsh = ok ? (float)(sc - so_t) : 0.f;
+        float cv[RE_MAX];
 #pragma unroll
-      for (int j = 0; j < RE_MAX; ++j) {
-        const int e = threadIdx.x + 128 * j;
-        if (!many || e >= ne) break;
-        const int64_t b = b0 + (e & 31);
-        if (b >= B) continue;
-        const double so = slab_shift(ws, os)[b], sc = slab_shift(ws, sl)[b];
-        const bool ok = so != -CUDART_INF && sc != -CUDART_INF;
-        const float dk = (ok ? (float)(sc - so) : 0.f) + oc[e] - oo[e];
-        const float ratio = (ok && isfinite(dk)) ? expf(dk) : 0.f;
-        const float contrib = rho[j] * wc * ratio;
-        dst[e] = contrib;
-        run += contrib;
+        for (int j = 0; j < RE_MAX; ++j) {
+          const int e = threadIdx.x + 128 * j;
+          cv[j] = e < ne ? __ldg(oc + e) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < RE_MAX; ++j) {
+          const int e = threadIdx.x + 128 * j;
+          if (e >= ne) break;
+          const float dk = dsh + cv[j] - ov[j];
+          const float ratio = (ok && isfinite(dk)) ? expf(dk) : 0.f;
+          const float contrib = rho[j] * wc * ratio;
+          dst[e] = contrib;
+          run += contrib;
+        }
       }
       for (int e = threadIdx.x; !many && e < ne; e += 128) {
         const int64_t b = b0 + (e & 31);
