@@ -19,6 +19,9 @@ tests = open(os.path.join(src, "tests.log")).read().strip().splitlines()[-1]
 smoke = open(os.path.join(src, "smoke.log")).read().strip().splitlines()[-1]
 tag = os.path.basename(src.rstrip("/"))
 k = b["kernels"]
+c5 = [json.loads(l) for l in open(os.path.join(src, "c5.jsonl"))] if os.path.exists(
+    os.path.join(src, "c5.jsonl")) else []
+c5max = lambda kk: max([d["fwd_tc_frac_issued"] or 0 for d in c5 if d["k"] == kk] or [float("nan")])
 rows = "\n".join(
     f"| {n} | {v['ms_per_step'] * 1e3:.1f} | {v['share'] * 100:.1f}% | "
     + (f"{v['tflops']:.0f} TF/s ({v['tc_frac']:.3f} alg, {v['tc_frac_issued_3xbf16']:.3f} issued)"
@@ -48,8 +51,8 @@ doc = f"""# Round 2 -- end-of-round evidence (`scripts/final_session.sh {tag}`, 
   {ref['cpu_baseline']['cores']} cores, kind `{ref['cpu_baseline']['kind']}`). Raw: `r02_reference_arm.json`.
 * **roofline** (dominant kernel `k_contract_tc`, EinsumLayer forward + child responsibilities): {r['achieved']:.0f} TF/s =
   {r['frac']:.3f} of the measured bf16 peak ({r['frac_issued_3xbf16']:.3f} counting the three MMAs of 3xBF16); largest
-  class `{r['largest_class']}`. At the C5 shape the contraction reaches 0.51 (K=40) to 0.80 (K=64) issued at the
-  tensor-bound points (`r02_c5_sweep.md`). Whole step: {r['step']['t_measured_ns_per_sample']:.1f} ns/sample vs the
+  class `{r['largest_class']}`. At the C5 shape the forward contraction reaches {c5max(40):.2f} (K=40) to {c5max(64):.2f} (K=64) and
+  {c5max(128):.2f} (K=128) of the bf16 peak counting issued MMAs (`r02_c5_sweep.md`). Whole step: {r['step']['t_measured_ns_per_sample']:.1f} ns/sample vs the
   SURVEY t_roof {r['step']['survey']['t_roof_ns_per_sample']:.1f} ns/sample ({r['step']['survey']['frac']:.3f}).
   (The per-class times come from a separate uncaptured pass with CUDA events per launch group; the
   W-statistics reductions run on a second stream beside the child-responsibility kernels, so that class
