@@ -202,6 +202,20 @@ int einet_sample(einet_plan *plan, const double *params, const void *workspace,
 int einet_decode_u8(const uint8_t *src, int64_t count, double divisor, float *dst,
                     void *stream);
 
+/* Host packing of a float64 batch for the device copy (host memory only, no
+ * device call). The reference up-casts every batch to float64
+ * (trainer.py:104) and its image datasets are v / 255 (modelio.py:145-166);
+ * this writes the smallest exact form of the count values of x: *kind = 255
+ * when every value is v / 255 for a byte v (bytes in u8_out; decode with
+ * divisor 255), 1 when every value is a byte count v (bytes; divisor 1),
+ * else 0 (fp32 values, round to nearest, in f32_out). Either way the fp32
+ * values the engine sees equal the host cast of x. NaN, inf, negative zero
+ * and off-grid values give kind 0; with f32_out NULL they give kind -1 and
+ * nothing is converted (the caller allocates fp32 staging only for batches
+ * that need it). threads <= 0: all host threads. */
+int einet_pack_f64(const double *x, int64_t count, uint8_t *u8_out, float *f32_out,
+                   int32_t threads, int32_t *kind);
+
 /* EINM1 model files (modelio.py:55-134, save_model / load_model) on the
  * device. The host parses the magic, the JSON header and the tensor manifest;
  * the blob section (per tensor: u32 ndim, u32 dims, f64 payload) lives in

@@ -82,6 +82,7 @@ EXPORTS = {
     "einet_sample": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_int64,
                                ctypes.c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "einet_decode_u8": (c_int32, [c_void_p, c_int64, ctypes.c_double, c_void_p, c_void_p]),
+    "einet_pack_f64": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_void_p]),
     "einet_crc32": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p]),
     "einet_params_from_blob": (c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_int64, c_void_p,
                                          c_void_p, c_void_p]),

@@ -774,6 +774,15 @@ int einet_decode_u8(const uint8_t *src, int64_t count, double divisor, float *ds
   return launch_decode_u8(src, count, divisor, dst, (cudaStream_t)stream);
 }
 
+int einet_pack_f64(const double *x, int64_t count, uint8_t *u8_out, float *f32_out,
+                   int32_t threads, int32_t *kind) {
+  if (count < 0) return fail(EINET_ERR_USAGE, "count must be >= 0");
+  if (!kind || (count > 0 && (!x || !u8_out)))
+    return fail(EINET_ERR_USAGE, "null argument");
+  *kind = host_pack_f64(x, count, u8_out, f32_out, threads);
+  return EINET_OK;
+}
+
 int einet_crc32(const uint8_t *data, int64_t len, uint32_t *crc, void *stream) {
   if (len < 0) return fail(EINET_ERR_USAGE, "len must be >= 0");
   if (!crc || (len > 0 && !data)) return fail(EINET_ERR_USAGE, "null argument");

@@ -259,6 +259,7 @@ int launch_contract_tc(Plan &p, const LayerPlan &L, int mode, const uint8_t *com
 int64_t sample_scratch_bytes(const Plan &p, int64_t n);
 int launch_decode_u8(const uint8_t *src, int64_t count, double divisor, float *dst,
                      cudaStream_t st);
+int host_pack_f64(const double *x, int64_t n, uint8_t *u8, float *f32, int threads);
 int launch_crc32(const uint8_t *data, int64_t len, uint32_t *crc, cudaStream_t st);
 int launch_blob_to_params(const uint8_t *blob, int64_t blob_len, const int64_t *table,
                           int n_tensors, int64_t max_count, double *params, int32_t *bad,

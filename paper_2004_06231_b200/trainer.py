@@ -86,6 +86,53 @@ def _graphs_enabled() -> bool:
     return os.environ.get("EINET_CUDA_GRAPHS", "1") != "0" and not _native.PROFILING
 
 
+def _f64_batch(batch):
+    """A float64 NumPy batch (the reference caller's type, trainer.py:104) as a
+    C-contiguous 2-D array, else None."""
+    if isinstance(batch, np.ndarray) and batch.dtype == np.float64 and batch.ndim in (1, 2):
+        return np.ascontiguousarray(batch if batch.ndim == 2 else batch[None, :])
+    return None
+
+
+def _pack_f64(model: EinetModel, a: np.ndarray, slot: int):
+    """Pack a float64 batch into the model's pinned host half ``slot`` with
+    ``einet_pack_f64`` (all host threads): one byte per value when the batch
+    is on the v/255 (or raw count) grid, else fp32 (the fp32 half is pinned
+    on first need). Returns (pinned tensor, ``decode_u8`` normalize flag:
+    None = /255, False = raw counts, or "f32" for an fp32 tensor). A half is
+    repacked only after its previous copy has ended (``ent["ev"]``)."""
+    import ctypes
+    pool = model.__dict__.setdefault("_pin_f64", {})
+    ent = pool.get(slot)
+    if ent is None or ent["shape"] != a.shape:
+        ent = pool[slot] = {"shape": a.shape, "f32": None, "ev": None,
+                            "u8": torch.empty(a.shape, dtype=torch.uint8, pin_memory=True)}
+    if ent["ev"] is not None:
+        ent["ev"].synchronize()
+    lib = _native.lib()
+    kind = ctypes.c_int32(-1)
+    for _ in range(2):
+        f32 = ent["f32"]
+        _native.check(lib.einet_pack_f64(a.ctypes.data, a.size, ent["u8"].data_ptr(),
+                                         f32.data_ptr() if f32 is not None else None, 0,
+                                         ctypes.byref(kind)), "einet_pack_f64")
+        if kind.value >= 0:
+            break
+        ent["f32"] = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+    k = kind.value
+    if k == 0:
+        return ent, ent["f32"], "f32"
+    return ent, ent["u8"], (None if k == 255 else False)
+
+
+def _staging(model, shape, dev):
+    st = model.__dict__.get("_staging")
+    if st is None or st.shape != shape:
+        st = torch.empty(shape, dtype=torch.float32, device=dev)
+        model.__dict__["_staging"] = st
+    return st
+
+
 def _stage_batch(model: EinetModel, batch, normalize=None) -> torch.Tensor:
     """Device batch for the graph path. Device fp32 tensors are used in place;
     host data is copied (asynchronously when pinned) into a persistent
@@ -94,12 +141,22 @@ def _stage_batch(model: EinetModel, batch, normalize=None) -> torch.Tensor:
     into the fp32 staging buffer (``engine.decode_u8``)."""
     if isinstance(batch, torch.Tensor) and batch.is_cuda and batch.dtype != torch.uint8:
         return engine.as_device_batch(batch)
-    t = _host_batch(batch)
     dev = model.params.flat.device
-    st = model.__dict__.get("_staging")
-    if st is None or st.shape != t.shape:
-        st = torch.empty(t.shape, dtype=torch.float32, device=dev)
-        model.__dict__["_staging"] = st
+    a = _f64_batch(batch)
+    if a is not None:
+        # float64 (the reference caller's type): packed on the host threads
+        # into pinned memory, copied as bytes when on the u8 grid
+        ent, t, norm = _pack_f64(model, a, 0)
+        st = _staging(model, t.shape, dev)
+        if norm == "f32":
+            st.copy_(t, non_blocking=True)
+        else:
+            engine.decode_u8(t.to(dev, non_blocking=True), norm, out=st)
+        ent["ev"] = torch.cuda.Event()
+        ent["ev"].record()
+        return st
+    t = _host_batch(batch)
+    st = _staging(model, t.shape, dev)
     if t.dtype == torch.uint8:
         if not t.is_cuda:
             t = t.to(dev, non_blocking=t.is_pinned())
@@ -272,16 +329,23 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     E-step graph, the all-reduces of the statistics and error words, and the
     M-step graph, still without a host wait; the error words cross ranks
     (a MIN all-reduce of the logs) only when some rank failed."""
-    hosts = [_host_batch(b) for b in batches]
+    batches = list(batches)
+    f64 = [_f64_batch(b) for b in batches]
+    # float64 NumPy batches (the reference caller's type) are packed lazily on
+    # the host threads (einet_pack_f64) into two pinned halves: batch i+1 is
+    # packed while step i runs, and crosses PCIe as bytes when on the grid
+    f64_mode = bool(batches) and all(a is not None for a in f64) and lam != 0.0 \
+        and _graphs_enabled()
+    hosts = f64 if f64_mode else [_host_batch(b) for b in batches]
     if not hosts:
         return []
     if lam == 0.0 or not _graphs_enabled():
         return [em_stochastic_step(model, b, lam, eps_w, chunk, process_group=process_group,
                                    normalize=normalize) for b in hosts]
-    if hosts[0].is_cuda:
+    if not f64_mode and hosts[0].is_cuda:
         return _device_steps(model, hosts, lam, eps_w, chunk, normalize, process_group)
     shape = tuple(hosts[0].shape)
-    dtype = hosts[0].dtype
+    dtype = "f64" if f64_mode else hosts[0].dtype
     if shape[0] == 0 and process_group is None:
         raise ValueError("empty batch")
     dev = model.params.flat.device
@@ -289,13 +353,15 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     if copy is None:
         copy = torch.cuda.Stream(device=dev)
         model.__dict__["_copy_stream"] = copy
-    key = "_stage2_u8" if dtype == torch.uint8 else "_stage2_f32"
+    u8 = dtype == torch.uint8
+    key = "_stage2_u8" if u8 or f64_mode else "_stage2_f32"
     bufs = model.__dict__.get(key)
     if bufs is None or tuple(bufs[0].shape) != shape:
-        bufs = [torch.empty(shape, dtype=dtype, device=dev) for _ in range(2)]
+        bufs = [torch.empty(shape, dtype=torch.uint8 if u8 or f64_mode else dtype, device=dev)
+                for _ in range(2)]
         model.__dict__[key] = bufs
-    u8 = dtype == torch.uint8
-    if u8:  # u8 batches are decoded on the copy stream into their own fp32 halves
+    dec = u8 or f64_mode
+    if dec:  # u8 batches are decoded on the copy stream into their own fp32 halves
         xfs = model.__dict__.get("_stage2_dec")
         if xfs is None or tuple(xfs[0].shape) != shape:
             xfs = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
@@ -307,15 +373,26 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     def issue_copy(i):
         # batch i's copy (and decode) into half i % 2 once step i - 2 is done with it
         s = i & 1
+        if f64_mode:  # host packing (waits only for this pinned half's last copy)
+            ent, t, norm = _pack_f64(model, hosts[i], s)
         copy.wait_stream(cur) if i < 2 else copy.wait_event(used[s])
         with torch.cuda.stream(copy):
-            bufs[s].copy_(hosts[i], non_blocking=hosts[i].is_pinned())
-            if u8:
-                engine.decode_u8(bufs[s], normalize, out=xfs[s])
+            if f64_mode:
+                if norm == "f32":
+                    xfs[s].copy_(t, non_blocking=True)
+                else:
+                    bufs[s].copy_(t, non_blocking=True)
+                    engine.decode_u8(bufs[s], norm, out=xfs[s])
+                ent["ev"] = torch.cuda.Event()
+                ent["ev"].record(copy)
+            else:
+                bufs[s].copy_(hosts[i], non_blocking=hosts[i].is_pinned())
+                if u8:
+                    engine.decode_u8(bufs[s], normalize, out=xfs[s])
             copied[s].record(copy)
 
     for h in hosts:
-        if tuple(h.shape) != shape or h.dtype != dtype:
+        if tuple(h.shape) != shape or (not f64_mode and h.dtype != dtype):
             raise ValueError("em_stochastic_steps needs batches of one shape and dtype")
     # No host sync between steps: the status words stay sticky over the
     # sequence (a failed step makes every later M-step a no-op, so the
@@ -330,7 +407,7 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     for i in range(len(hosts)):
         s = i & 1
         cur.wait_event(copied[s])
-        eng, stats, status = _graph_step(model, xfs[s] if u8 else bufs[s], lam, eps_w, chunk,
+        eng, stats, status = _graph_step(model, xfs[s] if dec else bufs[s], lam, eps_w, chunk,
                                          process_group, sticky=True)
         used[s].record(cur)
         if i + 1 < len(hosts):

@@ -544,6 +544,77 @@ def test_u8_em_steps_equal_float_steps():
     assert torch.equal(ma.params.flat, mb.params.flat)
 
 
+def _twin_models(cfg, x):
+    rg, fam, k, _ = config(cfg)
+    circuit = E.compile_graph(rg, k)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=x)
+    return [E.EinetModel(circuit, engine.Parameters.from_numpy(circuit, fam, ein, mix, phi), fam)
+            for _ in range(2)]
+
+
+@pytest.mark.parametrize("kind", ["image", "counts", "off_grid", "mixed"])
+def test_f64_numpy_em_steps_equal_fp32_tensor_steps(kind):
+    """float64 NumPy batches (the reference caller's type, trainer.py:104) are
+    packed on the host (einet_pack_f64: bytes on the u8 grid, else fp32) and
+    pipelined; parameters and LLs equal those of the same batches handed over
+    as pinned fp32 tensors, bit for bit."""
+    cfg = "C1" if kind == "counts" else "C2"
+    rg, fam, k, gen = config(cfg)
+    xs = [gen(300, seed=s) for s in (3, 4, 5)]
+    if kind == "counts":
+        xs = [np.random.default_rng(s).integers(0, 2, x.shape).astype(np.float64) * 1.0
+              for s, x in enumerate(xs)]
+    if kind == "off_grid":
+        xs = [x + 1e-3 for x in xs]
+    if kind == "mixed":
+        xs[1] = xs[1] + 1e-3
+    ma, mb = _twin_models(cfg, xs[0])
+    la = [trainer.em_stochastic_step(ma, xs[0], 0.5, chunk=256)]
+    lb = [trainer.em_stochastic_step(mb, torch.from_numpy(xs[0].astype(np.float32)).pin_memory(),
+                                     0.5, chunk=256)]
+    la += trainer.em_stochastic_steps(ma, xs + xs[::-1], 0.5, chunk=256)
+    lb += trainer.em_stochastic_steps(
+        mb, [torch.from_numpy(x.astype(np.float32)).pin_memory() for x in xs + xs[::-1]], 0.5,
+        chunk=256)
+    assert la == lb
+    assert torch.equal(ma.params.flat, mb.params.flat)
+
+
+def test_f64_numpy_raw_count_grid():
+    """Counts above 1 (categorical states) pack as raw bytes (divisor 1)."""
+    rg, fam, k, gen = config("C1")
+    from paper_2004_06231_b200 import builders
+    fam = builders.make_family("categorical", num_states=4)
+    circuit = E.compile_graph(rg, k)
+    x = np.random.default_rng(9).integers(0, 4, (200, circuit.d_vars)).astype(np.float64)
+    ein, mix, phi = engine.init_parameters_host(circuit, fam, seed=0, data=x)
+    ms = [E.EinetModel(circuit, engine.Parameters.from_numpy(circuit, fam, ein, mix, phi), fam)
+          for _ in range(2)]
+    la = trainer.em_stochastic_steps(ms[0], [x, x[::-1].copy()], 0.5, chunk=128)
+    lb = trainer.em_stochastic_steps(ms[1], [torch.from_numpy(x.astype(np.float32)),
+                                             torch.from_numpy(x[::-1].astype(np.float32))],
+                                     0.5, chunk=128)
+    assert la == lb
+    assert torch.equal(ms[0].params.flat, ms[1].params.flat)
+
+
+def test_f64_numpy_bad_value_raises_like_fp32():
+    """A NaN in a float64 batch goes the fp32 way and raises the reference's
+    exception at that step, parameters as after the steps before it."""
+    rg, fam, k, gen = config("C2")
+    xs = [gen(128, seed=s) for s in (1, 2, 3)]
+    xs[1] = xs[1].copy()
+    xs[1][5, 7] = np.nan
+    ma, mb = _twin_models("C2", xs[0])
+    errs = []
+    for m, batches in ((ma, xs), (mb, [torch.from_numpy(x.astype(np.float32)) for x in xs])):
+        with pytest.raises(Exception) as ei:
+            trainer.em_stochastic_steps(m, batches, 0.5, chunk=128)
+        errs.append((type(ei.value), str(ei.value)))
+    assert errs[0] == errs[1]
+    assert torch.equal(ma.params.flat, mb.params.flat)
+
+
 COND_CASES = [
     ("rat_gaussian", [1, 2], [0, 3, 5]),
     ("rat_categorical4", [0], [1, 2, 6]),
