@@ -120,7 +120,8 @@ struct Plan {
   // back-pass: the W-statistics batch reductions run on red_stream beside
   // the next layer's kernels (double-buffered partials, w_wpart halves)
   cudaStream_t red_stream = nullptr;
-  cudaEvent_t red_fork[3] = {nullptr, nullptr, nullptr}, red_done[3] = {nullptr, nullptr, nullptr};
+  // (index 3: the leaf P reductions beside the leaf statistics GEMM)
+  cudaEvent_t red_fork[4] = {}, red_done[4] = {};
   int64_t wpart_half = 0;          // doubles per partial buffer half
   // fused M-step (mstep.cu): per-einsum-layer tile geometry, temp leaf terms
   int64_t *d_tiledesc = nullptr;   // einsum layers x TD_WORDS (mstep.cu)
@@ -284,7 +285,8 @@ void launch_reduce_partials_store(double *dst, const double *part, int nparts, i
 bool leaf_tc_supported(const Plan &p);
 int64_t leaf_stats_slots(const Plan &p, int64_t B);
 int launch_leaf_stats_tc(Plan &p, const uint8_t *compute, const float *x, int64_t B,
-                         uint8_t *wsb, double *stats, const double *Pcall, cudaStream_t st);
+                         uint8_t *wsb, double *stats, const double *Pcall, cudaStream_t st,
+                         cudaEvent_t p_ready = nullptr);
 
 // Split factor s in [lo, hi] for a grid of ctas_per_split * s CTAs on
 // `slots` concurrently resident CTAs: the smallest s whose last wave is at

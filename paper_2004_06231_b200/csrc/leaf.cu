@@ -667,7 +667,10 @@ __global__ void __launch_bounds__(128) k_leaf_rho(WsView ws, const int *csr_off,
   const int slab = leaf_slab[leaf];
   const int q0 = csr_off[slab], q1 = csr_off[slab + 1];
   const bool one = ones[slab] != 0;
-  float *rho = ws.rho + tb_idx(leaf, b0, 0, ws.bc, K);
+  // tensor-core statistics (nn > 0, K <= 64): the block's rho only feeds the
+  // rho^T B tile below, so it stays in shared memory (no fp32 round trip)
+  __shared__ __align__(16) float srho[64 * 32];
+  float *rho = nn > 0 ? srho : ws.rho + tb_idx(leaf, b0, 0, ws.bc, K);
   constexpr int NE = 16;  // entries per thread gathered together (K <= 64)
   const int ne = K * 32;
   if (ne <= 128 * NE) {
@@ -905,14 +908,28 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
   launch_k(k_leaf_rho, dim3(nb, p.n_leaf), 128, 0, st, w, p.d_csr_off, p.d_csr_slot, p.d_slab_ones,
                                                  p.d_leaf_slab, B, K, p.n_leaf, w.ppart,
                                                  leaf_tc_supported(p) ? (K + 15) / 16 * 16 : 0);
+  // tensor-core path: the P reductions (read only by k_leaf_stats_finish and
+  // the M-step) run on the reduction stream beside k_leaf_stats_tc
+  const bool tcs = leaf_tc_supported(p);
+  cudaStream_t rs = tcs && p.red_stream && !profiling_enabled() ? p.red_stream : st;
+  if (rs != st) {
+    int rc = check_cuda(cudaEventRecord(p.red_fork[3], st), "leaf P fork");
+    if (!rc) rc = check_cuda(cudaStreamWaitEvent(rs, p.red_fork[3], 0), "leaf P fork");
+    if (rc) return rc;
+  }
   launch_reduce_partials_store(Pcall, w.ppart, nb, (int64_t)p.n_leaf * K,
-                               (int64_t)p.n_leaf * K, st);
+                               (int64_t)p.n_leaf * K, rs);
   launch_reduce_partials(stats + p.sizes.stats_p_offset, Pcall, 1, (int64_t)p.n_leaf * K,
-                         (int64_t)p.n_leaf * K, nullptr, st);
+                         (int64_t)p.n_leaf * K, nullptr, rs);
+  if (rs != st) {
+    int rc = check_cuda(cudaEventRecord(p.red_done[3], rs), "leaf P done");
+    if (rc) return rc;
+  }
   }
   ProfScope prof("leaf_stats", st);
   if (leaf_tc_supported(p)) {
-    int rc = launch_leaf_stats_tc(p, compute, x, B, wsb, stats, Pcall, st);
+    int rc = launch_leaf_stats_tc(p, compute, x, B, wsb, stats, Pcall, st,
+                                  p.red_stream && !profiling_enabled() ? p.red_done[3] : nullptr);
     count_launch(1);
     return rc;
   }

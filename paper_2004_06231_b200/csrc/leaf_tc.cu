@@ -11,8 +11,11 @@
 //     samples past the batch; warp 0 also bulk-copies the unit's rho^T B tiles
 //     (hi | lo, written by k_leaf_rho);
 //   * warp 4 owns TMEM and issues the 3xTF32 MMAs (A from TMEM);
-//   * warps 5..12 generate the A operand (y or y^2: round-to-nearest TF32 part
-//     and fp32 remainder) straight into TMEM and drain the accumulators.
+//   * warps 5..20 generate the A operand (y or y^2: round-to-nearest TF32 part
+//     and fp32 remainder) straight into TMEM, one (tile, TMEM lane quarter,
+//     16-sample half of each block) per warp (8 warps, one per (tile,
+//     quarter) walking both halves, left the generation on the critical path:
+//     two warps per scheduler); the half-0 warps drain the accumulators.
 // A CTA runs over <= 4096 samples of one or two segments (fp32 accumulation
 // runs); partials go to per-(segment, slot) fp32 buffers, summed in slot
 // order and un-centred in fp64 by k_leaf_stats_finish:
@@ -31,7 +34,7 @@ constexpr int LS_STAGES = 3;
 constexpr int LS_ASTAGES = 3;     // TMEM A ring (2 tiles x 64 columns per block)
 constexpr int LS_MAX_RUN = 64;    // units per CTA run (<= 4096 samples)
 constexpr int LS_GATHER_WARPS = 4;
-constexpr int LS_GEN_WARPS = 8;
+constexpr int LS_GEN_WARPS = 16;  // 2 tiles x 2 sample halves x 4 TMEM lane quarters
 constexpr int LS_THREADS = 32 * (LS_GATHER_WARPS + 1 + LS_GEN_WARPS);
 constexpr int LS_SEGV = 128;      // scope variables per segment
 
@@ -217,9 +220,10 @@ __global__ void __launch_bounds__(LS_THREADS, 1) k_leaf_stats_tc(LeafStatsArgs a
       }
     }
   } else {
-    // ---- generators / drainers: tile g (64 variables), TMEM lane quarter ----
-    const int gw = w - MMA_WARP - 1;  // 0..7
-    const int g = gw >> 2, quarter = w & 3;
+    // ---- generators / drainers: tile g (64 variables), TMEM lane quarter,
+    // sample half (16 of each 32-sample block); the half-0 warps drain ----
+    const int gw = w - MMA_WARP - 1;  // 0..15
+    const int g = (gw >> 2) & 1, shalf = gw >> 3, quarter = w & 3;
     const int r = 32 * quarter + lane;            // TMEM lane = A row
     const int vloc = 64 * g + (r & 63), tsel = r >> 6;
     const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
@@ -249,17 +253,16 @@ __global__ void __launch_bounds__(LS_THREADS, 1) k_leaf_stats_tc(LeafStatsArgs a
         tc::fence_after();
         const float *xv = st + sb * xs_floats + vloc;
         const uint32_t acol = tm + lane_off + 128 + (uint32_t)(as * 128 + g * 64);
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        {
           float hv[16], lv[16];
 #pragma unroll
           for (int z = 0; z < 16; ++z) {
-            const float y = act ? xv[(16 * half + z) * LS_SEGV] - cen : 0.f;
+            const float y = act ? xv[(16 * shalf + z) * LS_SEGV] - cen : 0.f;
             const float p = tsel ? y * y : y;
             tc::split_tf32(p, hv[z], lv[z]);  // round-to-nearest hi (kern_common.cuh)
           }
-          tc::tmem_st16(acol + 16 * half, hv);
-          tc::tmem_st16(acol + 32 + 16 * half, lv);
+          tc::tmem_st16(acol + 16 * shalf, hv);
+          tc::tmem_st16(acol + 32 + 16 * shalf, lv);
         }
         tc::tmem_wait_st();
         tc::fence_before();
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(LS_THREADS, 1) k_leaf_stats_tc(LeafStatsArgs a
         tc::fence_after();
         const int64_t slot = blockIdx.x - ls_cta_of((int64_t)seg * nq, a.units, a.grid);
         float *dst = a.part + slot * a.n_phi;
-        for (int c = 0; c < nn; c += 8) {
+        for (int c = 0; shalf == 0 && c < nn; c += 8) {
           float v[8];
           tc::tmem_ld8(tm + lane_off + (uint32_t)(g * nn + c), v);
           tc::tmem_wait_ld();
@@ -364,7 +367,8 @@ int64_t leaf_stats_slots(const Plan &p, int64_t B) {
 }
 
 int launch_leaf_stats_tc(Plan &p, const uint8_t *compute, const float *x, int64_t B,
-                         uint8_t *wsb, double *stats, const double *Pcall, cudaStream_t st) {
+                         uint8_t *wsb, double *stats, const double *Pcall, cudaStream_t st,
+                         cudaEvent_t p_ready) {
   CompView c = comp_view(p, compute);
   WsView w = ws_view(p, wsb);
   LeafStatsArgs a;
@@ -401,6 +405,10 @@ int launch_leaf_stats_tc(Plan &p, const uint8_t *compute, const float *x, int64_
     attr = smem;
   }
   launch_k(k_leaf_stats_tc, a.grid, LS_THREADS, smem, st, a);
+  if (p_ready) {  // P (Pcall) reduced on the reduction stream
+    const int rc = check_cuda(cudaStreamWaitEvent(st, p_ready, 0), "leaf P join");
+    if (rc) return rc;
+  }
   const int64_t n = (int64_t)p.d_vars * p.k * p.num_replicas;
   launch_k(k_leaf_stats_finish, (int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st, 
       a.part, Pcall, c.center, p.d_leaf_of, p.d_phi_seg, c.active,
