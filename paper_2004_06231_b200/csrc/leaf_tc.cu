@@ -346,8 +346,22 @@ bool leaf_tc_supported(const Plan &p) {
          leaf_tc_smem(nn) <= 220 * 1024;
 }
 
+// One CTA per SM, or the largest multiple of the segment count below it:
+// then every segment is cut at the same sample blocks, so the CTAs of the
+// segments covering the same image rows of neighbouring leaves walk the same
+// samples at the same time -- x pieces of 96 bytes per image row and strip
+// share 64-byte DRAM blocks with the next strip, which are then fetched once
+// (L2) instead of once per strip (the x traffic was 1.25x the batch).
+// EINET_LS_ALIGN=0 restores one CTA per SM (A/B).
 static int leaf_stats_grid(const Plan &p, int64_t units) {
   int64_t g = std::min<int64_t>(units, p.num_sms);
+  static const bool align = [] {
+    const char *e = getenv("EINET_LS_ALIGN");
+    return !(e && e[0] == '0');
+  }();
+  const int64_t nseg = std::max(1, p.n_lseg);
+  if (align && units >= p.num_sms && nseg <= p.num_sms && units % nseg == 0)
+    g = (p.num_sms / nseg) * nseg;
   g = std::max<int64_t>(g, (units + LS_MAX_RUN - 1) / LS_MAX_RUN);
   return (int)g;
 }
