@@ -190,6 +190,11 @@ struct LeafI8Args {
   // partial Q (fp64, C added by split 0) go to part[split][leaf][b][k], summed
   // in split order by k_leaf_finalize; nsplit == 1 writes the slabs directly
   int nsplit;
+  // tile_y: the sample tile is blockIdx.y and (group, split) blockIdx.x, so
+  // the CTAs of one tile are launched together: the leaf pairs' neighbouring
+  // strips (pair boundary mid 128-byte block of an image row) are then read
+  // at the same time and share the DRAM fetch; else the tile is blockIdx.x
+  int tile_y;
   double *part;
   int debug;                 // EINET_I8_DEBUG ablations (diagnostics only)
   long long *trace;          // EINET_I8_TRACE (diagnostics): per-chunk timestamps of CTA 0
@@ -291,9 +296,11 @@ __global__ void __launch_bounds__(LI_THREADS, 1) k_leaf_fwd_i8(LeafI8Args a) {
   uint8_t *xring = sm;                                 // [LI_XST][128][LI_XP] fp32
   uint8_t *aring = sm + (size_t)LI_XST * LI_XBYTES;    // [LI_AST][128 x 96] u8
   uint8_t *bring = aring + (size_t)LI_AST * LI_ABYTES; // [LI_BST][NG x 96] s8
-  const int64_t b0 = (int64_t)blockIdx.x * 128;
+  const int tile = a.tile_y ? blockIdx.y : blockIdx.x;
+  const int gy = a.tile_y ? blockIdx.x : blockIdx.y;
+  const int64_t b0 = (int64_t)tile * 128;
   // this CTA's chunks [pcb, pce) and leaves [lb, le)
-  const int grp = blockIdx.y / a.nsplit, split = blockIdx.y % a.nsplit;
+  const int grp = gy / a.nsplit, split = gy % a.nsplit;
   const int g0 = a.grouped ? a.grp_pc[grp] : 0;
   const int g1 = a.grouped ? a.grp_pc[grp + 1] : a.npc;
   const int pcb = g0 + (int)((int64_t)(g1 - g0) * split / a.nsplit);
@@ -752,7 +759,12 @@ int launch_leaf_fwd_i8(Plan &p, const uint8_t *compute, const float *x, int64_t 
     a.nsplit = std::max(1, std::min({kMaxDSplit, p.num_sms / (tiles * groups), min_chunks / 8}));
   }
   a.part = (double *)(wsb + p.w_leafpart);
-  const dim3 grid(tiles, groups * a.nsplit);
+  static const bool tile_y_env = [] {
+    const char *e = getenv("EINET_I8_TILEY");
+    return !(e && e[0] == '0');
+  }();
+  a.tile_y = tile_y_env && tiles <= 65535 && groups * a.nsplit > 1 ? 1 : 0;
+  const dim3 grid = a.tile_y ? dim3(groups * a.nsplit, tiles) : dim3(tiles, groups * a.nsplit);
   if (cond)
     launch_k(k_leaf_fwd_i8<true>, grid, LI_THREADS, smem, st, a);
   else

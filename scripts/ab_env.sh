@@ -13,5 +13,5 @@ print('$VAR=$v', round(d['ms_per_step']*1e3,1), [round(s['ms_per_step']*1e3,1) f
 done; done
 unset $VAR
 timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 > $OUT/tests.log 2>&1; echo "tests rc=$?" >> $OUT/status.txt
-EINET_LEAF_COND=0 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:k_leaf_stats_tc -c 2 --csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --small-batch 0 > $OUT/ncu_on.csv 2>/dev/null
-EINET_LS_ALIGN=0 EINET_LEAF_COND=0 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:k_leaf_stats_tc -c 2 --csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --small-batch 0 > $OUT/ncu_off.csv 2>/dev/null
+EINET_LEAF_COND=0 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:${KREGEX:-k_leaf_stats_tc} -c 2 --csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --small-batch 0 > $OUT/ncu_on.csv 2>/dev/null
+env $VAR=0 EINET_LEAF_COND=0 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:${KREGEX:-k_leaf_stats_tc} -c 2 --csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --small-batch 0 > $OUT/ncu_off.csv 2>/dev/null
