@@ -5,11 +5,7 @@
 // fp32 batches, so the device decode writes (float)((double)v / divisor) --
 // bit-identical to staging the reference's float64 array as fp32 on the host
 // -- and the host->device copy moves one byte per variable instead of four.
-#include <atomic>
 #include <cmath>
-#include <cstring>
-#include <thread>
-#include <vector>
 
 #include "einet_internal.h"
 
@@ -258,85 +254,5 @@ int launch_params_to_blob(const double *params, const int64_t *table, int n_tens
   return check_cuda(cudaGetLastError(), "params_to_blob");
 }
 
-
-// ---------------------------------------------------------------------------
-// Host packing of float64 batches (the reference caller's type: trainer.py:104
-// up-casts every batch to float64; image datasets are v / 255 in float64,
-// modelio.py:145-166). The bytes that cross PCIe are the smallest exact form
-// of the batch: when every value is v / 255 (or a raw count v) for a byte v,
-// one byte per value -- the device decode (k_decode_u8) restores exactly the
-// fp32 value the host cast would give -- else fp32 (round to nearest). All
-// host threads; a thread that meets an off-grid value stops the others.
-// ---------------------------------------------------------------------------
-
-namespace {
-
-// Exact-grid test: r = x * div clamped to [0, 255] (NaN -> 0) and rounded
-// to nearest (the 1.5 * 2^52 shift, no libm call); x must equal r / div
-// (correctly rounded, as the device decode computes it) and carry no sign
-// bit (negative zero's fp32 cast keeps the sign, the decoded byte would not).
-struct Grid {
-  double div;
-  inline bool pack(double x, uint8_t &out) const {
-    double y = x * div;
-    y = y > 0.0 ? y : 0.0;
-    y = y < 255.0 ? y : 255.0;
-    const double r = (y + 6755399441055744.0) - 6755399441055744.0;
-    uint64_t bits;
-    std::memcpy(&bits, &x, 8);
-    out = (uint8_t)(int)r;
-    return (r / div == x) & ((bits >> 63) == 0);
-  }
-};
-
-__attribute__((noinline)) bool pack_run(const double *__restrict__ x,
-                                        uint8_t *__restrict__ u8, int64_t n, const Grid grid) {
-  bool ok = true;
-  for (int64_t i = 0; i < n; ++i) ok &= grid.pack(x[i], u8[i]);
-  return ok;
-}
-
-template <class F>
-void host_parallel(int64_t n, int threads, F &&body) {
-  const int64_t min_per = 1 << 18;  // values per thread worth a thread
-  int t = (int)std::min<int64_t>(threads, std::max<int64_t>(1, n / min_per));
-  if (t <= 1) {
-    body(0, n);
-    return;
-  }
-  std::vector<std::thread> pool;
-  pool.reserve(t - 1);
-  for (int i = 1; i < t; ++i)
-    pool.emplace_back([&, i] { body(n * i / t, n * (i + 1) / t); });
-  body(0, n / t);
-  for (auto &th : pool) th.join();
-}
-
-}  // namespace
-
-int host_pack_f64(const double *x, int64_t n, uint8_t *u8, float *f32, int threads) {
-  if (threads <= 0) threads = (int)std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
-  for (const double div : {255.0, 1.0}) {
-    const Grid grid{div};
-    std::atomic<bool> off{false};
-    host_parallel(n, threads, [&](int64_t lo, int64_t hi) {
-      constexpr int64_t kStep = 4096;  // poll the stop flag every 4096 values
-      for (int64_t b = lo; b < hi; b += kStep) {
-        if (off.load(std::memory_order_relaxed)) return;
-        const int64_t e = std::min(hi, b + kStep);
-        if (!pack_run(x + b, u8 + b, e - b, grid)) {
-          off.store(true, std::memory_order_relaxed);
-          return;
-        }
-      }
-    });
-    if (!off.load()) return (int)div;
-  }
-  if (!f32) return -1;
-  host_parallel(n, threads, [&](int64_t lo, int64_t hi) {
-    for (int64_t i = lo; i < hi; ++i) f32[i] = (float)x[i];
-  });
-  return 0;
-}
 
 }  // namespace einet
