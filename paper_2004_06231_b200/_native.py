@@ -11,6 +11,7 @@ import os
 from ctypes import POINTER, c_double, c_int32, c_int64, c_uint8, c_void_p
 
 LIB_NAME = "libeinet_b200.so"
+_DEFAULT_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libeinet_b200.so")
 LIB_PATH = os.environ.get(  # EINET_LIB_PATH: A/B timing of another build (diagnostics)
     "EINET_LIB_PATH", os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME))
 
@@ -114,6 +115,8 @@ def load(path: str = LIB_PATH):
             f"{LIB_NAME} not built ({path} missing); run __graft_entry__.build()")
     lib = ctypes.CDLL(path)
     for name, (res, args) in EXPORTS.items():
+        if path != _DEFAULT_LIB and not hasattr(lib, name):
+            continue  # an older build under EINET_LIB_PATH (A/B timing only)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

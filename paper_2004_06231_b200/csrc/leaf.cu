@@ -903,15 +903,17 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
   const int K = p.k, D = p.d_vars, R = p.num_replicas, T = p.suff;
   const int nb = ceil_div(B, 32);
   double *Pcall = (double *)(wsb + p.w_tmp_p);
+  // tensor-core path: the P reductions (read only by k_leaf_stats_finish and
+  // the M-step) run beside k_leaf_stats_tc on the fork stream (idle until the
+  // M-step) -- not on the reduction stream, where they would queue behind the
+  // W-statistics reductions and hold k_leaf_stats_finish until those end
+  const bool tcs = leaf_tc_supported(p);
+  cudaStream_t rs = tcs && p.fork_stream && !profiling_enabled() ? p.fork_stream : st;
   {
   ProfScope prof("leaf_rho", st);
   launch_k(k_leaf_rho, dim3(nb, p.n_leaf), 128, 0, st, w, p.d_csr_off, p.d_csr_slot, p.d_slab_ones,
                                                  p.d_leaf_slab, B, K, p.n_leaf, w.ppart,
                                                  leaf_tc_supported(p) ? (K + 15) / 16 * 16 : 0);
-  // tensor-core path: the P reductions (read only by k_leaf_stats_finish and
-  // the M-step) run on the reduction stream beside k_leaf_stats_tc
-  const bool tcs = leaf_tc_supported(p);
-  cudaStream_t rs = tcs && p.red_stream && !profiling_enabled() ? p.red_stream : st;
   if (rs != st) {
     int rc = check_cuda(cudaEventRecord(p.red_fork[3], st), "leaf P fork");
     if (!rc) rc = check_cuda(cudaStreamWaitEvent(rs, p.red_fork[3], 0), "leaf P fork");
@@ -929,7 +931,7 @@ int launch_leaf_backward(Plan &p, const uint8_t *compute, const float *x, int64_
   ProfScope prof("leaf_stats", st);
   if (leaf_tc_supported(p)) {
     int rc = launch_leaf_stats_tc(p, compute, x, B, wsb, stats, Pcall, st,
-                                  p.red_stream && !profiling_enabled() ? p.red_done[3] : nullptr);
+                                  rs != st ? p.red_done[3] : nullptr);
     count_launch(1);
     return rc;
   }
