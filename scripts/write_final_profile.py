@@ -29,7 +29,7 @@ rows = "\n".join(
     + " |" for n, v in sorted(k.items(), key=lambda x: -x[1]["ms_per_step"]))
 r = b["roofline"]
 sb = b["secondary_batches"]
-doc = f"""# Round 2 -- end-of-round evidence (`scripts/final_session.sh {tag}`, one B200)
+doc = f"""# Round 2 -- end-of-round evidence (`scripts/final_session.sh` / `scripts/fin5.sh`, {tag}, one B200)
 
 * smoke: `{smoke}`; `pytest -m gpu`: {tests}.
 * **bench** (C3 SVHN-shape PD, K=40, 16384 samples/step, device-resident): **{b['value'] / 1e6:.2f}M samples/s**
@@ -71,7 +71,8 @@ doc = f"""# Round 2 -- end-of-round evidence (`scripts/final_session.sh {tag}`, 
 
 {full}
 `k_contract_tc<40, 1>` (forward) runs the tensor pipe at 50-52% on the 3- and 4-row layers
-(round 1: ~39%); the INT8 leaf forward reads 259 MB (x = 201 MB) in 117 us.
+(round 1: ~39%); the INT8 leaf forward reads 206 MB (x = 201 MB; 259 MB before its tile-major CTA
+order) in 115 us, the leaf statistics 227 MB (252 MB before the segment-aligned grid).
 """
 open(os.path.join(ROOT, "profiles", "r02_final.md"), "w").write(doc)
 print("wrote profiles/r02_final.md")
