@@ -367,29 +367,42 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
             xfs = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
             model.__dict__["_stage2_dec"] = xfs
     cur = torch.cuda.current_stream(dev)
-    copied = [torch.cuda.Event(), torch.cuda.Event()]
-    used = [torch.cuda.Event(), torch.cuda.Event()]
+    copied = [torch.cuda.Event(), torch.cuda.Event()]  # half ready for its step
+    used = [torch.cuda.Event(), torch.cuda.Event()]    # step done with the half
+    raw = [torch.cuda.Event(), torch.cuda.Event()]     # bytes landed (decode may start)
+    dstream = model.__dict__.get("_decode_stream")
+    if dec and dstream is None:
+        dstream = torch.cuda.Stream(device=dev)
+        model.__dict__["_decode_stream"] = dstream
 
     def issue_copy(i):
-        # batch i's copy (and decode) into half i % 2 once step i - 2 is done with it
+        # batch i into half i % 2. Byte batches: the copy stream only moves
+        # bytes (the u8 half is free once batch i-2's decode has read it) and
+        # the decode runs on its own stream once step i-2 is done with the fp32
+        # half, so consecutive copies keep the PCIe link busy back to back.
         s = i & 1
+        norm = normalize
         if f64_mode:  # host packing (waits only for this pinned half's last copy)
             ent, t, norm = _pack_f64(model, hosts[i], s)
-        copy.wait_stream(cur) if i < 2 else copy.wait_event(used[s])
+        direct = not dec or norm == "f32"  # the copy lands where the step reads
+        if i < 2:
+            copy.wait_stream(cur)
+        else:
+            copy.wait_event(used[s] if direct else copied[s])
         with torch.cuda.stream(copy):
             if f64_mode:
-                if norm == "f32":
-                    xfs[s].copy_(t, non_blocking=True)
-                else:
-                    bufs[s].copy_(t, non_blocking=True)
-                    engine.decode_u8(bufs[s], norm, out=xfs[s])
+                (xfs[s] if norm == "f32" else bufs[s]).copy_(t, non_blocking=True)
                 ent["ev"] = torch.cuda.Event()
                 ent["ev"].record(copy)
             else:
                 bufs[s].copy_(hosts[i], non_blocking=hosts[i].is_pinned())
-                if u8:
-                    engine.decode_u8(bufs[s], normalize, out=xfs[s])
-            copied[s].record(copy)
+            (copied if direct else raw)[s].record(copy)
+        if not direct:
+            dstream.wait_event(raw[s])
+            dstream.wait_stream(cur) if i < 2 else dstream.wait_event(used[s])
+            with torch.cuda.stream(dstream):
+                engine.decode_u8(bufs[s], norm, out=xfs[s])
+                copied[s].record(dstream)
 
     for h in hosts:
         if tuple(h.shape) != shape or (not f64_mode and h.dtype != dtype):
