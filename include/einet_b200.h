@@ -136,6 +136,16 @@ int einet_plan_set_tensor_cores(einet_plan *plan, int enable);
  * Call once per step; forward/backward only lower them (atomicMin). */
 int einet_status_reset(int32_t *status, void *stream);
 
+/* Per-step device log of a pipelined EM sequence (trainer.em_stochastic_steps,
+ * the reference's loop of em_stochastic_step calls, trainer.py:99-117, each
+ * returning its mean LL): copies ll2[0..1] (the stats buffer's LL sum and
+ * sample count) to log_ll[2 * r] and the status words to
+ * log_st[EINET_STATUS_WORDS * r] for r = *cursor (when r < cap), then
+ * increments *cursor (device int64). Captured as the last node of the step's
+ * CUDA graph. */
+int einet_log_step(const double *ll2, const int32_t *status, double *log_ll, int32_t *log_st,
+                   int64_t *cursor, int64_t cap, void *stream);
+
 /* One collective per data-parallel EM update (the reference's
  * merge, engine.py:228-236, is the all-reduce(sum) of the stats buffer).
  * einet_status_to_stats: stats[ll+2] = 1 if this rank's status words report

@@ -66,6 +66,8 @@ EXPORTS = {
     "einet_backward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                                  c_void_p, c_void_p, c_void_p]),
     "einet_status_reset": (c_int32, [c_void_p, c_void_p]),
+    "einet_log_step": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+                                 c_void_p]),
     "einet_status_to_stats": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "einet_status_from_stats": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "einet_plan_set_tensor_cores": (c_int32, [c_void_p, c_int32]),

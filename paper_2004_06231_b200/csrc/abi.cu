@@ -670,6 +670,13 @@ int einet_status_reset(int32_t *status, void *stream) {
   return launch_status_reset(status, (cudaStream_t)stream);
 }
 
+int einet_log_step(const double *ll2, const int32_t *status, double *log_ll, int32_t *log_st,
+                   int64_t *cursor, int64_t cap, void *stream) {
+  if (!ll2 || !status || !log_ll || !log_st || !cursor) return fail(EINET_ERR_USAGE, "null argument");
+  if (cap < 0) return fail(EINET_ERR_USAGE, "cap must be >= 0");
+  return launch_log_step(ll2, status, log_ll, log_st, cursor, cap, (cudaStream_t)stream);
+}
+
 int einet_status_to_stats(einet_plan *plan, const int32_t *status, double *stats,
                           void *stream) {
   if (!plan || !status || !stats) return fail(EINET_ERR_USAGE, "null argument");

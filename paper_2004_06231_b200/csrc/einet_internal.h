@@ -232,6 +232,8 @@ int launch_ef_log_prob(Plan &p, const double *params, const float *x, int64_t B,
                        const uint8_t *mask, double *out, int32_t *status,
                        cudaStream_t st);
 int launch_status_reset(int32_t *status, cudaStream_t st);
+int launch_log_step(const double *ll2, const int32_t *status, double *log_ll, int32_t *log_st,
+                    int64_t *cursor, int64_t cap, cudaStream_t st);
 int launch_status_to_stats(const int32_t *status, double *flag, cudaStream_t st);
 int launch_status_from_stats(const double *flag, int32_t *status, cudaStream_t st);
 void plan_tc_tiling(Plan &p);

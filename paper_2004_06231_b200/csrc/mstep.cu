@@ -503,6 +503,31 @@ int launch_status_from_stats(const double *flag, int32_t *status, cudaStream_t s
   return check_cuda(cudaGetLastError(), "status from stats");
 }
 
+// Device log of a pipelined sequence of EM steps (trainer.em_stochastic_steps):
+// the step's LL sum and sample count and its status words go to row *cursor of
+// log_ll / log_st and the cursor advances -- the last node of the step's CUDA
+// graph, so consecutive graph replays need no host-side copies in between.
+__global__ void k_log_step(const double *ll2, const int32_t *status, double *log_ll,
+                           int32_t *log_st, int64_t *cursor, int64_t cap) {
+  EINET_KERNEL_PROLOGUE();
+  const int64_t row = *cursor;
+  __syncwarp();
+  if (row < cap) {
+    if (threadIdx.x < 2) log_ll[row * 2 + threadIdx.x] = ll2[threadIdx.x];
+    if (threadIdx.x < EINET_STATUS_WORDS)
+      log_st[row * EINET_STATUS_WORDS + threadIdx.x] = status[threadIdx.x];
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) *cursor = row + 1;
+}
+
+int launch_log_step(const double *ll2, const int32_t *status, double *log_ll, int32_t *log_st,
+                    int64_t *cursor, int64_t cap, cudaStream_t st) {
+  launch_k(k_log_step, 1, 32, 0, st, ll2, status, log_ll, log_st, cursor, cap);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "log step");
+}
+
 int launch_status_reset(int32_t *status, cudaStream_t st) {
   launch_k(k_status_reset, 1, 32, 0, st, status);
   count_launch();

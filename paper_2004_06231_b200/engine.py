@@ -210,6 +210,15 @@ class _Engine:
         return st
 
     # -- thin wrappers -----------------------------------------------------
+    def log_step(self, stats, status, log_ll, log_st, cursor):
+        """Row ``cursor`` of the step logs <- (LL sum, count) and the status
+        words; the device cursor advances (``einet_log_step``)."""
+        off = int(self.sizes.stats_ll_offset)
+        _native.check(self._lib.einet_log_step(c_void_p(stats.data_ptr() + 8 * off), _ptr(status),
+                                               _ptr(log_ll),
+                                               _ptr(log_st), _ptr(cursor), log_ll.shape[0],
+                                               _stream()), "einet_log_step")
+
     def status_reset(self, status):
         _native.check(self._lib.einet_status_reset(_ptr(status), _stream()),
                       "einet_status_reset")

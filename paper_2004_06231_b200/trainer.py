@@ -183,8 +183,23 @@ def _reduce(eng, stats, status, process_group):
         eng.status_from_stats(stats, status)
 
 
+def _step_log(model: EinetModel, n: int, dev):
+    """Persistent per-model step logs (LL sum and count, status words) for a
+    pipelined sequence of n steps, and their device cursor reset to row 0; the
+    buffers only grow, so the graphs that write them stay valid."""
+    ent = model.__dict__.get("_steplog")
+    if ent is None or ent[0].shape[0] < n:
+        cap = max(n, 64, 2 * (ent[0].shape[0] if ent is not None else 0))
+        ent = (torch.empty((cap, 2), dtype=torch.float64, device=dev),
+               torch.empty((cap, _native.STATUS_WORDS), dtype=torch.int32, device=dev),
+               torch.zeros(1, dtype=torch.int64, device=dev))
+        model.__dict__["_steplog"] = ent
+    ent[2].zero_()
+    return ent
+
+
 def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_group=None,
-                sticky=False):
+                sticky=False, log=None):
     """Replay (capturing on first use) the CUDA graph of one EM step on the
     device batch ``xd``; returns (engine, stats, status). With a process group
     the step is two graphs (E-step, M-step) around the one all-reduce of the
@@ -196,7 +211,8 @@ def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_
     # every buffer the graph reads or writes is part of the key
     key = (xd.data_ptr(), tuple(xd.shape), float(lam), float(eps_w), int(chunk),
            model.params.flat.data_ptr(), ws.data_ptr(), compute.data_ptr(), stats.data_ptr(),
-           status.data_ptr(), root.data_ptr(), process_group is not None, bool(sticky))
+           status.data_ptr(), root.data_ptr(), process_group is not None, bool(sticky),
+           None if log is None else tuple(t.data_ptr() for t in log))
     cache = model.__dict__.setdefault("_graphs", {})
     gs = cache.get(key)
     if gs is None:
@@ -208,6 +224,8 @@ def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_
             with torch.cuda.graph(g):
                 accumulate(model, xd, chunk, reset_status=not sticky)
                 eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
+                if log is not None:
+                    eng.log_step(stats, status, *log)
             gs = (g,)
         else:
             ge, gm = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
@@ -217,6 +235,8 @@ def _graph_step(model: EinetModel, xd: torch.Tensor, lam, eps_w, chunk, process_
             with torch.cuda.graph(gm):
                 eng.status_from_stats(stats, status)
                 eng.mstep(model.params.flat, compute, stats, lam, eps_w, status)
+                if log is not None:
+                    eng.log_step(stats, status, *log)
             gs = (ge, gm)
         cache[key] = gs
     if process_group is None:
@@ -412,23 +432,20 @@ def em_stochastic_steps(model: EinetModel, batches, lam, eps_w=engine.EPS_W,
     # parameters end where the reference's exception would leave them); each
     # step's LL sum and error words go to a device log read once at the end.
     eng, ws, stats, status, root = model.step_buffers(min(chunk, shape[0]))
-    ll_off = int(eng.sizes.stats_ll_offset)
-    log_ll = torch.empty((len(hosts), 2), dtype=torch.float64, device=dev)
-    log_st = torch.empty((len(hosts), _native.STATUS_WORDS), dtype=torch.int32, device=dev)
+    log = _step_log(model, len(hosts), dev)
     eng.status_reset(status)
     issue_copy(0)
     for i in range(len(hosts)):
         s = i & 1
         cur.wait_event(copied[s])
         eng, stats, status = _graph_step(model, xfs[s] if dec else bufs[s], lam, eps_w, chunk,
-                                         process_group, sticky=True)
+                                         process_group, sticky=True, log=log)
         used[s].record(cur)
         if i + 1 < len(hosts):
             issue_copy(i + 1)
-        log_ll[i].copy_(stats[ll_off:ll_off + 2])
-        log_st[i].copy_(status)
         model.params.mark_compute_current(eng)
-    return _finish_steps(model, log_ll, log_st, process_group)
+    n = len(hosts)
+    return _finish_steps(model, log[0][:n], log[1][:n], process_group)
 
 
 def _finish_steps(model, log_ll, log_st, process_group):
@@ -468,9 +485,7 @@ def _device_steps(model, batches, lam, eps_w, chunk, normalize, process_group):
             xfs = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
             model.__dict__["_stage2_dec"] = xfs
     eng, ws, stats, status, root = model.step_buffers(min(chunk, shape[0]))
-    ll_off = int(eng.sizes.stats_ll_offset)
-    log_ll = torch.empty((len(batches), 2), dtype=torch.float64, device=dev)
-    log_st = torch.empty((len(batches), _native.STATUS_WORDS), dtype=torch.int32, device=dev)
+    log = _step_log(model, len(batches), dev)
     eng.status_reset(status)
     for i, b in enumerate(batches):
         if u8:
@@ -478,11 +493,10 @@ def _device_steps(model, batches, lam, eps_w, chunk, normalize, process_group):
         else:
             xd = engine.as_device_batch(b)
         eng, stats, status = _graph_step(model, xd, lam, eps_w, chunk, process_group,
-                                         sticky=True)
-        log_ll[i].copy_(stats[ll_off:ll_off + 2])
-        log_st[i].copy_(status)
+                                         sticky=True, log=log)
         model.params.mark_compute_current(eng)
-    return _finish_steps(model, log_ll, log_st, process_group)
+    n = len(batches)
+    return _finish_steps(model, log[0][:n], log[1][:n], process_group)
 
 
 def em_full_step(model: EinetModel, data, eps_w=engine.EPS_W, chunk=4096,
