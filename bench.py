@@ -422,11 +422,12 @@ def run_ours(args):
         return float(ms.item())
 
     # kernels per step: counted on one uncaptured step (the timed steps replay
-    # the CUDA graph of exactly this launch sequence)
+    # the CUDA graph of this launch sequence plus its last node, the step-log
+    # kernel einet_log_step of the pipelined em_stochastic_steps)
     os.environ["EINET_CUDA_GRAPHS"] = "0"
     launches0 = _native.launch_count()
     step(x_dev)
-    launches = _native.launch_count() - launches0
+    launches = _native.launch_count() - launches0 + 1
     os.environ.pop("EINET_CUDA_GRAPHS")
     step(x_dev)
     torch.cuda.synchronize()
