@@ -182,7 +182,7 @@ static void free_plan_memory(Plan *p) {
   p->fork_ev = p->join_ev = nullptr;
   if (p->red_stream) cudaStreamDestroy(p->red_stream);
   p->red_stream = nullptr;
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 5; ++i) {
     if (p->red_fork[i]) cudaEventDestroy(p->red_fork[i]);
     if (p->red_done[i]) cudaEventDestroy(p->red_done[i]);
     p->red_fork[i] = p->red_done[i] = nullptr;
@@ -551,7 +551,7 @@ static int build_plan(const einet_plan_desc *d, int64_t max_chunk, Plan *p) {
       (rc = check_cuda(cudaStreamCreateWithFlags(&p->red_stream, cudaStreamNonBlocking),
                        "reduction stream")))
     return rc;
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 5; ++i)
     if ((rc = check_cuda(cudaEventCreateWithFlags(&p->red_fork[i], cudaEventDisableTiming), "event")) ||
         (rc = check_cuda(cudaEventCreateWithFlags(&p->red_done[i], cudaEventDisableTiming), "event")))
       return rc;

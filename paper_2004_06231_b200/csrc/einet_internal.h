@@ -120,8 +120,9 @@ struct Plan {
   // back-pass: the W-statistics batch reductions run on red_stream beside
   // the next layer's kernels (double-buffered partials, w_wpart halves)
   cudaStream_t red_stream = nullptr;
-  // (index 3: the leaf P reductions beside the leaf statistics GEMM)
-  cudaEvent_t red_fork[4] = {}, red_done[4] = {};
+  // (index 3: the leaf P reductions beside the leaf statistics GEMM; 4: the
+  // log-likelihood sum beside the back-pass)
+  cudaEvent_t red_fork[5] = {}, red_done[5] = {};
   int64_t wpart_half = 0;          // doubles per partial buffer half
   // fused M-step (mstep.cu): per-einsum-layer tile geometry, temp leaf terms
   int64_t *d_tiledesc = nullptr;   // einsum layers x TD_WORDS (mstep.cu)

@@ -1305,14 +1305,24 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   const int K = p.k;
   int eo = 0, rc = 0;
   bool red_pending[3] = {false, false, false};
-  // log-likelihood sum of the batch (root entry 0) and the sample count
+  // log-likelihood sum of the batch (root entry 0) and the sample count: off
+  // the critical path on the reduction stream (it only reads the root slab and
+  // writes the stats' LL entries), joined with the other reductions at the end
+  const bool ll_side = p.red_stream && !profiling_enabled();
   {
     ProfScope prof("ll_sum", st);
+    cudaStream_t ls = ll_side ? p.red_stream : st;
+    if (ll_side) {
+      if ((rc = check_cuda(cudaEventRecord(p.red_fork[4], st), "ll fork")) ||
+          (rc = check_cuda(cudaStreamWaitEvent(ls, p.red_fork[4], 0), "ll fork")))
+        return rc;
+    }
     double *part = (double *)(wsb + p.w_llpart);
-    launch_k(k_ll_sum, ceil_div(B, 256), 256, 0, st, w, p.root_out_slab, B,
+    launch_k(k_ll_sum, ceil_div(B, 256), 256, 0, ls, w, p.root_out_slab, B,
              stats + p.sizes.stats_ll_offset, (double)B, part,
              (unsigned *)part + 2 * ceil_div(w.bc, 256));
     count_launch();
+    if (ll_side && (rc = check_cuda(cudaEventRecord(p.red_done[4], ls), "ll done"))) return rc;
   }
   for (int li = (int)p.layers.size() - 1; li >= 0; --li) {
     const LayerPlan &L = p.layers[li];
@@ -1420,6 +1430,8 @@ int launch_backward(Plan &p, const double *params, const uint8_t *compute, const
   }
   rc = launch_leaf_backward(p, compute, x, B, wsb, stats, st);
   if (rc) return rc;
+  if (ll_side && (rc = check_cuda(cudaStreamWaitEvent(st, p.red_done[4], 0), "ll join")))
+    return rc;
   for (int q = 0; q < 3; ++q)  // join the reduction stream
     if (red_pending[q] && (rc = check_cuda(cudaStreamWaitEvent(st, p.red_done[q], 0), "wstats join")))
       return rc;
